@@ -1,0 +1,330 @@
+#!/usr/bin/env python
+"""Benchmark: fused kernel-operator product K(X, X) S on B200 (BASELINE cfg3).
+
+BASELINE.json metric: "fused K^.S GFLOP/s (%roofline) ...".  One step is one
+kernel-operator product over the cfg3 workload (N = 1e6 points, D = 8,
+S of width 32, RBF l = 1.5; ``--workload cfg3-matern`` for the Matern
+variant) with inputs resident in HBM.  Algorithmic FLOPs per (i, j) pair are
+F = 2D + 2w, i.e. 80 at cfg3.
+
+Multi-GPU (torchrun): contiguous row blocks of X (multiples of 128 rows) per
+rank, X and S replicated, and each step ends with the all-gather of the
+output row blocks (the exchange the solver needs before the next product).
+Total work is fixed as N grows -> "strong" scaling.
+
+``--impl reference`` times the reference algorithm's CPU implementation (the
+numpy restatement in oracle/, bit-identical to the reference, run with all
+host cores over row samples of the same workload).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+P_MUFU_PER_SM_CLK = 16          # ex2 per clock per SM (cc 10.0 throughput table)
+TF32_FALLBACK_TFLOPS = None
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            d = json.load(fh)
+        return dict(hbm=d.get("hbm_gbs", 6552.0), bf16=d.get("bf16_tflops", 1668.4),
+                    sm_max_mhz=d.get("sm_max_mhz", 1965.0), source="measured")
+    return dict(hbm=6650.0, bf16=1590.0, sm_max_mhz=1965.0, source="fallback")
+
+
+def workload(name):
+    from paper_2310_20285_b200 import configs
+    fam = "matern32" if name.endswith("matern") else "rbf"
+    c = configs.cfg3(family=fam)
+    return c
+
+
+class ClockSampler(threading.Thread):
+    """Samples SM clock and clock-event reasons with NVML during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        super().__init__(daemon=True)
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop_evt = threading.Event()
+        self.ok = False
+
+    def run(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+            while not self._stop_evt.is_set():
+                self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                mask = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+                time.sleep(0.1)
+        except Exception as exc:  # NVML unavailable: report, do not fake
+            self.error = repr(exc)
+
+    def stop(self):
+        self._stop_evt.set()
+        self.join(timeout=2)
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def cpu_reference_sample(spec, X, S, rows, processes):
+    """Time the reference tile body (oracle restatement) on ``rows``."""
+    from oracle import ncgp_oracle as O
+    if processes <= 1:
+        t0 = time.perf_counter()
+        O.kernel_matmul_rows(spec, X[rows], X, S, tile=len(rows))
+        return time.perf_counter() - t0
+    import multiprocessing as mp
+    chunks = np.array_split(rows, processes)
+    ctx = mp.get_context("fork")
+    global _SHARED
+    _SHARED = (spec, X, S)
+    with ctx.Pool(processes) as pool:
+        pool.map(_cpu_chunk, [chunks[0][:1]] * processes)  # warm the workers
+        t0 = time.perf_counter()
+        pool.map(_cpu_chunk, chunks)
+        return time.perf_counter() - t0
+
+
+_SHARED = None
+
+
+def _cpu_chunk(rows):
+    from oracle import ncgp_oracle as O
+    spec, X, S = _SHARED
+    O.kernel_matmul_rows(spec, X[rows], X, S, tile=max(1, len(rows)))
+    return 0
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    c = workload(args.workload)
+    X, S, spec = c["X"], c["S"], c["kernel"]
+    n, d = X.shape
+    w = S.shape[1]
+    F = 2 * d + 2 * w
+    cores = os.cpu_count() or 1
+    rows_per_step = 2 * cores
+    rng = np.random.default_rng(1)
+    times = []
+    for it in range(args.warmup + args.steps):
+        rows = np.sort(rng.choice(n, size=rows_per_step, replace=False))
+        dt = cpu_reference_sample(spec, X, S, rows, cores)
+        if it >= args.warmup:
+            times.append(dt)
+    pairs = rows_per_step * n
+    value = F * pairs / statistics.mean(times) / 1e9
+    line = {
+        "impl": "reference", "metric": "fused K^.S GFLOP/s (cfg3 K(X,X)S)",
+        "value": round(value, 4), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(1e3 * statistics.mean(times), 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": c["name"], "n": n, "d": d, "w": w,
+                                        "kernel": list(spec), "flops_per_pair": F},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", "cores": cores,
+                         "kind": "port",
+                         "sample": f"{rows_per_step} random rows x all {n} columns per step "
+                                   f"(reference tile body gp.py:240-249, numpy fp64, "
+                                   f"{cores} worker processes)"},
+        "e2e": {"value": round(value, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    import paper_2310_20285_b200 as P
+    from paper_2310_20285_b200 import _native
+    from paper_2310_20285_b200.kernels import KernelOperator
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    c = workload(args.workload)
+    X, S, spec = c["X"], c["S"], c["kernel"]
+    n, d = X.shape
+    w = S.shape[1]
+    F = 2 * d + 2 * w
+    E = 1 if spec[0] == "rbf" else 2
+    Xd = torch.from_numpy(X).to(dev, torch.float32)
+    Sd = torch.from_numpy(S).to(dev, torch.float32)
+    op = KernelOperator(spec[0], spec[1], spec[2], Xd, w_max=w, impl=args.kop)
+    tiles = (n + 127) // 128
+    per = (tiles + world - 1) // world * 128
+    r0, r1 = min(n, rank * per), min(n, (rank + 1) * per)
+    out_full = torch.empty((per * world, w), dtype=torch.float32, device=dev)
+    out_local = torch.empty((per, w), dtype=torch.float32, device=dev)
+    local_out_view = torch.empty((n, w), dtype=torch.float32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        op.apply(Sd, out=local_out_view, row_begin=r0, row_end=r1)
+        if world > 1:
+            out_local[: r1 - r0].copy_(local_out_view[r0:r1])
+            dist.all_gather_into_tensor(out_full, out_local)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    launches0 = _native.launch_count()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kstarts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    for k in range(args.steps):
+        flush.zero_()  # evict L2 between timed steps (outside the events)
+        starts[k].record(stream)
+        kstarts[k].record(stream)
+        op.apply(Sd, out=local_out_view, row_begin=r0, row_end=r1)
+        kends[k].record(stream)
+        if world > 1:
+            out_local[: r1 - r0].copy_(local_out_view[r0:r1])
+            dist.all_gather_into_tensor(out_full, out_local)
+        ends[k].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = _native.launch_count() - launches0
+    clocks = sampler.stop()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    kern_ms = [s.elapsed_time(e) for s, e in zip(kstarts, kends)]
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms, sum(kern_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, kern_total = float(t[0]), float(t[1])
+    pairs = float(n) * float(n)
+    value = F * pairs * args.steps / (total_ms / 1e3) / 1e9
+
+    # ---- e2e through the public API: pinned host S in, host result out
+    e2e = None
+    if rank == 0 and world == 1:
+        Sh = torch.from_numpy(S).to(torch.float32).pin_memory()
+        prior = P.MultiOutputPrior(kernels=(P.KernelSpec(*spec),) * w)
+        Xh = torch.from_numpy(X).to(torch.float32)
+        P.prior_matvec(prior, Xh, Sh.view(-1))  # builds + caches the operator
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(max(1, args.steps)):
+            res = P.prior_matvec(prior, Xh, Sh.view(-1))
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / max(1, args.steps)
+        e2e = {"value": round(F * pairs / e2e_s / 1e9, 3), "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int(Sh.numel() * 4),
+               "d2h_bytes_per_step": int(res.numel() * res.element_size()),
+               "note": "X resident in the cached operator; S (pinned fp32) uploaded and "
+                       "the product downloaded every step"}
+
+    # ---- roofline of the dominant kernel (the fused kernel-matmul)
+    pk = peaks()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    mufu_rate = sms * P_MUFU_PER_SM_CLK * pk["sm_max_mhz"] * 1e6   # ex2 / s
+    tensor_tflops = pk["bf16"] / 2.0                                 # tf32-class dense
+    local_pairs = float(r1 - r0) * n
+    t_kernel = kern_total / args.steps / 1e3
+    achieved = F * local_pairs / t_kernel / 1e12
+    peak_tflops = min(tensor_tflops, F * mufu_rate / E / 1e12)
+    roofline = {"bound": "tensor", "limiter": "MUFU ex2" if peak_tflops < tensor_tflops
+                else "tensor pipe", "achieved": round(achieved, 3), "peak": round(peak_tflops, 3),
+                "unit": "TFLOP/s", "frac": round(achieved / peak_tflops, 4), "traffic": None,
+                "peak_basis": f"min({pk['source']} bf16 {pk['bf16']}/2 TF/s, "
+                              f"{sms} SM x {P_MUFU_PER_SM_CLK} ex2/clk x "
+                              f"{pk['sm_max_mhz']} MHz x F/E={F}/{E})",
+                "kernel_ms": round(1e3 * t_kernel, 3), "impl": op.impl}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rows = np.sort(np.random.default_rng(0).choice(n, size=args.cpu_rows, replace=False))
+        cpu_s = cpu_reference_sample(spec, X, S, rows, 1)
+        cpu = {"value": round(F * len(rows) * n / cpu_s / 1e9, 4), "unit": "GFLOP/s",
+               "cores": 1, "kind": "port",
+               "sample": f"{len(rows)} random rows x all {n} columns (reference tile body, "
+                         f"numpy fp64, 1 core), {cpu_s:.1f} s"}
+
+    if rank == 0:
+        line = {"metric": "fused K^.S GFLOP/s (cfg3 K(X,X)S)", "value": round(value, 3),
+                "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": round(total_ms / args.steps, 3), "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic",
+                "config": {"workload": c["name"], "n": n, "d": d, "w": w, "kernel": list(spec),
+                           "flops_per_pair": F, "exp_per_pair": E,
+                           "l2": "flushed (256 MiB write) before every timed step",
+                           "parallelism": f"row-sharded x{world}"},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(launches), "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg3", choices=["cfg3", "cfg3-matern"])
+    ap.add_argument("--kop", default="auto", choices=["auto", "tcgen05", "simt"])
+    ap.add_argument("--cpu-rows", type=int, default=24)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        return run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,196 @@
+/*
+ * ncgp_b200.h -- C ABI of the B200-native IterNCGP hot path (libncgp_b200.so).
+ *
+ * The reference package ``ncgp`` is pure Python; the seam this library
+ * replaces is its operator plug-in boundary:
+ *
+ *   RegressionSystem(apply_kernel, apply_noise, rhs)      solver.py:42-57
+ *   apply_kernel = prior_matvec(prior, X, ., tile)          outer.py:511-512, gp.py:222-250
+ *   apply_noise  = likelihood.w_inv_matvec(f, .)           outer.py:517, likelihoods.py:258-262
+ *
+ * Every entry point below names the reference function it replaces.
+ *
+ * Conventions
+ *  - Every function returns an int status: NCGP_OK (0) or one of
+ *    NCGP_DIMENSION_MISMATCH (1, -> ncgp.DimensionMismatch), NCGP_INVALID_INPUT
+ *    (2, -> ncgp.InvalidInput), NCGP_CUDA_ERROR (3), NCGP_UNSUPPORTED (4).
+ *    ncgp_last_error() returns a thread-local message for the last failure.
+ *  - All array arguments are caller-owned DEVICE pointers; the library does
+ *    no device allocation on the hot path.  Scratch space is passed in as a
+ *    ``workspace`` sized by the matching *_workspace_bytes query.
+ *  - All work is enqueued on the caller's ``stream`` (a cudaStream_t passed
+ *    as void*; NULL = legacy default stream).  Nothing synchronises except
+ *    functions documented as blocking.
+ *  - ``dtype`` selects NCGP_F32 (float) or NCGP_F64 (double) for every
+ *    floating-point array of the call.  Reductions accumulate in fp64 with
+ *    a fixed order, so results are deterministic run to run.
+ *  - Vectors over (point, output) pairs use the reference's CN layout
+ *    (gp.py:1-8): entry n*C + c, i.e. an N x C row-major matrix.
+ *  - Column blocks (solver buffers S, T, Q) are stored column-contiguous:
+ *    column b starts at ptr + b * ld.
+ *  - Operators are bound to the device current at creation; an operator
+ *    must not be used by two host threads at once.
+ */
+#ifndef NCGP_B200_H
+#define NCGP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  NCGP_OK = 0,
+  NCGP_DIMENSION_MISMATCH = 1,
+  NCGP_INVALID_INPUT = 2,
+  NCGP_CUDA_ERROR = 3,
+  NCGP_UNSUPPORTED = 4
+};
+
+enum { NCGP_F32 = 0, NCGP_F64 = 1 };
+enum { NCGP_RBF = 0, NCGP_MATERN32 = 1 };
+
+/* Kernel-operator implementation selector (NCGP_KOP_AUTO picks the tcgen05
+ * path for fp32 and the fp64 CUDA-core path for fp64). */
+enum { NCGP_KOP_AUTO = 0, NCGP_KOP_TCGEN05 = 1, NCGP_KOP_SIMT = 2 };
+
+const char* ncgp_last_error(void);
+int ncgp_version(void);
+/* Blocking: queries the current device. */
+int ncgp_device_info(int* sm_count, int* cc_major, int* cc_minor);
+/* Number of kernels this library has launched in this process. */
+int64_t ncgp_launch_count(void);
+
+/* ---------------------------------------------------------------------
+ * K1 fused kernel-matmul (replaces prior_matvec gp.py:222-250 with the
+ * tile body gp.py:240-249, _sqdist gp.py:179-191, kernel_from_sqdist
+ * gp.py:156-176; newton_update outer.py:465-468; and, with X_rows =
+ * X_test, the dense cross_covariance products of posterior.py:52-84).
+ *
+ *   out[i, c] = sum_j k(Xr[i], Xc[j]) * V[j, c]      0 <= i < n_rows, c < w
+ *
+ * for one stationary kernel (family, lengthscale, outputscale).  K is never
+ * materialised.  Xr: (n_rows, d) row-major, Xc: (n_cols, d) row-major,
+ * V: (n_cols, w) with row stride ldv, out: (n_rows, w) with row stride ldo.
+ * ------------------------------------------------------------------- */
+typedef struct ncgp_kop ncgp_kop;
+
+size_t ncgp_kop_workspace_bytes(int impl, int dtype, int64_t n_rows,
+                                int64_t n_cols, int d, int w_max);
+
+/* Packs Xr / Xc into the operator's tiled layout (enqueued on stream). */
+int ncgp_kop_create(ncgp_kop** op, int impl, int family, double lengthscale,
+                    double outputscale, int dtype, const void* Xr,
+                    int64_t n_rows, const void* Xc, int64_t n_cols, int d,
+                    int w_max, void* workspace, size_t workspace_bytes,
+                    void* stream);
+
+/* out[row_begin:row_end, :w] = K(Xr[row_begin:row_end], Xc) V.
+ * row_begin must be a multiple of 128 unless it equals 0 (row sharding). */
+int ncgp_kop_apply(ncgp_kop* op, const void* V, int64_t ldv, int w,
+                   void* out, int64_t ldo, int64_t row_begin,
+                   int64_t row_end, void* stream);
+
+/* Actual implementation chosen (NCGP_KOP_TCGEN05 or NCGP_KOP_SIMT). */
+int ncgp_kop_impl(const ncgp_kop* op);
+int ncgp_kop_destroy(ncgp_kop* op);
+
+/* ---------------------------------------------------------------------
+ * K3/K4/K5 likelihood kernels.
+ * ------------------------------------------------------------------- */
+
+/* Softmax per-point statistics (likelihoods.py:235-238 probabilities,
+ * :285-288 softmax_rows, :247-250 grad_log_lik, outer.py:460-462
+ * pseudo_targets).  f, grad, yhat: CN (n*C); pi: (n, C).  grad / yhat may
+ * be NULL. */
+int ncgp_softmax_stats(int dtype, const void* f, const int64_t* labels,
+                       int64_t n, int C, void* pi, void* grad, void* yhat,
+                       void* stream);
+
+/* out[:, b] = beta * base[:, b] + alpha * (W(f)^+ V[:, b])  for b < k
+ * with W^+ the blockwise softmax pseudo-inverse (likelihoods.py:291-310,
+ * via w_inv_matvec :258-262).  V, base, out: column blocks of length n*C.
+ * base may be NULL (then beta is ignored). */
+int ncgp_softmax_winv(int dtype, const void* pi, int64_t n, int C,
+                      const void* V, int64_t ldv, int k, const void* base,
+                      int64_t ldb, double alpha, double beta, void* out,
+                      int64_t ldo, void* stream);
+
+/* W_n products (diag(pi_n) - pi_n pi_n') v_n (likelihoods.py:252-256). */
+int ncgp_softmax_w(int dtype, const void* pi, int64_t n, int C,
+                   const void* V, int64_t ldv, int k, void* out, int64_t ldo,
+                   void* stream);
+
+/* Bernoulli-logit statistics (likelihoods.py:202-212, outer.py:460-462):
+ * winv = 1/(s(1-s)) with the reference's clamp, w = s(1-s),
+ * grad = y - s, yhat = f + winv * grad.  Any output may be NULL. */
+int ncgp_bernoulli_stats(int dtype, const void* f, const int64_t* labels,
+                         int64_t n, void* winv, void* w, void* grad,
+                         void* yhat, void* stream);
+
+/* out[:, b] = beta * base[:, b] + alpha * diag(dvec) V[:, b]
+ * (_apply_diag likelihoods.py:149-153). */
+int ncgp_diag_apply(int dtype, const void* dvec, int64_t n, const void* V,
+                    int64_t ldv, int k, const void* base, int64_t ldb,
+                    double alpha, double beta, void* out, int64_t ldo,
+                    void* stream);
+
+/* ---------------------------------------------------------------------
+ * K6 vector / tall-skinny kernels for the inner solver (solver.py:203-331,
+ * linalg.py:389-400).  Reductions write fp64 results to DEVICE memory.
+ * ------------------------------------------------------------------- */
+
+size_t ncgp_reduce_workspace_bytes(int64_t n, int k);
+
+/* out[p] = sum_i x_p[i] * y_p[i] for p < npairs (npairs <= 4); xs / ys are
+ * HOST arrays of device pointers. */
+int ncgp_dots(int dtype, int64_t n, int npairs, const void* const* xs,
+              const void* const* ys, double* out, void* workspace,
+              size_t workspace_bytes, void* stream);
+
+/* out[r] = sum_i Q[r*ldq + i] * z[i]  for r < k   (Q' z, linalg.py:400). */
+int ncgp_gemv_t(int dtype, const void* Q, int64_t ldq, int k, const void* z,
+                int64_t n, double* out, void* workspace,
+                size_t workspace_bytes, void* stream);
+
+/* out[i] = s[i] + alpha * sum_r Q[r*ldq + i] * y[r]   (y: device fp64). */
+int ncgp_gemv_n(int dtype, const void* Q, int64_t ldq, int k,
+                const double* y, const void* s, double alpha, void* out,
+                int64_t n, void* stream);
+
+/* out = a*x + b*y + c*z (any of y, z may be NULL). */
+int ncgp_lincomb(int dtype, int64_t n, double a, const void* x, double b,
+                 const void* y, double c, const void* z, void* out,
+                 void* stream);
+
+/* M[a*ldm + b] = sum_i S[a*lds + i] * Y[b*ldy + i] for a < ka, b < kb,
+ * fp64 result (the recycled Gram S'(T + W^+ S), solver.py:311). */
+size_t ncgp_gram_workspace_bytes(int64_t n, int ka, int kb);
+int ncgp_gram(int dtype, const void* S, int64_t lds, int ka, const void* Y,
+              int64_t ldy, int kb, int64_t n, double* M, int64_t ldm,
+              void* workspace, size_t workspace_bytes, void* stream);
+
+/* out[c*ldo + i] = sum_b S[b*lds + i] * U[b*ldu + c]  for c < kc
+ * (buffer rotation S U, T U, S diag(l)^-1/2: solver.py:325-330).  U is a
+ * device fp64 (kb x kc) matrix with row stride ldu. */
+int ncgp_rotate(int dtype, const void* S, int64_t lds, int kb,
+                const double* U, int64_t ldu, int kc, void* out, int64_t ldo,
+                int64_t n, void* stream);
+
+/* ---------------------------------------------------------------------
+ * K2 posterior helpers (posterior.py:52-84).
+ * ------------------------------------------------------------------- */
+
+/* var[t*C + c] = max(s2[c] - sum_{r<R} A[t*lda + c*R + r]^2, 0);
+ * s2: device fp64 array of C prior variances. */
+int ncgp_marginal_var(int dtype, const void* A, int64_t lda, int64_t nt,
+                      int C, int R, const double* s2, void* var,
+                      void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NCGP_B200_H */

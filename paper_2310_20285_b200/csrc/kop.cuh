@@ -1,0 +1,45 @@
+// Kernel-operator plan shared by the tcgen05 and CUDA-core implementations.
+#pragma once
+
+#include "common.cuh"
+
+struct ncgp_kop {
+  int impl;      // NCGP_KOP_TCGEN05 | NCGP_KOP_SIMT
+  int family;    // NCGP_RBF | NCGP_MATERN32
+  int dtype;     // NCGP_F32 | NCGP_F64
+  int d;
+  double ell, s2;
+  int64_t n_rows, n_cols;
+  int w_max;
+  int sms;
+  const void* Xr;  // caller-owned (SIMT path reads it on every apply)
+  const void* Xc;
+  uint8_t* ws;     // caller-owned workspace
+  size_t ws_bytes;
+  // ---- tcgen05 path state (see kop_tc.cu) ----
+  int ka;               // packed K of the distance GEMM (multiple of 16)
+  int wpad;             // padded RHS width of the contraction GEMM
+  int64_t row_tiles, col_tiles;
+  uint8_t* xa_pack;     // row operand tiles
+  uint8_t* col_pack;    // per column tile: [XB | Vhi | Vlo]
+  size_t col_tile_bytes;
+  double* col_scale;    // per RHS column power-of-two scale (wpad)
+  double* partial;      // fp64 partial sums
+  double k_scale;       // 2^s prescale of kernel values
+};
+
+namespace ncgp {
+
+// CUDA-core implementation (kop_simt.cu)
+size_t simt_workspace_bytes(int dtype, int64_t n_rows, int64_t n_cols, int d, int w_max);
+int simt_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, void* out, int64_t ldo,
+               int64_t r0, int64_t r1, cudaStream_t st);
+
+// tcgen05 implementation (kop_tc.cu)
+bool tc_supported(int dtype, int d, int w_max);
+size_t tc_workspace_bytes(int64_t n_rows, int64_t n_cols, int d, int w_max);
+int tc_prepare(ncgp_kop* op, cudaStream_t st);
+int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, void* out, int64_t ldo,
+             int64_t r0, int64_t r1, cudaStream_t st);
+
+}  // namespace ncgp

@@ -1,0 +1,106 @@
+// C ABI of the K1 kernel operator (see include/ncgp_b200.h).
+#include <new>
+
+#include "kop.cuh"
+
+namespace {
+
+int resolve_impl(int impl, int dtype, int d, int w_max) {
+  if (impl == NCGP_KOP_AUTO)
+    return (dtype == NCGP_F32 && ncgp::tc_supported(dtype, d, w_max)) ? NCGP_KOP_TCGEN05
+                                                                       : NCGP_KOP_SIMT;
+  return impl;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t ncgp_kop_workspace_bytes(int impl, int dtype, int64_t n_rows, int64_t n_cols, int d,
+                                int w_max) {
+  impl = resolve_impl(impl, dtype, d, w_max);
+  if (impl == NCGP_KOP_TCGEN05) return ncgp::tc_workspace_bytes(n_rows, n_cols, d, w_max);
+  return ncgp::simt_workspace_bytes(dtype, n_rows, n_cols, d, w_max);
+}
+
+int ncgp_kop_create(ncgp_kop** out, int impl, int family, double lengthscale, double outputscale,
+                    int dtype, const void* Xr, int64_t n_rows, const void* Xc, int64_t n_cols,
+                    int d, int w_max, void* workspace, size_t workspace_bytes, void* stream) {
+  NCGP_CHECK_ARG(out != nullptr, NCGP_INVALID_INPUT, "null output handle");
+  *out = nullptr;
+  NCGP_CHECK_ARG(family == NCGP_RBF || family == NCGP_MATERN32, NCGP_INVALID_INPUT,
+                 "unknown kernel family %d", family);
+  NCGP_CHECK_ARG(lengthscale > 0 && lengthscale < 1e300, NCGP_INVALID_INPUT,
+                 "lengthscale must be a positive finite real");
+  NCGP_CHECK_ARG(outputscale > 0 && outputscale < 1e300, NCGP_INVALID_INPUT,
+                 "outputscale must be a positive finite real");
+  NCGP_CHECK_ARG(dtype == NCGP_F32 || dtype == NCGP_F64, NCGP_UNSUPPORTED, "dtype %d", dtype);
+  NCGP_CHECK_ARG(n_rows >= 0 && n_cols >= 0 && d >= 1 && w_max >= 1, NCGP_DIMENSION_MISMATCH,
+                 "bad operator shape rows=%lld cols=%lld d=%d w_max=%d", (long long)n_rows,
+                 (long long)n_cols, d, w_max);
+  NCGP_CHECK_ARG(Xr != nullptr && Xc != nullptr, NCGP_INVALID_INPUT, "null input matrix");
+  const int res = resolve_impl(impl, dtype, d, w_max);
+  if (res == NCGP_KOP_TCGEN05)
+    NCGP_CHECK_ARG(ncgp::tc_supported(dtype, d, w_max), NCGP_UNSUPPORTED,
+                   "tcgen05 operator needs fp32, d <= 64, w_max <= 64 (d=%d w_max=%d)", d, w_max);
+  const size_t need = ncgp_kop_workspace_bytes(res, dtype, n_rows, n_cols, d, w_max);
+  NCGP_CHECK_ARG(workspace_bytes >= need, NCGP_INVALID_INPUT,
+                 "workspace too small: %zu < %zu bytes", workspace_bytes, need);
+  ncgp_kop* op = new (std::nothrow) ncgp_kop();
+  NCGP_CHECK_ARG(op != nullptr, NCGP_INVALID_INPUT, "host allocation failed");
+  op->impl = res;
+  op->family = family;
+  op->dtype = dtype;
+  op->d = d;
+  op->ell = lengthscale;
+  op->s2 = outputscale;
+  op->n_rows = n_rows;
+  op->n_cols = n_cols;
+  op->w_max = w_max;
+  op->sms = ncgp::sm_count();
+  op->Xr = Xr;
+  op->Xc = Xc;
+  op->ws = static_cast<uint8_t*>(workspace);
+  op->ws_bytes = workspace_bytes;
+  if (res == NCGP_KOP_TCGEN05) {
+    int rc = ncgp::tc_prepare(op, ncgp::as_stream(stream));
+    if (rc != NCGP_OK) {
+      delete op;
+      return rc;
+    }
+  }
+  *out = op;
+  return NCGP_OK;
+}
+
+int ncgp_kop_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, void* out, int64_t ldo,
+                   int64_t row_begin, int64_t row_end, void* stream) {
+  NCGP_CHECK_ARG(op != nullptr, NCGP_INVALID_INPUT, "null operator");
+  NCGP_CHECK_ARG(w >= 0 && w <= op->w_max, NCGP_DIMENSION_MISMATCH,
+                 "rhs width %d outside [0, %d]", w, op->w_max);
+  NCGP_CHECK_ARG(ldv >= w && ldo >= w, NCGP_DIMENSION_MISMATCH, "leading dimension < width");
+  NCGP_CHECK_ARG(0 <= row_begin && row_begin <= row_end && row_end <= op->n_rows,
+                 NCGP_DIMENSION_MISMATCH, "row range [%lld, %lld) outside [0, %lld)",
+                 (long long)row_begin, (long long)row_end, (long long)op->n_rows);
+  if (w == 0 || row_end == row_begin) return NCGP_OK;
+  NCGP_CHECK_ARG(V != nullptr && out != nullptr, NCGP_INVALID_INPUT, "null operand");
+  if (op->n_cols == 0) {
+    // empty sum: zero output rows
+    const size_t es = op->dtype == NCGP_F64 ? 8 : 4;
+    NCGP_CUDA(cudaMemset2DAsync(static_cast<uint8_t*>(out) + row_begin * ldo * es, ldo * es, 0,
+                                w * es, row_end - row_begin, ncgp::as_stream(stream)));
+    return NCGP_OK;
+  }
+  if (op->impl == NCGP_KOP_TCGEN05)
+    return ncgp::tc_apply(op, V, ldv, w, out, ldo, row_begin, row_end, ncgp::as_stream(stream));
+  return ncgp::simt_apply(op, V, ldv, w, out, ldo, row_begin, row_end, ncgp::as_stream(stream));
+}
+
+int ncgp_kop_impl(const ncgp_kop* op) { return op ? op->impl : -1; }
+
+int ncgp_kop_destroy(ncgp_kop* op) {
+  delete op;
+  return NCGP_OK;
+}
+
+}  // extern "C"

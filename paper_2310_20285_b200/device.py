@@ -1,0 +1,128 @@
+"""Device plumbing: dtype policy, streams, host<->device moves, workspaces.
+
+PyTorch is used only as the allocator / stream / collective provider; all
+arithmetic on the hot path runs in libncgp_b200.so.
+"""
+
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+import torch
+
+from . import _native
+
+_state = threading.local()
+_DTYPES = {"float32": torch.float32, "float64": torch.float64,
+           torch.float32: torch.float32, torch.float64: torch.float64,
+           np.float32: torch.float32, np.float64: torch.float64}
+_default_dtype = torch.float64
+
+
+def set_default_dtype(dtype) -> None:
+    """Working precision used when an API call does not pass ``dtype``.
+
+    float64 (the default) reproduces the reference's precision; float32
+    selects the tcgen05 kernel-operator path the BASELINE configs 2-5 use.
+    """
+    global _default_dtype
+    _default_dtype = resolve_dtype(dtype)
+
+
+def get_default_dtype() -> torch.dtype:
+    return _default_dtype
+
+
+def resolve_dtype(dtype=None) -> torch.dtype:
+    if dtype is None:
+        return _default_dtype
+    if isinstance(dtype, np.dtype):
+        dtype = dtype.type
+    try:
+        return _DTYPES[dtype]
+    except KeyError:
+        raise ValueError(f"unsupported dtype {dtype!r}; use float32 or float64")
+
+
+def code(t) -> int:
+    dt = t.dtype if isinstance(t, torch.Tensor) else t
+    if dt == torch.float64:
+        return _native.F64
+    if dt == torch.float32:
+        return _native.F32
+    raise ValueError(f"unsupported tensor dtype {dt}")
+
+
+def require_cuda() -> torch.device:
+    if not torch.cuda.is_available():
+        raise _native.NativeUnavailable("no CUDA device: the B200 path has no CPU fallback")
+    _native.load()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def device() -> torch.device:
+    return require_cuda()
+
+
+def stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t) -> int:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def to_device(x, dtype=None, contiguous=True) -> torch.Tensor:
+    """Move an array-like to the current CUDA device in the working dtype."""
+    dev = require_cuda()
+    dt = resolve_dtype(dtype)
+    if isinstance(x, torch.Tensor):
+        t = x.to(device=dev, dtype=dt)
+    else:
+        arr = np.asarray(x)
+        t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64 if dt == torch.float64
+                                                  else np.float32)).to(dev, non_blocking=False)
+    return t.contiguous() if contiguous else t
+
+
+def labels_to_device(y) -> torch.Tensor:
+    dev = require_cuda()
+    if isinstance(y, torch.Tensor):
+        return y.to(device=dev, dtype=torch.int64).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(y), dtype=np.int64)).to(dev)
+
+
+def to_host(t) -> np.ndarray:
+    if isinstance(t, torch.Tensor):
+        return t.detach().to("cpu", torch.float64).numpy()
+    return np.asarray(t, dtype=np.float64)
+
+
+def is_device(x) -> bool:
+    return isinstance(x, torch.Tensor) and x.is_cuda
+
+
+class Workspace:
+    """Growable per-device scratch buffers keyed by purpose."""
+
+    def __init__(self):
+        self._bufs = {}
+
+    def get(self, key: str, nbytes: int) -> torch.Tensor:
+        dev = require_cuda()
+        k = (dev.index, key)
+        buf = self._bufs.get(k)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=dev)
+            self._bufs[k] = buf
+        return buf
+
+
+def workspace() -> Workspace:
+    ws = getattr(_state, "ws", None)
+    if ws is None:
+        ws = _state.ws = Workspace()
+    return ws

@@ -1,0 +1,297 @@
+"""Multi-output GP priors on the device (mirror of ncgp/gp.py).
+
+Public names and semantics follow the reference: ``KernelSpec``
+(gp.py:123-141), ``MultiOutputPrior`` (gp.py:194-219), CN layout
+(gp.py:1-8, entry n*C + c), ``reorder`` (gp.py:109-120), ``kernel_eval``
+(gp.py:144-153), ``prior_matvec`` (gp.py:222-250) and ``cross_covariance``
+(gp.py:253-274).  The products run on the B200 through
+:class:`PriorOperator`, which groups outputs by unique kernel spec (the
+reference's per-tile dedup, gp.py:243-248) and issues one fused
+kernel-matmul per group with all of that group's outputs as right-hand
+columns.  The ``tile`` argument is accepted for signature compatibility;
+the device operator's reduction order does not depend on it.
+"""
+
+from __future__ import annotations
+
+import enum
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Tuple
+
+import numpy as np
+import torch
+
+from .device import is_device, resolve_dtype, to_device, to_host
+from .exceptions import DimensionMismatch, InvalidInput
+from .kernels import KernelOperator
+
+DOMAIN_TAGS = ("counts", "binary", "class-index", "real")
+
+
+class Ordering(enum.Enum):
+    CN = "cn"  # output index fastest
+    NC = "nc"  # point index fastest
+
+
+def reorder(v, src: Ordering, dst: Ordering, n_points: int, n_outputs: int):
+    """CN <-> NC permutation of a length N*C vector (gp.py:109-120)."""
+    dev = is_device(v)
+    a = v if dev else np.asarray(v)
+    if a.shape[0] != n_points * n_outputs:
+        raise DimensionMismatch(f"vector length {a.shape[0]} != {n_points} * {n_outputs}")
+    if src == dst:
+        return a.clone() if dev else a.copy()
+    shape = (n_points, n_outputs) if src == Ordering.CN else (n_outputs, n_points)
+    if dev:
+        return a.reshape(shape).t().contiguous().reshape(-1)
+    return a.reshape(shape).T.ravel().copy()
+
+
+@dataclass(frozen=True)
+class KernelSpec:
+    """Stationary kernel (gp.py:123-141).
+
+    rbf:      s2 * exp(-d^2 / (2 l^2))
+    matern32: s2 * (1 + sqrt(3) d / l) * exp(-sqrt(3) d / l)
+    """
+
+    family: str
+    lengthscale: float
+    outputscale: float
+
+    def __post_init__(self):
+        if self.family not in ("rbf", "matern32"):
+            raise InvalidInput(f"unknown kernel family {self.family!r}")
+        for name in ("lengthscale", "outputscale"):
+            val = getattr(self, name)
+            if not (val > 0 and np.isfinite(val)):
+                raise InvalidInput(f"{name} must be a positive finite real")
+
+
+@dataclass(frozen=True)
+class MultiOutputPrior:
+    """Independent constant-mean GPs, one kernel per output (gp.py:194-219)."""
+
+    kernels: Tuple[KernelSpec, ...]
+    mean: Tuple[float, ...] = ()
+
+    def __post_init__(self):
+        if len(self.kernels) < 1:
+            raise InvalidInput("at least one output kernel is required")
+        if self.mean and len(self.mean) != len(self.kernels):
+            raise DimensionMismatch("one mean constant per output is required")
+        if not self.mean:
+            object.__setattr__(self, "mean", (0.0,) * len(self.kernels))
+
+    @property
+    def num_outputs(self) -> int:
+        return len(self.kernels)
+
+    def mean_vector(self, n_points: int) -> np.ndarray:
+        """Prior mean at n_points inputs, CN layout."""
+        return np.tile(np.asarray(self.mean, dtype=np.float64), n_points)
+
+    def marginal_prior_variance(self) -> np.ndarray:
+        return np.array([k.outputscale for k in self.kernels])
+
+    def spec_groups(self) -> List[Tuple[KernelSpec, List[int]]]:
+        """Outputs grouped by identical spec, in first-appearance order."""
+        groups: Dict[KernelSpec, List[int]] = {}
+        for c, spec in enumerate(self.kernels):
+            groups.setdefault(spec, []).append(c)
+        return list(groups.items())
+
+
+def _check_inputs(X):
+    if isinstance(X, torch.Tensor):
+        ok = bool(torch.isfinite(X).all())
+    else:
+        ok = bool(np.isfinite(np.asarray(X, dtype=np.float64)).all())
+    if not ok:
+        raise InvalidInput("kernel inputs must be finite")
+
+
+class PriorOperator:
+    """Device K = blockdiag_c K_c(X_rows, X_cols) acting on CN vectors.
+
+    ``apply(v)`` takes a CN vector (n_cols*C,) or an (n_cols, C) matrix and
+    returns K v in the same layout over the rows.
+    """
+
+    def __init__(self, prior: MultiOutputPrior, X_rows, X_cols=None, dtype=None,
+                 impl: str = "auto"):
+        self.prior = prior
+        self.dtype = resolve_dtype(dtype)
+        _check_inputs(X_rows)
+        self.X_rows = to_device(X_rows, self.dtype)
+        if X_cols is None:
+            self.X_cols = self.X_rows
+        else:
+            _check_inputs(X_cols)
+            self.X_cols = to_device(X_cols, self.dtype)
+        if self.X_rows.dim() != 2 or self.X_cols.dim() != 2 or \
+                self.X_rows.shape[1] != self.X_cols.shape[1]:
+            raise DimensionMismatch(
+                f"incompatible input shapes {tuple(self.X_rows.shape)} vs "
+                f"{tuple(self.X_cols.shape)}")
+        self.C = prior.num_outputs
+        self.n_rows = self.X_rows.shape[0]
+        self.n_cols = self.X_cols.shape[0]
+        self.groups = []
+        for spec, cols in prior.spec_groups():
+            op = KernelOperator(spec.family, spec.lengthscale, spec.outputscale,
+                                self.X_rows, None if X_cols is None else self.X_cols,
+                                w_max=min(64, len(cols)), impl=impl)
+            self.groups.append((op, cols))
+        self.matvecs = 0
+
+    @property
+    def impl(self) -> str:
+        return self.groups[0][0].impl
+
+    def apply(self, v: torch.Tensor, out: Optional[torch.Tensor] = None,
+              row_begin: int = 0, row_end: Optional[int] = None) -> torch.Tensor:
+        C = self.C
+        flat = v.dim() == 1
+        if (v.numel() != self.n_cols * C):
+            raise DimensionMismatch(f"vector length {v.numel()} != {self.n_cols} * {C}")
+        V = v.reshape(self.n_cols, C)
+        if out is None:
+            out = torch.empty((self.n_rows, C), dtype=self.dtype, device=V.device)
+        O = out.view(self.n_rows, C)
+        for op, cols in self.groups:
+            if len(cols) == C:
+                op.apply(V, out=O, row_begin=row_begin, row_end=row_end)
+            else:
+                idx = torch.tensor(cols, device=V.device)
+                sub = op.apply(V.index_select(1, idx).contiguous(),
+                               row_begin=row_begin, row_end=row_end)
+                O[:, cols] = sub
+        self.matvecs += 1
+        return out.reshape(-1) if flat else out
+
+    __call__ = apply
+
+
+_OP_CACHE: Dict[tuple, PriorOperator] = {}
+
+
+def _cached_operator(prior, X, dtype) -> PriorOperator:
+    """Reuse the packed operator across calls on the same host array."""
+    key = (prior, id(X), getattr(X, "shape", None), resolve_dtype(dtype))
+    op = _OP_CACHE.get(key)
+    if op is None or op.X_host is not X:
+        op = PriorOperator(prior, X, dtype=dtype)
+        op.X_host = X
+        if len(_OP_CACHE) > 8:
+            _OP_CACHE.clear()
+        _OP_CACHE[key] = op
+    return op
+
+
+def prior_matvec(prior: MultiOutputPrior, X, v, tile: int = 256, dtype=None):
+    """K v for a CN vector (gp.py:222-250), computed by the fused device
+    kernel-matmul.  Returns the same kind of array it is given (numpy in,
+    numpy out; CUDA tensor in, CUDA tensor out)."""
+    if tile < 1:
+        raise InvalidInput("tile size must be >= 1")
+    n = X.shape[0]
+    if v.shape[0] != n * prior.num_outputs:
+        raise DimensionMismatch(f"vector length {v.shape[0]} != {n} * {prior.num_outputs}")
+    dt = resolve_dtype(dtype if dtype is not None else
+                       (v.dtype if isinstance(v, torch.Tensor) else None))
+    op = _cached_operator(prior, X, dt)
+    out = op.apply(to_device(v, dt))
+    if is_device(v):
+        return out
+    if isinstance(v, torch.Tensor):       # host tensor in -> host tensor out
+        return out.to("cpu")
+    return to_host(out)
+
+
+def kernel_eval(spec: KernelSpec, x, x2) -> float:
+    """Kernel on one pair of input vectors (gp.py:144-153), on the device."""
+    x = np.atleast_1d(np.asarray(x, dtype=np.float64))
+    x2 = np.atleast_1d(np.asarray(x2, dtype=np.float64))
+    if not (np.isfinite(x).all() and np.isfinite(x2).all()):
+        raise InvalidInput("kernel inputs must be finite")
+    if x.shape != x2.shape:
+        raise DimensionMismatch(f"input shapes differ: {x.shape} vs {x2.shape}")
+    op = KernelOperator(spec.family, spec.lengthscale, spec.outputscale,
+                        to_device(x[None, :], torch.float64), to_device(x2[None, :], torch.float64),
+                        w_max=1)
+    one = torch.ones((1, 1), dtype=torch.float64, device=op.X_rows.device)
+    return float(op.apply(one)[0, 0].item())
+
+
+def cross_covariance(prior: MultiOutputPrior, X_train, X_test, dtype=None) -> np.ndarray:
+    """Dense (N_test*C) x (N_train*C) cross-covariance (gp.py:253-274).
+
+    Materialised by applying the device operator to identity column blocks;
+    intended, like the reference, for small problems only.
+    """
+    X_train = np.asarray(X_train, dtype=np.float64)
+    X_test = np.asarray(X_test, dtype=np.float64)
+    if X_train.ndim != 2 or X_test.ndim != 2 or X_train.shape[1] != X_test.shape[1]:
+        raise DimensionMismatch(f"incompatible input shapes {X_test.shape} vs {X_train.shape}")
+    dt = resolve_dtype(dtype)
+    nt, n, C = X_test.shape[0], X_train.shape[0], prior.num_outputs
+    out = np.zeros((nt * C, n * C))
+    Xr, Xc = to_device(X_test, dt), to_device(X_train, dt)
+    for spec, cols in prior.spec_groups():
+        op = KernelOperator(spec.family, spec.lengthscale, spec.outputscale, Xr, Xc, w_max=64)
+        block = np.empty((nt, n))
+        for j0 in range(0, n, 64):
+            j1 = min(n, j0 + 64)
+            eye = torch.zeros((n, j1 - j0), dtype=dt, device=Xr.device)
+            eye[torch.arange(j0, j1), torch.arange(j1 - j0)] = 1.0
+            block[:, j0:j1] = to_host(op.apply(eye))
+        for c in cols:
+            out[c::C, c::C] = block
+    return out
+
+
+@dataclass(frozen=True)
+class Dataset:
+    """Inputs, targets and a target-domain tag (gp.py:277-319)."""
+
+    inputs: np.ndarray
+    targets: np.ndarray
+    domain: str
+    num_classes: int = 0
+
+    def __post_init__(self):
+        X = np.asarray(self.inputs, dtype=np.float64)
+        object.__setattr__(self, "inputs", X)
+        if X.ndim != 2 or X.shape[0] < 1:
+            raise DimensionMismatch("inputs must be a non-empty (N, D) matrix")
+        if self.domain not in DOMAIN_TAGS:
+            raise InvalidInput(f"unknown domain tag {self.domain!r}")
+        if self.domain == "real":
+            y = np.asarray(self.targets, dtype=np.float64)
+        else:
+            raw = np.asarray(self.targets)
+            rounded = np.round(np.asarray(raw, dtype=np.float64))
+            if not np.allclose(raw, rounded):
+                raise InvalidInput(f"{self.domain} targets must be integers")
+            y = rounded.astype(np.int64)
+        object.__setattr__(self, "targets", y)
+        if y.shape != (X.shape[0],):
+            raise DimensionMismatch("one target per input row is required")
+        if self.domain == "counts" and (y < 0).any():
+            raise InvalidInput("counts must be nonnegative")
+        if self.domain == "binary" and not np.isin(y, (0, 1)).all():
+            raise InvalidInput("binary labels must be in {0, 1}")
+        if self.domain == "class-index":
+            k = int(self.num_classes) if self.num_classes else int(y.max()) + 1
+            object.__setattr__(self, "num_classes", k)
+            if (y < 0).any() or (y >= k).any():
+                raise InvalidInput(f"class indices must lie in [0, {k})")
+
+    @property
+    def n_points(self) -> int:
+        return self.inputs.shape[0]
+
+    @property
+    def n_features(self) -> int:
+        return self.inputs.shape[1]

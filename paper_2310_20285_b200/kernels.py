@@ -1,0 +1,275 @@
+"""Thin Python wrappers over the C ABI (include/ncgp_b200.h).
+
+Conventions: every tensor is a CUDA tensor of the working dtype.  A "column
+block" of k vectors of length n is a (k, n) tensor whose rows are
+contiguous (stride (ld, 1)); it is what the C ABI calls column b at
+``ptr + b * ld``.  Reductions return fp64 device tensors.
+"""
+
+from __future__ import annotations
+
+from typing import Optional, Sequence, Tuple
+
+import torch
+
+from . import _native
+from .device import code, ptr, require_cuda, stream, workspace
+
+N = _native
+
+
+def _rows(t: torch.Tensor) -> Tuple[torch.Tensor, int]:
+    """Return a (k, n) view with unit inner stride and its leading dim."""
+    if t.dim() == 1:
+        t = t.unsqueeze(0)
+    if t.stride(-1) != 1:
+        t = t.contiguous()
+    return t, (t.stride(0) if t.shape[0] > 1 else t.shape[1])
+
+
+# --------------------------------------------------------------------- K1
+
+class KernelOperator:
+    """Device kernel operator for one stationary kernel spec:
+    ``apply(V) = K(X_rows, X_cols) @ V`` without materialising K.
+
+    Replaces the tile loop of prior_matvec (gp.py:222-250) and the dense
+    cross_covariance products (gp.py:253-274, posterior.py:52-84).
+    """
+
+    def __init__(self, family: str, lengthscale: float, outputscale: float,
+                 X_rows: torch.Tensor, X_cols: Optional[torch.Tensor] = None,
+                 w_max: int = 64, impl: str = "auto"):
+        require_cuda()
+        self.family = family
+        self.fam_code = {"rbf": N.RBF, "matern32": N.MATERN32}[family]
+        self.lengthscale = float(lengthscale)
+        self.outputscale = float(outputscale)
+        self.X_rows = X_rows.contiguous()
+        self.X_cols = self.X_rows if X_cols is None else X_cols.contiguous()
+        if self.X_rows.dim() != 2 or self.X_cols.dim() != 2 or \
+                self.X_rows.shape[1] != self.X_cols.shape[1]:
+            raise N.DimensionMismatch("kernel inputs must be (n, d) with equal d")
+        if self.X_rows.dtype != self.X_cols.dtype:
+            raise N.DimensionMismatch("row and column inputs must share a dtype")
+        self.dtype = self.X_rows.dtype
+        self.n_rows, self.d = self.X_rows.shape
+        self.n_cols = self.X_cols.shape[0]
+        self.w_max = int(max(1, min(w_max, 64)))
+        impl_code = {"auto": N.KOP_AUTO, "tcgen05": N.KOP_TCGEN05, "simt": N.KOP_SIMT}[impl]
+        dt = code(self.dtype)
+        nbytes = N.query("ncgp_kop_workspace_bytes", impl_code, dt, self.n_rows, self.n_cols,
+                         self.d, self.w_max)
+        self._ws = torch.empty(max(int(nbytes), 256), dtype=torch.uint8,
+                               device=self.X_rows.device)
+        h = N._vp()
+        N.call("ncgp_kop_create", N.ctypes.byref(h), impl_code, self.fam_code,
+               self.lengthscale, self.outputscale, dt, ptr(self.X_rows), self.n_rows,
+               ptr(self.X_cols), self.n_cols, self.d, self.w_max, ptr(self._ws),
+               self._ws.numel(), stream())
+        self._h = h
+        self.impl = {N.KOP_TCGEN05: "tcgen05", N.KOP_SIMT: "simt"}[
+            N.query("ncgp_kop_impl", h)]
+
+    def apply(self, V: torch.Tensor, out: Optional[torch.Tensor] = None,
+              row_begin: int = 0, row_end: Optional[int] = None) -> torch.Tensor:
+        """K(X_rows[row_begin:row_end], X_cols) @ V for V of shape (n_cols, w)."""
+        vec = V.dim() == 1
+        if vec:
+            V = V.unsqueeze(1)
+        if V.shape[0] != self.n_cols:
+            raise N.DimensionMismatch(f"operand has {V.shape[0]} rows, expected {self.n_cols}")
+        if V.dtype != self.dtype:
+            raise N.DimensionMismatch(f"operand dtype {V.dtype} != operator dtype {self.dtype}")
+        if V.stride(1) != 1:
+            V = V.contiguous()
+        w = V.shape[1]
+        row_end = self.n_rows if row_end is None else row_end
+        if out is None:
+            out = torch.empty((self.n_rows, w), dtype=self.dtype, device=V.device)
+        elif out.dim() == 1:
+            out = out.view(-1, 1)
+        ldv = V.stride(0) if V.shape[0] > 1 else w
+        ldo = out.stride(0) if out.shape[0] > 1 else w
+        for c0 in range(0, w, self.w_max):
+            c1 = min(w, c0 + self.w_max)
+            es = V.element_size()
+            N.call("ncgp_kop_apply", self._h, V.data_ptr() + c0 * es, ldv, c1 - c0,
+                   out.data_ptr() + c0 * es, ldo, row_begin, row_end, stream())
+        return out[:, 0] if vec else out
+
+    __call__ = apply
+
+    def close(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                N.query("ncgp_kop_destroy", h)
+            except Exception:
+                pass
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+# --------------------------------------------------------------------- K3-K5
+
+def softmax_stats(f: torch.Tensor, labels: Optional[torch.Tensor], n: int, C: int,
+                  want_grad=True, want_yhat=True):
+    pi = torch.empty((n, C), dtype=f.dtype, device=f.device)
+    grad = torch.empty(n * C, dtype=f.dtype, device=f.device) if want_grad else None
+    yhat = torch.empty(n * C, dtype=f.dtype, device=f.device) if want_yhat else None
+    N.call("ncgp_softmax_stats", code(f), ptr(f), ptr(labels), n, C, ptr(pi), ptr(grad),
+           ptr(yhat), stream())
+    return pi, grad, yhat
+
+
+def softmax_winv(pi: torch.Tensor, n: int, C: int, V: torch.Tensor,
+                 base: Optional[torch.Tensor] = None, alpha: float = 1.0, beta: float = 1.0,
+                 out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """beta*base + alpha*W^+ V on a column block V (k, n*C) (or a vector)."""
+    vec = V.dim() == 1
+    Vr, ldv = _rows(V)
+    k = Vr.shape[0]
+    if out is None:
+        out = torch.empty_like(Vr)
+    Or, ldo = _rows(out)
+    Br, ldb = _rows(base) if base is not None else (None, 0)
+    N.call("ncgp_softmax_winv", code(pi), ptr(pi), n, C, ptr(Vr), ldv, k, ptr(Br), ldb,
+           float(alpha), float(beta), ptr(Or), ldo, stream())
+    return Or[0] if vec else Or
+
+
+def softmax_w(pi: torch.Tensor, n: int, C: int, V: torch.Tensor) -> torch.Tensor:
+    vec = V.dim() == 1
+    Vr, ldv = _rows(V)
+    out = torch.empty_like(Vr)
+    N.call("ncgp_softmax_w", code(pi), ptr(pi), n, C, ptr(Vr), ldv, Vr.shape[0], ptr(out),
+           out.stride(0) if out.shape[0] > 1 else out.shape[1], stream())
+    return out[0] if vec else out
+
+
+def bernoulli_stats(f: torch.Tensor, labels: Optional[torch.Tensor]):
+    n = f.numel()
+    winv = torch.empty_like(f)
+    w = torch.empty_like(f)
+    grad = torch.empty_like(f) if labels is not None else None
+    yhat = torch.empty_like(f) if labels is not None else None
+    N.call("ncgp_bernoulli_stats", code(f), ptr(f), ptr(labels), n, ptr(winv), ptr(w),
+           ptr(grad), ptr(yhat), stream())
+    return winv, w, grad, yhat
+
+
+def diag_apply(dvec: torch.Tensor, V: torch.Tensor, base: Optional[torch.Tensor] = None,
+               alpha: float = 1.0, beta: float = 1.0,
+               out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    vec = V.dim() == 1
+    Vr, ldv = _rows(V)
+    if out is None:
+        out = torch.empty_like(Vr)
+    Or, ldo = _rows(out)
+    Br, ldb = _rows(base) if base is not None else (None, 0)
+    N.call("ncgp_diag_apply", code(dvec), ptr(dvec), dvec.numel(), ptr(Vr), ldv, Vr.shape[0],
+           ptr(Br), ldb, float(alpha), float(beta), ptr(Or), ldo, stream())
+    return Or[0] if vec else Or
+
+
+# --------------------------------------------------------------------- K6
+
+def _reduce_ws(n: int, k: int) -> torch.Tensor:
+    nbytes = N.query("ncgp_reduce_workspace_bytes", n, k)
+    return workspace().get("reduce", nbytes)
+
+
+def dots(pairs: Sequence[Tuple[torch.Tensor, torch.Tensor]],
+         out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """fp64 device vector of x_p . y_p (deterministic order), <= 4 pairs."""
+    x0 = pairs[0][0]
+    n = x0.numel()
+    if out is None:
+        out = torch.empty(len(pairs), dtype=torch.float64, device=x0.device)
+    ws = _reduce_ws(n, len(pairs))
+    xs = N.ptr_array([ptr(x) for x, _ in pairs])
+    ys = N.ptr_array([ptr(y) for _, y in pairs])
+    N.call("ncgp_dots", code(x0), n, len(pairs), xs, ys, ptr(out), ptr(ws), ws.numel(),
+           stream())
+    return out
+
+
+def gemv_t(Q: torch.Tensor, z: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Q' z for a column block Q (k, n): fp64 (k,)."""
+    Qr, ldq = _rows(Q)
+    k, n = Qr.shape
+    if out is None:
+        out = torch.empty(k, dtype=torch.float64, device=z.device)
+    if k == 0:
+        return out
+    ws = _reduce_ws(n, k)
+    N.call("ncgp_gemv_t", code(z), ptr(Qr), ldq, k, ptr(z), n, ptr(out), ptr(ws), ws.numel(),
+           stream())
+    return out
+
+
+def gemv_n(Q: torch.Tensor, y: torch.Tensor, s: Optional[torch.Tensor], alpha: float,
+           out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """s + alpha * Q y for a column block Q (k, n) and fp64 y (k,)."""
+    Qr, ldq = _rows(Q)
+    k, n = Qr.shape
+    if out is None:
+        out = torch.empty(n, dtype=Qr.dtype, device=Qr.device)
+    N.call("ncgp_gemv_n", code(out), ptr(Qr), ldq, k, ptr(y), ptr(s), float(alpha), ptr(out),
+           n, stream())
+    return out
+
+
+def lincomb(a: float, x: torch.Tensor, b: float = 0.0, y: Optional[torch.Tensor] = None,
+            c: float = 0.0, z: Optional[torch.Tensor] = None,
+            out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    if out is None:
+        out = torch.empty_like(x)
+    N.call("ncgp_lincomb", code(x), x.numel(), float(a), ptr(x), float(b), ptr(y), float(c),
+           ptr(z), ptr(out), stream())
+    return out
+
+
+def gram(S: torch.Tensor, Y: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """fp64 (ka, kb) matrix of S_a . Y_b for column blocks S (ka, n), Y (kb, n)."""
+    Sr, lds = _rows(S)
+    Yr, ldy = _rows(Y)
+    ka, n = Sr.shape
+    kb = Yr.shape[0]
+    if out is None:
+        out = torch.empty((ka, kb), dtype=torch.float64, device=Sr.device)
+    if ka == 0 or kb == 0:
+        return out
+    nbytes = N.query("ncgp_gram_workspace_bytes", n, ka, kb)
+    ws = workspace().get("gram", nbytes)
+    N.call("ncgp_gram", code(Sr), ptr(Sr), lds, ka, ptr(Yr), ldy, kb, n, ptr(out),
+           out.stride(0), ptr(ws), ws.numel(), stream())
+    return out
+
+
+def rotate(S: torch.Tensor, U: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Column block S U: S (kb, n), U fp64 (kb, kc) -> (kc, n)."""
+    Sr, lds = _rows(S)
+    kb, n = Sr.shape
+    U = U.to(device=Sr.device, dtype=torch.float64).contiguous()
+    kc = U.shape[1]
+    if out is None:
+        out = torch.empty((kc, n), dtype=Sr.dtype, device=Sr.device)
+    if kc == 0:
+        return out
+    N.call("ncgp_rotate", code(Sr), ptr(Sr), lds, kb, ptr(U), U.stride(0), kc, ptr(out),
+           out.stride(0) if kc > 1 else n, n, stream())
+    return out
+
+
+def marginal_var(A: torch.Tensor, C: int, R: int, s2: torch.Tensor,
+                 out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    nt = A.shape[0]
+    if out is None:
+        out = torch.empty((nt, C), dtype=A.dtype, device=A.device)
+    N.call("ncgp_marginal_var", code(A), ptr(A), A.stride(0), nt, C, R, ptr(s2), ptr(out),
+           stream())
+    return out

@@ -1,0 +1,116 @@
+"""Low-rank roots and the small symmetric eigensolve (mirror of ncgp/linalg.py).
+
+``LowRankRoot`` keeps Q on the device as a (rank, dim) column block (each
+column of Q contiguous), which is the layout the gemv / Gram / rotation
+kernels read at full HBM bandwidth.  ``.columns`` returns the reference's
+(dim, rank) host array lazily.
+
+``sym_eigh_truncated`` (linalg.py:403-424) is K7: a <= ~600 x 600 fp64
+eigensolve run on the host with LAPACK, as SURVEY.md 7 hard part 8 allows
+(it is latency-bound and must be computed identically on every rank).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import kernels as K
+from .device import is_device, resolve_dtype, to_device, to_host
+from .exceptions import DimensionMismatch, InvalidInput
+
+
+class LowRankRoot:
+    """Root Q of the PSD operator Q Q' (linalg.py:357-378)."""
+
+    def __init__(self, columns=None, *, block: torch.Tensor = None):
+        if block is not None:
+            self._block = block            # (rank, dim) device
+            self._host = None
+        else:
+            cols = columns if is_device(columns) else np.asarray(columns, dtype=np.float64)
+            if cols.ndim != 2:
+                raise DimensionMismatch("root columns must be a (dim, rank) matrix")
+            self._block = None
+            self._host = cols
+
+    @staticmethod
+    def zero(dim: int, dtype=None) -> "LowRankRoot":
+        return LowRankRoot(np.zeros((dim, 0)))
+
+    @property
+    def dim(self) -> int:
+        return self._block.shape[1] if self._block is not None else self._host.shape[0]
+
+    @property
+    def rank(self) -> int:
+        return self._block.shape[0] if self._block is not None else self._host.shape[1]
+
+    def block(self, dtype=None) -> torch.Tensor:
+        """(rank, dim) device column block in ``dtype``."""
+        dt = resolve_dtype(dtype)
+        b = self._block
+        if b is not None:
+            return b if b.dtype == dt else b.to(dt)
+        src = self._host
+        if is_device(src):
+            b = src.t().to(dt).contiguous()
+        else:
+            b = to_device(np.ascontiguousarray(src.T), dt)
+        self._block = b
+        return b
+
+    @property
+    def columns(self) -> np.ndarray:
+        """Q as a host (dim, rank) float64 array (reference layout)."""
+        if self._host is None or is_device(self._host):
+            src = self._block if self._block is not None else self._host.t()
+            self._host = to_host(src).T.copy()
+        return self._host
+
+
+@dataclass(frozen=True)
+class EigenPairs:
+    vectors: np.ndarray  # (n, r)
+    values: np.ndarray   # (r,)
+
+
+def apply_lowrank(root: LowRankRoot, w, dtype=None):
+    """Q (Q' w) without densifying (linalg.py:389-400); device gemv pair."""
+    dev = is_device(w)
+    dt = resolve_dtype(w.dtype if dev else dtype)
+    t = to_device(w, dt)
+    if t.shape[0] != root.dim:
+        raise DimensionMismatch(
+            f"operand has leading dimension {t.shape[0]}, expected {root.dim}")
+    if root.rank == 0:
+        out = torch.zeros_like(t)
+    else:
+        Q = root.block(dt)
+        if t.dim() == 1:
+            out = K.gemv_n(Q, K.gemv_t(Q, t), None, 1.0)
+        else:
+            cols = [K.gemv_n(Q, K.gemv_t(Q, t[:, j].contiguous()), None, 1.0)
+                    for j in range(t.shape[1])]
+            out = torch.stack(cols, dim=1)
+    return out if dev else to_host(out)
+
+
+def sym_eigh_truncated(M, rank_bound: int) -> EigenPairs:
+    """Symmetrise, eigendecompose, keep the ``rank_bound`` largest pairs
+    (linalg.py:403-424).  Host LAPACK, fp64."""
+    M = to_host(M) if is_device(M) else np.asarray(M, dtype=np.float64)
+    if M.ndim != 2 or M.shape[0] != M.shape[1]:
+        raise DimensionMismatch(f"expected a square matrix, got shape {M.shape}")
+    if not np.isfinite(M).all():
+        raise InvalidInput("matrix contains non-finite entries")
+    n = M.shape[0]
+    if not 0 <= rank_bound <= n:
+        raise DimensionMismatch(f"rank bound {rank_bound} outside [0, {n}]")
+    if n == 0 or rank_bound == 0:
+        return EigenPairs(np.zeros((n, 0)), np.zeros(0))
+    vals, vecs = np.linalg.eigh(0.5 * (M + M.T))
+    order = np.argsort(vals)[::-1][:rank_bound]
+    return EigenPairs(np.ascontiguousarray(vecs[:, order]), vals[order])
