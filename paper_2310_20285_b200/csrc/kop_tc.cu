@@ -1,18 +1,897 @@
-// tcgen05 / TMEM fused kernel-matmul -- placeholder until the kernel lands.
+// K1 on tcgen05/TMEM: fused kernel-matmul  out = K(Xr, Xc) V  with K never
+// materialised (replaces the tile body of prior_matvec, gp.py:240-249).
+//
+// Dataflow per CTA (persistent, one CTA per SM, 16 warps):
+//   warp 0        producer: 1-D bulk copies (cp.async.bulk -> UBLKCP) of the
+//                 pre-packed row tile and of each column tile into a ring of
+//                 shared-memory stages (mbarrier complete_tx).
+//   warp 1        MMA issuer (one thread):
+//                   GEMM1  S[128x128] = XA_i . XB_j   (kind::f16, A,B in smem)
+//                   GEMM2  O[128xWP] += P . V_j       (kind::f16, A=P in TMEM)
+//   warps 4-7,    two epilogue warpgroups, alternating column tiles: TMEM->regs
+//   warps 8-11    (tcgen05.ld), kernel transform (one MUFU ex2 per pair for RBF,
+//                 sqrt+ex2 for Matern), fp16 hi/lo split, regs->TMEM (tcgen05.st)
+//                 over the S columns (P aliases S, as in FlashAttention-4).
+//   warps 12-15   correction warpgroup: drains O every CH column tiles into
+//                 fp64 registers (chunked fp32 -> fp64 accumulation), applies
+//                 the power-of-two scales and writes the output rows.
+//
+// Precision (hard part 2): the distance GEMM uses a 3-term fp16
+// split packed along K,  [u_hi u_lo u_hi a_hi a_lo 1 1] . [x_hi x_hi x_lo 1 1 b_hi b_lo],
+// which returns the exponent argument  L - |x~_i - x~_j|^2  (RBF) or
+// |x~_i - x~_j|^2 (Matern) directly, with x~ = (x - mean) * scale, so no
+// per-pair FMAs are needed before the MUFU op.  The contraction uses the
+// 3-term fp16 split  P_hi V_hi + P_lo V_hi + P_hi V_lo  with kernel values
+// pre-scaled by 2^s and RHS columns by 2^e_c into fp16 range; fp32 tensor
+// accumulation is flushed to fp64 every CH*128 columns.
+#include <cuda_fp16.h>
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+
 #include "kop.cuh"
+
+namespace {
+
+constexpr int BM = 128;          // rows per tile (MMA M)
+constexpr int BN = 128;          // columns per tile (MMA1 N, MMA2 K)
+constexpr int CH = 16;           // column tiles per fp32 accumulation chunk
+constexpr int NTHREADS = 512;
+constexpr int SMEM_BUDGET = 225 * 1024;
+constexpr int TMEM_COLS = 512;
+
+// ------------------------------------------------------------------ PTX
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// Bounded wait: a pipeline bug traps (kernel error) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t spins = 0;
+  while (!mbar_try(bar, parity)) {
+    if (++spins > (1u << 26)) __trap();
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+// D[tmem] (+)= A[smem] . B[smem]^T  (both K-major)
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                       uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// D[tmem] (+)= A[tmem] . B[smem]^T
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc,
+                                       uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15]));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// pack (lo element, hi element) -> f16x2 with lo in the low half
+__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
+  uint32_t d;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
+}
+
+// Shared-memory matrix descriptor, K-major, no swizzle (canonical layout
+// ((8,m),(8,2)) : ((16B, SBO), (2B, LBO)) in bytes).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | ((uint64_t)1 << 46);
+}
+// Instruction descriptor: kind::f16, A/B = F16 (K-major), D = F32, M = 128.
+__host__ __device__ constexpr uint32_t idesc_f16(int n) {
+  return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+struct TcParams {
+  const uint8_t* xa_pack;
+  const uint8_t* col_pack;
+  int64_t tile_stride;   // bytes between column tiles in col_pack
+  uint32_t a_bytes;      // one packed row tile (= XB bytes)
+  uint32_t v_bytes;      // one of Vhi / Vlo for a column tile
+  int ka;                // K of GEMM1 (multiple of 16)
+  int w;                 // real RHS width
+  int64_t rt0;           // first global row tile of this launch
+  int64_t row_tiles;     // local row tiles
+  int64_t nloc;          // local rows
+  int64_t col_tiles;
+  int splits;
+  int64_t tiles_per_split;
+  float L;               // RBF clamp / Matern exponent offset (log2 of s2 * 2^s)
+  const int* col_exp;    // per RHS column exponent e_c
+  int s_exp;             // kernel prescale exponent s
+  void* out;
+  int64_t ldo;
+  int out_f64;
+  double* partial;       // [splits][nloc][w] when splits > 1
+  int stages;
+};
+
+struct Item {
+  int64_t rt, c0, c1;
+};
+
+__device__ __forceinline__ Item item_of(const TcParams& p, int64_t it) {
+  Item r;
+  r.rt = it / p.splits;
+  const int64_t sp = it % p.splits;
+  r.c0 = sp * p.tiles_per_split;
+  r.c1 = min(p.col_tiles, r.c0 + p.tiles_per_split);
+  return r;
+}
+
+// Iterates the CTA's global column-tile sequence across its items.
+struct TileIter {
+  int64_t it, ct;
+  Item cur;
+  bool valid;
+  __device__ void start(const TcParams& p, int64_t items) {
+    it = blockIdx.x;
+    valid = it < items;
+    if (valid) {
+      cur = item_of(p, it);
+      ct = cur.c0;
+    }
+  }
+  __device__ void next(const TcParams& p, int64_t items) {
+    if (++ct >= cur.c1) {
+      it += gridDim.x;
+      valid = it < items;
+      if (valid) {
+        cur = item_of(p, it);
+        ct = cur.c0;
+      }
+    }
+  }
+  __device__ bool first_in_item() const { return ct == cur.c0; }
+  __device__ bool last_in_item() const { return ct == cur.c1 - 1; }
+  __device__ bool first_in_chunk() const { return ct == cur.c0 || (ct % CH) == 0; }
+  __device__ bool last_in_chunk() const { return ct == cur.c1 - 1 || (ct % CH) == CH - 1; }
+};
+
+template <int FAM, int WP>
+__global__ void __launch_bounds__(NTHREADS, 1) kop_tc_kernel(const TcParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t items = p.row_tiles * p.splits;
+
+  // ---- shared-memory carve-up
+  const uint32_t stage_bytes = p.a_bytes + 2 * p.v_bytes;
+  uint8_t* sA = smem;                                   // 2 x a_bytes
+  uint8_t* sStage = smem + 2 * p.a_bytes;               // stages x stage_bytes
+  double* sAcc = reinterpret_cast<double*>(sStage + (size_t)p.stages * stage_bytes);  // [WP][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sAcc + WP * BM);
+  uint64_t* full = bars;                 // [stages]
+  uint64_t* empty = full + p.stages;     // [stages]
+  uint64_t* a_full = empty + p.stages;   // [2]
+  uint64_t* a_empty = a_full + 2;        // [2]
+  uint64_t* s_full = a_empty + 2;        // [2]
+  uint64_t* p_full = s_full + 2;         // [2]
+  uint64_t* o_full = p_full + 2;         // [2]
+  uint64_t* o_empty = o_full + 2;        // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&a_full[b], 1);
+      mbar_init(&a_empty[b], 1);
+      mbar_init(&s_full[b], 1);
+      mbar_init(&p_full[b], 128);
+      mbar_init(&o_full[b], 1);
+      mbar_init(&o_empty[b], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  auto tS = [&](int b) -> uint32_t { return tmem + (uint32_t)(b * BN); };
+  auto tO = [&](int b) -> uint32_t { return tmem + 2u * BN + (uint32_t)(b * WP); };
+
+  if (warp == 0) {
+    // ================= producer =================
+    if (lane == 0) {
+      TileIter ti;
+      ti.start(p, items);
+      int64_t g = 0, nitem = 0;
+      while (ti.valid) {
+        if (ti.first_in_item()) {
+          const int ab = nitem & 1;
+          mbar_wait(&a_empty[ab], ((nitem >> 1) & 1) ^ 1);
+          mbar_expect_tx(&a_full[ab], p.a_bytes);
+          bulk_g2s(sA + ab * p.a_bytes, p.xa_pack + (p.rt0 + ti.cur.rt) * (int64_t)p.a_bytes,
+                   p.a_bytes, &a_full[ab]);
+          ++nitem;
+        }
+        const int s = (int)(g % p.stages);
+        const uint32_t ph = (uint32_t)((g / p.stages) & 1);
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_expect_tx(&full[s], stage_bytes);
+        bulk_g2s(sStage + (size_t)s * stage_bytes, p.col_pack + ti.ct * p.tile_stride,
+                 stage_bytes, &full[s]);
+        ++g;
+        ti.next(p, items);
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer =================
+    if (lane == 0) {
+      const uint32_t id1 = idesc_f16(BN), id2 = idesc_f16(WP);
+      const uint32_t sbo_x = (uint32_t)(p.ka / 8) * 128u;
+      const int ksteps1 = p.ka / 16;
+      TileIter look;  // tile whose GEMM1 is issued next
+      look.start(p, items);
+      int64_t g1 = 0, item1 = 0;
+      auto issue_gemm1 = [&]() {
+        const int b = (int)(g1 & 1);
+        if (look.first_in_item()) {
+          mbar_wait(&a_full[item1 & 1], (uint32_t)((item1 >> 1) & 1));
+          ++item1;
+        }
+        const int ab = (int)((item1 - 1) & 1);
+        const int s = (int)(g1 % p.stages);
+        mbar_wait(&full[s], (uint32_t)((g1 / p.stages) & 1));
+        tc_fence_after();
+        const uint32_t a0 = smem_u32(sA + ab * p.a_bytes);
+        const uint32_t b0 = smem_u32(sStage + (size_t)s * stage_bytes);
+        for (int k = 0; k < ksteps1; ++k)
+          mma_ss(tS(b), sdesc(a0 + 256u * k, 128u, sbo_x), sdesc(b0 + 256u * k, 128u, sbo_x),
+                 id1, k > 0);
+        tc_commit(&s_full[b]);
+        if (look.last_in_item()) tc_commit(&a_empty[ab]);
+        ++g1;
+        look.next(p, items);
+      };
+      if (look.valid) issue_gemm1();
+      if (look.valid) issue_gemm1();
+      TileIter cur;
+      cur.start(p, items);
+      int64_t g = 0, q = 0;
+      while (cur.valid) {
+        const int b = (int)(g & 1);
+        const int s = (int)(g % p.stages);
+        mbar_wait(&p_full[b], (uint32_t)((g >> 1) & 1));
+        tc_fence_after();
+        const int ob = (int)(q & 1);
+        if (cur.first_in_chunk()) {
+          mbar_wait(&o_empty[ob], (uint32_t)(((q >> 1) & 1) ^ 1));
+          tc_fence_after();
+        }
+        const uint32_t vhi = smem_u32(sStage + (size_t)s * stage_bytes + p.a_bytes);
+        const uint32_t vlo = vhi + p.v_bytes;
+        const bool fresh = cur.first_in_chunk();
+#pragma unroll
+        for (int m = 0; m < BN / 16; ++m) {
+          const uint32_t ahi = tS(b) + 32u * (m >> 1) + 8u * (m & 1);
+          const uint32_t alo = ahi + 16u;
+          const uint64_t bhi = sdesc(vhi + 256u * m, 128u, 2048u);
+          const uint64_t blo = sdesc(vlo + 256u * m, 128u, 2048u);
+          mma_ts(tO(ob), ahi, bhi, id2, (fresh && m == 0) ? 0u : 1u);
+          mma_ts(tO(ob), alo, bhi, id2, 1u);
+          mma_ts(tO(ob), ahi, blo, id2, 1u);
+        }
+        tc_commit(&empty[s]);
+        if (cur.last_in_chunk()) {
+          tc_commit(&o_full[ob]);
+          ++q;
+        }
+        if (look.valid) issue_gemm1();
+        ++g;
+        cur.next(p, items);
+      }
+    }
+  } else if (warp >= 4 && warp < 12) {
+    // ================= epilogue warpgroups =================
+    const int e = (warp - 4) >> 2;           // 0 or 1
+    const int wq = warp & 3;                 // TMEM lane quarter
+    const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
+    TileIter ti;
+    ti.start(p, items);
+    int64_t g = 0;
+    int64_t k = 0;
+    const float L = p.L;
+    while (ti.valid) {
+      if ((g & 1) == e) {
+        mbar_wait(&s_full[e], (uint32_t)(k & 1));
+        tc_fence_after();
+        const uint32_t base = tS(e) + lane_off;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(base + 32 * c, r);
+          tmem_wait_ld();
+          uint32_t hi[16], lo[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float k0, k1;
+            const float g0 = __uint_as_float(r[2 * i]);
+            const float g1 = __uint_as_float(r[2 * i + 1]);
+            if (FAM == NCGP_RBF) {
+              k0 = ex2(fminf(g0, L));
+              k1 = ex2(fminf(g1, L));
+            } else {
+              const float a0 = sqrt_approx(fmaxf(g0, 0.f));
+              const float a1 = sqrt_approx(fmaxf(g1, 0.f));
+              const float e0 = ex2(fmaf(a0, -1.4426950408889634f, L));
+              const float e1 = ex2(fmaf(a1, -1.4426950408889634f, L));
+              k0 = fmaf(a0, e0, e0);
+              k1 = fmaf(a1, e1, e1);
+            }
+            const float h0 = __uint_as_float(__float_as_uint(k0) & 0xFFFFE000u);
+            const float h1 = __uint_as_float(__float_as_uint(k1) & 0xFFFFE000u);
+            hi[i] = pack_h2(h0, h1);
+            lo[i] = pack_h2(k0 - h0, k1 - h1);
+          }
+          tmem_st16(base + 32 * c, hi);
+          tmem_st16(base + 32 * c + 16, lo);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&p_full[e]);
+        ++k;
+      }
+      ++g;
+      ti.next(p, items);
+    }
+  } else if (warp >= 12) {
+    // ================= correction warpgroup =================
+    const int wq = warp & 3;
+    const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
+    const int row = 32 * wq + lane;
+    double* acc = sAcc + row;  // acc[c * BM], conflict-free across the warp
+#pragma unroll
+    for (int c = 0; c < WP; ++c) acc[c * BM] = 0.0;
+    TileIter ti;
+    ti.start(p, items);
+    int64_t q = 0;
+    while (ti.valid) {
+      if (ti.last_in_chunk()) {
+        const int ob = (int)(q & 1);
+        mbar_wait(&o_full[ob], (uint32_t)((q >> 1) & 1));
+        tc_fence_after();
+#pragma unroll
+        for (int h = 0; h < WP / 16; ++h) {
+          uint32_t r[16];
+          tmem_ld16(tO(ob) + lane_off + 16 * h, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 16; ++c) acc[(16 * h + c) * BM] += (double)__uint_as_float(r[c]);
+        }
+        tc_fence_before();
+        mbar_arrive(&o_empty[ob]);
+        ++q;
+        if (ti.last_in_item()) {
+          const int64_t i = ti.cur.rt * BM + row;  // local row
+          if (i < p.nloc) {
+            const int64_t sp = ti.it % p.splits;
+            for (int c = 0; c < p.w; ++c) {
+              const double v = ldexp(acc[c * BM], -(p.s_exp + __ldg(&p.col_exp[c])));
+              if (p.splits > 1)
+                p.partial[(sp * p.nloc + i) * p.w + c] = v;
+              else if (p.out_f64)
+                static_cast<double*>(p.out)[i * p.ldo + c] = v;
+              else
+                static_cast<float*>(p.out)[i * p.ldo + c] = (float)v;
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < WP; ++c) acc[c * BM] = 0.0;
+        }
+      }
+      ti.next(p, items);
+    }
+  }
+
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TMEM_COLS));
+  }
+}
+
+// ------------------------------------------------------------------ packing
+
+// column means of Xc in fp64 (single block, fixed order)
+template <typename T>
+__global__ void col_mean_kernel(const T* __restrict__ X, int64_t n, int d, double* __restrict__ mu) {
+  __shared__ double sm[32];
+  for (int f = 0; f < d; ++f) {
+    double acc = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += (double)X[i * d + f];
+    double s = ncgp::block_sum(acc, sm);
+    if (threadIdx.x == 0) mu[f] = n > 0 ? s / (double)n : 0.0;
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ __half h_of(double v) { return __double2half(v); }
+
+// Writes the augmented rows of one operand into the canonical K-major
+// no-swizzle layout: tile | row-group g | k-chunk q | row r | k.
+// role 0 = row operand (A), role 1 = column operand (B).
+template <typename T>
+__global__ void pack_x_kernel(const T* __restrict__ X, int64_t n, int d, int ka,
+                              const double* __restrict__ mu, double alpha, double sign,
+                              double L, int role, uint8_t* __restrict__ pack, int64_t stride) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int qn = ka / 8;
+  const int64_t rows = (n + BM - 1) / BM * BM;
+  if (e >= rows * qn) return;
+  const int64_t row = e / qn;
+  const int q = (int)(e % qn);
+  const int64_t tile = row / BM;
+  const int r = (int)(row % BM);
+  uint16_t out[8];
+  if (row >= n) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) out[k] = 0;
+  } else {
+    double nrm = 0.0;
+    for (int f = 0; f < d; ++f) {
+      const double x = ((double)X[row * d + f] - mu[f]) * alpha;
+      nrm += x * x;
+    }
+    // a/b term: RBF  a = -|x|^2 (+L on the column side), Matern  a = +|x|^2
+    const double ab = (sign > 0 ? -nrm : nrm) + (role == 1 ? L : 0.0);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int idx = q * 8 + k;
+      double v = 0.0;
+      if (idx < 3 * d) {
+        const int f = idx % d;
+        const int part = idx / d;  // 0,1,2
+        const double x = ((double)X[row * d + f] - mu[f]) * alpha;
+        const double xs = role == 0 ? 2.0 * sign * x : x;
+        const double hi = (double)__half2float(h_of(xs));
+        const double lo = (double)__half2float(h_of(xs - hi));
+        if (role == 0)
+          v = (part == 1) ? lo : hi;  // [u_hi, u_lo, u_hi]
+        else
+          v = (part == 2) ? lo : hi;  // [x_hi, x_hi, x_lo]
+      } else if (idx < 3 * d + 4) {
+        const int t = idx - 3 * d;
+        const double hi = (double)__half2float(h_of(ab));
+        const double lo = (double)__half2float(h_of(ab - hi));
+        if (role == 0)
+          v = (t == 0) ? hi : (t == 1 ? lo : 1.0);       // [a_hi, a_lo, 1, 1]
+        else
+          v = (t == 2) ? hi : (t == 3 ? lo : 1.0);       // [1, 1, b_hi, b_lo]
+      }
+      out[k] = __half_as_ushort(h_of(v));
+    }
+  }
+  const int g = r / 8, rr = r % 8;
+  uint8_t* dst = pack + tile * stride + ((int64_t)(g * qn + q) * 8 + rr) * 16;
+  uint4 val;
+  val.x = out[0] | ((uint32_t)out[1] << 16);
+  val.y = out[2] | ((uint32_t)out[3] << 16);
+  val.z = out[4] | ((uint32_t)out[5] << 16);
+  val.w = out[6] | ((uint32_t)out[7] << 16);
+  *reinterpret_cast<uint4*>(dst) = val;
+}
+
+// max |x~|^2 over rows (precision guard), atomicMax on the float bit pattern
+template <typename T>
+__global__ void max_norm_kernel(const T* __restrict__ X, int64_t n, int d,
+                                const double* __restrict__ mu, double alpha,
+                                unsigned int* __restrict__ out_bits) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  float v = 0.f;
+  if (i < n) {
+    double nrm = 0.0;
+    for (int f = 0; f < d; ++f) {
+      const double x = ((double)X[i * d + f] - mu[f]) * alpha;
+      nrm += x * x;
+    }
+    v = (float)nrm;
+  }
+  v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 16));
+  v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 8));
+  v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 4));
+  v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 2));
+  v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 1));
+  if ((threadIdx.x & 31) == 0) atomicMax(out_bits, __float_as_uint(v));
+}
+
+// per RHS column: exponent e_c with max|v_c| * 2^e_c < 2^14  (max is order-free)
+template <typename T>
+__global__ void col_absmax_kernel(const T* __restrict__ V, int64_t ldv, int64_t n, int w,
+                                  unsigned int* __restrict__ bits) {
+  const int c = threadIdx.x % 32 + 32 * blockIdx.y;
+  if (c >= w) return;
+  float m = 0.f;
+  for (int64_t j = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; j < n;
+       j += (int64_t)gridDim.x * (blockDim.x / 32))
+    m = fmaxf(m, fabsf((float)V[j * ldv + c]));
+  atomicMax(&bits[c], __float_as_uint(m));
+}
+
+__global__ void col_exp_kernel(const unsigned int* __restrict__ bits, int w, int wp,
+                               int* __restrict__ col_exp) {
+  const int c = threadIdx.x;
+  if (c >= wp) return;
+  int e = 0;
+  if (c < w) {
+    const float m = __uint_as_float(bits[c]);
+    if (m > 0.f && isfinite(m)) {
+      int p;
+      frexpf(m, &p);  // m < 2^p
+      e = 14 - p;
+    }
+  }
+  col_exp[c] = e;
+}
+
+// V (n x w, row stride ldv) -> per column tile [Vhi | Vlo], each a K-major
+// no-swizzle (WP x 128) fp16 block: c-group g | j-chunk q | row c%8 | j%8.
+template <typename T>
+__global__ void pack_v_kernel(const T* __restrict__ V, int64_t ldv, int64_t n, int w, int wp,
+                              const int* __restrict__ col_exp, uint8_t* __restrict__ col_pack,
+                              int64_t tile_stride, uint32_t xb_bytes, uint32_t v_bytes,
+                              int64_t col_tiles) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t chunks = col_tiles * (BN / 8);
+  if (e >= chunks * wp) return;
+  const int c = (int)(e % wp);
+  const int64_t qg = e / wp;
+  const int64_t tile = qg / (BN / 8);
+  const int q = (int)(qg % (BN / 8));
+  const int64_t j0 = qg * 8;
+  const float sc = ldexpf(1.f, col_exp[c]);
+  uint16_t hi[8], lo[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int64_t j = j0 + k;
+    float v = (j < n && c < w) ? (float)V[j * ldv + c] * sc : 0.f;
+    const __half h = __float2half_rn(v);
+    hi[k] = __half_as_ushort(h);
+    lo[k] = __half_as_ushort(__float2half_rn(v - __half2float(h)));
+  }
+  const int g = c / 8, rr = c % 8;
+  uint8_t* base = col_pack + tile * tile_stride + xb_bytes;
+  const int64_t off = ((int64_t)(g * (BN / 8) + q) * 8 + rr) * 16;
+  uint4 a, b;
+  a.x = hi[0] | ((uint32_t)hi[1] << 16); a.y = hi[2] | ((uint32_t)hi[3] << 16);
+  a.z = hi[4] | ((uint32_t)hi[5] << 16); a.w = hi[6] | ((uint32_t)hi[7] << 16);
+  b.x = lo[0] | ((uint32_t)lo[1] << 16); b.y = lo[2] | ((uint32_t)lo[3] << 16);
+  b.z = lo[4] | ((uint32_t)lo[5] << 16); b.w = lo[6] | ((uint32_t)lo[7] << 16);
+  *reinterpret_cast<uint4*>(base + off) = a;
+  *reinterpret_cast<uint4*>(base + v_bytes + off) = b;
+}
+
+template <typename T>
+__global__ void reduce_partial_kernel(const double* __restrict__ partial, int splits,
+                                      int64_t nloc, int w, T* __restrict__ out, int64_t ldo) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nloc * w) return;
+  double s = 0.0;
+  for (int p = 0; p < splits; ++p) s += partial[(int64_t)p * nloc * w + e];
+  out[(e / w) * ldo + (e % w)] = (T)s;
+}
+
+// ------------------------------------------------------------------ host
+
+int ka_of(int d) { return ((3 * d + 4) + 15) / 16 * 16; }
+int wp_of(int w) { return w <= 16 ? 16 : 32; }
+
+struct Layout {
+  size_t mu, guard, colexp, bits, xa, col, partial, total;
+  uint32_t a_bytes, v_bytes;
+  int64_t tile_stride, row_tiles, col_tiles;
+};
+
+int splits_for(int64_t row_tiles, int64_t col_tiles, int sms) {
+  if (row_tiles >= 2 * sms) return 1;
+  int64_t s = (2 * sms + row_tiles - 1) / row_tiles;
+  if (s > col_tiles) s = col_tiles;
+  return (int)(s < 1 ? 1 : s);
+}
+
+Layout layout_of(int64_t n_rows, int64_t n_cols, int d, int w_max, int sms) {
+  Layout L{};
+  const int ka = ka_of(d);
+  const int wpm = wp_of(w_max);
+  L.a_bytes = (uint32_t)(BM * ka * 2);
+  L.v_bytes = (uint32_t)(wpm * BN * 2);
+  L.row_tiles = (n_rows + BM - 1) / BM;
+  L.col_tiles = (n_cols + BN - 1) / BN;
+  L.tile_stride = (int64_t)L.a_bytes + 2 * L.v_bytes;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = ncgp::align_up(off + bytes, 256);
+    return o;
+  };
+  L.mu = take(64 * sizeof(double));
+  L.guard = take(16);
+  L.colexp = take(64 * sizeof(int));
+  L.bits = take(64 * sizeof(unsigned));
+  L.xa = take((size_t)L.row_tiles * L.a_bytes);
+  L.col = take((size_t)L.col_tiles * L.tile_stride);
+  // partial rows when splits > 1: splits * local rows <= 4 * sms * 128
+  L.partial = take((size_t)4 * sms * BM * w_max * sizeof(double));
+  L.total = off;
+  return L;
+}
+
+}  // namespace
 
 namespace ncgp {
 
-bool tc_supported(int, int, int) { return false; }
-size_t tc_workspace_bytes(int64_t, int64_t, int, int) { return 0; }
-int tc_prepare(ncgp_kop*, cudaStream_t) {
-  set_error("tcgen05 operator not built");
-  return NCGP_UNSUPPORTED;
+bool tc_supported(int dtype, int d, int w_max) {
+  if (dtype != NCGP_F32) return false;
+  if (d < 1 || d > 64 || w_max < 1 || w_max > 32) return false;
+  // shared memory: 2 row tiles + >= 2 stages
+  const int ka = ka_of(d);
+  const size_t a = (size_t)BM * ka * 2, st = a + 2 * (size_t)wp_of(w_max) * BN * 2;
+  return 2 * a + 2 * st + (size_t)wp_of(w_max) * BM * 8 + 1024 <= (size_t)SMEM_BUDGET;
 }
-int tc_apply(ncgp_kop*, const void*, int64_t, int, void*, int64_t, int64_t, int64_t,
-             cudaStream_t) {
-  set_error("tcgen05 operator not built");
-  return NCGP_UNSUPPORTED;
+
+size_t tc_workspace_bytes(int64_t n_rows, int64_t n_cols, int d, int w_max) {
+  return layout_of(n_rows, n_cols, d, w_max, sm_count()).total;
+}
+
+int tc_prepare(ncgp_kop* op, cudaStream_t st) {
+  const Layout L = layout_of(op->n_rows, op->n_cols, op->d, op->w_max, op->sms);
+  NCGP_CHECK_ARG(op->ws_bytes >= L.total, NCGP_INVALID_INPUT, "tcgen05 workspace too small");
+  op->ka = ka_of(op->d);
+  op->wpad = wp_of(op->w_max);
+  op->row_tiles = L.row_tiles;
+  op->col_tiles = L.col_tiles;
+  op->xa_pack = op->ws + L.xa;
+  op->col_pack = op->ws + L.col;
+  op->col_tile_bytes = (size_t)L.tile_stride;
+  op->partial = reinterpret_cast<double*>(op->ws + L.partial);
+  // prescale kernel values into fp16 range: s2 * 2^s in (2^13, 2^14]
+  const int s_exp = 14 - (int)ceil(log2(op->s2));
+  op->k_scale = ldexp(1.0, s_exp);
+  const double log2e = 1.4426950408889634;
+  double alpha, sign, Lc;
+  if (op->family == NCGP_RBF) {
+    alpha = sqrt(log2e / (2.0 * op->ell * op->ell));  // -|x~|^2 = -d^2 log2e / (2 l^2)
+    sign = 1.0;
+    Lc = log2(op->s2) + s_exp;
+  } else {
+    alpha = sqrt(3.0) / op->ell;                     // |x~| = sqrt(3) d / l
+    sign = -1.0;
+    Lc = 0.0;
+  }
+  double* mu = reinterpret_cast<double*>(op->ws + L.mu);
+  const float* Xr = static_cast<const float*>(op->Xr);
+  const float* Xc = static_cast<const float*>(op->Xc);
+  col_mean_kernel<float><<<1, 1024, 0, st>>>(Xc, op->n_cols, op->d, mu);
+  NCGP_LAUNCHED();
+  const int qn = op->ka / 8;
+  {
+    const int64_t tot = L.row_tiles * BM * qn;
+    pack_x_kernel<float><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+        Xr, op->n_rows, op->d, op->ka, mu, alpha, sign, Lc, 0, op->xa_pack, L.a_bytes);
+    NCGP_LAUNCHED();
+  }
+  {
+    const int64_t tot = L.col_tiles * BN * qn;
+    pack_x_kernel<float><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+        Xc, op->n_cols, op->d, op->ka, mu, alpha, sign, Lc, 1, op->col_pack, L.tile_stride);
+    NCGP_LAUNCHED();
+  }
+  // precision guard: the expanded distance loses ~2^-22 |x~|^2 absolute
+  unsigned int* gbits = reinterpret_cast<unsigned int*>(op->ws + L.guard);
+  NCGP_CUDA(cudaMemsetAsync(gbits, 0, 8, st));
+  max_norm_kernel<float><<<(unsigned)((op->n_rows + 255) / 256), 256, 0, st>>>(
+      Xr, op->n_rows, op->d, mu, alpha, gbits);
+  NCGP_LAUNCHED();
+  max_norm_kernel<float><<<(unsigned)((op->n_cols + 255) / 256), 256, 0, st>>>(
+      Xc, op->n_cols, op->d, mu, alpha, gbits);
+  NCGP_LAUNCHED();
+  unsigned int hb = 0;
+  NCGP_CUDA(cudaMemcpyAsync(&hb, gbits, 4, cudaMemcpyDeviceToHost, st));
+  NCGP_CUDA(cudaStreamSynchronize(st));
+  float mx;
+  memcpy(&mx, &hb, 4);
+  NCGP_CHECK_ARG(mx <= 256.f, NCGP_UNSUPPORTED,
+                 "inputs span %.3g squared (scaled) lengthscales from their mean: beyond the "
+                 "tcgen05 operator's precision range, use the CUDA-core operator",
+                 (double)mx);
+  return NCGP_OK;
+}
+
+int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, void* out, int64_t ldo, int64_t r0,
+             int64_t r1, cudaStream_t st) {
+  NCGP_CHECK_ARG(r0 % BM == 0, NCGP_DIMENSION_MISMATCH,
+                 "row_begin must be a multiple of %d for the tcgen05 operator", BM);
+  const Layout L = layout_of(op->n_rows, op->n_cols, op->d, op->w_max, op->sms);
+  const int wp = wp_of(w);
+  int* col_exp = reinterpret_cast<int*>(op->ws + L.colexp);
+  unsigned int* bits = reinterpret_cast<unsigned int*>(op->ws + L.bits);
+  const float* Vf = static_cast<const float*>(V);
+  NCGP_CUDA(cudaMemsetAsync(bits, 0, 64 * sizeof(unsigned), st));
+  {
+    dim3 grid((unsigned)std::min<int64_t>(1024, (op->n_cols + 7) / 8), (unsigned)((w + 31) / 32));
+    col_absmax_kernel<float><<<grid, 256, 0, st>>>(Vf, ldv, op->n_cols, w, bits);
+    NCGP_LAUNCHED();
+    col_exp_kernel<<<1, 64, 0, st>>>(bits, w, wp, col_exp);
+    NCGP_LAUNCHED();
+  }
+  const uint32_t v_bytes = (uint32_t)(wp * BN * 2);
+  {
+    const int64_t tot = op->col_tiles * (BN / 8) * wp;
+    pack_v_kernel<float><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+        Vf, ldv, op->n_cols, w, wp, col_exp, op->col_pack, L.tile_stride, L.a_bytes, v_bytes,
+        op->col_tiles);
+    NCGP_LAUNCHED();
+  }
+  TcParams p{};
+  p.xa_pack = op->xa_pack;
+  p.col_pack = op->col_pack;
+  p.tile_stride = L.tile_stride;
+  p.a_bytes = L.a_bytes;
+  p.v_bytes = v_bytes;
+  p.ka = op->ka;
+  p.w = w;
+  p.rt0 = r0 / BM;
+  p.nloc = r1 - r0;
+  p.row_tiles = (p.nloc + BM - 1) / BM;
+  p.col_tiles = op->col_tiles;
+  p.splits = splits_for(p.row_tiles, p.col_tiles, op->sms);
+  p.tiles_per_split = (p.col_tiles + p.splits - 1) / p.splits;
+  p.splits = (int)((p.col_tiles + p.tiles_per_split - 1) / p.tiles_per_split);
+  const int s_exp = (int)lround(log2(op->k_scale));
+  p.s_exp = s_exp;
+  p.L = (float)(log2(op->s2) + s_exp);  // RBF clamp / Matern exponent offset
+  p.col_exp = col_exp;
+  p.out_f64 = op->dtype == NCGP_F64;
+  p.out = static_cast<uint8_t*>(out) + r0 * ldo * (p.out_f64 ? 8 : 4);
+  p.ldo = ldo;
+  p.partial = op->partial;
+  const uint32_t stage_bytes = p.a_bytes + 2 * v_bytes;
+  int stages = (int)((SMEM_BUDGET - 2 * (size_t)p.a_bytes - (size_t)wp * BM * 8 - 512) /
+                     stage_bytes);
+  if (stages > 6) stages = 6;
+  NCGP_CHECK_ARG(stages >= 2, NCGP_UNSUPPORTED, "shared memory too small for d=%d", op->d);
+  p.stages = stages;
+  NCGP_CHECK_ARG((int64_t)p.splits * p.nloc * w * 8 <= (int64_t)(L.total - L.partial) ||
+                     p.splits == 1,
+                 NCGP_INVALID_INPUT, "partial workspace too small");
+  const size_t smem = 2 * (size_t)p.a_bytes + (size_t)stages * stage_bytes +
+                      (size_t)wp * BM * sizeof(double) + (2 * stages + 12) * sizeof(uint64_t) + 16;
+  const int64_t items = p.row_tiles * p.splits;
+  const unsigned grid = (unsigned)std::min<int64_t>(items, op->sms);
+  auto launch = [&](auto kern) -> int {
+    NCGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+    kern<<<grid, NTHREADS, smem, st>>>(p);
+    NCGP_LAUNCHED();
+    return NCGP_OK;
+  };
+  int rc;
+  if (op->family == NCGP_RBF)
+    rc = wp == 16 ? launch(kop_tc_kernel<NCGP_RBF, 16>) : launch(kop_tc_kernel<NCGP_RBF, 32>);
+  else
+    rc = wp == 16 ? launch(kop_tc_kernel<NCGP_MATERN32, 16>)
+                  : launch(kop_tc_kernel<NCGP_MATERN32, 32>);
+  if (rc != NCGP_OK) return rc;
+  if (p.splits > 1) {
+    const int64_t tot = p.nloc * w;
+    if (p.out_f64)
+      reduce_partial_kernel<double><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+          p.partial, p.splits, p.nloc, w, static_cast<double*>(p.out), ldo);
+    else
+      reduce_partial_kernel<float><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+          p.partial, p.splits, p.nloc, w, static_cast<float*>(p.out), ldo);
+    NCGP_LAUNCHED();
+  }
+  return NCGP_OK;
 }
 
 }  // namespace ncgp

@@ -39,7 +39,7 @@ class KernelOperator:
 
     def __init__(self, family: str, lengthscale: float, outputscale: float,
                  X_rows: torch.Tensor, X_cols: Optional[torch.Tensor] = None,
-                 w_max: int = 64, impl: str = "auto"):
+                 w_max: int = 32, impl: str = "auto"):
         require_cuda()
         self.family = family
         self.fam_code = {"rbf": N.RBF, "matern32": N.MATERN32}[family]
@@ -55,7 +55,7 @@ class KernelOperator:
         self.dtype = self.X_rows.dtype
         self.n_rows, self.d = self.X_rows.shape
         self.n_cols = self.X_cols.shape[0]
-        self.w_max = int(max(1, min(w_max, 64)))
+        self.w_max = int(max(1, min(w_max, 32)))
         impl_code = {"auto": N.KOP_AUTO, "tcgen05": N.KOP_TCGEN05, "simt": N.KOP_SIMT}[impl]
         dt = code(self.dtype)
         nbytes = N.query("ncgp_kop_workspace_bytes", impl_code, dt, self.n_rows, self.n_cols,
