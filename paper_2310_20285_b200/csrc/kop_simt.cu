@@ -168,7 +168,8 @@ template <typename T, int FAM, int DMAX, int WT>
 int launch_t(ncgp_kop* op, const T* Xr, int64_t nloc, const T* V, int64_t ldv, int w,
              T* out, int64_t ldo, cudaStream_t st) {
   const int zs = (w + WT - 1) / WT;
-  const int splits = plan_splits(nloc, op->n_cols, zs, op->sms);
+  // planned on the full row count: row shards reduce in the same order
+  const int splits = plan_splits(op->n_rows, op->n_cols, zs, op->sms);
   int64_t cps = (op->n_cols + splits - 1) / splits;
   cps = (cps + JT - 1) / JT * JT;
   const size_t need = (size_t)splits * nloc * w * sizeof(double);

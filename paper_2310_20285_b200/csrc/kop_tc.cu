@@ -843,7 +843,9 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, void* out, int64_t
   p.nloc = r1 - r0;
   p.row_tiles = (p.nloc + BM - 1) / BM;
   p.col_tiles = op->col_tiles;
-  p.splits = splits_for(p.row_tiles, p.col_tiles, op->sms);
+  // splits depend on the operator's full row count only, so every row is
+  // reduced in the same order whichever row range (shard) is launched
+  p.splits = splits_for(op->row_tiles, p.col_tiles, op->sms);
   p.tiles_per_split = (p.col_tiles + p.splits - 1) / p.splits;
   p.splits = (int)((p.col_tiles + p.tiles_per_split - 1) / p.tiles_per_split);
   const int s_exp = (int)lround(log2(op->k_scale));
