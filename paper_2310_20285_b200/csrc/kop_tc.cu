@@ -61,18 +61,19 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
       "selp.b32 %0, 1, 0, P1;\n\t}"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
       : "memory");
   return ok != 0;
 }
-// Bounded wait: a pipeline bug traps (kernel error) instead of hanging the GPU.
+// Bounded wait: a pipeline bug traps (kernel error, ~17 s) instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t spins = 0;
+  if (mbar_try(bar, parity)) return;
+  const long long t0 = clock64();
   while (!mbar_try(bar, parity)) {
-    if (++spins > (1u << 26)) __trap();
+    if (clock64() - t0 > (1ll << 35)) __trap();
   }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
@@ -183,7 +184,7 @@ struct TcParams {
   const uint8_t* xa_pack;
   const uint8_t* col_pack;
   int64_t tile_stride;   // bytes between column tiles in col_pack
-  uint32_t a_bytes;      // one packed row tile (= XB bytes)
+  uint32_t a_bytes;      // one packed row tile (= one XB tile)
   uint32_t v_bytes;      // one of Vhi / Vlo for a column tile
   int ka;                // K of GEMM1 (multiple of 16)
   int w;                 // real RHS width
@@ -193,35 +194,35 @@ struct TcParams {
   int64_t col_tiles;
   int splits;
   int64_t tiles_per_split;
-  float L;               // RBF clamp / Matern exponent offset (log2 of s2 * 2^s)
+  float L;               // log2(s2 * 2^s): Matern exponent offset
   const int* col_exp;    // per RHS column exponent e_c
   int s_exp;             // kernel prescale exponent s
   void* out;
   int64_t ldo;
   int out_f64;
   double* partial;       // [splits][nloc][w] when splits > 1
-  int stages;
+  int sx, sv;            // depths of the XB and V shared-memory rings
 };
 
 struct Item {
-  int64_t rt, c0, c1;
+  int rt, c0, c1;
 };
 
-__device__ __forceinline__ Item item_of(const TcParams& p, int64_t it) {
+__device__ __forceinline__ Item item_of(const TcParams& p, int it) {
   Item r;
   r.rt = it / p.splits;
-  const int64_t sp = it % p.splits;
-  r.c0 = sp * p.tiles_per_split;
-  r.c1 = min(p.col_tiles, r.c0 + p.tiles_per_split);
+  const int sp = it - r.rt * p.splits;
+  r.c0 = sp * (int)p.tiles_per_split;
+  r.c1 = min((int)p.col_tiles, r.c0 + (int)p.tiles_per_split);
   return r;
 }
 
 // Iterates the CTA's global column-tile sequence across its items.
 struct TileIter {
-  int64_t it, ct;
+  int it, ct;
   Item cur;
   bool valid;
-  __device__ void start(const TcParams& p, int64_t items) {
+  __device__ __forceinline__ void start(const TcParams& p, int items) {
     it = blockIdx.x;
     valid = it < items;
     if (valid) {
@@ -229,7 +230,7 @@ struct TileIter {
       ct = cur.c0;
     }
   }
-  __device__ void next(const TcParams& p, int64_t items) {
+  __device__ __forceinline__ void next(const TcParams& p, int items) {
     if (++ct >= cur.c1) {
       it += gridDim.x;
       valid = it < items;
@@ -239,47 +240,116 @@ struct TileIter {
       }
     }
   }
-  __device__ bool first_in_item() const { return ct == cur.c0; }
-  __device__ bool last_in_item() const { return ct == cur.c1 - 1; }
-  __device__ bool first_in_chunk() const { return ct == cur.c0 || (ct % CH) == 0; }
-  __device__ bool last_in_chunk() const { return ct == cur.c1 - 1 || (ct % CH) == CH - 1; }
+  __device__ __forceinline__ bool first_in_item() const { return ct == cur.c0; }
+  __device__ __forceinline__ bool last_in_item() const { return ct == cur.c1 - 1; }
+  __device__ __forceinline__ bool first_in_chunk() const {
+    return ct == cur.c0 || (ct & (CH - 1)) == 0;
+  }
+  __device__ __forceinline__ bool last_in_chunk() const {
+    return ct == cur.c1 - 1 || (ct & (CH - 1)) == CH - 1;
+  }
 };
+
+// Position in a ring of mbarrier-guarded slots (no divisions on the hot path).
+struct Ring {
+  uint32_t idx, phase, size;
+  __device__ __forceinline__ void init(uint32_t n) {
+    idx = 0;
+    phase = 0;
+    size = n;
+  }
+  __device__ __forceinline__ void adv() {
+    if (++idx == size) {
+      idx = 0;
+      phase ^= 1u;
+    }
+  }
+};
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+constexpr int NS = 3;  // S/P buffers in TMEM (3 x 128 columns)
+
+// Kernel transform of one 32-column chunk: S (fp32 exponent argument) ->
+// P_hi / P_lo packed fp16 pairs.
+template <int FAM>
+__device__ __forceinline__ void transform_chunk(const uint32_t (&r)[32], float L,
+                                                uint32_t (&hi)[16], uint32_t (&lo)[16]) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    float k0, k1;
+    const float g0 = __uint_as_float(r[2 * i]);
+    const float g1 = __uint_as_float(r[2 * i + 1]);
+    if (FAM == NCGP_RBF) {
+      k0 = ex2(g0);  // g <= L up to the rounding of the d^2 expansion
+      k1 = ex2(g1);
+    } else {
+      const float a0 = sqrt_approx(fmaxf(g0, 0.f));
+      const float a1 = sqrt_approx(fmaxf(g1, 0.f));
+      const float e0 = ex2(fmaf(a0, -1.4426950408889634f, L));
+      const float e1 = ex2(fmaf(a1, -1.4426950408889634f, L));
+      k0 = fmaf(a0, e0, e0);
+      k1 = fmaf(a1, e1, e1);
+    }
+    const float h0 = __uint_as_float(__float_as_uint(k0) & 0xFFFFE000u);
+    const float h1 = __uint_as_float(__float_as_uint(k1) & 0xFFFFE000u);
+    hi[i] = pack_h2(h0, h1);
+    lo[i] = pack_h2(k0 - h0, k1 - h1);
+  }
+}
 
 template <int FAM, int WP>
 __global__ void __launch_bounds__(NTHREADS, 1) kop_tc_kernel(const TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int64_t items = p.row_tiles * p.splits;
+  const int items = (int)(p.row_tiles * p.splits);
 
   // ---- shared-memory carve-up
-  const uint32_t stage_bytes = p.a_bytes + 2 * p.v_bytes;
-  uint8_t* sA = smem;                                   // 2 x a_bytes
-  uint8_t* sStage = smem + 2 * p.a_bytes;               // stages x stage_bytes
-  double* sAcc = reinterpret_cast<double*>(sStage + (size_t)p.stages * stage_bytes);  // [WP][128]
+  const uint32_t vpair = 2 * p.v_bytes;                 // [Vhi ; Vlo]
+  uint8_t* sA = smem;                                   // 2 x a_bytes (row tiles)
+  uint8_t* sXB = sA + 2 * p.a_bytes;                    // sx x a_bytes
+  uint8_t* sV = sXB + (size_t)p.sx * p.a_bytes;         // sv x vpair
+  double* sAcc = reinterpret_cast<double*>(sV + (size_t)p.sv * vpair);  // [WP][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sAcc + WP * BM);
-  uint64_t* full = bars;                 // [stages]
-  uint64_t* empty = full + p.stages;     // [stages]
-  uint64_t* a_full = empty + p.stages;   // [2]
-  uint64_t* a_empty = a_full + 2;        // [2]
-  uint64_t* s_full = a_empty + 2;        // [2]
-  uint64_t* p_full = s_full + 2;         // [2]
-  uint64_t* o_full = p_full + 2;         // [2]
-  uint64_t* o_empty = o_full + 2;        // [2]
+  uint64_t* xb_full = bars;             // [sx]
+  uint64_t* xb_empty = xb_full + p.sx;  // [sx]
+  uint64_t* v_full = xb_empty + p.sx;   // [sv]
+  uint64_t* v_empty = v_full + p.sv;    // [sv]
+  uint64_t* a_full = v_empty + p.sv;    // [2]
+  uint64_t* a_empty = a_full + 2;       // [2]
+  uint64_t* s_full = a_empty + 2;       // [NS]
+  uint64_t* p_full = s_full + NS;       // [NS]
+  uint64_t* o_full = p_full + NS;       // [2]
+  uint64_t* o_empty = o_full + 2;       // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < p.stages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+    for (int s = 0; s < p.sx; ++s) {
+      mbar_init(&xb_full[s], 1);
+      mbar_init(&xb_empty[s], 1);
+    }
+    for (int s = 0; s < p.sv; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&a_full[b], 1);
       mbar_init(&a_empty[b], 1);
-      mbar_init(&s_full[b], 1);
-      mbar_init(&p_full[b], 128);
       mbar_init(&o_full[b], 1);
       mbar_init(&o_empty[b], 128);
+    }
+    for (int b = 0; b < NS; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&p_full[b], 128);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -293,152 +363,167 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_tc_kernel(const TcParams p) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // TMEM columns: S/P buffers [0, 384), O double buffer [384, 384 + 4 WP)
   auto tS = [&](int b) -> uint32_t { return tmem + (uint32_t)(b * BN); };
-  auto tO = [&](int b) -> uint32_t { return tmem + 2u * BN + (uint32_t)(b * WP); };
+  auto tO = [&](int b) -> uint32_t { return tmem + (uint32_t)(NS * BN + b * 2 * WP); };
 
   if (warp == 0) {
-    // ================= producer =================
+    // ================= producer: row tiles + XB ring =================
     if (lane == 0) {
       TileIter ti;
       ti.start(p, items);
-      int64_t g = 0, nitem = 0;
+      Ring xr;
+      xr.init(p.sx);
+      uint32_t nitem = 0;
       while (ti.valid) {
         if (ti.first_in_item()) {
-          const int ab = nitem & 1;
-          mbar_wait(&a_empty[ab], ((nitem >> 1) & 1) ^ 1);
+          const uint32_t ab = nitem & 1u;
+          mbar_wait(&a_empty[ab], ((nitem >> 1) & 1u) ^ 1u);
           mbar_expect_tx(&a_full[ab], p.a_bytes);
           bulk_g2s(sA + ab * p.a_bytes, p.xa_pack + (p.rt0 + ti.cur.rt) * (int64_t)p.a_bytes,
                    p.a_bytes, &a_full[ab]);
           ++nitem;
         }
-        const int s = (int)(g % p.stages);
-        const uint32_t ph = (uint32_t)((g / p.stages) & 1);
-        mbar_wait(&empty[s], ph ^ 1);
-        mbar_expect_tx(&full[s], stage_bytes);
-        bulk_g2s(sStage + (size_t)s * stage_bytes, p.col_pack + ti.ct * p.tile_stride,
-                 stage_bytes, &full[s]);
-        ++g;
+        mbar_wait(&xb_empty[xr.idx], xr.phase ^ 1u);
+        mbar_expect_tx(&xb_full[xr.idx], p.a_bytes);
+        bulk_g2s(sXB + (size_t)xr.idx * p.a_bytes, p.col_pack + (int64_t)ti.ct * p.tile_stride,
+                 p.a_bytes, &xb_full[xr.idx]);
+        xr.adv();
+        ti.next(p, items);
+      }
+    }
+  } else if (warp == 3) {
+    // ================= producer: V ring =================
+    if (lane == 0) {
+      TileIter ti;
+      ti.start(p, items);
+      Ring vr;
+      vr.init(p.sv);
+      while (ti.valid) {
+        mbar_wait(&v_empty[vr.idx], vr.phase ^ 1u);
+        mbar_expect_tx(&v_full[vr.idx], vpair);
+        bulk_g2s(sV + (size_t)vr.idx * vpair,
+                 p.col_pack + (int64_t)ti.ct * p.tile_stride + p.a_bytes, vpair, &v_full[vr.idx]);
+        vr.adv();
         ti.next(p, items);
       }
     }
   } else if (warp == 1) {
-    // ================= MMA issuer =================
-    if (lane == 0) {
-      const uint32_t id1 = idesc_f16(BN), id2 = idesc_f16(WP);
-      const uint32_t sbo_x = (uint32_t)(p.ka / 8) * 128u;
-      const int ksteps1 = p.ka / 16;
-      TileIter look;  // tile whose GEMM1 is issued next
-      look.start(p, items);
-      int64_t g1 = 0, item1 = 0;
-      auto issue_gemm1 = [&]() {
-        const int b = (int)(g1 & 1);
-        if (look.first_in_item()) {
-          mbar_wait(&a_full[item1 & 1], (uint32_t)((item1 >> 1) & 1));
-          ++item1;
-        }
-        const int ab = (int)((item1 - 1) & 1);
-        const int s = (int)(g1 % p.stages);
-        mbar_wait(&full[s], (uint32_t)((g1 / p.stages) & 1));
-        tc_fence_after();
-        const uint32_t a0 = smem_u32(sA + ab * p.a_bytes);
-        const uint32_t b0 = smem_u32(sStage + (size_t)s * stage_bytes);
+    // ================= MMA issuer (whole warp, one elected lane issues) =================
+    const uint32_t id1 = idesc_f16(BN), id2 = idesc_f16(2 * WP), id2h = idesc_f16(WP);
+    const uint32_t sbo_x = (uint32_t)(p.ka / 8) * 128u;
+    const int ksteps1 = p.ka / 16;
+    const uint32_t sA0 = smem_u32(sA), sXB0 = smem_u32(sXB), sV0 = smem_u32(sV);
+    TileIter look;  // tile whose GEMM1 is issued next
+    look.start(p, items);
+    Ring xr;
+    xr.init(p.sx);
+    uint32_t b1 = 0, item1 = 0;
+    auto issue_gemm1 = [&]() {
+      if (look.first_in_item()) {
+        mbar_wait(&a_full[item1 & 1u], (item1 >> 1) & 1u);
+        ++item1;
+      }
+      const uint32_t ab = (item1 - 1u) & 1u;
+      mbar_wait(&xb_full[xr.idx], xr.phase);
+      tc_fence_after();
+      const uint64_t adesc = sdesc(sA0 + ab * p.a_bytes, 128u, sbo_x);
+      const uint64_t bdesc = sdesc(sXB0 + xr.idx * p.a_bytes, 128u, sbo_x);
+      const uint32_t d = tS((int)b1);
+      if (elect_one()) {
         for (int k = 0; k < ksteps1; ++k)
-          mma_ss(tS(b), sdesc(a0 + 256u * k, 128u, sbo_x), sdesc(b0 + 256u * k, 128u, sbo_x),
-                 id1, k > 0);
-        tc_commit(&s_full[b]);
+          mma_ss(d, adesc + (uint64_t)(16 * k), bdesc + (uint64_t)(16 * k), id1, k > 0);
+        tc_commit(&s_full[b1]);
+        tc_commit(&xb_empty[xr.idx]);
         if (look.last_in_item()) tc_commit(&a_empty[ab]);
-        ++g1;
-        look.next(p, items);
-      };
-      if (look.valid) issue_gemm1();
-      if (look.valid) issue_gemm1();
-      TileIter cur;
-      cur.start(p, items);
-      int64_t g = 0, q = 0;
-      while (cur.valid) {
-        const int b = (int)(g & 1);
-        const int s = (int)(g % p.stages);
-        mbar_wait(&p_full[b], (uint32_t)((g >> 1) & 1));
+      }
+      __syncwarp();
+      xr.adv();
+      b1 = (b1 + 1u == (uint32_t)NS) ? 0u : b1 + 1u;
+      look.next(p, items);
+    };
+    for (int i = 0; i < NS && look.valid; ++i) issue_gemm1();
+    TileIter cur;
+    cur.start(p, items);
+    Ring pr, vr;
+    pr.init(NS);
+    vr.init(p.sv);
+    uint32_t q = 0;
+    while (cur.valid) {
+      mbar_wait(&p_full[pr.idx], pr.phase);
+      tc_fence_after();
+      const uint32_t ob = q & 1u;
+      const bool fresh = cur.first_in_chunk();
+      if (fresh) {
+        mbar_wait(&o_empty[ob], ((q >> 1) & 1u) ^ 1u);
         tc_fence_after();
-        const int ob = (int)(q & 1);
-        if (cur.first_in_chunk()) {
-          mbar_wait(&o_empty[ob], (uint32_t)(((q >> 1) & 1) ^ 1));
-          tc_fence_after();
-        }
-        const uint32_t vhi = smem_u32(sStage + (size_t)s * stage_bytes + p.a_bytes);
-        const uint32_t vlo = vhi + p.v_bytes;
-        const bool fresh = cur.first_in_chunk();
+      }
+      mbar_wait(&v_full[vr.idx], vr.phase);
+      tc_fence_after();
+      // B = [Vhi ; Vlo] (2*WP rows, one K-major block): P_hi x [Vhi|Vlo] as one
+      // N = 2*WP instruction, then P_lo x Vhi accumulated onto the Vhi half.
+      const uint64_t bdesc = sdesc(sV0 + vr.idx * vpair, 128u, 2048u);
+      const uint32_t abase = tS((int)pr.idx);
+      const uint32_t dO = tO((int)ob);
+      const bool last = cur.last_in_chunk();
+      if (elect_one()) {
 #pragma unroll
         for (int m = 0; m < BN / 16; ++m) {
-          const uint32_t ahi = tS(b) + 32u * (m >> 1) + 8u * (m & 1);
-          const uint32_t alo = ahi + 16u;
-          const uint64_t bhi = sdesc(vhi + 256u * m, 128u, 2048u);
-          const uint64_t blo = sdesc(vlo + 256u * m, 128u, 2048u);
-          mma_ts(tO(ob), ahi, bhi, id2, (fresh && m == 0) ? 0u : 1u);
-          mma_ts(tO(ob), alo, bhi, id2, 1u);
-          mma_ts(tO(ob), ahi, blo, id2, 1u);
+          const uint32_t ahi = abase + 32u * (m >> 1) + 8u * (m & 1);
+          mma_ts(dO, ahi, bdesc + (uint64_t)(16 * m), id2, (fresh && m == 0) ? 0u : 1u);
+          mma_ts(dO, ahi + 16u, bdesc + (uint64_t)(16 * m), id2h, 1u);
         }
-        tc_commit(&empty[s]);
-        if (cur.last_in_chunk()) {
-          tc_commit(&o_full[ob]);
-          ++q;
-        }
-        if (look.valid) issue_gemm1();
-        ++g;
-        cur.next(p, items);
+        tc_commit(&v_empty[vr.idx]);
+        if (last) tc_commit(&o_full[ob]);
       }
+      __syncwarp();
+      if (last) ++q;
+      pr.adv();
+      vr.adv();
+      if (look.valid) issue_gemm1();  // reuses this S buffer: ordered after this GEMM2
+      cur.next(p, items);
     }
   } else if (warp >= 4 && warp < 12) {
     // ================= epilogue warpgroups =================
-    const int e = (warp - 4) >> 2;           // 0 or 1
+    const int e = (warp - 4) >> 2;           // 0 or 1: tiles g = e (mod 2)
     const int wq = warp & 3;                 // TMEM lane quarter
     const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
     TileIter ti;
     ti.start(p, items);
-    int64_t g = 0;
-    int64_t k = 0;
+    Ring er;
+    er.init(NS);
+    uint32_t g = 0;
     const float L = p.L;
     while (ti.valid) {
-      if ((g & 1) == e) {
-        mbar_wait(&s_full[e], (uint32_t)(k & 1));
+      if ((int)(g & 1u) == e) {
+        const int b = (int)er.idx;
+        mbar_wait(&s_full[b], er.phase);
         tc_fence_after();
-        const uint32_t base = tS(e) + lane_off;
-#pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld32(base + 32 * c, r);
-          tmem_wait_ld();
-          uint32_t hi[16], lo[16];
+        const uint32_t base = tS(b) + lane_off;
+        uint32_t ra[32], rb[32];
+        tmem_ld32(base, ra);
+        tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            float k0, k1;
-            const float g0 = __uint_as_float(r[2 * i]);
-            const float g1 = __uint_as_float(r[2 * i + 1]);
-            if (FAM == NCGP_RBF) {
-              k0 = ex2(fminf(g0, L));
-              k1 = ex2(fminf(g1, L));
-            } else {
-              const float a0 = sqrt_approx(fmaxf(g0, 0.f));
-              const float a1 = sqrt_approx(fmaxf(g1, 0.f));
-              const float e0 = ex2(fmaf(a0, -1.4426950408889634f, L));
-              const float e1 = ex2(fmaf(a1, -1.4426950408889634f, L));
-              k0 = fmaf(a0, e0, e0);
-              k1 = fmaf(a1, e1, e1);
-            }
-            const float h0 = __uint_as_float(__float_as_uint(k0) & 0xFFFFE000u);
-            const float h1 = __uint_as_float(__float_as_uint(k1) & 0xFFFFE000u);
-            hi[i] = pack_h2(h0, h1);
-            lo[i] = pack_h2(k0 - h0, k1 - h1);
-          }
+        for (int c = 0; c < BN / 32; c += 2) {
+          // software pipeline: load chunk c+1 while transforming chunk c
+          uint32_t hi[16], lo[16];
+          tmem_ld32(base + 32 * (c + 1), rb);
+          transform_chunk<FAM>(ra, L, hi, lo);
           tmem_st16(base + 32 * c, hi);
           tmem_st16(base + 32 * c + 16, lo);
+          tmem_wait_ld();
+          if (c + 2 < BN / 32) tmem_ld32(base + 32 * (c + 2), ra);
+          transform_chunk<FAM>(rb, L, hi, lo);
+          tmem_st16(base + 32 * (c + 1), hi);
+          tmem_st16(base + 32 * (c + 1) + 16, lo);
+          if (c + 2 < BN / 32) tmem_wait_ld();
         }
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(&p_full[e]);
-        ++k;
+        mbar_arrive(&p_full[b]);
       }
       ++g;
+      er.adv();
       ti.next(p, items);
     }
   } else if (warp >= 12) {
@@ -451,19 +536,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_tc_kernel(const TcParams p) {
     for (int c = 0; c < WP; ++c) acc[c * BM] = 0.0;
     TileIter ti;
     ti.start(p, items);
-    int64_t q = 0;
+    uint32_t q = 0;
     while (ti.valid) {
       if (ti.last_in_chunk()) {
-        const int ob = (int)(q & 1);
-        mbar_wait(&o_full[ob], (uint32_t)((q >> 1) & 1));
+        const int ob = (int)(q & 1u);
+        mbar_wait(&o_full[ob], (q >> 1) & 1u);
         tc_fence_after();
 #pragma unroll
         for (int h = 0; h < WP / 16; ++h) {
-          uint32_t r[16];
-          tmem_ld16(tO(ob) + lane_off + 16 * h, r);
+          uint32_t r[16], t[16];
+          tmem_ld16(tO(ob) + lane_off + 16 * h, r);       // P_hi Vhi + P_lo Vhi
+          tmem_ld16(tO(ob) + lane_off + WP + 16 * h, t);  // P_hi Vlo
           tmem_wait_ld();
 #pragma unroll
-          for (int c = 0; c < 16; ++c) acc[(16 * h + c) * BM] += (double)__uint_as_float(r[c]);
+          for (int c = 0; c < 16; ++c)
+            acc[(16 * h + c) * BM] += (double)__uint_as_float(r[c]) + (double)__uint_as_float(t[c]);
         }
         tc_fence_before();
         mbar_arrive(&o_empty[ob]);
@@ -734,8 +821,9 @@ bool tc_supported(int dtype, int d, int w_max) {
   if (d < 1 || d > 64 || w_max < 1 || w_max > 32) return false;
   // shared memory: 2 row tiles + >= 2 stages
   const int ka = ka_of(d);
-  const size_t a = (size_t)BM * ka * 2, st = a + 2 * (size_t)wp_of(w_max) * BN * 2;
-  return 2 * a + 2 * st + (size_t)wp_of(w_max) * BM * 8 + 1024 <= (size_t)SMEM_BUDGET;
+  const size_t a = (size_t)BM * ka * 2;
+  return 4 * a + 4 * 2 * (size_t)wp_of(w_max) * BN * 2 + (size_t)wp_of(w_max) * BM * 8 + 1024 <=
+         (size_t)SMEM_BUDGET;
 }
 
 size_t tc_workspace_bytes(int64_t n_rows, int64_t n_cols, int d, int w_max) {
@@ -856,17 +944,28 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, void* out, int64_t
   p.out = static_cast<uint8_t*>(out) + r0 * ldo * (p.out_f64 ? 8 : 4);
   p.ldo = ldo;
   p.partial = op->partial;
-  const uint32_t stage_bytes = p.a_bytes + 2 * v_bytes;
-  int stages = (int)((SMEM_BUDGET - 2 * (size_t)p.a_bytes - (size_t)wp * BM * 8 - 512) /
-                     stage_bytes);
-  if (stages > 6) stages = 6;
-  NCGP_CHECK_ARG(stages >= 2, NCGP_UNSUPPORTED, "shared memory too small for d=%d", op->d);
-  p.stages = stages;
+  // shared memory: 2 row tiles + XB ring + V ring + fp64 accumulators
+  const size_t fixed = 2 * (size_t)p.a_bytes + (size_t)wp * BM * 8 + 1024;
+  NCGP_CHECK_ARG(fixed + 2 * (size_t)p.a_bytes + 4 * (size_t)v_bytes <= (size_t)SMEM_BUDGET,
+                 NCGP_UNSUPPORTED, "shared memory too small for d=%d", op->d);
+  int sv = 4, sx = (int)((SMEM_BUDGET - fixed - 4 * (size_t)v_bytes) / p.a_bytes);
+  if (sx > 4) sx = 4;
+  if (sx < 2) {
+    sv = 2;
+    sx = 2;
+  } else {
+    // give leftover space to the V ring
+    const size_t left = SMEM_BUDGET - fixed - (size_t)sx * p.a_bytes;
+    sv = (int)std::min<size_t>(6, left / (2 * (size_t)v_bytes));
+  }
+  p.sx = sx;
+  p.sv = sv;
   NCGP_CHECK_ARG((int64_t)p.splits * p.nloc * w * 8 <= (int64_t)(L.total - L.partial) ||
                      p.splits == 1,
                  NCGP_INVALID_INPUT, "partial workspace too small");
-  const size_t smem = 2 * (size_t)p.a_bytes + (size_t)stages * stage_bytes +
-                      (size_t)wp * BM * sizeof(double) + (2 * stages + 12) * sizeof(uint64_t) + 16;
+  const size_t smem = 2 * (size_t)p.a_bytes + (size_t)sx * p.a_bytes + (size_t)sv * 2 * v_bytes +
+                      (size_t)wp * BM * sizeof(double) +
+                      (2 * sx + 2 * sv + 8 + 2 * NS) * sizeof(uint64_t) + 16;
   const int64_t items = p.row_tiles * p.splits;
   const unsigned grid = (unsigned)std::min<int64_t>(items, op->sms);
   auto launch = [&](auto kern) -> int {
