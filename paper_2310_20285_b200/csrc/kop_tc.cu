@@ -201,7 +201,9 @@ struct TcParams {
   int64_t ldo;
   int out_f64;
   double* partial;       // [splits][nloc][w] when splits > 1
-  int sx, sv;            // depths of the XB and V shared-memory rings
+  int na;                // row-tile buffers in shared memory (1 or 2)
+  long long* trace;      // debug: per-tile timestamps of CTA 0 (nullptr in production)
+  int debug_mode;        // debug: 1 = epilogue skips TMEM traffic, 2 = no GEMM2, 3 = no GEMM1
 };
 
 struct Item {
@@ -277,6 +279,13 @@ __device__ __forceinline__ bool elect_one() {
 }
 
 constexpr int NS = 3;  // S/P buffers in TMEM (3 x 128 columns)
+constexpr int TRACE_TILES = 256, TRACE_EV = 8;
+
+template <bool DBG>
+__device__ __forceinline__ void trace_ev(const TcParams& p, uint32_t tile, int ev) {
+  if (DBG && p.trace != nullptr && blockIdx.x == 0 && tile < (uint32_t)TRACE_TILES)
+    p.trace[tile * TRACE_EV + ev] = clock64();
+}
 
 // Kernel transform of one 32-column chunk: S (fp32 exponent argument) ->
 // P_hi / P_lo packed fp16 pairs.
@@ -306,7 +315,7 @@ __device__ __forceinline__ void transform_chunk(const uint32_t (&r)[32], float L
   }
 }
 
-template <int FAM, int WP>
+template <int FAM, int WP, bool DBG>
 __global__ void __launch_bounds__(NTHREADS, 1) kop_tc_kernel(const TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5;
@@ -315,42 +324,32 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_tc_kernel(const TcParams p) {
 
   // ---- shared-memory carve-up
   const uint32_t vpair = 2 * p.v_bytes;                 // [Vhi ; Vlo]
-  uint8_t* sA = smem;                                   // 2 x a_bytes (row tiles)
-  uint8_t* sXB = sA + 2 * p.a_bytes;                    // sx x a_bytes
-  uint8_t* sV = sXB + (size_t)p.sx * p.a_bytes;         // sv x vpair
-  double* sAcc = reinterpret_cast<double*>(sV + (size_t)p.sv * vpair);  // [WP][128]
+  uint8_t* sA = smem;                                   // na x a_bytes (row tiles)
+  uint8_t* sXB = sA + (size_t)p.na * p.a_bytes;         // NS x a_bytes
+  uint8_t* sV = sXB + (size_t)NS * p.a_bytes;           // 2NS x vpair
+  double* sAcc = reinterpret_cast<double*>(sV + (size_t)2 * NS * vpair);  // [WP][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sAcc + WP * BM);
-  uint64_t* xb_full = bars;             // [sx]
-  uint64_t* xb_empty = xb_full + p.sx;  // [sx]
-  uint64_t* v_full = xb_empty + p.sx;   // [sv]
-  uint64_t* v_empty = v_full + p.sv;    // [sv]
-  uint64_t* a_full = v_empty + p.sv;    // [2]
+  uint64_t* xb_full = bars;             // [NS]
+  uint64_t* v_full = xb_full + NS;      // [2NS]
+  uint64_t* a_full = v_full + 2 * NS;   // [2]
   uint64_t* a_empty = a_full + 2;       // [2]
-  uint64_t* s_full = a_empty + 2;       // [NS]
-  uint64_t* p_full = s_full + NS;       // [NS]
+  uint64_t* s_full = a_empty + 2;       // [2NS], indexed by tile mod 2NS
+  uint64_t* p_full = s_full + 2 * NS;   // [NS]
   uint64_t* o_full = p_full + NS;       // [2]
   uint64_t* o_empty = o_full + 2;       // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < p.sx; ++s) {
-      mbar_init(&xb_full[s], 1);
-      mbar_init(&xb_empty[s], 1);
-    }
-    for (int s = 0; s < p.sv; ++s) {
-      mbar_init(&v_full[s], 1);
-      mbar_init(&v_empty[s], 1);
-    }
+    for (int s = 0; s < NS; ++s) mbar_init(&xb_full[s], 1);
+    for (int s = 0; s < 2 * NS; ++s) mbar_init(&v_full[s], 1);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&a_full[b], 1);
       mbar_init(&a_empty[b], 1);
       mbar_init(&o_full[b], 1);
       mbar_init(&o_empty[b], 128);
     }
-    for (int b = 0; b < NS; ++b) {
-      mbar_init(&s_full[b], 1);
-      mbar_init(&p_full[b], 128);
-    }
+    for (int b = 0; b < 2 * NS; ++b) mbar_init(&s_full[b], 1);
+    for (int b = 0; b < NS; ++b) mbar_init(&p_full[b], 128);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -369,26 +368,38 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_tc_kernel(const TcParams p) {
 
   if (warp == 0) {
     // ================= producer: row tiles + XB ring =================
+    // Slot reuse is signalled by GEMM1 completions (s_full, one commit per tile):
+    // XB slot g mod NS is free once GEMM1(g - NS) completed, and V slot g mod 2NS
+    // once GEMM2(g - 2NS) did, which the in-order tensor pipe finishes before
+    // GEMM1(g - NS).  s_full has 2NS entries so no waiter can lag two phases.
     if (lane == 0) {
       TileIter ti;
       ti.start(p, items);
-      Ring xr;
-      xr.init(p.sx);
-      uint32_t nitem = 0;
+      Ring xr, sr;  // XB slot ring (NS); position of tile g - NS in the s_full ring
+      xr.init(NS);
+      sr.init(2 * NS);
+      uint32_t nitem = 0, g = 0;
       while (ti.valid) {
         if (ti.first_in_item()) {
-          const uint32_t ab = nitem & 1u;
-          mbar_wait(&a_empty[ab], ((nitem >> 1) & 1u) ^ 1u);
+          const uint32_t ab = p.na == 2 ? (nitem & 1u) : 0u;
+          const uint32_t aph = p.na == 2 ? ((nitem >> 1) & 1u) : (nitem & 1u);
+          mbar_wait(&a_empty[ab], aph ^ 1u);
           mbar_expect_tx(&a_full[ab], p.a_bytes);
           bulk_g2s(sA + ab * p.a_bytes, p.xa_pack + (p.rt0 + ti.cur.rt) * (int64_t)p.a_bytes,
                    p.a_bytes, &a_full[ab]);
           ++nitem;
         }
-        mbar_wait(&xb_empty[xr.idx], xr.phase ^ 1u);
-        mbar_expect_tx(&xb_full[xr.idx], p.a_bytes);
-        bulk_g2s(sXB + (size_t)xr.idx * p.a_bytes, p.col_pack + (int64_t)ti.ct * p.tile_stride,
-                 p.a_bytes, &xb_full[xr.idx]);
+        if (g >= (uint32_t)NS) mbar_wait(&s_full[sr.idx], sr.phase);
+        if (DBG && p.debug_mode >= 4) {
+          mbar_arrive(&xb_full[xr.idx]);
+        } else {
+          mbar_expect_tx(&xb_full[xr.idx], p.a_bytes);
+          bulk_g2s(sXB + (size_t)xr.idx * p.a_bytes, p.col_pack + (int64_t)ti.ct * p.tile_stride,
+                   p.a_bytes, &xb_full[xr.idx]);
+        }
         xr.adv();
+        if (g >= (uint32_t)NS) sr.adv();
+        ++g;
         ti.next(p, items);
       }
     }
@@ -397,14 +408,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_tc_kernel(const TcParams p) {
     if (lane == 0) {
       TileIter ti;
       ti.start(p, items);
-      Ring vr;
-      vr.init(p.sv);
+      Ring vr, sr;  // V slot ring (2NS); position of tile g - NS in the s_full ring
+      vr.init(2 * NS);
+      sr.init(2 * NS);
+      uint32_t g = 0;
       while (ti.valid) {
-        mbar_wait(&v_empty[vr.idx], vr.phase ^ 1u);
-        mbar_expect_tx(&v_full[vr.idx], vpair);
-        bulk_g2s(sV + (size_t)vr.idx * vpair,
-                 p.col_pack + (int64_t)ti.ct * p.tile_stride + p.a_bytes, vpair, &v_full[vr.idx]);
+        if (g >= (uint32_t)(2 * NS)) mbar_wait(&s_full[sr.idx], sr.phase);
+        if (DBG && p.debug_mode >= 4) {
+          mbar_arrive(&v_full[vr.idx]);
+        } else {
+          mbar_expect_tx(&v_full[vr.idx], vpair);
+          bulk_g2s(sV + (size_t)vr.idx * vpair,
+                   p.col_pack + (int64_t)ti.ct * p.tile_stride + p.a_bytes, vpair, &v_full[vr.idx]);
+        }
         vr.adv();
+        if (g >= (uint32_t)NS) sr.adv();
+        ++g;
         ti.next(p, items);
       }
     }
@@ -416,29 +435,33 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_tc_kernel(const TcParams p) {
     const uint32_t sA0 = smem_u32(sA), sXB0 = smem_u32(sXB), sV0 = smem_u32(sV);
     TileIter look;  // tile whose GEMM1 is issued next
     look.start(p, items);
-    Ring xr;
-    xr.init(p.sx);
+    Ring xr, cr;  // XB slot ring (NS); s_full ring (2NS)
+    xr.init(NS);
+    cr.init(2 * NS);
     uint32_t b1 = 0, item1 = 0;
     auto issue_gemm1 = [&]() {
       if (look.first_in_item()) {
-        mbar_wait(&a_full[item1 & 1u], (item1 >> 1) & 1u);
+        if (p.na == 2)
+          mbar_wait(&a_full[item1 & 1u], (item1 >> 1) & 1u);
+        else
+          mbar_wait(&a_full[0], item1 & 1u);
         ++item1;
       }
-      const uint32_t ab = (item1 - 1u) & 1u;
+      const uint32_t ab = p.na == 2 ? ((item1 - 1u) & 1u) : 0u;
       mbar_wait(&xb_full[xr.idx], xr.phase);
       tc_fence_after();
       const uint64_t adesc = sdesc(sA0 + ab * p.a_bytes, 128u, sbo_x);
       const uint64_t bdesc = sdesc(sXB0 + xr.idx * p.a_bytes, 128u, sbo_x);
       const uint32_t d = tS((int)b1);
       if (elect_one()) {
-        for (int k = 0; k < ksteps1; ++k)
+        for (int k = 0; k < ksteps1 && !(DBG && p.debug_mode == 3); ++k)
           mma_ss(d, adesc + (uint64_t)(16 * k), bdesc + (uint64_t)(16 * k), id1, k > 0);
-        tc_commit(&s_full[b1]);
-        tc_commit(&xb_empty[xr.idx]);
+        tc_commit(&s_full[cr.idx]);  // also releases XB / V slots (see producers)
         if (look.last_in_item()) tc_commit(&a_empty[ab]);
       }
       __syncwarp();
       xr.adv();
+      cr.adv();
       b1 = (b1 + 1u == (uint32_t)NS) ? 0u : b1 + 1u;
       look.next(p, items);
     };
@@ -447,11 +470,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_tc_kernel(const TcParams p) {
     cur.start(p, items);
     Ring pr, vr;
     pr.init(NS);
-    vr.init(p.sv);
-    uint32_t q = 0;
+    vr.init(2 * NS);
+    uint32_t q = 0, gt = 0;
     while (cur.valid) {
       mbar_wait(&p_full[pr.idx], pr.phase);
       tc_fence_after();
+      if (lane == 0) trace_ev<DBG>(p, gt, 0);
       const uint32_t ob = q & 1u;
       const bool fresh = cur.first_in_chunk();
       if (fresh) {
@@ -469,61 +493,76 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_tc_kernel(const TcParams p) {
       if (elect_one()) {
 #pragma unroll
         for (int m = 0; m < BN / 16; ++m) {
+          if (DBG && p.debug_mode == 2) break;
           const uint32_t ahi = abase + 32u * (m >> 1) + 8u * (m & 1);
           mma_ts(dO, ahi, bdesc + (uint64_t)(16 * m), id2, (fresh && m == 0) ? 0u : 1u);
           mma_ts(dO, ahi + 16u, bdesc + (uint64_t)(16 * m), id2h, 1u);
         }
-        tc_commit(&v_empty[vr.idx]);
         if (last) tc_commit(&o_full[ob]);
       }
       __syncwarp();
+      if (lane == 0) trace_ev<DBG>(p, gt, 1);
       if (last) ++q;
       pr.adv();
       vr.adv();
       if (look.valid) issue_gemm1();  // reuses this S buffer: ordered after this GEMM2
+      if (lane == 0) trace_ev<DBG>(p, gt, 2);
+      ++gt;
       cur.next(p, items);
     }
   } else if (warp >= 4 && warp < 12) {
     // ================= epilogue warpgroups =================
-    const int e = (warp - 4) >> 2;           // 0 or 1: tiles g = e (mod 2)
+    // WG e transforms tiles g = e (mod 2); the two groups run out of phase so
+    // each hides the other's TMEM / barrier latencies on the shared MUFU.
+    const int e = (warp - 4) >> 2;           // 0 or 1
     const int wq = warp & 3;                 // TMEM lane quarter
     const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
     TileIter ti;
     ti.start(p, items);
-    Ring er;
-    er.init(NS);
-    uint32_t g = 0;
+    Ring er;  // s_full ring (2NS)
+    er.init(2 * NS);
+    uint32_t bb = 0;  // S buffer of the current tile (g mod NS)
     const float L = p.L;
+    uint32_t gt = 0;
+    const bool tr = (wq == 0 && lane == 0);
     while (ti.valid) {
-      if ((int)(g & 1u) == e) {
-        const int b = (int)er.idx;
-        mbar_wait(&s_full[b], er.phase);
+      if ((int)(gt & 1u) == e) {
+        const int b = (int)bb;
+        if (tr) trace_ev<DBG>(p, gt, 3 + 2 * e);
+        mbar_wait(&s_full[er.idx], er.phase);
         tc_fence_after();
-        const uint32_t base = tS(b) + lane_off;
-        uint32_t ra[32], rb[32];
-        tmem_ld32(base, ra);
-        tmem_wait_ld();
-#pragma unroll
-        for (int c = 0; c < BN / 32; c += 2) {
-          // software pipeline: load chunk c+1 while transforming chunk c
-          uint32_t hi[16], lo[16];
-          tmem_ld32(base + 32 * (c + 1), rb);
-          transform_chunk<FAM>(ra, L, hi, lo);
-          tmem_st16(base + 32 * c, hi);
-          tmem_st16(base + 32 * c + 16, lo);
+        if (tr) trace_ev<DBG>(p, gt, 4 + 2 * e);
+        if (DBG && (p.debug_mode == 1 || p.debug_mode == 5)) {
+          tc_fence_before();
+          mbar_arrive(&p_full[b]);
+        } else {
+          const uint32_t base = tS(b) + lane_off;
+          uint32_t ra[32], rb[32], hi[16], lo[16];
+          tmem_ld32(base, ra);
           tmem_wait_ld();
-          if (c + 2 < BN / 32) tmem_ld32(base + 32 * (c + 2), ra);
-          transform_chunk<FAM>(rb, L, hi, lo);
-          tmem_st16(base + 32 * (c + 1), hi);
-          tmem_st16(base + 32 * (c + 1) + 16, lo);
-          if (c + 2 < BN / 32) tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < BN / 32; c += 2) {
+            // software pipeline: the next chunk's TMEM load overlaps this chunk's math
+            tmem_ld32(base + 32 * (c + 1), rb);
+            transform_chunk<FAM>(ra, L, hi, lo);
+            tmem_st16(base + 32 * c, hi);
+            tmem_st16(base + 32 * c + 16, lo);
+            tmem_wait_ld();
+            if (c + 2 < BN / 32) tmem_ld32(base + 32 * (c + 2), ra);
+            transform_chunk<FAM>(rb, L, hi, lo);
+            tmem_st16(base + 32 * (c + 1), hi);
+            tmem_st16(base + 32 * (c + 1) + 16, lo);
+            if (c + 2 < BN / 32) tmem_wait_ld();
+          }
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(&p_full[b]);
         }
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(&p_full[b]);
+        if (tr && e == 0) trace_ev<DBG>(p, gt, 7);
       }
-      ++g;
+      ++gt;
       er.adv();
+      bb = (bb + 1u == (uint32_t)NS) ? 0u : bb + 1u;
       ti.next(p, items);
     }
   } else if (warp >= 12) {
@@ -769,6 +808,9 @@ __global__ void reduce_partial_kernel(const double* __restrict__ partial, int sp
 
 // ------------------------------------------------------------------ host
 
+long long* g_trace = nullptr;  // debug hook (ncgp_debug_set_trace)
+int g_debug_mode = 0;          // debug hook (ncgp_debug_set_mode)
+
 int ka_of(int d) { return ((3 * d + 4) + 15) / 16 * 16; }
 int wp_of(int w) { return w <= 16 ? 16 : 32; }
 
@@ -822,7 +864,8 @@ bool tc_supported(int dtype, int d, int w_max) {
   // shared memory: 2 row tiles + >= 2 stages
   const int ka = ka_of(d);
   const size_t a = (size_t)BM * ka * 2;
-  return 4 * a + 4 * 2 * (size_t)wp_of(w_max) * BN * 2 + (size_t)wp_of(w_max) * BM * 8 + 1024 <=
+  return (1 + NS) * a + 2 * NS * 2 * (size_t)wp_of(w_max) * BN * 2 +
+             (size_t)wp_of(w_max) * BM * 8 + 1024 <=
          (size_t)SMEM_BUDGET;
 }
 
@@ -944,28 +987,21 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, void* out, int64_t
   p.out = static_cast<uint8_t*>(out) + r0 * ldo * (p.out_f64 ? 8 : 4);
   p.ldo = ldo;
   p.partial = op->partial;
-  // shared memory: 2 row tiles + XB ring + V ring + fp64 accumulators
-  const size_t fixed = 2 * (size_t)p.a_bytes + (size_t)wp * BM * 8 + 1024;
-  NCGP_CHECK_ARG(fixed + 2 * (size_t)p.a_bytes + 4 * (size_t)v_bytes <= (size_t)SMEM_BUDGET,
-                 NCGP_UNSUPPORTED, "shared memory too small for d=%d", op->d);
-  int sv = 4, sx = (int)((SMEM_BUDGET - fixed - 4 * (size_t)v_bytes) / p.a_bytes);
-  if (sx > 4) sx = 4;
-  if (sx < 2) {
-    sv = 2;
-    sx = 2;
-  } else {
-    // give leftover space to the V ring
-    const size_t left = SMEM_BUDGET - fixed - (size_t)sx * p.a_bytes;
-    sv = (int)std::min<size_t>(6, left / (2 * (size_t)v_bytes));
-  }
-  p.sx = sx;
-  p.sv = sv;
+  p.trace = g_trace;
+  p.debug_mode = g_debug_mode;
+  // shared memory: row tiles (double-buffered when it fits) + XB ring (NS)
+  // + V ring (2 NS) + fp64 accumulators
+  const size_t base_smem = (size_t)NS * p.a_bytes + (size_t)2 * NS * 2 * v_bytes +
+                           (size_t)wp * BM * 8 + 1024;
+  NCGP_CHECK_ARG(base_smem + p.a_bytes <= (size_t)SMEM_BUDGET, NCGP_UNSUPPORTED,
+                 "shared memory too small for d=%d", op->d);
+  p.na = (base_smem + 2 * (size_t)p.a_bytes <= (size_t)SMEM_BUDGET) ? 2 : 1;
   NCGP_CHECK_ARG((int64_t)p.splits * p.nloc * w * 8 <= (int64_t)(L.total - L.partial) ||
                      p.splits == 1,
                  NCGP_INVALID_INPUT, "partial workspace too small");
-  const size_t smem = 2 * (size_t)p.a_bytes + (size_t)sx * p.a_bytes + (size_t)sv * 2 * v_bytes +
-                      (size_t)wp * BM * sizeof(double) +
-                      (2 * sx + 2 * sv + 8 + 2 * NS) * sizeof(uint64_t) + 16;
+  const size_t smem = (size_t)p.na * p.a_bytes + (size_t)NS * p.a_bytes +
+                      (size_t)2 * NS * 2 * v_bytes + (size_t)wp * BM * sizeof(double) +
+                      (3 * NS + 8 + 3 * NS) * sizeof(uint64_t) + 16;
   const int64_t items = p.row_tiles * p.splits;
   const unsigned grid = (unsigned)std::min<int64_t>(items, op->sms);
   auto launch = [&](auto kern) -> int {
@@ -976,11 +1012,22 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, void* out, int64_t
     return NCGP_OK;
   };
   int rc;
-  if (op->family == NCGP_RBF)
-    rc = wp == 16 ? launch(kop_tc_kernel<NCGP_RBF, 16>) : launch(kop_tc_kernel<NCGP_RBF, 32>);
-  else
-    rc = wp == 16 ? launch(kop_tc_kernel<NCGP_MATERN32, 16>)
-                  : launch(kop_tc_kernel<NCGP_MATERN32, 32>);
+  const bool dbg = (g_trace != nullptr) || (g_debug_mode != 0);
+  if (op->family == NCGP_RBF) {
+    if (dbg)
+      rc = wp == 16 ? launch(kop_tc_kernel<NCGP_RBF, 16, true>)
+                    : launch(kop_tc_kernel<NCGP_RBF, 32, true>);
+    else
+      rc = wp == 16 ? launch(kop_tc_kernel<NCGP_RBF, 16, false>)
+                    : launch(kop_tc_kernel<NCGP_RBF, 32, false>);
+  } else {
+    if (dbg)
+      rc = wp == 16 ? launch(kop_tc_kernel<NCGP_MATERN32, 16, true>)
+                    : launch(kop_tc_kernel<NCGP_MATERN32, 32, true>);
+    else
+      rc = wp == 16 ? launch(kop_tc_kernel<NCGP_MATERN32, 16, false>)
+                    : launch(kop_tc_kernel<NCGP_MATERN32, 32, false>);
+  }
   if (rc != NCGP_OK) return rc;
   if (p.splits > 1) {
     const int64_t tot = p.nloc * w;
@@ -996,3 +1043,13 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, void* out, int64_t
 }
 
 }  // namespace ncgp
+
+extern "C" int ncgp_debug_set_trace(void* dev_buf) {
+  g_trace = static_cast<long long*>(dev_buf);
+  return NCGP_OK;
+}
+
+extern "C" int ncgp_debug_set_mode(int mode) {
+  g_debug_mode = mode;
+  return NCGP_OK;
+}

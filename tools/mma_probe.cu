@@ -107,6 +107,86 @@ __global__ void mufuprobe(int reps, float* sink, long long* out) {
   if (threadIdx.x == 0) out[0] = t1 - t0;
 }
 
+
+// the kernel's per-tile pattern: 8 x (TS N=2W, TS N=W) + 2 x SS N=128, rotating S buffers
+template <int W, int MODE>
+__global__ void patprobe(int tiles, long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint64_t bar2[3];
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
+    for (int i = 0; i < 3; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 100000;" ::"r"(su32(&bar2[i])));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) {
+    uint32_t h = (uint32_t)i * 2654435761u;
+    ((uint32_t*)smem)[i] = (MODE >= 5) ? ((h & 0x03ff03ffu) | 0x38003800u) : 0x3c003c00u;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tm = slot;
+  if (threadIdx.x == 0) {
+    const uint32_t a = su32(smem), b = su32(smem + 32768);
+    const uint64_t ad = sdesc(a, 128, 512), bd = sdesc(b, 128, 2048);
+    const uint32_t id2 = idesc(128, 2 * W), id2h = idesc(128, W), id1 = idesc(128, 128);
+    long long t0 = clock64();
+    for (int t = 0; t < tiles; ++t) {
+      const uint32_t S = tm + (t % 3) * 128, O = tm + 384;
+      if (MODE == 6 || MODE == 7) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (MODE == 7) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (MODE != 2)
+        for (int m = 0; m < 8; ++m) {
+          const uint32_t ahi = S + 32 * (m >> 1) + 8 * (m & 1);
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(O),
+                       "r"(ahi), "l"(bd + 16 * m), "r"(id2), "r"(1));
+          if (MODE != 1)
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(O),
+                         "r"(ahi + 16), "l"(bd + 16 * m), "r"(id2h), "r"(1));
+        }
+      if (MODE == 3 || MODE == 4)
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar2[0])));
+      const uint32_t S3 = tm + ((t + 3) % 3) * 128;
+      if (MODE == 7) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (MODE == 8) asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      for (int k = 0; k < 2; ++k)
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(S3),
+                     "l"(ad + 16 * k), "l"(ad + 16 * k + 2048), "r"(id1), "r"(k));
+      if (MODE == 3) {
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar2[1])));
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar2[2])));
+      }
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar)));
+    asm volatile("{\n\t.reg .pred P1;\n\tW:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n\t@!P1 bra W;\n\t}" ::"r"(su32(&bar)));
+    long long t1 = clock64();
+    out[0] = t1 - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm));
+}
+
+template <int W, int MODE>
+void runpat(long long* d, const char* name, int grid = 1) {
+  cudaFuncSetAttribute(patprobe<W, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70 * 1024);
+  patprobe<W, MODE><<<grid, 128, 70 * 1024>>>(2000, d);
+  long long h;
+  cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+  printf("pattern W=%d %-34s: %7.1f cycles/tile\n", W, name, (double)h / 2000);
+}
+
 template <int N, bool TS>
 void run(long long* d) {
   cudaFuncSetAttribute(probe<N, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70 * 1024);
@@ -132,6 +212,18 @@ int main() {
     double bytes = 4096.0 * warps * 32 * 32 * 4;
     printf("tcgen05.ld x32 with %2d warps: %.1f B/clk per SM\n", warps, bytes / mx);
   }
+  runpat<32, 0>(d, "8x(TS 64 + TS 32) + 2x SS128");
+  runpat<32, 1>(d, "8x(TS 64) + 2x SS128");
+  runpat<32, 2>(d, "2x SS128 only");
+  runpat<16, 0>(d, "8x(TS 32 + TS 16) + 2x SS128");
+  runpat<32, 3>(d, "pattern + 3 commits per tile");
+  runpat<32, 4>(d, "pattern + 1 commit per tile");
+  runpat<32, 6>(d, "pattern + 1 fence::after per tile");
+  runpat<32, 7>(d, "pattern + 3 fence::after per tile");
+  runpat<32, 8>(d, "pattern + 1 fence::before per tile");
+  runpat<32, 0>(d, "pattern, 148 CTAs, ones", 148);
+  runpat<32, 5>(d, "pattern, 1 CTA, random data", 1);
+  runpat<32, 5>(d, "pattern, 148 CTAs, random data", 148);
   float* sink;
   cudaMalloc(&sink, 4096 * 4);
   for (int th : {128, 256, 512, 1024}) {
