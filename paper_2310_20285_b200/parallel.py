@@ -1,0 +1,135 @@
+"""Row-block sharding of the kernel operator across the GPUs of one node.
+
+SURVEY.md 8(e): output rows of K V are independent.  Each rank keeps the full
+inputs X (replicated, <= 200 MB at cfg5), computes a contiguous, 128-aligned
+block of output rows with the fused kernel-matmul, and the blocks are
+all-gathered (NCCL over NVLink) so every rank holds the full product for the
+next solver step.  Solver state (v, r, s, z, d, Q, S, T) is replicated: the
+vector work is O(N C R) against the O(N^2) operator, and replication keeps
+every rank's control flow (tolerance / breakdown exits) identical without
+extra collectives.
+
+Because the operator plans its column splits on the *full* row count and
+flushes its fp32 partial sums at fixed global column boundaries, a row is
+reduced in exactly the same order on 1 or P GPUs: the sharded product is
+bitwise identical to the single-GPU one.
+
+The partition and gather logic takes the local compute as a callable so it
+is unit-tested on CPU with the ``gloo`` backend (tests/test_parallel_gloo.py).
+"""
+
+from __future__ import annotations
+
+from typing import Callable, Optional, Tuple
+
+import torch
+import torch.distributed as dist
+
+ROW_ALIGN = 128  # the tcgen05 operator's row tile
+
+
+def row_partition(n: int, world: int, rank: int, align: int = ROW_ALIGN) -> Tuple[int, int, int]:
+    """(row_begin, row_end, rows_per_rank) of ``rank``'s contiguous block.
+
+    Blocks are multiples of ``align`` rows (the last one may be short or
+    empty), so every block starts on a row-tile boundary.
+    """
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} / world {world}")
+    tiles = (n + align - 1) // align
+    per = (tiles + world - 1) // world * align
+    r0 = min(n, rank * per)
+    r1 = min(n, (rank + 1) * per)
+    return r0, r1, per
+
+
+class RowShardedOperator:
+    """y = K V with rows of K split across ranks and gathered with all_gather.
+
+    ``local_apply(V, out, row_begin, row_end)`` must write rows
+    [row_begin, row_end) of K V into ``out`` (an (n_rows, w) tensor); in
+    production it is :meth:`KernelOperator.apply` / :meth:`PriorOperator.apply`.
+    """
+
+    def __init__(self, n_rows: int, local_apply: Callable, group=None,
+                 dtype: torch.dtype = torch.float32, device=None):
+        self.n_rows = n_rows
+        self.local_apply = local_apply
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.r0, self.r1, self.per = row_partition(n_rows, self.world, self.rank)
+        self.dtype = dtype
+        self.device = device
+        self._bufs = {}
+
+    def _buffers(self, w: int, device):
+        key = (w, str(device))
+        b = self._bufs.get(key)
+        if b is None:
+            full = torch.empty((self.per * self.world, w), dtype=self.dtype, device=device)
+            local = torch.empty((self.per, w), dtype=self.dtype, device=device)
+            stage = torch.empty((self.n_rows, w), dtype=self.dtype, device=device)
+            b = (full, local, stage)
+            self._bufs[key] = b
+        return b
+
+    def apply(self, V: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        vec = V.dim() == 1
+        V2 = V.view(-1, 1) if vec else V
+        w = V2.shape[1]
+        full, local, stage = self._buffers(w, V2.device)
+        if self.world == 1:
+            dst = out.view(self.n_rows, w) if out is not None else torch.empty(
+                (self.n_rows, w), dtype=self.dtype, device=V2.device)
+            self.local_apply(V2, dst, 0, self.n_rows)
+            res = dst
+        else:
+            self.local_apply(V2, stage, self.r0, self.r1)
+            local.zero_()
+            local[: self.r1 - self.r0].copy_(stage[self.r0:self.r1])
+            dist.all_gather_into_tensor(full, local, group=self.group)
+            res = full[: self.n_rows]
+            if out is not None:
+                out.view(self.n_rows, w).copy_(res)
+                res = out.view(self.n_rows, w)
+            else:
+                res = res.clone()
+        return res.view(-1) if vec else res
+
+    __call__ = apply
+
+
+class ShardedPriorOperator:
+    """Drop-in for :class:`gp.PriorOperator` in ``fit(..., operator=...)``:
+    the block-diagonal prior product on CN vectors, row-sharded across the
+    ranks of ``group``."""
+
+    def __init__(self, prior, X, dtype=None, group=None):
+        from .gp import PriorOperator
+        self.inner = PriorOperator(prior, X, dtype=dtype)
+        self.C = self.inner.C
+        self.n_rows = self.inner.n_rows
+        self.dtype = self.inner.dtype
+        self.matvecs = 0
+        C = self.C
+
+        def local_apply(V, out, r0, r1):
+            self.inner.apply(V.reshape(-1), out=out.view(-1), row_begin=r0, row_end=r1)
+
+        self.sharded = RowShardedOperator(self.n_rows, local_apply, group=group,
+                                          dtype=self.dtype)
+        self._C = C
+
+    @property
+    def impl(self):
+        return self.inner.impl
+
+    def apply(self, v: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        flat = v.dim() == 1
+        V = v.reshape(self.n_rows, self._C)
+        res = self.sharded.apply(V, out=None if out is None else out.view(self.n_rows, self._C))
+        self.matvecs += 1
+        return res.reshape(-1) if flat else res
+
+    __call__ = apply

@@ -236,3 +236,19 @@ def test_posterior_large_width_path():
     specs = [("rbf", 1.0, 2.0)] * C
     ref = O.posterior_marginal_var(specs, X, Q, Xt)
     assert rel(P.posterior_marginal_var(b, Xt, dtype=F64), ref) < 1e-12
+
+
+def test_sharded_operator_single_rank_equals_plain():
+    from paper_2310_20285_b200.parallel import ShardedPriorOperator
+    g = golden("fit_cfg2s")
+    prior = P.MultiOutputPrior(kernels=(P.KernelSpec("rbf", 1.0, 2.0),) * 3)
+    plain = P.PriorOperator(prior, g["X"], dtype=F32)
+    sharded = ShardedPriorOperator(prior, g["X"], dtype=F32)
+    v = dev(np.random.default_rng(0).standard_normal(g["X"].shape[0] * 3), F32)
+    assert torch.equal(plain(v), sharded(v))
+    ds = P.Dataset(g["X"], g["y"], "class-index", 3)
+    lik = P.SoftmaxLikelihood(ds.targets, 3)
+    oc = P.OuterConfig(max_newton_steps=3, delta=0.01, inner_schedule=10, recycle=True)
+    b1, _ = P.fit(prior, ds, lik, oc, P.InnerConfig(max_iters=1), dtype=F32)
+    b2, _ = P.fit(prior, ds, lik, oc, P.InnerConfig(max_iters=1), dtype=F32, operator=sharded)
+    np.testing.assert_array_equal(b1.weights, b2.weights)
