@@ -180,9 +180,8 @@ def run_ours(args, rank, world, local_rank):
     Xd = torch.from_numpy(X).to(dev, torch.float32)
     Sd = torch.from_numpy(S).to(dev, torch.float32)
     op = KernelOperator(spec[0], spec[1], spec[2], Xd, w_max=w, impl=args.kop)
-    tiles = (n + 127) // 128
-    per = (tiles + world - 1) // world * 128
-    r0, r1 = min(n, rank * per), min(n, (rank + 1) * per)
+    from paper_2310_20285_b200.parallel import row_partition
+    r0, r1, per = row_partition(n, world, rank)
     out_full = torch.empty((per * world, w), dtype=torch.float32, device=dev)
     out_local = torch.empty((per, w), dtype=torch.float32, device=dev)
     local_out_view = torch.empty((n, w), dtype=torch.float32, device=dev)

@@ -88,7 +88,7 @@ int ncgp_kop_create(ncgp_kop** op, int impl, int family, double lengthscale,
                     void* stream);
 
 /* out[row_begin:row_end, :w] = K(Xr[row_begin:row_end], Xc) V.
- * row_begin must be a multiple of 128 unless it equals 0 (row sharding). */
+ * row_begin must be a multiple of 256 (a row-tile pair) for row sharding. */
 int ncgp_kop_apply(ncgp_kop* op, const void* V, int64_t ldv, int w,
                    void* out, int64_t ldo, int64_t row_begin,
                    int64_t row_end, void* stream);

@@ -1,20 +1,29 @@
 // K1 on tcgen05/TMEM: fused kernel-matmul  out = K(Xr, Xc) V  with K never
 // materialised (replaces the tile body of prior_matvec, gp.py:240-249).
 //
-// Dataflow per CTA (persistent, one CTA per SM, 16 warps):
-//   warp 0        producer: 1-D bulk copies (cp.async.bulk -> UBLKCP) of the
-//                 pre-packed row tile and of each column tile into a ring of
-//                 shared-memory stages (mbarrier complete_tx).
-//   warp 1        MMA issuer (one thread):
-//                   GEMM1  S[128x128] = XA_i . XB_j   (kind::f16, A,B in smem)
-//                   GEMM2  O[128xWP] += P . V_j       (kind::f16, A=P in TMEM)
-//   warps 4-7,    two epilogue warpgroups, alternating column tiles: TMEM->regs
-//   warps 8-11    (tcgen05.ld), kernel transform (one MUFU ex2 per pair for RBF,
-//                 sqrt+ex2 for Matern), fp16 hi/lo split, regs->TMEM (tcgen05.st)
-//                 over the S columns (P aliases S, as in FlashAttention-4).
+// One CTA pair (cluster of 2, cta_group::2 MMAs with M = 256) per two SMs;
+// each CTA owns a 128-row tile and both sweep the same column tiles.
+// Roles per CTA (16 warps):
+//   warp 0        producer: the CTA's row tile + its half of each XB column
+//                 tile (1-D bulk copies, cp.async.bulk -> UBLKCP).
+//   warp 3        producer: the CTA's half of each V column tile.
+//   warp 2        relay: forwards this CTA's copy completions to the leader
+//                 CTA's barriers (the MMA needs both halves).
+//   warp 1        (leader only) MMA issuer, whole warp in uniform registers:
+//                   GEMM1  S[256x128] = XA . XB^T        (kind::f16, SS)
+//                   GEMM2  O[256x2WP] += P_hi . [Vhi|Vlo] and O[:, :WP] += P_lo . Vhi
+//                                                         (kind::f16, A = P in TMEM)
+//   warps 4-11    two epilogue warpgroups, alternating column tiles:
+//                 TMEM -> regs, kernel transform (ex2 for RBF, sqrt + ex2 for
+//                 Matern), fp16 hi/lo split, regs -> TMEM over S (P aliases S).
 //   warps 12-15   correction warpgroup: drains O every CH column tiles into
-//                 fp64 registers (chunked fp32 -> fp64 accumulation), applies
-//                 the power-of-two scales and writes the output rows.
+//                 fp64 shared-memory accumulators, scales, writes rows.
+// cta_group::2 splits B by rows: CTA0 supplies B rows [0, N/2), CTA1 rows
+// [N/2, N), each at the same shared-memory offset (tools/mma2sm_layout.cu),
+// so CTA0 holds [XB rows 0-63 | Vhi | Vhi rows 0..WP/2) and CTA1
+// [XB rows 64-127 | Vlo | Vhi rows WP/2..WP).  A pair instruction costs the
+// same cycles as a single-CTA one (tools/mma2sm_probe.cu), halving the
+// tensor time per SM.
 //
 // Precision (hard part 2): the distance GEMM uses a 3-term fp16
 // split packed along K,  [u_hi u_lo u_hi a_hi a_lo 1 1] . [x_hi x_hi x_lo 1 1 b_hi b_lo],
@@ -23,7 +32,8 @@
 // per-pair FMAs are needed before the MUFU op.  The contraction uses the
 // 3-term fp16 split  P_hi V_hi + P_lo V_hi + P_hi V_lo  with kernel values
 // pre-scaled by 2^s and RHS columns by 2^e_c into fp16 range; fp32 tensor
-// accumulation is flushed to fp64 every CH*128 columns.
+// accumulation is flushed to fp64 every CH*128 columns at fixed global
+// column boundaries (reduction order independent of row sharding).
 #include <cuda_fp16.h>
 #include <math.h>
 #include <string.h>
@@ -34,12 +44,15 @@
 
 namespace {
 
-constexpr int BM = 128;          // rows per tile (MMA M)
-constexpr int BN = 128;          // columns per tile (MMA1 N, MMA2 K)
+constexpr int BM = 128;          // rows per CTA tile (a pair covers 256)
+constexpr int BN = 128;          // columns per tile (GEMM1 N, GEMM2 K)
 constexpr int CH = 16;           // column tiles per fp32 accumulation chunk
 constexpr int NTHREADS = 512;
 constexpr int SMEM_BUDGET = 225 * 1024;
 constexpr int TMEM_COLS = 512;
+constexpr int NS = 3;            // S/P buffers in TMEM (3 x 128 columns)
+constexpr int NR = 12;           // s_full ring: >= max wait lag (XB depth, V depth, 4)
+constexpr int TRACE_TILES = 256, TRACE_EV = 8;
 
 // ------------------------------------------------------------------ PTX
 
@@ -90,11 +103,34 @@ __device__ __forceinline__ void tc_fence_before() {
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+// Arrive (once) on the barrier at this smem offset in BOTH CTAs of the pair
+// when all previously issued tcgen05 ops of this thread have completed.
+__device__ __forceinline__ void tc_commit2(uint64_t* bar) {
   asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          smem_u32(bar))
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
       : "memory");
+}
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile(
+      "barrier.cluster.arrive.release.aligned;\n\t"
+      "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of `p` in the leader CTA (rank 0)
+__device__ __forceinline__ uint32_t leader_addr(const void* p) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_u32(p)));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
 }
 // D[tmem] (+)= A[smem] . B[smem]^T  (both K-major)
 __device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
@@ -102,7 +138,7 @@ __device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint3
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
@@ -112,7 +148,7 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint3
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
       "r"(a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
@@ -175,21 +211,26 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | ((uint64_t)1 << 46);
 }
-// Instruction descriptor: kind::f16, A/B = F16 (K-major), D = F32, M = 128.
+// Instruction descriptor: kind::f16, A/B = F16 (K-major), D = F32,
+// M = 256 (a CTA pair, 128 rows per CTA).
 __host__ __device__ constexpr uint32_t idesc_f16(int n) {
-  return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+  return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
 }
+
 
 struct TcParams {
   const uint8_t* xa_pack;
   const uint8_t* col_pack;
-  int64_t tile_stride;   // bytes between column tiles in col_pack
-  uint32_t a_bytes;      // one packed row tile (= one XB tile)
-  uint32_t v_bytes;      // one of Vhi / Vlo for a column tile
+  int64_t tile_stride;   // bytes between column-tile records
+  uint32_t rec_bytes;    // one CTA's half record (offset of CTA1's half)
+  uint32_t a_bytes;      // one packed 128-row tile
+  uint32_t xbh_bytes;    // half an XB tile (64 rows)
+  uint32_t v2_bytes;     // WP rows x 128 columns fp16 (GEMM2 B half, N = 2 WP)
+  uint32_t v3_bytes;     // WP/2 rows (GEMM2 B half, N = WP)
   int ka;                // K of GEMM1 (multiple of 16)
   int w;                 // real RHS width
-  int64_t rt0;           // first global row tile of this launch
-  int64_t row_tiles;     // local row tiles
+  int64_t rt0;           // first global row tile of this launch (even)
+  int64_t pairs;         // local row-tile pairs
   int64_t nloc;          // local rows
   int64_t col_tiles;
   int splits;
@@ -202,30 +243,37 @@ struct TcParams {
   int out_f64;
   double* partial;       // [splits][nloc][w] when splits > 1
   int na;                // row-tile buffers in shared memory (1 or 2)
-  long long* trace;      // debug: per-tile timestamps of CTA 0 (nullptr in production)
+  int sx, sv;            // XB ring depth (3 or 6), V ring depth (6 or 9)
+  long long* trace;      // debug: per-tile timestamps of cluster 0 (nullptr in production)
   int debug_mode;        // debug: 1 = epilogue skips TMEM traffic, 2 = no GEMM2, 3 = no GEMM1
 };
 
+template <bool DBG>
+__device__ __forceinline__ void trace_ev(const TcParams& p, uint32_t tile, int ev) {
+  if (DBG && p.trace != nullptr && blockIdx.x == 0 && tile < (uint32_t)TRACE_TILES)
+    p.trace[tile * TRACE_EV + ev] = clock64();
+}
+
 struct Item {
-  int rt, c0, c1;
+  int pp, c0, c1;  // row-tile pair, column-tile range
 };
 
 __device__ __forceinline__ Item item_of(const TcParams& p, int it) {
   Item r;
-  r.rt = it / p.splits;
-  const int sp = it - r.rt * p.splits;
+  r.pp = it / p.splits;
+  const int sp = it - r.pp * p.splits;
   r.c0 = sp * (int)p.tiles_per_split;
   r.c1 = min((int)p.col_tiles, r.c0 + (int)p.tiles_per_split);
   return r;
 }
 
-// Iterates the CTA's global column-tile sequence across its items.
+// Iterates the cluster's global column-tile sequence across its items.
 struct TileIter {
   int it, ct;
   Item cur;
   bool valid;
   __device__ __forceinline__ void start(const TcParams& p, int items) {
-    it = blockIdx.x;
+    it = (int)(blockIdx.x >> 1);
     valid = it < items;
     if (valid) {
       cur = item_of(p, it);
@@ -234,7 +282,7 @@ struct TileIter {
   }
   __device__ __forceinline__ void next(const TcParams& p, int items) {
     if (++ct >= cur.c1) {
-      it += gridDim.x;
+      it += (int)(gridDim.x >> 1);
       valid = it < items;
       if (valid) {
         cur = item_of(p, it);
@@ -278,15 +326,6 @@ __device__ __forceinline__ bool elect_one() {
   return pred != 0;
 }
 
-constexpr int NS = 3;  // S/P buffers in TMEM (3 x 128 columns)
-constexpr int TRACE_TILES = 256, TRACE_EV = 8;
-
-template <bool DBG>
-__device__ __forceinline__ void trace_ev(const TcParams& p, uint32_t tile, int ev) {
-  if (DBG && p.trace != nullptr && blockIdx.x == 0 && tile < (uint32_t)TRACE_TILES)
-    p.trace[tile * TRACE_EV + ev] = clock64();
-}
-
 // Kernel transform of one 32-column chunk: S (fp32 exponent argument) ->
 // P_hi / P_lo packed fp16 pairs.
 template <int FAM>
@@ -316,199 +355,222 @@ __device__ __forceinline__ void transform_chunk(const uint32_t (&r)[32], float L
 }
 
 template <int FAM, int WP, bool DBG>
-__global__ void __launch_bounds__(NTHREADS, 1) kop_tc_kernel(const TcParams p) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
+    kop_tc_kernel(const TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int items = (int)(p.row_tiles * p.splits);
+  const uint32_t rank = cta_rank();
+  const int items = (int)(p.pairs * p.splits);
 
-  // ---- shared-memory carve-up
-  const uint32_t vpair = 2 * p.v_bytes;                 // [Vhi ; Vlo]
-  uint8_t* sA = smem;                                   // na x a_bytes (row tiles)
-  uint8_t* sXB = sA + (size_t)p.na * p.a_bytes;         // NS x a_bytes
-  uint8_t* sV = sXB + (size_t)NS * p.a_bytes;           // 2NS x vpair
-  double* sAcc = reinterpret_cast<double*>(sV + (size_t)2 * NS * vpair);  // [WP][128]
+  // ---- shared-memory carve-up (identical offsets in both CTAs)
+  const uint32_t vslot = p.v2_bytes + p.v3_bytes;       // this CTA's V half
+  uint8_t* sA = smem;                                   // na x a_bytes (own row tile)
+  uint8_t* sXB = sA + (size_t)p.na * p.a_bytes;         // sx x xbh_bytes
+  uint8_t* sV = sXB + (size_t)p.sx * p.xbh_bytes;       // sv x vslot
+  double* sAcc = reinterpret_cast<double*>(sV + (size_t)p.sv * vslot);  // [WP][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sAcc + WP * BM);
-  uint64_t* xb_full = bars;             // [NS]
-  uint64_t* v_full = xb_full + NS;      // [2NS]
-  uint64_t* a_full = v_full + 2 * NS;   // [2]
-  uint64_t* a_empty = a_full + 2;       // [2]
-  uint64_t* s_full = a_empty + 2;       // [2NS], indexed by tile mod 2NS
-  uint64_t* p_full = s_full + 2 * NS;   // [NS]
-  uint64_t* o_full = p_full + NS;       // [2]
-  uint64_t* o_empty = o_full + 2;       // [2]
+  uint64_t* xb_land = bars;               // [6]   local copy completion
+  uint64_t* v_land = xb_land + 6;         // [9]   local copy completion
+  uint64_t* a_land = v_land + 9;          // [2]   local copy completion
+  uint64_t* xb_full = a_land + 2;         // [6]   leader: both halves landed (2 arrivals)
+  uint64_t* v_full = xb_full + 6;         // [9]   leader: both halves landed
+  uint64_t* a_full = v_full + 9;          // [2]   leader: both row tiles landed
+  uint64_t* a_empty = a_full + 2;         // [2]   both: row tile free (multicast commit)
+  uint64_t* s_full = a_empty + 2;         // [NR]  both: GEMM1 of a tile done (multicast)
+  uint64_t* p_full = s_full + NR;         // [NS]  leader: P written (8 warp arrivals)
+  uint64_t* o_full = p_full + NS;         // [2]   both: O chunk complete (multicast)
+  uint64_t* o_empty = o_full + 2;         // [2]   leader: O drained (8 warp arrivals)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NS; ++s) mbar_init(&xb_full[s], 1);
-    for (int s = 0; s < 2 * NS; ++s) mbar_init(&v_full[s], 1);
+    for (int s = 0; s < 6; ++s) {
+      mbar_init(&xb_land[s], 1);
+      mbar_init(&xb_full[s], 2);
+    }
+    for (int s = 0; s < 9; ++s) {
+      mbar_init(&v_land[s], 1);
+      mbar_init(&v_full[s], 2);
+    }
+    for (int s = 0; s < NR; ++s) mbar_init(&s_full[s], 1);
+    for (int s = 0; s < NS; ++s) mbar_init(&p_full[s], 8);
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&a_full[b], 1);
+      mbar_init(&a_land[b], 1);
+      mbar_init(&a_full[b], 2);
       mbar_init(&a_empty[b], 1);
       mbar_init(&o_full[b], 1);
-      mbar_init(&o_empty[b], 128);
+      mbar_init(&o_empty[b], 8);
     }
-    for (int b = 0; b < 2 * NS; ++b) mbar_init(&s_full[b], 1);
-    for (int b = 0; b < NS; ++b) mbar_init(&p_full[b], 128);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
                  "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   tc_fence_before();
   __syncthreads();
+  cluster_sync();  // barriers of both CTAs initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   // TMEM columns: S/P buffers [0, 384), O double buffer [384, 384 + 4 WP)
   auto tS = [&](int b) -> uint32_t { return tmem + (uint32_t)(b * BN); };
   auto tO = [&](int b) -> uint32_t { return tmem + (uint32_t)(NS * BN + b * 2 * WP); };
+  const int64_t half_off = (int64_t)rank * p.rec_bytes;   // this CTA's half of a record
 
-  if (warp == 0) {
-    // ================= producer: row tiles + XB ring =================
-    // Slot reuse is signalled by GEMM1 completions (s_full, one commit per tile):
-    // XB slot g mod NS is free once GEMM1(g - NS) completed, and V slot g mod 2NS
-    // once GEMM2(g - 2NS) did, which the in-order tensor pipe finishes before
-    // GEMM1(g - NS).  s_full has 2NS entries so no waiter can lag two phases.
+  if (warp == 0 || warp == 3) {
+    // ================= producers (lane 0) and relays (lane 1) =================
+    // Slot reuse is signalled by GEMM1 completions (s_full, one multicast commit
+    // per tile): XB slot g mod sx is free once GEMM1(g - sx) completed; V slot
+    // g mod sv once GEMM2(g - sv) did, which the in-order tensor pipe finishes
+    // before GEMM1(g - sv + NS).  s_full has NR >= max(sx, sv) entries so no
+    // waiter can lag two phases.  Relays forward this CTA's copy completions
+    // to the leader CTA's barriers (the MMA consumes both CTAs' halves).
+    const bool is_x = (warp == 0);
+    const uint32_t depth = is_x ? (uint32_t)p.sx : (uint32_t)p.sv;
+    const uint32_t lagt = is_x ? (uint32_t)p.sx : (uint32_t)(p.sv - NS);  // tile g - lagt
+    uint64_t* land = is_x ? xb_land : v_land;
+    uint64_t* full = is_x ? xb_full : v_full;
     if (lane == 0) {
       TileIter ti;
       ti.start(p, items);
-      Ring xr, sr;  // XB slot ring (NS); position of tile g - NS in the s_full ring
-      xr.init(NS);
-      sr.init(2 * NS);
+      Ring r, sr;
+      r.init(depth);
+      sr.init(NR);
       uint32_t nitem = 0, g = 0;
       while (ti.valid) {
-        if (ti.first_in_item()) {
+        if (is_x && ti.first_in_item()) {
           const uint32_t ab = p.na == 2 ? (nitem & 1u) : 0u;
           const uint32_t aph = p.na == 2 ? ((nitem >> 1) & 1u) : (nitem & 1u);
           mbar_wait(&a_empty[ab], aph ^ 1u);
-          mbar_expect_tx(&a_full[ab], p.a_bytes);
-          bulk_g2s(sA + ab * p.a_bytes, p.xa_pack + (p.rt0 + ti.cur.rt) * (int64_t)p.a_bytes,
-                   p.a_bytes, &a_full[ab]);
+          mbar_expect_tx(&a_land[ab], p.a_bytes);
+          const int64_t rt = p.rt0 + 2 * (int64_t)ti.cur.pp + rank;
+          bulk_g2s(sA + ab * p.a_bytes, p.xa_pack + rt * (int64_t)p.a_bytes, p.a_bytes,
+                   &a_land[ab]);
           ++nitem;
         }
-        if (g >= (uint32_t)NS) mbar_wait(&s_full[sr.idx], sr.phase);
-        if (DBG && p.debug_mode >= 4) {
-          mbar_arrive(&xb_full[xr.idx]);
+        if (g >= depth) mbar_wait(&s_full[sr.idx], sr.phase);
+        const int64_t src = (int64_t)ti.ct * p.tile_stride + half_off;
+        if (is_x) {
+          mbar_expect_tx(&land[r.idx], p.xbh_bytes);
+          bulk_g2s(sXB + (size_t)r.idx * p.xbh_bytes, p.col_pack + src, p.xbh_bytes,
+                   &land[r.idx]);
         } else {
-          mbar_expect_tx(&xb_full[xr.idx], p.a_bytes);
-          bulk_g2s(sXB + (size_t)xr.idx * p.a_bytes, p.col_pack + (int64_t)ti.ct * p.tile_stride,
-                   p.a_bytes, &xb_full[xr.idx]);
+          mbar_expect_tx(&land[r.idx], vslot);
+          bulk_g2s(sV + (size_t)r.idx * vslot, p.col_pack + src + p.xbh_bytes, vslot,
+                   &land[r.idx]);
         }
-        xr.adv();
-        if (g >= (uint32_t)NS) sr.adv();
+        r.adv();
+        if (g >= lagt) sr.adv();
         ++g;
         ti.next(p, items);
       }
-    }
-  } else if (warp == 3) {
-    // ================= producer: V ring =================
-    if (lane == 0) {
+    } else if (lane == 1) {
       TileIter ti;
       ti.start(p, items);
-      Ring vr, sr;  // V slot ring (2NS); position of tile g - NS in the s_full ring
-      vr.init(2 * NS);
-      sr.init(2 * NS);
-      uint32_t g = 0;
+      Ring r;
+      r.init(depth);
+      uint32_t nitem = 0;
       while (ti.valid) {
-        if (g >= (uint32_t)(2 * NS)) mbar_wait(&s_full[sr.idx], sr.phase);
-        if (DBG && p.debug_mode >= 4) {
-          mbar_arrive(&v_full[vr.idx]);
-        } else {
-          mbar_expect_tx(&v_full[vr.idx], vpair);
-          bulk_g2s(sV + (size_t)vr.idx * vpair,
-                   p.col_pack + (int64_t)ti.ct * p.tile_stride + p.a_bytes, vpair, &v_full[vr.idx]);
+        if (is_x && ti.first_in_item()) {
+          const uint32_t ab = p.na == 2 ? (nitem & 1u) : 0u;
+          const uint32_t aph = p.na == 2 ? ((nitem >> 1) & 1u) : (nitem & 1u);
+          mbar_wait(&a_land[ab], aph);
+          mbar_arrive_cluster(leader_addr(&a_full[ab]));
+          ++nitem;
         }
-        vr.adv();
-        if (g >= (uint32_t)NS) sr.adv();
-        ++g;
+        mbar_wait(&land[r.idx], r.phase);
+        mbar_arrive_cluster(leader_addr(&full[r.idx]));
+        r.adv();
         ti.next(p, items);
       }
     }
   } else if (warp == 1) {
-    // ================= MMA issuer (whole warp, one elected lane issues) =================
-    const uint32_t id1 = idesc_f16(BN), id2 = idesc_f16(2 * WP), id2h = idesc_f16(WP);
-    const uint32_t sbo_x = (uint32_t)(p.ka / 8) * 128u;
-    const int ksteps1 = p.ka / 16;
-    const uint32_t sA0 = smem_u32(sA), sXB0 = smem_u32(sXB), sV0 = smem_u32(sV);
-    TileIter look;  // tile whose GEMM1 is issued next
-    look.start(p, items);
-    Ring xr, cr;  // XB slot ring (NS); s_full ring (2NS)
-    xr.init(NS);
-    cr.init(2 * NS);
-    uint32_t b1 = 0, item1 = 0;
-    auto issue_gemm1 = [&]() {
-      if (look.first_in_item()) {
-        if (p.na == 2)
-          mbar_wait(&a_full[item1 & 1u], (item1 >> 1) & 1u);
-        else
-          mbar_wait(&a_full[0], item1 & 1u);
-        ++item1;
-      }
-      const uint32_t ab = p.na == 2 ? ((item1 - 1u) & 1u) : 0u;
-      mbar_wait(&xb_full[xr.idx], xr.phase);
-      tc_fence_after();
-      const uint64_t adesc = sdesc(sA0 + ab * p.a_bytes, 128u, sbo_x);
-      const uint64_t bdesc = sdesc(sXB0 + xr.idx * p.a_bytes, 128u, sbo_x);
-      const uint32_t d = tS((int)b1);
-      if (elect_one()) {
-        for (int k = 0; k < ksteps1 && !(DBG && p.debug_mode == 3); ++k)
-          mma_ss(d, adesc + (uint64_t)(16 * k), bdesc + (uint64_t)(16 * k), id1, k > 0);
-        tc_commit(&s_full[cr.idx]);  // also releases XB / V slots (see producers)
-        if (look.last_in_item()) tc_commit(&a_empty[ab]);
-      }
-      __syncwarp();
-      xr.adv();
-      cr.adv();
-      b1 = (b1 + 1u == (uint32_t)NS) ? 0u : b1 + 1u;
-      look.next(p, items);
-    };
-    for (int i = 0; i < NS && look.valid; ++i) issue_gemm1();
-    TileIter cur;
-    cur.start(p, items);
-    Ring pr, vr;
-    pr.init(NS);
-    vr.init(2 * NS);
-    uint32_t q = 0, gt = 0;
-    while (cur.valid) {
-      mbar_wait(&p_full[pr.idx], pr.phase);
-      tc_fence_after();
-      if (lane == 0) trace_ev<DBG>(p, gt, 0);
-      const uint32_t ob = q & 1u;
-      const bool fresh = cur.first_in_chunk();
-      if (fresh) {
-        mbar_wait(&o_empty[ob], ((q >> 1) & 1u) ^ 1u);
-        tc_fence_after();
-      }
-      mbar_wait(&v_full[vr.idx], vr.phase);
-      tc_fence_after();
-      // B = [Vhi ; Vlo] (2*WP rows, one K-major block): P_hi x [Vhi|Vlo] as one
-      // N = 2*WP instruction, then P_lo x Vhi accumulated onto the Vhi half.
-      const uint64_t bdesc = sdesc(sV0 + vr.idx * vpair, 128u, 2048u);
-      const uint32_t abase = tS((int)pr.idx);
-      const uint32_t dO = tO((int)ob);
-      const bool last = cur.last_in_chunk();
-      if (elect_one()) {
-#pragma unroll
-        for (int m = 0; m < BN / 16; ++m) {
-          if (DBG && p.debug_mode == 2) break;
-          const uint32_t ahi = abase + 32u * (m >> 1) + 8u * (m & 1);
-          mma_ts(dO, ahi, bdesc + (uint64_t)(16 * m), id2, (fresh && m == 0) ? 0u : 1u);
-          mma_ts(dO, ahi + 16u, bdesc + (uint64_t)(16 * m), id2h, 1u);
+    // ================= MMA issuer (leader CTA; whole warp, elected lane issues) =====
+    if (rank == 0) {
+      const uint32_t id1 = idesc_f16(BN), id2 = idesc_f16(2 * WP), id2h = idesc_f16(WP);
+      const uint32_t sbo_x = (uint32_t)(p.ka / 8) * 128u;
+      const int ksteps1 = p.ka / 16;
+      const uint32_t sA0 = smem_u32(sA), sXB0 = smem_u32(sXB), sV0 = smem_u32(sV);
+      TileIter look;  // tile whose GEMM1 is issued next
+      look.start(p, items);
+      Ring xr, cr;    // XB slot ring (sx); s_full ring (NR)
+      xr.init(p.sx);
+      cr.init(NR);
+      uint32_t b1 = 0, item1 = 0;
+      auto issue_gemm1 = [&]() {
+        if (look.first_in_item()) {
+          if (p.na == 2)
+            mbar_wait(&a_full[item1 & 1u], (item1 >> 1) & 1u);
+          else
+            mbar_wait(&a_full[0], item1 & 1u);
+          ++item1;
         }
-        if (last) tc_commit(&o_full[ob]);
+        const uint32_t ab = p.na == 2 ? ((item1 - 1u) & 1u) : 0u;
+        mbar_wait(&xb_full[xr.idx], xr.phase);
+        tc_fence_after();
+        const uint64_t adesc = sdesc(sA0 + ab * p.a_bytes, 128u, sbo_x);
+        const uint64_t bdesc = sdesc(sXB0 + xr.idx * p.xbh_bytes, 128u, sbo_x);
+        const uint32_t d = tS((int)b1);
+        if (elect_one()) {
+          for (int k = 0; k < ksteps1 && !(DBG && p.debug_mode == 3); ++k)
+            mma_ss(d, adesc + (uint64_t)(16 * k), bdesc + (uint64_t)(16 * k), id1, k > 0);
+          tc_commit2(&s_full[cr.idx]);  // also releases XB / V slots (see producers)
+          if (look.last_in_item()) tc_commit2(&a_empty[ab]);
+        }
+        __syncwarp();
+        xr.adv();
+        cr.adv();
+        b1 = (b1 + 1u == (uint32_t)NS) ? 0u : b1 + 1u;
+        look.next(p, items);
+      };
+      for (int i = 0; i < NS && look.valid; ++i) issue_gemm1();
+      TileIter cur;
+      cur.start(p, items);
+      Ring pr, vr;
+      pr.init(NS);
+      vr.init(p.sv);
+      uint32_t q = 0, gt = 0;
+      while (cur.valid) {
+        mbar_wait(&p_full[pr.idx], pr.phase);
+        tc_fence_after();
+        if (lane == 0) trace_ev<DBG>(p, gt, 0);
+        const uint32_t ob = q & 1u;
+        const bool fresh = cur.first_in_chunk();
+        if (fresh) {
+          mbar_wait(&o_empty[ob], ((q >> 1) & 1u) ^ 1u);
+          tc_fence_after();
+        }
+        mbar_wait(&v_full[vr.idx], vr.phase);
+        tc_fence_after();
+        // GEMM2: P_hi x [Vhi | Vlo] (N = 2 WP: CTA0 supplies Vhi, CTA1 Vlo), then
+        // P_lo x Vhi (N = WP: each CTA supplies half of Vhi's rows).
+        const uint64_t b2 = sdesc(sV0 + vr.idx * vslot, 128u, 2048u);
+        const uint64_t b3 = sdesc(sV0 + vr.idx * vslot + p.v2_bytes, 128u, 2048u);
+        const uint32_t abase = tS((int)pr.idx);
+        const uint32_t dO = tO((int)ob);
+        const bool last = cur.last_in_chunk();
+        if (elect_one()) {
+#pragma unroll
+          for (int m = 0; m < BN / 16; ++m) {
+            if (DBG && p.debug_mode == 2) break;
+            const uint32_t ahi = abase + 32u * (m >> 1) + 8u * (m & 1);
+            mma_ts(dO, ahi, b2 + (uint64_t)(16 * m), id2, (fresh && m == 0) ? 0u : 1u);
+            mma_ts(dO, ahi + 16u, b3 + (uint64_t)(16 * m), id2h, 1u);
+          }
+          if (last) tc_commit2(&o_full[ob]);
+        }
+        __syncwarp();
+        if (lane == 0) trace_ev<DBG>(p, gt, 1);
+        if (last) ++q;
+        pr.adv();
+        vr.adv();
+        if (look.valid) issue_gemm1();  // reuses this S buffer: ordered after this GEMM2
+        if (lane == 0) trace_ev<DBG>(p, gt, 2);
+        ++gt;
+        cur.next(p, items);
       }
-      __syncwarp();
-      if (lane == 0) trace_ev<DBG>(p, gt, 1);
-      if (last) ++q;
-      pr.adv();
-      vr.adv();
-      if (look.valid) issue_gemm1();  // reuses this S buffer: ordered after this GEMM2
-      if (lane == 0) trace_ev<DBG>(p, gt, 2);
-      ++gt;
-      cur.next(p, items);
     }
   } else if (warp >= 4 && warp < 12) {
     // ================= epilogue warpgroups =================
@@ -519,8 +581,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_tc_kernel(const TcParams p) {
     const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
     TileIter ti;
     ti.start(p, items);
-    Ring er;  // s_full ring (2NS)
-    er.init(2 * NS);
+    Ring er;  // s_full ring (NR)
+    er.init(NR);
     uint32_t bb = 0;  // S buffer of the current tile (g mod NS)
     const float L = p.L;
     uint32_t gt = 0;
@@ -532,10 +594,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_tc_kernel(const TcParams p) {
         mbar_wait(&s_full[er.idx], er.phase);
         tc_fence_after();
         if (tr) trace_ev<DBG>(p, gt, 4 + 2 * e);
-        if (DBG && (p.debug_mode == 1 || p.debug_mode == 5)) {
-          tc_fence_before();
-          mbar_arrive(&p_full[b]);
-        } else {
+        if (!(DBG && (p.debug_mode == 1 || p.debug_mode == 5))) {
           const uint32_t base = tS(b) + lane_off;
           uint32_t ra[32], rb[32], hi[16], lo[16];
           tmem_ld32(base, ra);
@@ -555,9 +614,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_tc_kernel(const TcParams p) {
             if (c + 2 < BN / 32) tmem_wait_ld();
           }
           tmem_wait_st();
-          tc_fence_before();
-          mbar_arrive(&p_full[b]);
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(leader_addr(&p_full[b]));
         if (tr && e == 0) trace_ev<DBG>(p, gt, 7);
       }
       ++gt;
@@ -592,12 +652,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_tc_kernel(const TcParams p) {
             acc[(16 * h + c) * BM] += (double)__uint_as_float(r[c]) + (double)__uint_as_float(t[c]);
         }
         tc_fence_before();
-        mbar_arrive(&o_empty[ob]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(leader_addr(&o_empty[ob]));
         ++q;
         if (ti.last_in_item()) {
-          const int64_t i = ti.cur.rt * BM + row;  // local row
+          const int64_t i = (2 * (int64_t)ti.cur.pp + rank) * BM + row;  // local row
           if (i < p.nloc) {
-            const int64_t sp = ti.it % p.splits;
+            const int64_t sp = ti.it % p.splits;  // once per item
             for (int c = 0; c < p.w; ++c) {
               const double v = ldexp(acc[c * BM], -(p.s_exp + __ldg(&p.col_exp[c])));
               if (p.splits > 1)
@@ -619,9 +680,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_tc_kernel(const TcParams p) {
   __syncwarp();
   tc_fence_before();
   __syncthreads();
+  cluster_sync();  // both CTAs done with TMEM / remote barriers
   tc_fence_after();
   if (warp == 2) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(TMEM_COLS));
   }
 }
@@ -646,13 +708,16 @@ __device__ __forceinline__ __half h_of(double v) { return __double2half(v); }
 // Writes the augmented rows of one operand into the canonical K-major
 // no-swizzle layout: tile | row-group g | k-chunk q | row r | k.
 // role 0 = row operand (A), role 1 = column operand (B).
+// Column operand tiles are split in two 64-row halves, one per CTA of a pair:
+// rows 0-63 at the record start, rows 64-127 at +half (CTA1's half record).
 template <typename T>
 __global__ void pack_x_kernel(const T* __restrict__ X, int64_t n, int d, int ka,
                               const double* __restrict__ mu, double alpha, double sign,
-                              double L, int role, uint8_t* __restrict__ pack, int64_t stride) {
+                              double L, int role, uint8_t* __restrict__ pack, int64_t stride,
+                              int64_t half, int64_t n_tiles) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int qn = ka / 8;
-  const int64_t rows = (n + BM - 1) / BM * BM;
+  const int64_t rows = n_tiles * BM;
   if (e >= rows * qn) return;
   const int64_t row = e / qn;
   const int q = (int)(e % qn);
@@ -698,7 +763,11 @@ __global__ void pack_x_kernel(const T* __restrict__ X, int64_t n, int d, int ka,
     }
   }
   const int g = r / 8, rr = r % 8;
-  uint8_t* dst = pack + tile * stride + ((int64_t)(g * qn + q) * 8 + rr) * 16;
+  uint8_t* dst;
+  if (role == 0)
+    dst = pack + tile * stride + ((int64_t)(g * qn + q) * 8 + rr) * 16;
+  else
+    dst = pack + tile * stride + (g >= 8 ? half : 0) + ((int64_t)((g & 7) * qn + q) * 8 + rr) * 16;
   uint4 val;
   val.x = out[0] | ((uint32_t)out[1] << 16);
   val.y = out[2] | ((uint32_t)out[3] << 16);
@@ -759,13 +828,15 @@ __global__ void col_exp_kernel(const unsigned int* __restrict__ bits, int w, int
   col_exp[c] = e;
 }
 
-// V (n x w, row stride ldv) -> per column tile [Vhi | Vlo], each a K-major
-// no-swizzle (WP x 128) fp16 block: c-group g | j-chunk q | row c%8 | j%8.
+// V (n x w, row stride ldv) -> per column tile and CTA half: B2 (GEMM2 B rows
+// for N = 2 WP: CTA0 = Vhi, CTA1 = Vlo) then B3 (N = WP: CTA0 = Vhi rows
+// [0, WP/2), CTA1 = Vhi rows [WP/2, WP)).  Each block is K-major no-swizzle:
+// c-group g | j-chunk q | row c%8 | j%8 (SBO = 2048 B).
 template <typename T>
 __global__ void pack_v_kernel(const T* __restrict__ V, int64_t ldv, int64_t n, int w, int wp,
                               const int* __restrict__ col_exp, uint8_t* __restrict__ col_pack,
-                              int64_t tile_stride, uint32_t xb_bytes, uint32_t v_bytes,
-                              int64_t col_tiles) {
+                              int64_t tile_stride, int64_t half, uint32_t xbh_bytes,
+                              uint32_t v2_bytes, int64_t col_tiles) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t chunks = col_tiles * (BN / 8);
   if (e >= chunks * wp) return;
@@ -785,15 +856,21 @@ __global__ void pack_v_kernel(const T* __restrict__ V, int64_t ldv, int64_t n, i
     lo[k] = __half_as_ushort(__float2half_rn(v - __half2float(h)));
   }
   const int g = c / 8, rr = c % 8;
-  uint8_t* base = col_pack + tile * tile_stride + xb_bytes;
-  const int64_t off = ((int64_t)(g * (BN / 8) + q) * 8 + rr) * 16;
+  uint8_t* rec = col_pack + tile * tile_stride + xbh_bytes;
+  const int64_t in_blk = ((int64_t)q * 8 + rr) * 16;
   uint4 a, b;
   a.x = hi[0] | ((uint32_t)hi[1] << 16); a.y = hi[2] | ((uint32_t)hi[3] << 16);
   a.z = hi[4] | ((uint32_t)hi[5] << 16); a.w = hi[6] | ((uint32_t)hi[7] << 16);
   b.x = lo[0] | ((uint32_t)lo[1] << 16); b.y = lo[2] | ((uint32_t)lo[3] << 16);
   b.z = lo[4] | ((uint32_t)lo[5] << 16); b.w = lo[6] | ((uint32_t)lo[7] << 16);
-  *reinterpret_cast<uint4*>(base + off) = a;
-  *reinterpret_cast<uint4*>(base + v_bytes + off) = b;
+  // B2: CTA0 <- Vhi, CTA1 <- Vlo, c-group g at g * 2048
+  *reinterpret_cast<uint4*>(rec + (int64_t)g * 2048 + in_blk) = a;
+  *reinterpret_cast<uint4*>(rec + half + (int64_t)g * 2048 + in_blk) = b;
+  // B3: Vhi c-groups split between the CTAs
+  const int gh = wp / 16;  // c-groups per CTA in B3
+  const int cta = g / gh;
+  *reinterpret_cast<uint4*>(rec + (cta ? half : 0) + v2_bytes + (int64_t)(g - cta * gh) * 2048 +
+                            in_blk) = a;
 }
 
 template <typename T>
@@ -816,13 +893,13 @@ int wp_of(int w) { return w <= 16 ? 16 : 32; }
 
 struct Layout {
   size_t mu, guard, colexp, bits, xa, col, partial, total;
-  uint32_t a_bytes, v_bytes;
+  uint32_t a_bytes, xbh_bytes, rec_bytes;
   int64_t tile_stride, row_tiles, col_tiles;
 };
 
-int splits_for(int64_t row_tiles, int64_t col_tiles, int sms) {
-  if (row_tiles >= 2 * sms) return 1;
-  int64_t s = (2 * sms + row_tiles - 1) / row_tiles;
+int splits_for(int64_t pairs, int64_t col_tiles, int clusters) {
+  if (pairs >= 2 * clusters) return 1;
+  int64_t s = (2 * clusters + pairs - 1) / pairs;
   if (s > col_tiles) s = col_tiles;
   return (int)(s < 1 ? 1 : s);
 }
@@ -832,10 +909,12 @@ Layout layout_of(int64_t n_rows, int64_t n_cols, int d, int w_max, int sms) {
   const int ka = ka_of(d);
   const int wpm = wp_of(w_max);
   L.a_bytes = (uint32_t)(BM * ka * 2);
-  L.v_bytes = (uint32_t)(wpm * BN * 2);
-  L.row_tiles = (n_rows + BM - 1) / BM;
+  L.xbh_bytes = L.a_bytes / 2;
+  const uint32_t v2 = (uint32_t)(wpm * BN * 2), v3 = v2 / 2;
+  L.rec_bytes = L.xbh_bytes + v2 + v3;
+  L.row_tiles = ((n_rows + BM - 1) / BM + 1) / 2 * 2;  // whole pairs
   L.col_tiles = (n_cols + BN - 1) / BN;
-  L.tile_stride = (int64_t)L.a_bytes + 2 * L.v_bytes;
+  L.tile_stride = 2 * (int64_t)L.rec_bytes;
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
@@ -854,6 +933,12 @@ Layout layout_of(int64_t n_rows, int64_t n_cols, int d, int w_max, int sms) {
   return L;
 }
 
+size_t smem_bytes(uint32_t a_bytes, int wp, int na, int sx, int sv) {
+  const size_t v2 = (size_t)wp * BN * 2, v3 = v2 / 2;
+  return (size_t)na * a_bytes + (size_t)sx * (a_bytes / 2) + (size_t)sv * (v2 + v3) +
+         (size_t)wp * BM * 8 + (2 * 6 + 2 * 9 + 10 + NR + NS) * sizeof(uint64_t) + 16 + 1024;
+}
+
 }  // namespace
 
 namespace ncgp {
@@ -861,12 +946,7 @@ namespace ncgp {
 bool tc_supported(int dtype, int d, int w_max) {
   if (dtype != NCGP_F32) return false;
   if (d < 1 || d > 64 || w_max < 1 || w_max > 32) return false;
-  // shared memory: 2 row tiles + >= 2 stages
-  const int ka = ka_of(d);
-  const size_t a = (size_t)BM * ka * 2;
-  return (1 + NS) * a + 2 * NS * 2 * (size_t)wp_of(w_max) * BN * 2 +
-             (size_t)wp_of(w_max) * BM * 8 + 1024 <=
-         (size_t)SMEM_BUDGET;
+  return smem_bytes((uint32_t)(BM * ka_of(d) * 2), wp_of(w_max), 1, 3, 6) <= (size_t)SMEM_BUDGET;
 }
 
 size_t tc_workspace_bytes(int64_t n_rows, int64_t n_cols, int d, int w_max) {
@@ -907,13 +987,15 @@ int tc_prepare(ncgp_kop* op, cudaStream_t st) {
   {
     const int64_t tot = L.row_tiles * BM * qn;
     pack_x_kernel<float><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
-        Xr, op->n_rows, op->d, op->ka, mu, alpha, sign, Lc, 0, op->xa_pack, L.a_bytes);
+        Xr, op->n_rows, op->d, op->ka, mu, alpha, sign, Lc, 0, op->xa_pack, L.a_bytes, 0,
+        L.row_tiles);
     NCGP_LAUNCHED();
   }
   {
     const int64_t tot = L.col_tiles * BN * qn;
     pack_x_kernel<float><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
-        Xc, op->n_cols, op->d, op->ka, mu, alpha, sign, Lc, 1, op->col_pack, L.tile_stride);
+        Xc, op->n_cols, op->d, op->ka, mu, alpha, sign, Lc, 1, op->col_pack, L.tile_stride,
+        L.rec_bytes, L.col_tiles);
     NCGP_LAUNCHED();
   }
   // precision guard: the expanded distance loses ~2^-22 |x~|^2 absolute
@@ -939,8 +1021,8 @@ int tc_prepare(ncgp_kop* op, cudaStream_t st) {
 
 int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, void* out, int64_t ldo, int64_t r0,
              int64_t r1, cudaStream_t st) {
-  NCGP_CHECK_ARG(r0 % BM == 0, NCGP_DIMENSION_MISMATCH,
-                 "row_begin must be a multiple of %d for the tcgen05 operator", BM);
+  NCGP_CHECK_ARG(r0 % (2 * BM) == 0, NCGP_DIMENSION_MISMATCH,
+                 "row_begin must be a multiple of %d for the tcgen05 operator", 2 * BM);
   const Layout L = layout_of(op->n_rows, op->n_cols, op->d, op->w_max, op->sms);
   const int wp = wp_of(w);
   int* col_exp = reinterpret_cast<int*>(op->ws + L.colexp);
@@ -954,29 +1036,33 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, void* out, int64_t
     col_exp_kernel<<<1, 64, 0, st>>>(bits, w, wp, col_exp);
     NCGP_LAUNCHED();
   }
-  const uint32_t v_bytes = (uint32_t)(wp * BN * 2);
+  const uint32_t v2 = (uint32_t)(wp * BN * 2);
   {
     const int64_t tot = op->col_tiles * (BN / 8) * wp;
     pack_v_kernel<float><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
-        Vf, ldv, op->n_cols, w, wp, col_exp, op->col_pack, L.tile_stride, L.a_bytes, v_bytes,
-        op->col_tiles);
+        Vf, ldv, op->n_cols, w, wp, col_exp, op->col_pack, L.tile_stride, L.rec_bytes,
+        L.xbh_bytes, v2, op->col_tiles);
     NCGP_LAUNCHED();
   }
   TcParams p{};
   p.xa_pack = op->xa_pack;
   p.col_pack = op->col_pack;
   p.tile_stride = L.tile_stride;
+  p.rec_bytes = L.rec_bytes;
   p.a_bytes = L.a_bytes;
-  p.v_bytes = v_bytes;
+  p.xbh_bytes = L.xbh_bytes;
+  p.v2_bytes = v2;
+  p.v3_bytes = v2 / 2;
   p.ka = op->ka;
   p.w = w;
   p.rt0 = r0 / BM;
   p.nloc = r1 - r0;
-  p.row_tiles = (p.nloc + BM - 1) / BM;
+  p.pairs = (p.nloc + 2 * BM - 1) / (2 * BM);
   p.col_tiles = op->col_tiles;
   // splits depend on the operator's full row count only, so every row is
   // reduced in the same order whichever row range (shard) is launched
-  p.splits = splits_for(op->row_tiles, p.col_tiles, op->sms);
+  const int clusters = std::max(1, op->sms / 2);
+  p.splits = splits_for(op->row_tiles / 2, p.col_tiles, clusters);
   p.tiles_per_split = (p.col_tiles + p.splits - 1) / p.splits;
   p.splits = (int)((p.col_tiles + p.tiles_per_split - 1) / p.tiles_per_split);
   const int s_exp = (int)lround(log2(op->k_scale));
@@ -989,21 +1075,26 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, void* out, int64_t
   p.partial = op->partial;
   p.trace = g_trace;
   p.debug_mode = g_debug_mode;
-  // shared memory: row tiles (double-buffered when it fits) + XB ring (NS)
-  // + V ring (2 NS) + fp64 accumulators
-  const size_t base_smem = (size_t)NS * p.a_bytes + (size_t)2 * NS * 2 * v_bytes +
-                           (size_t)wp * BM * 8 + 1024;
-  NCGP_CHECK_ARG(base_smem + p.a_bytes <= (size_t)SMEM_BUDGET, NCGP_UNSUPPORTED,
-                 "shared memory too small for d=%d", op->d);
-  p.na = (base_smem + 2 * (size_t)p.a_bytes <= (size_t)SMEM_BUDGET) ? 2 : 1;
+  // deepest rings that fit: (na, sx, sv) from (2, 6, 9) down to (1, 3, 6)
+  {
+    const int cand[][3] = {{2, 6, 9}, {2, 6, 6}, {2, 3, 9}, {2, 3, 6}, {1, 6, 6}, {1, 3, 6}};
+    bool ok = false;
+    for (auto& c : cand)
+      if (smem_bytes(p.a_bytes, wp, c[0], c[1], c[2]) <= (size_t)SMEM_BUDGET) {
+        p.na = c[0];
+        p.sx = c[1];
+        p.sv = c[2];
+        ok = true;
+        break;
+      }
+    NCGP_CHECK_ARG(ok, NCGP_UNSUPPORTED, "shared memory too small for d=%d", op->d);
+  }
   NCGP_CHECK_ARG((int64_t)p.splits * p.nloc * w * 8 <= (int64_t)(L.total - L.partial) ||
                      p.splits == 1,
                  NCGP_INVALID_INPUT, "partial workspace too small");
-  const size_t smem = (size_t)p.na * p.a_bytes + (size_t)NS * p.a_bytes +
-                      (size_t)2 * NS * 2 * v_bytes + (size_t)wp * BM * sizeof(double) +
-                      (3 * NS + 8 + 3 * NS) * sizeof(uint64_t) + 16;
-  const int64_t items = p.row_tiles * p.splits;
-  const unsigned grid = (unsigned)std::min<int64_t>(items, op->sms);
+  const size_t smem = smem_bytes(p.a_bytes, wp, p.na, p.sx, p.sv);
+  const int64_t items = p.pairs * p.splits;
+  const unsigned grid = 2u * (unsigned)std::min<int64_t>(items, clusters);
   auto launch = [&](auto kern) -> int {
     NCGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));

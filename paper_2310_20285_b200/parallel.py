@@ -25,7 +25,7 @@ from typing import Callable, Optional, Tuple
 import torch
 import torch.distributed as dist
 
-ROW_ALIGN = 128  # the tcgen05 operator's row tile
+ROW_ALIGN = 256  # the tcgen05 operator's row-tile pair (2 x 128 rows)
 
 
 def row_partition(n: int, world: int, rank: int, align: int = ROW_ALIGN) -> Tuple[int, int, int]:

@@ -23,8 +23,8 @@ def test_row_partition_covers_rows_once():
             seen = np.zeros(n, dtype=int)
             for r in range(world):
                 r0, r1, per = row_partition(n, world, r)
-                assert per % 128 == 0
-                assert r0 % 128 == 0 or r0 == n
+                assert per % 256 == 0
+                assert r0 % 256 == 0 or r0 == n
                 seen[r0:r1] += 1
             assert (seen == 1).all(), (n, world)
 
