@@ -51,8 +51,8 @@ constexpr int NTHREADS = 512;
 constexpr int SMEM_BUDGET = 225 * 1024;
 constexpr int TMEM_COLS = 512;
 constexpr int NS = 3;            // S/P buffers in TMEM (3 x 128 columns)
-constexpr int NR = 12;           // s_full ring: >= max wait lag (XB depth, V depth, 4)
-constexpr int TRACE_TILES = 256, TRACE_EV = 8;
+constexpr int NR = 12;           // s_full / rdy rings: >= max wait lag (XB depth, V depth, 4)
+constexpr int TRACE_TILES = 256, TRACE_EV = 12;
 
 // ------------------------------------------------------------------ PTX
 
@@ -70,8 +70,12 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifndef NCGP_WAIT_MODE
+#define NCGP_WAIT_MODE 0  // 0: try_wait + suspend hint, 1: try_wait (default limit), 2: test_wait spin
+#endif
 __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
+#if NCGP_WAIT_MODE == 0
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
@@ -79,6 +83,23 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
       : "memory");
+#elif NCGP_WAIT_MODE == 1
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+#else
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+#endif
   return ok != 0;
 }
 // Bounded wait: a pipeline bug traps (kernel error, ~17 s) instead of hanging the GPU.
@@ -245,7 +266,8 @@ struct TcParams {
   int na;                // row-tile buffers in shared memory (1 or 2)
   int sx, sv;            // XB ring depth (3 or 6), V ring depth (6 or 9)
   long long* trace;      // debug: per-tile timestamps of cluster 0 (nullptr in production)
-  int debug_mode;        // debug: 1 = epilogue skips TMEM traffic, 2 = no GEMM2, 3 = no GEMM1
+  int debug_mode;        // debug (timing only, wrong results): 1 = epilogue skips TMEM traffic,
+                         // 2 = no GEMM2, 3 = no GEMM1, 4 = no column copies (8: XB only, 9: V only)
 };
 
 template <bool DBG>
@@ -373,27 +395,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   uint64_t* xb_land = bars;               // [6]   local copy completion
   uint64_t* v_land = xb_land + 6;         // [9]   local copy completion
   uint64_t* a_land = v_land + 9;          // [2]   local copy completion
-  uint64_t* xb_full = a_land + 2;         // [6]   leader: both halves landed (2 arrivals)
-  uint64_t* v_full = xb_full + 6;         // [9]   leader: both halves landed
-  uint64_t* a_full = v_full + 9;          // [2]   leader: both row tiles landed
+  uint64_t* xb_pro = a_land + 2;          // [NS]  leader: XB of tiles 0..NS-1 landed (2 halves)
+  // rdy[g mod NR] (leader): everything step g of the MMA warp needs -- P(g)
+  // written (8 epilogue warps), V(g) landed (2 halves), XB(g + NS) landed (2
+  // halves) -- so the MMA warp waits once per step.  A wait issued behind
+  // in-flight tcgen05 ops stalls the tensor pipe ~130 cycles
+  // (tools/mma2sm_pattern.cu), so waits in the MMA warp are kept to a minimum.
+  uint64_t* rdy = xb_pro + NS;            // [NR]
+  uint64_t* a_full = rdy + NR;            // [2]   leader: both row tiles landed
   uint64_t* a_empty = a_full + 2;         // [2]   both: row tile free (multicast commit)
   uint64_t* s_full = a_empty + 2;         // [NR]  both: GEMM1 of a tile done (multicast)
-  uint64_t* p_full = s_full + NR;         // [NS]  leader: P written (8 warp arrivals)
-  uint64_t* o_full = p_full + NS;         // [2]   both: O chunk complete (multicast)
+  uint64_t* o_full = s_full + NR;         // [2]   both: O chunk complete (multicast)
   uint64_t* o_empty = o_full + 2;         // [2]   leader: O drained (8 warp arrivals)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 6; ++s) {
-      mbar_init(&xb_land[s], 1);
-      mbar_init(&xb_full[s], 2);
+    for (int s = 0; s < 6; ++s) mbar_init(&xb_land[s], 1);
+    for (int s = 0; s < 9; ++s) mbar_init(&v_land[s], 1);
+    for (int s = 0; s < NS; ++s) mbar_init(&xb_pro[s], 2);
+    for (int s = 0; s < NR; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&rdy[s], 8 + 2 + 2);
     }
-    for (int s = 0; s < 9; ++s) {
-      mbar_init(&v_land[s], 1);
-      mbar_init(&v_full[s], 2);
-    }
-    for (int s = 0; s < NR; ++s) mbar_init(&s_full[s], 1);
-    for (int s = 0; s < NS; ++s) mbar_init(&p_full[s], 8);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&a_land[b], 1);
       mbar_init(&a_full[b], 2);
@@ -431,7 +454,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     const uint32_t depth = is_x ? (uint32_t)p.sx : (uint32_t)p.sv;
     const uint32_t lagt = is_x ? (uint32_t)p.sx : (uint32_t)(p.sv - NS);  // tile g - lagt
     uint64_t* land = is_x ? xb_land : v_land;
-    uint64_t* full = is_x ? xb_full : v_full;
     if (lane == 0) {
       TileIter ti;
       ti.start(p, items);
@@ -452,7 +474,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         }
         if (g >= depth) mbar_wait(&s_full[sr.idx], sr.phase);
         const int64_t src = (int64_t)ti.ct * p.tile_stride + half_off;
-        if (is_x) {
+        if (DBG && (p.debug_mode == 4 || p.debug_mode == 5 || p.debug_mode == (is_x ? 8 : 9))) {
+          mbar_expect_tx(&land[r.idx], 0);  // timing only: no copy
+        } else if (is_x) {
           mbar_expect_tx(&land[r.idx], p.xbh_bytes);
           bulk_g2s(sXB + (size_t)r.idx * p.xbh_bytes, p.col_pack + src, p.xbh_bytes,
                    &land[r.idx]);
@@ -469,9 +493,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     } else if (lane == 1) {
       TileIter ti;
       ti.start(p, items);
-      Ring r;
+      Ring r, rr;
       r.init(depth);
-      uint32_t nitem = 0;
+      rr.init(NR);
+      uint32_t nitem = 0, g = 0;
       while (ti.valid) {
         if (is_x && ti.first_in_item()) {
           const uint32_t ab = p.na == 2 ? (nitem & 1u) : 0u;
@@ -481,25 +506,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           ++nitem;
         }
         mbar_wait(&land[r.idx], r.phase);
-        mbar_arrive_cluster(leader_addr(&full[r.idx]));
+        // V(g) -> rdy[g]; XB(t) -> rdy[t - NS] (prologue tiles: xb_pro[t])
+        if (!is_x)
+          mbar_arrive_cluster(leader_addr(&rdy[rr.idx]));
+        else if (g < (uint32_t)NS)
+          mbar_arrive_cluster(leader_addr(&xb_pro[g]));
+        else
+          mbar_arrive_cluster(leader_addr(&rdy[rr.idx]));
+        if (!is_x || g >= (uint32_t)NS) rr.adv();
         r.adv();
+        ++g;
         ti.next(p, items);
       }
+      // the last NS steps have no XB(g + NS): stand in for those arrivals
+      if (is_x)
+        for (uint32_t t = g < (uint32_t)NS ? (uint32_t)NS : g; t < g + (uint32_t)NS; ++t) {
+          mbar_arrive_cluster(leader_addr(&rdy[rr.idx]));
+          rr.adv();
+        }
     }
   } else if (warp == 1) {
     // ================= MMA issuer (leader CTA; whole warp, elected lane issues) =====
+    // The issuing warp is latency-bound (tools/issue_probe.cu: the bare MMA
+    // sequence of a step takes ~540 cycles), so the loop keeps all state as
+    // running descriptors / indices and spends as few instructions as possible
+    // between MMAs.
     if (rank == 0) {
       const uint32_t id1 = idesc_f16(BN), id2 = idesc_f16(2 * WP), id2h = idesc_f16(WP);
       const uint32_t sbo_x = (uint32_t)(p.ka / 8) * 128u;
       const int ksteps1 = p.ka / 16;
-      const uint32_t sA0 = smem_u32(sA), sXB0 = smem_u32(sXB), sV0 = smem_u32(sV);
-      TileIter look;  // tile whose GEMM1 is issued next
+      const uint64_t dA0 = sdesc(smem_u32(sA), 128u, sbo_x);
+      const uint64_t dX0 = sdesc(smem_u32(sXB), 128u, sbo_x);
+      const uint64_t dV0 = sdesc(smem_u32(sV), 128u, (uint32_t)(BN * 16));
+      const uint64_t astep = p.a_bytes >> 4, xstep = p.xbh_bytes >> 4, vstep = vslot >> 4;
+      const uint64_t xend = dX0 + (uint64_t)p.sx * xstep, vend = dV0 + (uint64_t)p.sv * vstep;
+      const uint64_t v3off = p.v2_bytes >> 4;
+      // GEMM1 state: tile `look`, its XB slot descriptor, S buffer, s_full entry
+      TileIter look;
       look.start(p, items);
-      Ring xr, cr;    // XB slot ring (sx); s_full ring (NR)
-      xr.init(p.sx);
-      cr.init(NR);
-      uint32_t b1 = 0, item1 = 0;
-      auto issue_gemm1 = [&]() {
+      uint64_t dx = dX0;
+      uint32_t s1 = 0, c1 = 0, item1 = 0, g1n = 0;
+      auto gemm1 = [&]() {
+        const bool li = look.last_in_item();
         if (look.first_in_item()) {
           if (p.na == 2)
             mbar_wait(&a_full[item1 & 1u], (item1 >> 1) & 1u);
@@ -507,66 +555,65 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             mbar_wait(&a_full[0], item1 & 1u);
           ++item1;
         }
-        const uint32_t ab = p.na == 2 ? ((item1 - 1u) & 1u) : 0u;
-        mbar_wait(&xb_full[xr.idx], xr.phase);
+        if (g1n < (uint32_t)NS) mbar_wait(&xb_pro[g1n], 0);  // later tiles: via rdy
         tc_fence_after();
-        const uint64_t adesc = sdesc(sA0 + ab * p.a_bytes, 128u, sbo_x);
-        const uint64_t bdesc = sdesc(sXB0 + xr.idx * p.xbh_bytes, 128u, sbo_x);
-        const uint32_t d = tS((int)b1);
+        const uint32_t ab = p.na == 2 ? ((item1 - 1u) & 1u) : 0u;
+        const uint64_t da = dA0 + ab * astep;
+        const uint32_t d = tmem + s1 * (uint32_t)BN;
         if (elect_one()) {
-          for (int k = 0; k < ksteps1 && !(DBG && p.debug_mode == 3); ++k)
-            mma_ss(d, adesc + (uint64_t)(16 * k), bdesc + (uint64_t)(16 * k), id1, k > 0);
-          tc_commit2(&s_full[cr.idx]);  // also releases XB / V slots (see producers)
-          if (look.last_in_item()) tc_commit2(&a_empty[ab]);
+          if (!(DBG && p.debug_mode == 3))
+            for (int k = 0; k < ksteps1; ++k)
+              mma_ss(d, da + (uint64_t)(16 * k), dx + (uint64_t)(16 * k), id1, k > 0);
+          tc_commit2(&s_full[c1]);  // also releases XB / V slots (see producers)
+          if (li) tc_commit2(&a_empty[ab]);
         }
         __syncwarp();
-        xr.adv();
-        cr.adv();
-        b1 = (b1 + 1u == (uint32_t)NS) ? 0u : b1 + 1u;
+        ++g1n;
+        c1 = (c1 + 1u == (uint32_t)NR) ? 0u : c1 + 1u;
+        s1 = (s1 + 1u == (uint32_t)NS) ? 0u : s1 + 1u;
+        dx += xstep;
+        if (dx == xend) dx = dX0;
         look.next(p, items);
       };
-      for (int i = 0; i < NS && look.valid; ++i) issue_gemm1();
+      for (int i = 0; i < NS && look.valid; ++i) gemm1();
+      // GEMM2 state: tile `cur`, its V slot descriptor, S buffer, rdy entry
       TileIter cur;
       cur.start(p, items);
-      Ring pr, vr;
-      pr.init(NS);
-      vr.init(p.sv);
-      uint32_t q = 0, gt = 0;
+      uint64_t dv = dV0;
+      uint32_t s2 = 0, r = 0, rph = 0, q = 0, gt = 0;
       while (cur.valid) {
-        mbar_wait(&p_full[pr.idx], pr.phase);
+        const bool fresh = cur.first_in_chunk(), last = cur.last_in_chunk();
+        if (lane == 0) trace_ev<DBG>(p, gt, 11);
+        mbar_wait(&rdy[r], rph);  // P(g), V(g) and XB(g + NS) all present
+        const uint32_t ob = q & 1u;
+        if (fresh) mbar_wait(&o_empty[ob], ((q >> 1) & 1u) ^ 1u);
         tc_fence_after();
         if (lane == 0) trace_ev<DBG>(p, gt, 0);
-        const uint32_t ob = q & 1u;
-        const bool fresh = cur.first_in_chunk();
-        if (fresh) {
-          mbar_wait(&o_empty[ob], ((q >> 1) & 1u) ^ 1u);
-          tc_fence_after();
-        }
-        mbar_wait(&v_full[vr.idx], vr.phase);
-        tc_fence_after();
         // GEMM2: P_hi x [Vhi | Vlo] (N = 2 WP: CTA0 supplies Vhi, CTA1 Vlo), then
         // P_lo x Vhi (N = WP: each CTA supplies half of Vhi's rows).
-        const uint64_t b2 = sdesc(sV0 + vr.idx * vslot, 128u, 2048u);
-        const uint64_t b3 = sdesc(sV0 + vr.idx * vslot + p.v2_bytes, 128u, 2048u);
-        const uint32_t abase = tS((int)pr.idx);
-        const uint32_t dO = tO((int)ob);
-        const bool last = cur.last_in_chunk();
+        const uint32_t a0 = tmem + s2 * (uint32_t)BN, dO = tO((int)ob);
         if (elect_one()) {
+          if (!(DBG && p.debug_mode == 2)) {
 #pragma unroll
-          for (int m = 0; m < BN / 16; ++m) {
-            if (DBG && p.debug_mode == 2) break;
-            const uint32_t ahi = abase + 32u * (m >> 1) + 8u * (m & 1);
-            mma_ts(dO, ahi, b2 + (uint64_t)(16 * m), id2, (fresh && m == 0) ? 0u : 1u);
-            mma_ts(dO, ahi + 16u, b3 + (uint64_t)(16 * m), id2h, 1u);
+            for (int m = 0; m < BN / 16; ++m) {
+              const uint32_t ahi = a0 + 32u * (m >> 1) + 8u * (m & 1);
+              mma_ts(dO, ahi, dv + (uint64_t)(16 * m), id2, (fresh && m == 0) ? 0u : 1u);
+              mma_ts(dO, ahi + 16u, dv + v3off + (uint64_t)(16 * m), id2h, 1u);
+            }
           }
           if (last) tc_commit2(&o_full[ob]);
         }
         __syncwarp();
         if (lane == 0) trace_ev<DBG>(p, gt, 1);
-        if (last) ++q;
-        pr.adv();
-        vr.adv();
-        if (look.valid) issue_gemm1();  // reuses this S buffer: ordered after this GEMM2
+        q += last ? 1u : 0u;
+        s2 = (s2 + 1u == (uint32_t)NS) ? 0u : s2 + 1u;
+        dv += vstep;
+        if (dv == vend) dv = dV0;
+        if (++r == (uint32_t)NR) {
+          r = 0;
+          rph ^= 1u;
+        }
+        if (look.valid) gemm1();  // reuses this S buffer: ordered after this GEMM2
         if (lane == 0) trace_ev<DBG>(p, gt, 2);
         ++gt;
         cur.next(p, items);
@@ -617,8 +664,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(leader_addr(&p_full[b]));
-        if (tr && e == 0) trace_ev<DBG>(p, gt, 7);
+        if (lane == 0) mbar_arrive_cluster(leader_addr(&rdy[er.idx]));
+        if (tr) trace_ev<DBG>(p, gt, e == 0 ? 7 : 10);
       }
       ++gt;
       er.adv();
@@ -936,7 +983,7 @@ Layout layout_of(int64_t n_rows, int64_t n_cols, int d, int w_max, int sms) {
 size_t smem_bytes(uint32_t a_bytes, int wp, int na, int sx, int sv) {
   const size_t v2 = (size_t)wp * BN * 2, v3 = v2 / 2;
   return (size_t)na * a_bytes + (size_t)sx * (a_bytes / 2) + (size_t)sv * (v2 + v3) +
-         (size_t)wp * BM * 8 + (2 * 6 + 2 * 9 + 10 + NR + NS) * sizeof(uint64_t) + 16 + 1024;
+         (size_t)wp * BM * 8 + (6 + 9 + 2 + NS + 2 * NR + 8) * sizeof(uint64_t) + 16 + 1024;
 }
 
 }  // namespace

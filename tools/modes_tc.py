@@ -13,12 +13,12 @@ for fam in ("rbf", "matern32"):
     X = torch.from_numpy(rng.standard_normal((n, 8))).float().cuda()
     S = torch.from_numpy(rng.standard_normal((n, 32))).float().cuda()
     op = KernelOperator(fam, 1.5, 1.0, X, w_max=32, impl="tcgen05")
-    for mode, name in ((0, "full"), (1, "no epilogue TMEM/MUFU"), (2, "no GEMM2"), (3, "no GEMM1"), (4, "no bulk copies"), (5, "no copies, no epilogue")):
+    for mode, name in ((0, "full"), (1, "no epilogue TMEM/MUFU"), (2, "no GEMM2"), (3, "no GEMM1"), (5, "no copies, no epilogue")):
         lib.ncgp_debug_set_mode(mode)
         op.apply(S); torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
         e0.record(); op.apply(S); e1.record(); torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
-        tiles = ((n + 127) // 128) ** 2 / 148
+        tiles = ((n + 127) // 128) ** 2 / 148  # per SM
         print(f"{fam:8s} mode {mode} {name:24s}: {ms:7.3f} ms  {ms*1e-3*1.965e9/tiles:7.0f} clk/tile")
     lib.ncgp_debug_set_mode(0)
