@@ -133,6 +133,14 @@ __device__ __forceinline__ void tc_commit2(uint64_t* bar) {
       "h"((uint16_t)3)
       : "memory");
 }
+// Same, but arriving only on the leader CTA's barrier.
+__device__ __forceinline__ void tc_commit2_leader(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)1)
+      : "memory");
+}
 __device__ __forceinline__ uint32_t cta_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -205,6 +213,20 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
 }
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+// wait::ld that also "defines" the destination registers of an in-flight
+// tcgen05.ld, so the compiler cannot copy them (e.g. across a loop back-edge)
+// before the data has landed.
+__device__ __forceinline__ void tmem_wait_ld(uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.wait::ld.sync.aligned;"
+      : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),
+        "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]),
+        "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]),
+        "+r"(r[21]), "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]),
+        "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+      :
+      : "memory");
 }
 __device__ __forceinline__ void tmem_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -407,7 +429,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   uint64_t* s_full = a_empty + 2;         // [NR]  both: GEMM1 of a tile done (multicast)
   uint64_t* o_full = s_full + NR;         // [2]   both: O chunk complete (multicast)
   uint64_t* o_empty = o_full + 2;         // [2]   leader: O drained (8 warp arrivals)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
+  uint64_t* g2done = o_empty + 2;         // [NR]  leader: GEMM2 of a step done (commit)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(g2done + NR);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < 6; ++s) mbar_init(&xb_land[s], 1);
@@ -415,6 +438,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     for (int s = 0; s < NS; ++s) mbar_init(&xb_pro[s], 2);
     for (int s = 0; s < NR; ++s) {
       mbar_init(&s_full[s], 1);
+      mbar_init(&g2done[s], 1);
       mbar_init(&rdy[s], 8 + 2 + 2);
     }
     for (int b = 0; b < 2; ++b) {
@@ -525,98 +549,111 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           rr.adv();
         }
     }
-  } else if (warp == 1) {
-    // ================= MMA issuer (leader CTA; whole warp, elected lane issues) =====
-    // The issuing warp is latency-bound (tools/issue_probe.cu: the bare MMA
-    // sequence of a step takes ~540 cycles), so the loop keeps all state as
-    // running descriptors / indices and spends as few instructions as possible
-    // between MMAs.
+  } else if (warp == 1 || warp == 2) {
+    // ================= MMA issuers (leader CTA; whole warp, elected lane issues) =====
+    // One thread issues a tcgen05.mma only every ~46 cycles and blocks once
+    // the ~7-deep tensor queue is full (tools/mma_queue_probe.cu), so the two
+    // GEMMs get their own issuing warps: warp 1 issues GEMM2 (16 MMAs per
+    // step), warp 2 issues GEMM1.  GEMM1(t) overwrites the S buffer GEMM2(t -
+    // NS) reads, so warp 2 waits for GEMM2(t - NS)'s completion (g2done) first.
     if (rank == 0) {
       const uint32_t id1 = idesc_f16(BN), id2 = idesc_f16(2 * WP), id2h = idesc_f16(WP);
-      const uint32_t sbo_x = (uint32_t)(p.ka / 8) * 128u;
-      const int ksteps1 = p.ka / 16;
-      const uint64_t dA0 = sdesc(smem_u32(sA), 128u, sbo_x);
-      const uint64_t dX0 = sdesc(smem_u32(sXB), 128u, sbo_x);
-      const uint64_t dV0 = sdesc(smem_u32(sV), 128u, (uint32_t)(BN * 16));
-      const uint64_t astep = p.a_bytes >> 4, xstep = p.xbh_bytes >> 4, vstep = vslot >> 4;
-      const uint64_t xend = dX0 + (uint64_t)p.sx * xstep, vend = dV0 + (uint64_t)p.sv * vstep;
-      const uint64_t v3off = p.v2_bytes >> 4;
-      // GEMM1 state: tile `look`, its XB slot descriptor, S buffer, s_full entry
-      TileIter look;
-      look.start(p, items);
-      uint64_t dx = dX0;
-      uint32_t s1 = 0, c1 = 0, item1 = 0, g1n = 0;
-      auto gemm1 = [&]() {
-        const bool li = look.last_in_item();
-        if (look.first_in_item()) {
-          if (p.na == 2)
-            mbar_wait(&a_full[item1 & 1u], (item1 >> 1) & 1u);
-          else
-            mbar_wait(&a_full[0], item1 & 1u);
-          ++item1;
-        }
-        if (g1n < (uint32_t)NS) mbar_wait(&xb_pro[g1n], 0);  // later tiles: via rdy
-        tc_fence_after();
-        const uint32_t ab = p.na == 2 ? ((item1 - 1u) & 1u) : 0u;
-        const uint64_t da = dA0 + ab * astep;
-        const uint32_t d = tmem + s1 * (uint32_t)BN;
-        if (elect_one()) {
-          if (!(DBG && p.debug_mode == 3))
-            for (int k = 0; k < ksteps1; ++k)
-              mma_ss(d, da + (uint64_t)(16 * k), dx + (uint64_t)(16 * k), id1, k > 0);
-          tc_commit2(&s_full[c1]);  // also releases XB / V slots (see producers)
-          if (li) tc_commit2(&a_empty[ab]);
-        }
-        __syncwarp();
-        ++g1n;
-        c1 = (c1 + 1u == (uint32_t)NR) ? 0u : c1 + 1u;
-        s1 = (s1 + 1u == (uint32_t)NS) ? 0u : s1 + 1u;
-        dx += xstep;
-        if (dx == xend) dx = dX0;
-        look.next(p, items);
-      };
-      for (int i = 0; i < NS && look.valid; ++i) gemm1();
-      // GEMM2 state: tile `cur`, its V slot descriptor, S buffer, rdy entry
-      TileIter cur;
-      cur.start(p, items);
-      uint64_t dv = dV0;
-      uint32_t s2 = 0, r = 0, rph = 0, q = 0, gt = 0;
-      while (cur.valid) {
-        const bool fresh = cur.first_in_chunk(), last = cur.last_in_chunk();
-        if (lane == 0) trace_ev<DBG>(p, gt, 11);
-        mbar_wait(&rdy[r], rph);  // P(g), V(g) and XB(g + NS) all present
-        const uint32_t ob = q & 1u;
-        if (fresh) mbar_wait(&o_empty[ob], ((q >> 1) & 1u) ^ 1u);
-        tc_fence_after();
-        if (lane == 0) trace_ev<DBG>(p, gt, 0);
-        // GEMM2: P_hi x [Vhi | Vlo] (N = 2 WP: CTA0 supplies Vhi, CTA1 Vlo), then
-        // P_lo x Vhi (N = WP: each CTA supplies half of Vhi's rows).
-        const uint32_t a0 = tmem + s2 * (uint32_t)BN, dO = tO((int)ob);
-        if (elect_one()) {
-          if (!(DBG && p.debug_mode == 2)) {
-#pragma unroll
-            for (int m = 0; m < BN / 16; ++m) {
-              const uint32_t ahi = a0 + 32u * (m >> 1) + 8u * (m & 1);
-              mma_ts(dO, ahi, dv + (uint64_t)(16 * m), id2, (fresh && m == 0) ? 0u : 1u);
-              mma_ts(dO, ahi + 16u, dv + v3off + (uint64_t)(16 * m), id2h, 1u);
+      if (warp == 2) {
+        // ---------------- GEMM1 issuer
+        const uint32_t sbo_x = (uint32_t)(p.ka / 8) * 128u;
+        const int ksteps1 = p.ka / 16;
+        const uint64_t dA0 = sdesc(smem_u32(sA), 128u, sbo_x);
+        const uint64_t dX0 = sdesc(smem_u32(sXB), 128u, sbo_x);
+        const uint64_t astep = p.a_bytes >> 4, xstep = p.xbh_bytes >> 4;
+        const uint64_t xend = dX0 + (uint64_t)p.sx * xstep;
+        TileIter look;
+        look.start(p, items);
+        uint64_t dx = dX0;
+        uint32_t s1 = 0, c1 = 0, item1 = 0, g1n = 0, gd = 0, gdph = 0;
+        while (look.valid) {
+          const bool li = look.last_in_item();
+          if (look.first_in_item()) {
+            if (p.na == 2)
+              mbar_wait(&a_full[item1 & 1u], (item1 >> 1) & 1u);
+            else
+              mbar_wait(&a_full[0], item1 & 1u);
+            ++item1;
+          }
+          if (g1n < (uint32_t)NS) {
+            mbar_wait(&xb_pro[g1n], 0);
+          } else {  // S buffer free; XB(t) landed (it is part of rdy(t - NS))
+            mbar_wait(&g2done[gd], gdph);
+            if (++gd == (uint32_t)NR) {
+              gd = 0;
+              gdph ^= 1u;
             }
           }
-          if (last) tc_commit2(&o_full[ob]);
+          tc_fence_after();
+          if (lane == 0) trace_ev<DBG>(p, g1n, 9);
+          const uint32_t ab = p.na == 2 ? ((item1 - 1u) & 1u) : 0u;
+          const uint64_t da = dA0 + ab * astep;
+          const uint32_t d = tmem + s1 * (uint32_t)BN;
+          if (elect_one()) {
+            if (!(DBG && p.debug_mode == 3))
+              for (int k = 0; k < ksteps1; ++k)
+                mma_ss(d, da + (uint64_t)(16 * k), dx + (uint64_t)(16 * k), id1, k > 0);
+            tc_commit2(&s_full[c1]);  // also releases XB / V slots (see producers)
+            if (li) tc_commit2(&a_empty[ab]);
+          }
+          __syncwarp();
+          if (lane == 0) trace_ev<DBG>(p, g1n, 2);
+          ++g1n;
+          c1 = (c1 + 1u == (uint32_t)NR) ? 0u : c1 + 1u;
+          s1 = (s1 + 1u == (uint32_t)NS) ? 0u : s1 + 1u;
+          dx += xstep;
+          if (dx == xend) dx = dX0;
+          look.next(p, items);
         }
-        __syncwarp();
-        if (lane == 0) trace_ev<DBG>(p, gt, 1);
-        q += last ? 1u : 0u;
-        s2 = (s2 + 1u == (uint32_t)NS) ? 0u : s2 + 1u;
-        dv += vstep;
-        if (dv == vend) dv = dV0;
-        if (++r == (uint32_t)NR) {
-          r = 0;
-          rph ^= 1u;
+      } else {
+        // ---------------- GEMM2 issuer
+        const uint64_t dV0 = sdesc(smem_u32(sV), 128u, (uint32_t)(BN * 16));
+        const uint64_t vstep = vslot >> 4, vend = dV0 + (uint64_t)p.sv * vstep;
+        const uint64_t v3off = p.v2_bytes >> 4;
+        TileIter cur;
+        cur.start(p, items);
+        uint64_t dv = dV0;
+        uint32_t s2 = 0, r = 0, rph = 0, q = 0, gt = 0;
+        while (cur.valid) {
+          const bool fresh = cur.first_in_chunk(), last = cur.last_in_chunk();
+          if (lane == 0) trace_ev<DBG>(p, gt, 11);
+          mbar_wait(&rdy[r], rph);  // P(g), V(g) (and XB(g + NS)) present
+          const uint32_t ob = q & 1u;
+          if (fresh) mbar_wait(&o_empty[ob], ((q >> 1) & 1u) ^ 1u);
+          tc_fence_after();
+          if (lane == 0) trace_ev<DBG>(p, gt, 0);
+          // GEMM2: P_hi x [Vhi | Vlo] (N = 2 WP: CTA0 supplies Vhi, CTA1 Vlo), then
+          // P_lo x Vhi (N = WP: each CTA supplies half of Vhi's rows).
+          const uint32_t a0 = tmem + s2 * (uint32_t)BN, dO = tO((int)ob);
+          if (elect_one()) {
+            if (!(DBG && p.debug_mode == 2)) {
+#pragma unroll
+              for (int m = 0; m < BN / 16; ++m) {
+                const uint32_t ahi = a0 + 32u * (m >> 1) + 8u * (m & 1);
+                mma_ts(dO, ahi, dv + (uint64_t)(16 * m), id2, (fresh && m == 0) ? 0u : 1u);
+                mma_ts(dO, ahi + 16u, dv + v3off + (uint64_t)(16 * m), id2h, 1u);
+              }
+            }
+            tc_commit2_leader(&g2done[r]);  // frees S buffer g for GEMM1(g + NS)
+            if (last) tc_commit2(&o_full[ob]);
+          }
+          __syncwarp();
+          if (lane == 0) trace_ev<DBG>(p, gt, 1);
+          q += last ? 1u : 0u;
+          s2 = (s2 + 1u == (uint32_t)NS) ? 0u : s2 + 1u;
+          dv += vstep;
+          if (dv == vend) dv = dV0;
+          if (++r == (uint32_t)NR) {
+            r = 0;
+            rph ^= 1u;
+          }
+          ++gt;
+          cur.next(p, items);
         }
-        if (look.valid) gemm1();  // reuses this S buffer: ordered after this GEMM2
-        if (lane == 0) trace_ev<DBG>(p, gt, 2);
-        ++gt;
-        cur.next(p, items);
       }
     }
   } else if (warp >= 4 && warp < 12) {
@@ -983,7 +1020,7 @@ Layout layout_of(int64_t n_rows, int64_t n_cols, int d, int w_max, int sms) {
 size_t smem_bytes(uint32_t a_bytes, int wp, int na, int sx, int sv) {
   const size_t v2 = (size_t)wp * BN * 2, v3 = v2 / 2;
   return (size_t)na * a_bytes + (size_t)sx * (a_bytes / 2) + (size_t)sv * (v2 + v3) +
-         (size_t)wp * BM * 8 + (6 + 9 + 2 + NS + 2 * NR + 8) * sizeof(uint64_t) + 16 + 1024;
+         (size_t)wp * BM * 8 + (6 + 9 + 2 + NS + 3 * NR + 8) * sizeof(uint64_t) + 16 + 1024;
 }
 
 }  // namespace

@@ -252,3 +252,40 @@ def test_sharded_operator_single_rank_equals_plain():
     b1, _ = P.fit(prior, ds, lik, oc, P.InnerConfig(max_iters=1), dtype=F32)
     b2, _ = P.fit(prior, ds, lik, oc, P.InnerConfig(max_iters=1), dtype=F32, operator=sharded)
     np.testing.assert_array_equal(b1.weights, b2.weights)
+
+
+def _cfg5_fixture():
+    import json
+    import os
+    from conftest import GOLDEN
+    p = os.path.join(GOLDEN, "cfg5_trajectory.json")
+    return json.load(open(p)) if os.path.exists(p) else {}
+
+
+@pytest.mark.parametrize("n", ["1500", "5000"])
+def test_fit_cfg5_trajectory_matches_oracle(n):
+    """cfg5 at reduced N, fp64: the Newton trajectory (inner iterations,
+    termination, |yhat| per step) and the mean-label accuracy follow the
+    oracle's step for step -- including the divergence of the reference's
+    undamped Newton iteration that cfg5 triggers from N ~ 5000 up
+    (tests/golden/make_cfg5_trajectory.py)."""
+    from paper_2310_20285_b200 import configs
+    ref = _cfg5_fixture().get(n)
+    if ref is None:
+        pytest.skip("fixture tests/golden/cfg5_trajectory.json lacks N=" + n)
+    c = configs.cfg5(n=int(n), n_test=2000)
+    prior = P.MultiOutputPrior(kernels=(P.KernelSpec(*c["kernel"]),) * 10)
+    ds = P.Dataset(c["X"], c["y"], "class-index", 10)
+    lik = P.SoftmaxLikelihood(ds.targets, 10)
+    belief, trace = P.fit(prior, ds, lik,
+                          P.OuterConfig(max_newton_steps=6, delta=0.01, inner_schedule=64,
+                                        recycle=True, compression_rank=256),
+                          P.InnerConfig(max_iters=1), policy_kind="residual", dtype=F64)
+    got = [(s.inner_iterations, s.inner_termination, s.pseudo_target_norm) for s in trace.steps]
+    want = [(s["iterations"], s["termination"], s["yhat_norm"]) for s in ref["steps"]]
+    assert [g[:2] for g in got] == [w[:2] for w in want]
+    for (_, _, a), (_, _, b) in zip(got, want):
+        assert abs(a - b) <= 1e-2 * abs(b), (a, b)
+    mean = P.posterior_mean(belief, c["X_test"][:500])
+    acc = float(np.mean(mean.argmax(1) == c["y_test"][:500]))
+    assert abs(acc - ref["accuracy_mean_500"]) <= 0.01

@@ -62,10 +62,10 @@ print("EPI: busy (go -> done)       ", st(done - go))
 print("EPI: done -> MMA p_ready     ", st(e[:, 0] - done))
 print("g1 issued(g) -> epi go(g+3)  ", st(t[lo + 3:hi + 3][:, [4, 6]].max(1) - e[:, 2]))
 
-if len(sys.argv) > 4:  # raw per-step dump (split epilogue: 3/4 = s_full wait start/end, 7 = rdy arrive)
+if len(sys.argv) > 4:  # raw per-step dump
     base = t[lo, 0]
-    print(" g   mma_pre  rdy_seen  g2_iss  g1_iss | epi_wait  epi_go  epi_done")
+    print(" g   g2_pre  rdy_seen  g2_iss  g1_iss | epiA_wait epiA_go epiA_done | epiB_wait epiB_go epiB_done")
     for g in range(lo, lo + int(sys.argv[4])):
         r = t[g]
-        print("%3d %8d %8d %7d %7d | %8d %7d %8d" % (g, r[11] - base, r[0] - base, r[1] - base,
-              r[2] - base, r[3] - base, r[4] - base, r[7] - base))
+        print("%3d %7d %8d %7d %7d | %8d %7d %8d | %8d %7d %8d" % (g, r[11] - base, r[0] - base, r[1] - base,
+              r[2] - base, r[3] - base, r[4] - base, r[7] - base, r[5] - base, r[6] - base, r[10] - base))
