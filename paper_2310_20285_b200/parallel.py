@@ -1,10 +1,10 @@
 """Row-block sharding of the kernel operator across the GPUs of one node.
 
 SURVEY.md 8(e): output rows of K V are independent.  Each rank keeps the full
-inputs X (replicated, <= 200 MB at cfg5), computes a contiguous, 128-aligned
-block of output rows with the fused kernel-matmul, and the blocks are
-all-gathered (NCCL over NVLink) so every rank holds the full product for the
-next solver step.  Solver state (v, r, s, z, d, Q, S, T) is replicated: the
+inputs X (replicated, <= 200 MB at cfg5), computes a contiguous, 256-aligned
+block of output rows with the fused kernel-matmul directly into its slice of
+the gather buffer, and the blocks are all-gathered in place (NCCL over
+NVLink) so every rank holds the full product for the next solver step.  Solver state (v, r, s, z, d, Q, S, T) is replicated: the
 vector work is O(N C R) against the O(N^2) operator, and replication keeps
 every rank's control flow (tolerance / breakdown exits) identical without
 extra collectives.
@@ -63,32 +63,31 @@ class RowShardedOperator:
         self.device = device
         self._bufs = {}
 
-    def _buffers(self, w: int, device):
+    def _buffer(self, w: int, device):
         key = (w, str(device))
-        b = self._bufs.get(key)
-        if b is None:
+        full = self._bufs.get(key)
+        if full is None:
             full = torch.empty((self.per * self.world, w), dtype=self.dtype, device=device)
-            local = torch.empty((self.per, w), dtype=self.dtype, device=device)
-            stage = torch.empty((self.n_rows, w), dtype=self.dtype, device=device)
-            b = (full, local, stage)
-            self._bufs[key] = b
-        return b
+            self._bufs[key] = full
+        return full
 
     def apply(self, V: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         vec = V.dim() == 1
         V2 = V.view(-1, 1) if vec else V
         w = V2.shape[1]
-        full, local, stage = self._buffers(w, V2.device)
         if self.world == 1:
             dst = out.view(self.n_rows, w) if out is not None else torch.empty(
                 (self.n_rows, w), dtype=self.dtype, device=V2.device)
             self.local_apply(V2, dst, 0, self.n_rows)
             res = dst
         else:
-            self.local_apply(V2, stage, self.r0, self.r1)
-            local.zero_()
-            local[: self.r1 - self.r0].copy_(stage[self.r0:self.r1])
-            dist.all_gather_into_tensor(full, local, group=self.group)
+            # rank r's rows [r0, r1) are rows [r * per, r * per + (r1 - r0)) of the
+            # gather buffer: the operator writes them in place and the gather
+            # runs in place (input = this rank's slice of the output)
+            full = self._buffer(w, V2.device)
+            self.local_apply(V2, full, self.r0, self.r1)
+            mine = full[self.rank * self.per:(self.rank + 1) * self.per]
+            dist.all_gather_into_tensor(full, mine, group=self.group)
             res = full[: self.n_rows]
             if out is not None:
                 out.view(self.n_rows, w).copy_(res)
@@ -115,7 +114,10 @@ class ShardedPriorOperator:
         C = self.C
 
         def local_apply(V, out, r0, r1):
-            self.inner.apply(V.reshape(-1), out=out.view(-1), row_begin=r0, row_end=r1)
+            # ``out`` may be the (per * world)-row gather buffer: rows >= n_rows
+            # are padding and never written
+            self.inner.apply(V.reshape(-1), out=out[: self.n_rows].reshape(-1),
+                             row_begin=r0, row_end=r1)
 
         self.sharded = RowShardedOperator(self.n_rows, local_apply, group=group,
                                           dtype=self.dtype)

@@ -289,3 +289,24 @@ def test_fit_cfg5_trajectory_matches_oracle(n):
     mean = P.posterior_mean(belief, c["X_test"][:500])
     acc = float(np.mean(mean.argmax(1) == c["y_test"][:500]))
     assert abs(acc - ref["accuracy_mean_500"]) <= 0.01
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_sharded_local_blocks_fill_gather_buffer(world):
+    """The per-rank blocks the sharded operator writes into its (per * world)-row
+    gather buffer (before the in-place all-gather) assemble the plain product
+    bitwise (the multi-rank path itself is covered with gloo on CPU)."""
+    from paper_2310_20285_b200.parallel import ShardedPriorOperator, row_partition
+    rng = np.random.default_rng(1)
+    n, C = 3000, 3
+    X = rng.standard_normal((n, 2))
+    prior = P.MultiOutputPrior(kernels=(P.KernelSpec("rbf", 1.0, 2.0),) * C)
+    plain = P.PriorOperator(prior, X, dtype=F32)
+    sharded = ShardedPriorOperator(prior, X, dtype=F32)
+    V = dev(rng.standard_normal((n, C)), F32)
+    per = row_partition(n, world, 0)[2]
+    full = torch.full((per * world, C), float("nan"), dtype=F32, device="cuda")
+    for r in range(world):
+        r0, r1, _ = row_partition(n, world, r)
+        sharded.sharded.local_apply(V, full, r0, r1)
+    assert torch.equal(full[:n], plain(V.reshape(-1)).reshape(n, C))
