@@ -25,7 +25,9 @@ from .exceptions import DimensionMismatch, InvalidInput
 class LowRankRoot:
     """Root Q of the PSD operator Q Q' (linalg.py:357-378)."""
 
-    def __init__(self, columns=None, *, block: torch.Tensor = None):
+    def __init__(self, columns=None, *, block: torch.Tensor = None,
+                 kblock: torch.Tensor = None):
+        self._kblock = kblock              # optional (rank, dim) device K^ Q
         if block is not None:
             self._block = block            # (rank, dim) device
             self._host = None
@@ -47,6 +49,14 @@ class LowRankRoot:
     @property
     def rank(self) -> int:
         return self._block.shape[0] if self._block is not None else self._host.shape[1]
+
+    def kblock(self, dtype=None):
+        """K^ Q as a (rank, dim) device block when known, else None."""
+        kb = self._kblock
+        if kb is None:
+            return None
+        dt = resolve_dtype(dtype)
+        return kb if kb.dtype == dt else kb.to(dt)
 
     def block(self, dtype=None) -> torch.Tensor:
         """(rank, dim) device column block in ``dtype``."""

@@ -310,3 +310,51 @@ def test_sharded_local_blocks_fill_gather_buffer(world):
         r0, r1, _ = row_partition(n, world, r)
         sharded.sharded.local_apply(V, full, r0, r1)
     assert torch.equal(full[:n], plain(V.reshape(-1)).reshape(n, C))
+
+
+def test_recurrence_residual_mode_matches_explicit():
+    """Opt-in recurrence residual: one kernel product per
+    inner iteration instead of two, same iterates up to rounding (fp64)."""
+    g, op, lik = _solver_setup(F64)
+    n1 = lik.noise_state(dev(g["f1"]))
+    runs = {}
+    for mode in ("explicit", "recurrence"):
+        buf = P.SolverBuffers.empty(180, F64)
+        runs[mode] = P.itergp_solve(P.RegressionSystem(op, n1, dev(g["rhs"])),
+                                    P.make_policy("residual", 180), buf,
+                                    P.InnerConfig(max_iters=12, residual=mode))
+    e, r = runs["explicit"], runs["recurrence"]
+    assert r.iterations_run == e.iterations_run
+    assert r.kernel_matvecs == r.iterations_run
+    assert e.kernel_matvecs == int(g["r_matvecs"])
+    assert rel(r.weights.cpu().numpy(), e.weights.cpu().numpy()) < 1e-9
+    assert rel(r.root.columns, e.root.columns) < 1e-9
+    # from a recycled belief: K^ Q0 comes from the virtual solver run, no products
+    n2 = lik.noise_state(dev(g["f2"]))
+    outs = {}
+    for mode in ("explicit", "recurrence"):
+        buf = P.SolverBuffers.empty(180, F64)
+        buf.replace(g["r_S"], g["r_T"])
+        root, buf = P.virtual_solver_run(buf, n2, 5, with_kq=mode == "recurrence")
+        outs[mode] = P.itergp_solve(P.RegressionSystem(op, n2, dev(g["rhs2"])),
+                                    P.make_policy("residual", 180), buf,
+                                    P.InnerConfig(max_iters=6, residual=mode),
+                                    initial_root=root)
+    assert outs["recurrence"].kernel_matvecs == outs["recurrence"].iterations_run
+    assert rel(outs["recurrence"].weights.cpu().numpy(),
+               outs["explicit"].weights.cpu().numpy()) < 1e-8
+
+
+def test_fit_recurrence_mode_cfg2_small():
+    g = golden("fit_cfg2s")
+    prior = P.MultiOutputPrior(kernels=(P.KernelSpec("rbf", 1.0, 2.0),) * 3)
+    ds = P.Dataset(g["X"], g["y"], "class-index", 3)
+    lik = P.SoftmaxLikelihood(ds.targets, 3)
+    oc = P.OuterConfig(max_newton_steps=10, delta=0.01, inner_schedule=20, recycle=True)
+    be, te = P.fit(prior, ds, lik, oc, P.InnerConfig(max_iters=1), dtype=F64)
+    br, tr = P.fit(prior, ds, lik, oc, P.InnerConfig(max_iters=1, residual="recurrence"),
+                   dtype=F64)
+    assert tr.total_kernel_matvecs < te.total_kernel_matvecs
+    me, mr = P.posterior_mean(be, g["X_test"]), P.posterior_mean(br, g["X_test"])
+    assert rel(mr, me) < 1e-3
+    assert np.mean(mr.argmax(1) == me.argmax(1)) >= 0.999

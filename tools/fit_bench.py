@@ -22,6 +22,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("cfgs", nargs="+")
 ap.add_argument("--dtype", default=None)
 ap.add_argument("--n", type=int, default=None, help="override N (smoke runs)")
+ap.add_argument("--residual", default="explicit", choices=["explicit", "recurrence"],
+                help="inner residual mode (recurrence: opt-in, one K product per iteration)")
 args = ap.parse_args()
 torch.cuda.set_device(0)
 for name in args.cfgs:
@@ -41,7 +43,7 @@ for name in args.cfgs:
                        recycle=c["recycle"], compression_rank=c["rank"])
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    belief, trace = P.fit(prior, ds, lik, oc, P.InnerConfig(max_iters=1),
+    belief, trace = P.fit(prior, ds, lik, oc, P.InnerConfig(max_iters=1, residual=args.residual),
                           policy_kind=c["policy"], dtype=dt)
     torch.cuda.synchronize()
     t_fit = time.perf_counter() - t0
@@ -53,6 +55,7 @@ for name in args.cfgs:
     probs = P.probit_predict(mean, var)
     acc = P.metric_accuracy(probs, c["y_test"])
     out = {"cfg": name, "n": int(c["X"].shape[0]), "C": C, "dtype": str(dt).split(".")[-1],
+           "residual": args.residual,
            "fit_wallclock_s": round(trace.wallclock_s, 3), "fit_total_s": round(t_fit, 3),
            "steps": len(trace.steps), "inner_iters": [s.inner_iterations for s in trace.steps],
            "kernel_matvecs": trace.total_kernel_matvecs, "final_rank": belief.root.rank,
