@@ -358,3 +358,27 @@ def test_fit_recurrence_mode_cfg2_small():
     me, mr = P.posterior_mean(be, g["X_test"]), P.posterior_mean(br, g["X_test"])
     assert rel(mr, me) < 1e-3
     assert np.mean(mr.argmax(1) == me.argmax(1)) >= 0.999
+
+
+def test_belief_artifact_device_round_trip(tmp_path):
+    """A fitted belief (device weights and root block) saves to the same bytes
+    as its host copy, and a device load predicts identically."""
+    from paper_2310_20285_b200.artifact import load_belief, save_belief
+    g = golden("fit_cfg2s")
+    prior = P.MultiOutputPrior(kernels=(P.KernelSpec("rbf", 1.0, 2.0),) * 3)
+    ds = P.Dataset(g["X"], g["y"], "class-index", 3)
+    lik = P.SoftmaxLikelihood(ds.targets, 3)
+    belief, _ = P.fit(prior, ds, lik, P.OuterConfig(max_newton_steps=2, inner_schedule=10),
+                      P.InnerConfig(max_iters=1), dtype=F64)
+    echo = {"prior": {"kernel": {"family": "rbf", "lengthscale": 1.0, "outputscale": 2.0}}}
+    p1, p2 = tmp_path / "dev.ncgp", tmp_path / "host.ncgp"
+    save_belief(p1, belief, echo)
+    host = P.PosteriorBelief(prior, g["X"], belief.weights, P.LowRankRoot(belief.root.columns),
+                             belief.newton_step, belief.solver_iterations)
+    save_belief(p2, host, echo)
+    assert p1.read_bytes() == p2.read_bytes()
+    b2, _ = load_belief(p1, device=True, dtype=F64)
+    np.testing.assert_array_equal(P.posterior_mean(b2, g["X_test"]),
+                                  P.posterior_mean(belief, g["X_test"]))
+    np.testing.assert_allclose(P.posterior_marginal_var(b2, g["X_test"]),
+                               P.posterior_marginal_var(belief, g["X_test"]), rtol=0, atol=0)
