@@ -47,7 +47,10 @@ namespace {
 constexpr int BM = 128;          // rows per CTA tile (a pair covers 256)
 constexpr int BN = 128;          // columns per tile (GEMM1 N, GEMM2 K)
 constexpr int CH = 16;           // column tiles per fp32 accumulation chunk
-constexpr int NTHREADS = 512;
+#ifndef NEPI
+#define NEPI 2  // epilogue warpgroups (tiles round-robin; 3 measured: Matern -4 %, RBF +4 %)
+#endif
+constexpr int NTHREADS = 128 * (2 + NEPI);
 constexpr int SMEM_BUDGET = 225 * 1024;
 constexpr int TMEM_COLS = 512;
 constexpr int NS = 3;            // S/P buffers in TMEM (3 x 128 columns)
@@ -594,7 +597,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           const uint64_t da = dA0 + ab * astep;
           const uint32_t d = tmem + s1 * (uint32_t)BN;
           if (elect_one()) {
-            if (!(DBG && p.debug_mode == 3))
+            if (!(DBG && (p.debug_mode == 3 || p.debug_mode == 6)))
               for (int k = 0; k < ksteps1; ++k)
                 mma_ss(d, da + (uint64_t)(16 * k), dx + (uint64_t)(16 * k), id1, k > 0);
             tc_commit2(&s_full[c1]);  // also releases XB / V slots (see producers)
@@ -630,7 +633,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           // P_lo x Vhi (N = WP: each CTA supplies half of Vhi's rows).
           const uint32_t a0 = tmem + s2 * (uint32_t)BN, dO = tO((int)ob);
           if (elect_one()) {
-            if (!(DBG && p.debug_mode == 2)) {
+            if (!(DBG && (p.debug_mode == 2 || p.debug_mode == 6))) {
 #pragma unroll
               for (int m = 0; m < BN / 16; ++m) {
                 const uint32_t ahi = a0 + 32u * (m >> 1) + 8u * (m & 1);
@@ -656,11 +659,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         }
       }
     }
-  } else if (warp >= 4 && warp < 12) {
+  } else if (warp >= 4 && warp < 4 + 4 * NEPI) {
     // ================= epilogue warpgroups =================
     // WG e transforms tiles g = e (mod 2); the two groups run out of phase so
     // each hides the other's TMEM / barrier latencies on the shared MUFU.
-    const int e = (warp - 4) >> 2;           // 0 or 1
+    const int e = (warp - 4) >> 2;           // 0 .. NEPI-1
     const int wq = warp & 3;                 // TMEM lane quarter
     const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
     TileIter ti;
@@ -672,7 +675,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     uint32_t gt = 0;
     const bool tr = (wq == 0 && lane == 0);
     while (ti.valid) {
-      if ((int)(gt & 1u) == e) {
+      if ((int)(gt % (uint32_t)NEPI) == e) {
         const int b = (int)bb;
         if (tr) trace_ev<DBG>(p, gt, 3 + 2 * e);
         mbar_wait(&s_full[er.idx], er.phase);
@@ -709,7 +712,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       bb = (bb + 1u == (uint32_t)NS) ? 0u : bb + 1u;
       ti.next(p, items);
     }
-  } else if (warp >= 12) {
+  } else if (warp >= 4 + 4 * NEPI) {
     // ================= correction warpgroup =================
     const int wq = warp & 3;
     const uint32_t lane_off = (uint32_t)(32 * wq) << 16;

@@ -1,0 +1,79 @@
+// Throughput of K1's epilogue instruction mix, registers only (no TMEM):
+// 8 warps per SM (2 per SMSP, like the two epilogue warpgroups) transforming
+// 32-element chunks.  Reports SM cycles per element.
+//   V0: ex2 only                      V1: ex2 + hi mask + lo sub (no packing)
+//   V2: full RBF transform (+ f16x2 packs)   V3: V2 with cvt.rn.f16x2 via intrinsics
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o epi_probe epi_probe.cu
+#include <cstdint>
+#include <cstdio>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+template <int V>
+__global__ void epi(int iters, float seed, uint32_t* sink, long long* out) {
+  float g[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) g[i] = seed * (float)(threadIdx.x + i) * 1e-3f - 4.f;
+  uint32_t acc = 0;
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float k0 = ex2(g[2 * i]), k1 = ex2(g[2 * i + 1]);
+      if (V == 0) {
+        acc += __float_as_uint(k0) ^ __float_as_uint(k1);
+      } else {
+        const float h0 = __uint_as_float(__float_as_uint(k0) & 0xFFFFE000u);
+        const float h1 = __uint_as_float(__float_as_uint(k1) & 0xFFFFE000u);
+        if (V == 1) {
+          acc += __float_as_uint(h0 + (k0 - h0)) ^ __float_as_uint(k1 - h1);
+        } else {
+          const uint32_t hi = pack_h2(h0, h1), lo = pack_h2(k0 - h0, k1 - h1);
+          acc += hi ^ lo;
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) g[i] += 1e-7f;  // defeat hoisting (1 FADD / element)
+  }
+  const long long t1 = clock64();
+  if (acc == 0x12345678u) sink[0] = acc;
+  if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+}
+
+template <int V>
+void run(long long* d, uint32_t* s, const char* name, int threads = 256) {
+  const int iters = 2000;
+  epi<V><<<148, threads>>>(iters, 1.0f, s, d);
+  cudaDeviceSynchronize();
+  long long h;
+  cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+  const double elems = (double)iters * 32 * threads;  // per SM
+  printf("%-40s %4d thr %6.3f SM cycles / element  (MUFU bound 0.0625)\n", name, threads, h / elems);
+}
+
+int main() {
+  long long* d;
+  uint32_t* s;
+  cudaMalloc(&d, 148 * 8);
+  cudaMalloc(&s, 8);
+  run<0>(d, s, "ex2 only");
+  run<1>(d, s, "ex2 + hi mask + lo sub");
+  run<2>(d, s, "full transform (f16x2 packs)");
+  run<2>(d, s, "full transform (f16x2 packs)", 128);
+  run<2>(d, s, "full transform (f16x2 packs)", 384);
+  run<2>(d, s, "full transform (f16x2 packs)", 512);
+  return 0;
+}

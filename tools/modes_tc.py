@@ -13,7 +13,7 @@ for fam in ("rbf", "matern32"):
     X = torch.from_numpy(rng.standard_normal((n, 8))).float().cuda()
     S = torch.from_numpy(rng.standard_normal((n, 32))).float().cuda()
     op = KernelOperator(fam, 1.5, 1.0, X, w_max=32, impl="tcgen05")
-    for mode, name in ((0, "full"), (1, "no epilogue TMEM/MUFU"), (2, "no GEMM2"), (3, "no GEMM1"), (5, "no copies, no epilogue")):
+    for mode, name in ((0, "full"), (1, "no epilogue TMEM/MUFU"), (2, "no GEMM2"), (3, "no GEMM1"), (5, "no copies, no epilogue"), (6, "no GEMMs (sync + epilogue)")):
         lib.ncgp_debug_set_mode(mode)
         op.apply(S); torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
