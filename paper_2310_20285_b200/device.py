@@ -95,9 +95,29 @@ def labels_to_device(y) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(np.asarray(y), dtype=np.int64)).to(dev)
 
 
+def to_host_tensor(t: torch.Tensor, dtype=None) -> torch.Tensor:
+    """Device tensor -> host tensor through page-locked memory.
+
+    A copy into pageable memory runs at ~2 GB/s here (67 ms for cfg3's
+    128 MB product); into pinned memory at full PCIe/C2C speed.  The pinned
+    block comes from torch's caching host allocator, so repeated calls reuse
+    it once the previous result is released.  ``dtype`` conversion happens on
+    the device.
+    """
+    t = t.detach()
+    if dtype is not None and t.dtype != dtype:
+        t = t.to(dtype)
+    if not t.is_cuda:
+        return t
+    out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    out.copy_(t, non_blocking=True)
+    torch.cuda.current_stream(t.device).synchronize()
+    return out
+
+
 def to_host(t) -> np.ndarray:
     if isinstance(t, torch.Tensor):
-        return t.detach().to("cpu", torch.float64).numpy()
+        return to_host_tensor(t, torch.float64).numpy()
     return np.asarray(t, dtype=np.float64)
 
 

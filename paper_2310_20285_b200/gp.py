@@ -21,7 +21,7 @@ from typing import Dict, List, Optional, Tuple
 import numpy as np
 import torch
 
-from .device import is_device, resolve_dtype, to_device, to_host
+from .device import to_host_tensor, is_device, resolve_dtype, to_device, to_host
 from .exceptions import DimensionMismatch, InvalidInput
 from .kernels import KernelOperator
 
@@ -205,7 +205,7 @@ def prior_matvec(prior: MultiOutputPrior, X, v, tile: int = 256, dtype=None):
     if is_device(v):
         return out
     if isinstance(v, torch.Tensor):       # host tensor in -> host tensor out
-        return out.to("cpu")
+        return to_host_tensor(out)
     return to_host(out)
 
 
