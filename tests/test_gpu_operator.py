@@ -174,3 +174,25 @@ def test_cfg3_full_size_row_sampled(family):
     bound = O.kernel_matmul_rows(spec, X[rows], X, np.abs(S), tile=8)
     assert np.all(np.abs(got - ref) <= 1e-4 * bound)
     assert rel(got, ref) < 1e-4
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", ["cfg4", "cfg5"])
+def test_fit_shape_full_size_row_sampled(cfg):
+    """The operator a cfg4 / cfg5 fit applies (N=1e5, D=20, Matern / N=1e6,
+    D=50, RBF; w = C = 10), at full size, against the oracle on sampled rows."""
+    from paper_2310_20285_b200 import configs
+    c = configs.CONFIGS[cfg](n_test=10)
+    X = c["X"]
+    n = X.shape[0]
+    V = np.random.default_rng(5).standard_normal((n, c["C"]))
+    spec = c["kernel"]
+    op, _ = op_for(spec, X, torch.float32, w=c["C"])
+    assert op.impl == "tcgen05"
+    out = op.apply(torch.from_numpy(V).float().cuda())
+    rows = np.array([0, 7, n // 3, n // 2 + 1, n - 1])
+    got = out[torch.from_numpy(rows).cuda()].double().cpu().numpy()
+    ref = O.kernel_matmul_rows(spec, X[rows], X, V, tile=8)
+    bound = O.kernel_matmul_rows(spec, X[rows], X, np.abs(V), tile=8)
+    assert np.all(np.abs(got - ref) <= 1e-4 * bound)
+    assert rel(got, ref) < 1e-4
