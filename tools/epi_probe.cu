@@ -20,6 +20,23 @@ __device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
   return r;
 }
 
+__device__ __forceinline__ float ex2v(float x) {
+  float y;
+  asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void split_pack_v(float k0, float k1, uint32_t& hi, uint32_t& lo) {
+  // hi = k & 0xFFFFE000, lo = k - hi, packed f16x2; fixed order (asm volatile)
+  uint32_t h0, h1;
+  float l0, l1;
+  asm volatile("and.b32 %0, %1, 0xFFFFE000;" : "=r"(h0) : "r"(__float_as_uint(k0)));
+  asm volatile("and.b32 %0, %1, 0xFFFFE000;" : "=r"(h1) : "r"(__float_as_uint(k1)));
+  asm volatile("sub.f32 %0, %1, %2;" : "=f"(l0) : "f"(k0), "f"(__uint_as_float(h0)));
+  asm volatile("sub.f32 %0, %1, %2;" : "=f"(l1) : "f"(k1), "f"(__uint_as_float(h1)));
+  asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(__uint_as_float(h1)), "f"(__uint_as_float(h0)));
+  asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(l1), "f"(l0));
+}
+
 template <int V>
 __global__ void epi(int iters, float seed, uint32_t* sink, long long* out) {
   float g[32];
@@ -29,8 +46,27 @@ __global__ void epi(int iters, float seed, uint32_t* sink, long long* out) {
   __syncthreads();
   const long long t0 = clock64();
   for (int it = 0; it < iters; ++it) {
+    if (V == 3) {  // software-pipelined: ex2 of pair i+D overlaps the split/pack of pair i
+      constexpr int D = 4;
+      float k[32];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+      for (int i = 0; i < D; ++i) {
+        k[2 * i] = ex2v(g[2 * i]);
+        k[2 * i + 1] = ex2v(g[2 * i + 1]);
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (i + D < 16) {
+          k[2 * (i + D)] = ex2v(g[2 * (i + D)]);
+          k[2 * (i + D) + 1] = ex2v(g[2 * (i + D) + 1]);
+        }
+        uint32_t hi, lo;
+        split_pack_v(k[2 * i], k[2 * i + 1], hi, lo);
+        acc += hi ^ lo;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 16 && V != 3; ++i) {
       const float k0 = ex2(g[2 * i]), k1 = ex2(g[2 * i + 1]);
       if (V == 0) {
         acc += __float_as_uint(k0) ^ __float_as_uint(k1);
@@ -73,6 +109,8 @@ int main() {
   run<1>(d, s, "ex2 + hi mask + lo sub");
   run<2>(d, s, "full transform (f16x2 packs)");
   run<2>(d, s, "full transform (f16x2 packs)", 128);
+  run<3>(d, s, "pipelined (asm order)", 128);
+  run<3>(d, s, "pipelined (asm order)", 256);
   run<2>(d, s, "full transform (f16x2 packs)", 384);
   run<2>(d, s, "full transform (f16x2 packs)", 512);
   return 0;
