@@ -8,6 +8,8 @@ from __future__ import annotations
 
 import threading
 
+import contextlib
+
 import numpy as np
 import torch
 
@@ -93,6 +95,19 @@ def labels_to_device(y) -> torch.Tensor:
     if isinstance(y, torch.Tensor):
         return y.to(device=dev, dtype=torch.int64).contiguous()
     return torch.from_numpy(np.ascontiguousarray(np.asarray(y), dtype=np.int64)).to(dev)
+
+
+@contextlib.contextmanager
+def nvtx_range(name: str):
+    """NVTX range for ncu / Nsight filtering (no-op cost when no tool listens)."""
+    if torch.cuda.is_available():
+        torch.cuda.nvtx.range_push(name)
+        try:
+            yield
+        finally:
+            torch.cuda.nvtx.range_pop()
+    else:
+        yield
 
 
 def to_host_tensor(t: torch.Tensor, dtype=None) -> torch.Tensor:

@@ -21,7 +21,7 @@ from typing import Dict, List, Optional, Tuple
 import numpy as np
 import torch
 
-from .device import to_host_tensor, is_device, resolve_dtype, to_device, to_host
+from .device import nvtx_range, to_host_tensor, is_device, resolve_dtype, to_device, to_host
 from .exceptions import DimensionMismatch, InvalidInput
 from .kernels import KernelOperator
 
@@ -159,6 +159,12 @@ class PriorOperator:
         if out is None:
             out = torch.empty((self.n_rows, C), dtype=self.dtype, device=V.device)
         O = out.view(self.n_rows, C)
+        with nvtx_range("K product"):
+            self._apply_groups(V, O, C, row_begin, row_end)
+        self.matvecs += 1
+        return out.reshape(-1) if flat else out
+
+    def _apply_groups(self, V, O, C, row_begin, row_end):
         for op, cols in self.groups:
             if len(cols) == C:
                 op.apply(V, out=O, row_begin=row_begin, row_end=row_end)
@@ -167,8 +173,6 @@ class PriorOperator:
                 sub = op.apply(V.index_select(1, idx).contiguous(),
                                row_begin=row_begin, row_end=row_end)
                 O[:, cols] = sub
-        self.matvecs += 1
-        return out.reshape(-1) if flat else out
 
     __call__ = apply
 
