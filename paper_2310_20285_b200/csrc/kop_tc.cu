@@ -4,15 +4,20 @@
 // One CTA pair (cluster of 2, cta_group::2 MMAs with M = 256) per two SMs;
 // each CTA owns a 128-row tile and both sweep the same column tiles.
 // Roles per CTA (16 warps):
-//   warp 0        producer: the CTA's row tile + its half of each XB column
+//   warp 0 lane 0 producer: the CTA's row tile + its half of each XB column
 //                 tile (1-D bulk copies, cp.async.bulk -> UBLKCP).
-//   warp 3        producer: the CTA's half of each V column tile.
-//   warp 2        relay: forwards this CTA's copy completions to the leader
-//                 CTA's barriers (the MMA needs both halves).
-//   warp 1        (leader only) MMA issuer, whole warp in uniform registers:
-//                   GEMM1  S[256x128] = XA . XB^T        (kind::f16, SS)
-//                   GEMM2  O[256x2WP] += P_hi . [Vhi|Vlo] and O[:, :WP] += P_lo . Vhi
-//                                                         (kind::f16, A = P in TMEM)
+//   warp 3 lane 0 producer: the CTA's half of each V column tile.
+//   warps 0/3 lane 1  relays: forward this CTA's copy completions to the
+//                 leader CTA's barriers (the MMAs need both halves).
+//   warp 1        (leader only) GEMM2 issuer, whole warp, elect.sync issues:
+//                   O[256x2WP] += P_hi . [Vhi|Vlo],  O[:, :WP] += P_lo . Vhi
+//                   (kind::f16, A = P in TMEM); one wait per step on rdy[g]
+//                   (P(g) written, V(g) and XB(g+3) landed).
+//   warp 2        TMEM allocation, then (leader only) GEMM1 issuer:
+//                   S[256x128] = XA . XB^T  (kind::f16, SS) for tile t after
+//                   GEMM2(t-3) completed (it overwrites that S/P buffer).
+//                 Two issuing warps because one thread issues a tcgen05.mma
+//                 only every ~46 cycles (tools/mma_queue_probe.cu).
 //   warps 4-11    two epilogue warpgroups, alternating column tiles:
 //                 TMEM -> regs, kernel transform (ex2 for RBF, sqrt + ex2 for
 //                 Matern), fp16 hi/lo split, regs -> TMEM over S (P aliases S).
