@@ -4,6 +4,8 @@
 // Every long reduction is two-pass with a fixed block partition and fp64
 // partials summed in index order, so results are bit-reproducible for a
 // given (n, SM count) and never use atomics.
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace {
@@ -26,12 +28,16 @@ __global__ void dots_partial_kernel(int64_t n, int npairs, const T* x0, const T*
   const int64_t hi = min(n, lo + chunk);
   const T* xs[4] = {x0, x1, x2, x3};
   const T* ys[4] = {y0, y1, y2, y3};
+  // one sweep for all pairs: every iteration issues the loads of all pairs
+  // (independent accumulators, fixed order), then one block reduction each
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t i = lo + threadIdx.x; i < hi; i += RB) {
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+      if (p < npairs) acc[p] += (double)xs[p][i] * (double)ys[p][i];
+  }
   for (int p = 0; p < npairs; ++p) {
-    double acc = 0.0;
-    const T* x = xs[p];
-    const T* y = ys[p];
-    for (int64_t i = lo + threadIdx.x; i < hi; i += RB) acc += (double)x[i] * (double)y[i];
-    double s = ncgp::block_sum(acc, sm);
+    double s = ncgp::block_sum(acc[p], sm);
     if (threadIdx.x == 0) partial[(int64_t)p * gridDim.x + blockIdx.x] = s;
   }
 }
@@ -76,6 +82,37 @@ __global__ void gemv_n_kernel(const T* __restrict__ Q, int64_t ldq, int k,
   double acc = 0.0;
   for (int r = 0; r < k; ++r) acc += (double)Q[(int64_t)r * ldq + i] * ys[r];
   out[i] = (T)((s ? (double)s[i] : 0.0) + alpha * acc);
+}
+
+// 4 elements per thread through 16-byte (fp32) / 2 x 16-byte (fp64) accesses
+template <typename T>
+__global__ void lincomb4_kernel(int64_t n4, double a, const T* __restrict__ x, double b,
+                                const T* __restrict__ y, double c, const T* __restrict__ z,
+                                T* __restrict__ out) {
+  using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+  constexpr int PER = sizeof(T) == 4 ? 1 : 2;  // vectors per 4 elements
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n4) return;
+#pragma unroll
+  for (int h = 0; h < PER; ++h) {
+    const int64_t o = q * PER + h;
+    const V xv = reinterpret_cast<const V*>(x)[o];
+    const V yv = y ? reinterpret_cast<const V*>(y)[o] : V{};
+    const V zv = z ? reinterpret_cast<const V*>(z)[o] : V{};
+    const T* xe = reinterpret_cast<const T*>(&xv);
+    const T* ye = reinterpret_cast<const T*>(&yv);
+    const T* ze = reinterpret_cast<const T*>(&zv);
+    V rv;
+    T* re = reinterpret_cast<T*>(&rv);
+#pragma unroll
+    for (int e = 0; e < (int)(sizeof(V) / sizeof(T)); ++e) {
+      double r = a * (double)xe[e];
+      if (y) r += b * (double)ye[e];
+      if (z) r += c * (double)ze[e];
+      re[e] = (T)r;
+    }
+    reinterpret_cast<V*>(out)[o] = rv;
+  }
 }
 
 template <typename T>
@@ -293,6 +330,19 @@ int ncgp_lincomb(int dtype, int64_t n, double a, const void* x, double b, const 
                  const void* z, void* out, void* stream) {
   if (n == 0) return NCGP_OK;
   cudaStream_t st = ncgp::as_stream(stream);
+  auto al16 = [](const void* p) { return p == nullptr || ((uintptr_t)p & 15u) == 0; };
+  if (n % 4 == 0 && al16(x) && al16(y) && al16(z) && al16(out)) {
+    const int64_t n4 = n / 4;
+    const unsigned g4 = (unsigned)((n4 + 255) / 256);
+    if (dtype == NCGP_F64)
+      lincomb4_kernel<double><<<g4, 256, 0, st>>>(n4, a, (const double*)x, b, (const double*)y,
+                                                  c, (const double*)z, (double*)out);
+    else
+      lincomb4_kernel<float><<<g4, 256, 0, st>>>(n4, a, (const float*)x, b, (const float*)y, c,
+                                                 (const float*)z, (float*)out);
+    NCGP_LAUNCHED();
+    return NCGP_OK;
+  }
   const unsigned g = (unsigned)((n + 255) / 256);
   if (dtype == NCGP_F64)
     lincomb_kernel<double><<<g, 256, 0, st>>>(n, a, (const double*)x, b, (const double*)y, c,
