@@ -18,9 +18,13 @@ extern "C" {
 
 size_t ncgp_kop_workspace_bytes(int impl, int dtype, int64_t n_rows, int64_t n_cols, int d,
                                 int w_max) {
-  impl = resolve_impl(impl, dtype, d, w_max);
-  if (impl == NCGP_KOP_TCGEN05) return ncgp::tc_workspace_bytes(n_rows, n_cols, d, w_max);
-  return ncgp::simt_workspace_bytes(dtype, n_rows, n_cols, d, w_max);
+  const int res = resolve_impl(impl, dtype, d, w_max);
+  const size_t simt = ncgp::simt_workspace_bytes(dtype, n_rows, n_cols, d, w_max);
+  if (res != NCGP_KOP_TCGEN05) return simt;
+  const size_t tc = ncgp::tc_workspace_bytes(n_rows, n_cols, d, w_max);
+  // AUTO may fall back to the CUDA-core operator when the inputs fail the
+  // tcgen05 precision guard (see ncgp_kop_create): room for either
+  return impl == NCGP_KOP_AUTO && simt > tc ? simt : tc;
 }
 
 int ncgp_kop_create(ncgp_kop** out, int impl, int family, double lengthscale, double outputscale,
@@ -64,6 +68,13 @@ int ncgp_kop_create(ncgp_kop** out, int impl, int family, double lengthscale, do
   op->ws_bytes = workspace_bytes;
   if (res == NCGP_KOP_TCGEN05) {
     int rc = ncgp::tc_prepare(op, ncgp::as_stream(stream));
+    if (rc == NCGP_UNSUPPORTED && impl == NCGP_KOP_AUTO &&
+        workspace_bytes >= ncgp::simt_workspace_bytes(dtype, n_rows, n_cols, d, w_max)) {
+      // the inputs fail the tcgen05 precision guard: AUTO uses the CUDA-core
+      // operator instead (still on the GPU)
+      op->impl = NCGP_KOP_SIMT;
+      rc = NCGP_OK;
+    }
     if (rc != NCGP_OK) {
       delete op;
       return rc;

@@ -196,3 +196,21 @@ def test_fit_shape_full_size_row_sampled(cfg):
     bound = O.kernel_matmul_rows(spec, X[rows], X, np.abs(V), tile=8)
     assert np.all(np.abs(got - ref) <= 1e-4 * bound)
     assert rel(got, ref) < 1e-4
+
+
+def test_precision_guard_auto_falls_back_on_gpu():
+    """Inputs spread beyond the tcgen05 split's precision range (scaled
+    |x~|^2 > 256): AUTO switches to the CUDA-core operator (on the GPU, same
+    results); an explicit tcgen05 request is refused."""
+    rng = np.random.default_rng(3)
+    X = rng.standard_normal((600, 4))
+    X[0] *= 60.0  # one far point: (60 * 2)^2 / (2 l^2) >> 256 in log2 units
+    V = rng.standard_normal((600, 5))
+    spec = ("rbf", 1.0, 1.0)
+    op, _ = op_for(spec, X, torch.float32, w=8)
+    assert op.impl == "simt"
+    out = op.apply(torch.from_numpy(V).float().cuda()).double().cpu().numpy()
+    ref = O.kernel_matmul_rows(spec, X, X, V)
+    assert rel(out, ref) < 1e-4
+    with pytest.raises(P.NcgpError):
+        op_for(spec, X, torch.float32, impl="tcgen05", w=8)
