@@ -219,6 +219,19 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
       "r"(r[15]));
 }
+// hi (16 columns) then lo (16 columns): one 32-column store
+__device__ __forceinline__ void tmem_st_hilo(uint32_t taddr, const uint32_t (&h)[16],
+                                             const uint32_t (&l)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(h[0]), "r"(h[1]), "r"(h[2]), "r"(h[3]), "r"(h[4]), "r"(h[5]), "r"(h[6]), "r"(h[7]),
+      "r"(h[8]), "r"(h[9]), "r"(h[10]), "r"(h[11]), "r"(h[12]), "r"(h[13]), "r"(h[14]),
+      "r"(h[15]), "r"(l[0]), "r"(l[1]), "r"(l[2]), "r"(l[3]), "r"(l[4]), "r"(l[5]), "r"(l[6]),
+      "r"(l[7]), "r"(l[8]), "r"(l[9]), "r"(l[10]), "r"(l[11]), "r"(l[12]), "r"(l[13]),
+      "r"(l[14]), "r"(l[15]));
+}
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -696,13 +709,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             // software pipeline: the next chunk's TMEM load overlaps this chunk's math
             tmem_ld32(base + 32 * (c + 1), rb);
             transform_chunk<FAM>(ra, L, hi, lo);
-            tmem_st16(base + 32 * c, hi);
-            tmem_st16(base + 32 * c + 16, lo);
+            if (FAM == NCGP_RBF) {  // one 32-column store (Matern: register pressure)
+              tmem_st_hilo(base + 32 * c, hi, lo);
+            } else {
+              tmem_st16(base + 32 * c, hi);
+              tmem_st16(base + 32 * c + 16, lo);
+            }
             tmem_wait_ld();
             if (c + 2 < BN / 32) tmem_ld32(base + 32 * (c + 2), ra);
             transform_chunk<FAM>(rb, L, hi, lo);
-            tmem_st16(base + 32 * (c + 1), hi);
-            tmem_st16(base + 32 * (c + 1) + 16, lo);
+            if (FAM == NCGP_RBF) {
+              tmem_st_hilo(base + 32 * (c + 1), hi, lo);
+            } else {
+              tmem_st16(base + 32 * (c + 1), hi);
+              tmem_st16(base + 32 * (c + 1) + 16, lo);
+            }
             if (c + 2 < BN / 32) tmem_wait_ld();
           }
           tmem_wait_st();
