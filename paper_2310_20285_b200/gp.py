@@ -180,13 +180,35 @@ class PriorOperator:
 _OP_CACHE: Dict[tuple, PriorOperator] = {}
 
 
+def _fingerprint(X):
+    """Cheap content fingerprint of an input array: ~4k strided samples plus the
+    buffer address, so an in-place update of a cached host array is noticed."""
+    if isinstance(X, torch.Tensor):
+        flat = X.detach().reshape(-1)
+        addr = X.data_ptr()
+    else:
+        arr = np.asarray(X)
+        flat = arr.reshape(-1)
+        addr = arr.__array_interface__["data"][0]
+    step = max(1, flat.shape[0] // 4096)
+    sample = flat[::step]
+    total = float(sample.double().sum()) if isinstance(sample, torch.Tensor) else \
+        float(np.asarray(sample, dtype=np.float64).sum())
+    return addr, total
+
+
 def _cached_operator(prior, X, dtype) -> PriorOperator:
-    """Reuse the packed operator across calls on the same host array."""
+    """Reuse the packed operator across calls on the same input array (the
+    reference rebuilds nothing to cache, gp.py:222-250; packing K1's operands
+    costs about one product's worth of HBM traffic).  A content fingerprint
+    invalidates the entry when the array was modified in place."""
     key = (prior, id(X), getattr(X, "shape", None), resolve_dtype(dtype))
+    fp = _fingerprint(X)
     op = _OP_CACHE.get(key)
-    if op is None or op.X_host is not X:
+    if op is None or op.X_host is not X or op.X_fingerprint != fp:
         op = PriorOperator(prior, X, dtype=dtype)
         op.X_host = X
+        op.X_fingerprint = fp
         if len(_OP_CACHE) > 8:
             _OP_CACHE.clear()
         _OP_CACHE[key] = op

@@ -214,3 +214,17 @@ def test_precision_guard_auto_falls_back_on_gpu():
     assert rel(out, ref) < 1e-4
     with pytest.raises(P.NcgpError):
         op_for(spec, X, torch.float32, impl="tcgen05", w=8)
+
+
+def test_prior_matvec_cache_sees_in_place_updates():
+    """prior_matvec caches the packed operator per input array; an in-place
+    update of that array must not return products of the stale inputs."""
+    rng = np.random.default_rng(11)
+    X = rng.standard_normal((300, 3))
+    v = rng.standard_normal(300 * 2)
+    prior = P.MultiOutputPrior(kernels=(P.KernelSpec("rbf", 1.0, 1.0),) * 2)
+    a = P.prior_matvec(prior, X, v, dtype=torch.float64)
+    X *= 1.5  # same object, new contents
+    b = P.prior_matvec(prior, X, v, dtype=torch.float64)
+    ref = O.prior_matvec([("rbf", 1.0, 1.0)] * 2, X, v)
+    assert rel(b, ref) < 1e-12 and rel(a, ref) > 1e-3
