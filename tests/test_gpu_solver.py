@@ -262,13 +262,14 @@ def _cfg5_fixture():
     return json.load(open(p)) if os.path.exists(p) else {}
 
 
-@pytest.mark.parametrize("n", ["1500", "5000"])
-def test_fit_cfg5_trajectory_matches_oracle(n):
+@pytest.mark.parametrize("n,dt", [("1500", F64), ("5000", F64), ("1500", F32)])
+def test_fit_cfg5_trajectory_matches_oracle(n, dt):
     """cfg5 at reduced N, fp64: the Newton trajectory (inner iterations,
     termination, |yhat| per step) and the mean-label accuracy follow the
     oracle's step for step -- including the divergence of the reference's
     undamped Newton iteration that cfg5 triggers from N ~ 5000 up
-    (tests/golden/make_cfg5_trajectory.py)."""
+    (tests/golden/make_cfg5_trajectory.py).  fp32 (the tcgen05 path) is
+    checked where the iteration converges (N = 1500)."""
     from paper_2310_20285_b200 import configs
     ref = _cfg5_fixture().get(n)
     if ref is None:
@@ -280,7 +281,7 @@ def test_fit_cfg5_trajectory_matches_oracle(n):
     belief, trace = P.fit(prior, ds, lik,
                           P.OuterConfig(max_newton_steps=6, delta=0.01, inner_schedule=64,
                                         recycle=True, compression_rank=256),
-                          P.InnerConfig(max_iters=1), policy_kind="residual", dtype=F64)
+                          P.InnerConfig(max_iters=1), policy_kind="residual", dtype=dt)
     got = [(s.inner_iterations, s.inner_termination, s.pseudo_target_norm) for s in trace.steps]
     want = [(s["iterations"], s["termination"], s["yhat_norm"]) for s in ref["steps"]]
     assert [g[:2] for g in got] == [w[:2] for w in want]
