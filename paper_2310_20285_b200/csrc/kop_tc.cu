@@ -52,10 +52,14 @@ namespace {
 constexpr int BM = 128;          // rows per CTA tile (a pair covers 256)
 constexpr int BN = 128;          // columns per tile (GEMM1 N, GEMM2 K)
 constexpr int CH = 16;           // column tiles per fp32 accumulation chunk
-#ifndef NEPI
-#define NEPI 2  // epilogue warpgroups (tiles round-robin; 3 measured: Matern -4 %, RBF +4 %)
-#endif
-constexpr int NTHREADS = 128 * (2 + NEPI);
+// Epilogue: two groups (tile parity) of two warpgroups each; the two warps
+// of a group that share a TMEM lane quarter split the tile's columns, so four
+// warps per SMSP feed the MUFU (tools/epi_probe.cu: one warp per SMSP reaches
+// 56 % of the MUFU rate, two 83 %) and a group waiting on s_full leaves two.
+// Registers are rebalanced with setmaxnreg: 40 for the producer / MMA and the
+// correction warpgroups, 96 for the four epilogue warpgroups.
+constexpr int EPI_WARPS = 16;
+constexpr int NTHREADS = 32 * (4 + EPI_WARPS + 4);
 constexpr int SMEM_BUDGET = 225 * 1024;
 constexpr int TMEM_COLS = 512;
 constexpr int NS = 3;            // S/P buffers in TMEM (3 x 128 columns)
@@ -231,6 +235,13 @@ __device__ __forceinline__ void tmem_st_hilo(uint32_t taddr, const uint32_t (&h)
       "r"(h[15]), "r"(l[0]), "r"(l[1]), "r"(l[2]), "r"(l[3]), "r"(l[4]), "r"(l[5]), "r"(l[6]),
       "r"(l[7]), "r"(l[8]), "r"(l[9]), "r"(l[10]), "r"(l[11]), "r"(l[12]), "r"(l[13]),
       "r"(l[14]), "r"(l[15]));
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7])
+      : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -460,7 +471,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     for (int s = 0; s < NR; ++s) {
       mbar_init(&s_full[s], 1);
       mbar_init(&g2done[s], 1);
-      mbar_init(&rdy[s], 8 + 2 + 2);
+      mbar_init(&rdy[s], 16 + 2 + 2);  // epilogue group (8 warps x 2 CTAs), V, XB
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&a_land[b], 1);
@@ -487,6 +498,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   auto tO = [&](int b) -> uint32_t { return tmem + (uint32_t)(NS * BN + b * 2 * WP); };
   const int64_t half_off = (int64_t)rank * p.rec_bytes;   // this CTA's half of a record
 
+  // setmaxnreg sits at the top of each warpgroup's branch so that ptxas sees
+  // one register budget per region (a shared prologue would cap all at 40).
+  if (warp < 4) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
   if (warp == 0 || warp == 3) {
     // ================= producers (lane 0) and relays (lane 1) =================
     // Slot reuse is signalled by GEMM1 completions (s_full, one multicast commit
@@ -677,13 +692,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         }
       }
     }
-  } else if (warp >= 4 && warp < 4 + 4 * NEPI) {
-    // ================= epilogue warpgroups =================
-    // WG e transforms tiles g = e (mod 2); the two groups run out of phase so
-    // each hides the other's TMEM / barrier latencies on the shared MUFU.
-    const int e = (warp - 4) >> 2;           // 0 .. NEPI-1
+  }
+  } else if (warp < 4 + EPI_WARPS) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 96;");
+    // ================= epilogue: two groups of 8 warps =================
+    // group e transforms tiles g = e (mod 2); within a group, the warp with
+    // TMEM lane quarter wq and column half hc does chunks 2hc, 2hc + 1.
+    const int e = (warp - 4) / 8;            // 0 or 1
+    const int hc = ((warp - 4) % 8) / 4;     // column half
     const int wq = warp & 3;                 // TMEM lane quarter
     const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
+    const uint32_t col0 = (uint32_t)(hc * (BN / 2));
     TileIter ti;
     ti.start(p, items);
     Ring er;  // s_full ring (NR)
@@ -691,40 +710,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     uint32_t bb = 0;  // S buffer of the current tile (g mod NS)
     const float L = p.L;
     uint32_t gt = 0;
-    const bool tr = (wq == 0 && lane == 0);
+    const bool tr = (wq == 0 && hc == 0 && lane == 0);
     while (ti.valid) {
-      if ((int)(gt % (uint32_t)NEPI) == e) {
+      if ((int)(gt & 1u) == e) {
         const int b = (int)bb;
         if (tr) trace_ev<DBG>(p, gt, 3 + 2 * e);
         mbar_wait(&s_full[er.idx], er.phase);
         tc_fence_after();
         if (tr) trace_ev<DBG>(p, gt, 4 + 2 * e);
         if (!(DBG && (p.debug_mode == 1 || p.debug_mode == 5))) {
-          const uint32_t base = tS(b) + lane_off;
-          uint32_t ra[32], rb[32], hi[16], lo[16];
-          tmem_ld32(base, ra);
-          tmem_wait_ld();
+          const uint32_t base = tS(b) + lane_off + col0;
+          uint32_t ra[32], hi[16], lo[16];
 #pragma unroll
-          for (int c = 0; c < BN / 32; c += 2) {
-            // software pipeline: the next chunk's TMEM load overlaps this chunk's math
-            tmem_ld32(base + 32 * (c + 1), rb);
+          for (int c = 0; c < BN / 64; ++c) {
+            tmem_ld32(base + 32 * c, ra);
+            tmem_wait_ld(ra);
             transform_chunk<FAM>(ra, L, hi, lo);
-            if (FAM == NCGP_RBF) {  // one 32-column store (Matern: register pressure)
+            if (FAM == NCGP_RBF) {
               tmem_st_hilo(base + 32 * c, hi, lo);
             } else {
               tmem_st16(base + 32 * c, hi);
               tmem_st16(base + 32 * c + 16, lo);
             }
-            tmem_wait_ld();
-            if (c + 2 < BN / 32) tmem_ld32(base + 32 * (c + 2), ra);
-            transform_chunk<FAM>(rb, L, hi, lo);
-            if (FAM == NCGP_RBF) {
-              tmem_st_hilo(base + 32 * (c + 1), hi, lo);
-            } else {
-              tmem_st16(base + 32 * (c + 1), hi);
-              tmem_st16(base + 32 * (c + 1) + 16, lo);
-            }
-            if (c + 2 < BN / 32) tmem_wait_ld();
           }
           tmem_wait_st();
         }
@@ -738,7 +745,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       bb = (bb + 1u == (uint32_t)NS) ? 0u : bb + 1u;
       ti.next(p, items);
     }
-  } else if (warp >= 4 + 4 * NEPI) {
+  } else {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
     // ================= correction warpgroup =================
     const int wq = warp & 3;
     const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
@@ -754,15 +762,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         const int ob = (int)(q & 1u);
         mbar_wait(&o_full[ob], (q >> 1) & 1u);
         tc_fence_after();
-#pragma unroll
-        for (int h = 0; h < WP / 16; ++h) {
-          uint32_t r[16], t[16];
-          tmem_ld16(tO(ob) + lane_off + 16 * h, r);       // P_hi Vhi + P_lo Vhi
-          tmem_ld16(tO(ob) + lane_off + WP + 16 * h, t);  // P_hi Vlo
+#pragma unroll 1
+        for (int h = 0; h < WP / 8; ++h) {  // 8 columns at a time (40-register budget)
+          uint32_t r[8], t[8];
+          tmem_ld8(tO(ob) + lane_off + 8 * h, r);       // P_hi Vhi + P_lo Vhi
+          tmem_ld8(tO(ob) + lane_off + WP + 8 * h, t);  // P_hi Vlo
           tmem_wait_ld();
 #pragma unroll
-          for (int c = 0; c < 16; ++c)
-            acc[(16 * h + c) * BM] += (double)__uint_as_float(r[c]) + (double)__uint_as_float(t[c]);
+          for (int c = 0; c < 8; ++c)
+            acc[(8 * h + c) * BM] += (double)__uint_as_float(r[c]) + (double)__uint_as_float(t[c]);
         }
         tc_fence_before();
         __syncwarp();
