@@ -278,14 +278,14 @@ def run_ours(args, rank, world, local_rank):
     achieved = F * local_pairs / t_kernel / 1e12
     peak_tflops = min(tensor_tflops, F * mufu_rate / E / 1e12)
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "r01d_summary.json")
+    prof = os.path.join(ROOT, "profiles", "r01e_summary.json")
     if os.path.exists(prof) and c["name"] == "cfg3" and world == 1:
         with open(prof) as fh:
             traffic = json.load(fh).get("traffic_bytes_per_launch")
     roofline = {"bound": "tensor", "limiter": "MUFU ex2" if peak_tflops < tensor_tflops
                 else "tensor pipe", "achieved": round(achieved, 3), "peak": round(peak_tflops, 3),
                 "unit": "TFLOP/s", "frac": round(achieved / peak_tflops, 4), "traffic": traffic,
-                "traffic_source": "profiles/r01d_summary.json (ncu --set full, dram read+write)"
+                "traffic_source": "profiles/r01e_summary.json (ncu --set full, dram read+write)"
                 if traffic else None,
                 "peak_basis": f"min({pk['source']} bf16 {pk['bf16']}/2 TF/s, "
                               f"{sms} SM x {P_MUFU_PER_SM_CLK} ex2/clk x "
