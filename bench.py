@@ -182,18 +182,38 @@ def run_ours(args, rank, world, local_rank):
     op = KernelOperator(spec[0], spec[1], spec[2], Xd, w_max=w, impl=args.kop)
     from paper_2310_20285_b200.parallel import row_partition
     r0, r1, per = row_partition(n, world, rank)
-    # each rank writes its rows straight into its slice of the gather buffer;
-    # the all-gather then runs in place (parallel.RowShardedOperator does the same)
-    out_full = torch.empty((per * world, w), dtype=torch.float32, device=dev)
+    # nccl: each rank writes its rows straight into its slice of the gather
+    # buffer and the all-gather runs in place.  fused: the gather buffers are
+    # symmetric memory and K1 stores every row into all ranks' buffers
+    # (parallel.RowShardedOperator implements both).
+    fused = world > 1 and args.gather == "fused"
+    peer_rows = None
+    if fused:
+        from paper_2310_20285_b200.parallel import TorchSymmetricMemory
+        out_full, barrier, peers = TorchSymmetricMemory().alloc((per * world, w), torch.float32,
+                                                                dev)
+        peer_rows = [q[:n] for q in peers]
+    else:
+        out_full = torch.empty((per * world, w), dtype=torch.float32, device=dev)
     out_rows = out_full[:n]
     mine = out_full[rank * per:(rank + 1) * per]
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
-    def step():
-        op.apply(Sd, out=out_rows, row_begin=r0, row_end=r1)
-        if world > 1:
+    def pre():
+        if fused:
+            barrier(0)
+
+    def post():
+        if fused:
+            barrier(1)
+        elif world > 1:
             dist.all_gather_into_tensor(out_full, mine)
+
+    def step():
+        pre()
+        op.apply(Sd, out=out_rows, row_begin=r0, row_end=r1, peers=peer_rows)
+        post()
 
     for _ in range(args.warmup):
         step()
@@ -213,11 +233,11 @@ def run_ours(args, rank, world, local_rank):
     for k in range(args.steps):
         flush.zero_()  # evict L2 between timed steps (outside the events)
         starts[k].record(stream)
+        pre()
         kstarts[k].record(stream)
-        op.apply(Sd, out=out_rows, row_begin=r0, row_end=r1)
+        op.apply(Sd, out=out_rows, row_begin=r0, row_end=r1, peers=peer_rows)
         kends[k].record(stream)
-        if world > 1:
-            dist.all_gather_into_tensor(out_full, mine)
+        post()
         ends[k].record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -246,7 +266,8 @@ def run_ours(args, rank, world, local_rank):
         call = lambda: P.prior_matvec(prior, Xh, Sh.view(-1))  # noqa: E731
     else:
         from paper_2310_20285_b200.parallel import ShardedPriorOperator
-        sop = ShardedPriorOperator(prior, X.astype(np.float32), dtype=torch.float32)
+        sop = ShardedPriorOperator(prior, X.astype(np.float32), dtype=torch.float32,
+                                   gather=args.gather)
         call = lambda: to_host_tensor(sop(Sh.view(-1).to(dev, non_blocking=True)))  # noqa: E731
     res = call()  # builds + caches the operator
     torch.cuda.synchronize()
@@ -266,7 +287,9 @@ def run_ours(args, rank, world, local_rank):
            "note": "X resident in the cached operator; S (pinned fp32) uploaded and the "
                    "product downloaded every step" +
                    ("" if world == 1 else f" on each of the {world} ranks (row-sharded "
-                                          "operator, in-place all-gather)")}
+                                          "operator, " + ("rows stored into every rank's "
+                                                          "symmetric-memory buffer by K1)"
+                                                          if fused else "in-place all-gather)"))}
 
     # ---- roofline of the dominant kernel (the fused kernel-matmul)
     pk = peaks()
@@ -310,7 +333,8 @@ def run_ours(args, rank, world, local_rank):
                 "config": {"workload": c["name"], "n": n, "d": d, "w": w, "kernel": list(spec),
                            "flops_per_pair": F, "exp_per_pair": E,
                            "l2": "flushed (256 MiB write) before every timed step",
-                           "parallelism": f"row-sharded x{world}"},
+                           "parallelism": f"row-sharded x{world}",
+                           "gather": args.gather if world > 1 else None},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clocks}
         print(json.dumps(line), flush=True)
@@ -336,7 +360,7 @@ def run_fit(args, rank, world, local_rank):
     prior = P.MultiOutputPrior(kernels=(P.KernelSpec(*c["kernel"]),) * C)
     ds = P.Dataset(c["X"], c["y"], "class-index", C)
     lik = P.SoftmaxLikelihood(ds.targets, C)
-    op = ShardedPriorOperator(prior, c["X"], dtype=dt) if world > 1 else None
+    op = ShardedPriorOperator(prior, c["X"], dtype=dt, gather=args.gather) if world > 1 else None
     inner = P.InnerConfig(max_iters=1, residual=args.residual)
     for _ in range(max(0, args.warmup)):
         P.fit(prior, ds, lik, P.OuterConfig(max_newton_steps=1, inner_schedule=2), inner,
@@ -372,7 +396,8 @@ def run_fit(args, rank, world, local_rank):
             "config": {"workload": args.workload, "n": int(c["X"].shape[0]), "C": C,
                        "kernel": list(c["kernel"]), "schedule": [c["steps"], c["inner"]],
                        "rank": c["rank"], "residual": args.residual,
-                       "parallelism": f"row-sharded x{world}"},
+                       "parallelism": f"row-sharded x{world}",
+                       "gather": args.gather if world > 1 else None},
             "kernel_matvecs": trace.total_kernel_matvecs,
             "inner_iters": [s.inner_iterations for s in trace.steps],
             "test_accuracy_mean_2000": round(acc, 4),
@@ -400,6 +425,9 @@ def main():
     ap.add_argument("--residual", default="explicit", choices=["explicit", "recurrence"],
                     help="fit workloads: inner residual mode (recurrence is opt-in)")
     ap.add_argument("--kop", default="auto", choices=["auto", "tcgen05", "simt"])
+    ap.add_argument("--gather", default="nccl", choices=["nccl", "fused"],
+                    help="N>1 row exchange: in-place NCCL all-gather after K1, or K1 storing "
+                         "each row into every rank's symmetric-memory buffer")
     ap.add_argument("--cpu-rows", type=int, default=24)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

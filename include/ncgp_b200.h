@@ -93,6 +93,20 @@ int ncgp_kop_apply(ncgp_kop* op, const void* V, int64_t ldv, int w,
                    void* out, int64_t ldo, int64_t row_begin,
                    int64_t row_end, void* stream);
 
+/* Row-sharded apply with the all-gather fused into the store (SURVEY.md
+ * 8(e); replaces ncgp_kop_apply + an all-gather of the output rows).  Rows
+ * [row_begin, row_end) of K V are stored, at their global row offsets, into
+ * every buffer outs[0..n_out): this rank's own (n_rows, w) output and the
+ * gather buffers of its peers mapped into this process (CUDA IPC / symmetric
+ * memory over NVLink), so the exchange overlaps the kernel instead of
+ * following it.  `outs` is a host array of device pointers; all buffers
+ * share the row stride ldo.  The caller orders the peers' reads after this
+ * stream (a cross-rank barrier).  1 <= n_out <= NCGP_MAX_OUTS. */
+#define NCGP_MAX_OUTS 8
+int ncgp_kop_apply_multi(ncgp_kop* op, const void* V, int64_t ldv, int w,
+                         void* const* outs, int n_out, int64_t ldo,
+                         int64_t row_begin, int64_t row_end, void* stream);
+
 /* Actual implementation chosen (NCGP_KOP_TCGEN05 or NCGP_KOP_SIMT). */
 int ncgp_kop_impl(const ncgp_kop* op);
 int ncgp_kop_destroy(ncgp_kop* op);

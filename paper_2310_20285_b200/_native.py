@@ -48,6 +48,8 @@ _SIGS = {
     "ncgp_kop_create": (_i32, [ctypes.POINTER(_vp), _i32, _i32, _f64, _f64, _i32, _vp, _i64,
                                _vp, _i64, _i32, _i32, _vp, _sz, _vp]),
     "ncgp_kop_apply": (_i32, [_vp, _vp, _i64, _i32, _vp, _i64, _i64, _i64, _vp]),
+    "ncgp_kop_apply_multi": (_i32, [_vp, _vp, _i64, _i32, ctypes.POINTER(_vp), _i32, _i64, _i64,
+                                    _i64, _vp]),
     "ncgp_kop_impl": (_i32, [_vp]),
     "ncgp_kop_destroy": (_i32, [_vp]),
     "ncgp_softmax_stats": (_i32, [_i32, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp]),

@@ -30,16 +30,37 @@ struct ncgp_kop {
 
 namespace ncgp {
 
+// Destinations of an apply: the caller's output plus, for a row-sharded
+// product with the all-gather fused into the store, every peer's (n_rows, w)
+// gather buffer mapped into this process (CUDA IPC / symmetric memory).
+// Row i of the product is stored to p[k] + i * ldo for every k.
+struct OutSet {
+  void* p[NCGP_MAX_OUTS];
+  int n;
+};
+template <typename T>
+struct OutPtrs {  // typed, already offset to this launch's first row
+  T* p[NCGP_MAX_OUTS];
+  int n;
+};
+template <typename T>
+inline OutPtrs<T> out_ptrs(const OutSet& o, int64_t r0, int64_t ldo) {
+  OutPtrs<T> r{};
+  r.n = o.n;
+  for (int k = 0; k < o.n; ++k) r.p[k] = static_cast<T*>(o.p[k]) + r0 * ldo;
+  return r;
+}
+
 // CUDA-core implementation (kop_simt.cu)
 size_t simt_workspace_bytes(int dtype, int64_t n_rows, int64_t n_cols, int d, int w_max);
-int simt_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, void* out, int64_t ldo,
+int simt_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out, int64_t ldo,
                int64_t r0, int64_t r1, cudaStream_t st);
 
 // tcgen05 implementation (kop_tc.cu)
 bool tc_supported(int dtype, int d, int w_max);
 size_t tc_workspace_bytes(int64_t n_rows, int64_t n_cols, int d, int w_max);
 int tc_prepare(ncgp_kop* op, cudaStream_t st);
-int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, void* out, int64_t ldo,
+int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out, int64_t ldo,
              int64_t r0, int64_t r1, cudaStream_t st);
 
 }  // namespace ncgp

@@ -84,8 +84,9 @@ int ncgp_kop_create(ncgp_kop** out, int impl, int family, double lengthscale, do
   return NCGP_OK;
 }
 
-int ncgp_kop_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, void* out, int64_t ldo,
-                   int64_t row_begin, int64_t row_end, void* stream) {
+static int kop_apply_outs(ncgp_kop* op, const void* V, int64_t ldv, int w,
+                          const ncgp::OutSet& outs, int64_t ldo, int64_t row_begin,
+                          int64_t row_end, void* stream) {
   NCGP_CHECK_ARG(op != nullptr, NCGP_INVALID_INPUT, "null operator");
   NCGP_CHECK_ARG(w >= 0 && w <= op->w_max, NCGP_DIMENSION_MISMATCH,
                  "rhs width %d outside [0, %d]", w, op->w_max);
@@ -93,18 +94,44 @@ int ncgp_kop_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, void* out, i
   NCGP_CHECK_ARG(0 <= row_begin && row_begin <= row_end && row_end <= op->n_rows,
                  NCGP_DIMENSION_MISMATCH, "row range [%lld, %lld) outside [0, %lld)",
                  (long long)row_begin, (long long)row_end, (long long)op->n_rows);
+  NCGP_CHECK_ARG(outs.n >= 1 && outs.n <= NCGP_MAX_OUTS, NCGP_INVALID_INPUT,
+                 "%d output buffers (1..%d)", outs.n, NCGP_MAX_OUTS);
   if (w == 0 || row_end == row_begin) return NCGP_OK;
-  NCGP_CHECK_ARG(V != nullptr && out != nullptr, NCGP_INVALID_INPUT, "null operand");
+  NCGP_CHECK_ARG(V != nullptr, NCGP_INVALID_INPUT, "null operand");
+  for (int k = 0; k < outs.n; ++k)
+    NCGP_CHECK_ARG(outs.p[k] != nullptr, NCGP_INVALID_INPUT, "null output %d", k);
   if (op->n_cols == 0) {
     // empty sum: zero output rows
     const size_t es = op->dtype == NCGP_F64 ? 8 : 4;
-    NCGP_CUDA(cudaMemset2DAsync(static_cast<uint8_t*>(out) + row_begin * ldo * es, ldo * es, 0,
-                                w * es, row_end - row_begin, ncgp::as_stream(stream)));
+    for (int k = 0; k < outs.n; ++k)
+      NCGP_CUDA(cudaMemset2DAsync(static_cast<uint8_t*>(outs.p[k]) + row_begin * ldo * es,
+                                  ldo * es, 0, w * es, row_end - row_begin,
+                                  ncgp::as_stream(stream)));
     return NCGP_OK;
   }
   if (op->impl == NCGP_KOP_TCGEN05)
-    return ncgp::tc_apply(op, V, ldv, w, out, ldo, row_begin, row_end, ncgp::as_stream(stream));
-  return ncgp::simt_apply(op, V, ldv, w, out, ldo, row_begin, row_end, ncgp::as_stream(stream));
+    return ncgp::tc_apply(op, V, ldv, w, outs, ldo, row_begin, row_end, ncgp::as_stream(stream));
+  return ncgp::simt_apply(op, V, ldv, w, outs, ldo, row_begin, row_end, ncgp::as_stream(stream));
+}
+
+int ncgp_kop_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, void* out, int64_t ldo,
+                   int64_t row_begin, int64_t row_end, void* stream) {
+  ncgp::OutSet o{};
+  o.p[0] = out;
+  o.n = 1;
+  return kop_apply_outs(op, V, ldv, w, o, ldo, row_begin, row_end, stream);
+}
+
+int ncgp_kop_apply_multi(ncgp_kop* op, const void* V, int64_t ldv, int w, void* const* outs,
+                         int n_out, int64_t ldo, int64_t row_begin, int64_t row_end,
+                         void* stream) {
+  NCGP_CHECK_ARG(outs != nullptr, NCGP_INVALID_INPUT, "null output list");
+  NCGP_CHECK_ARG(n_out >= 1 && n_out <= NCGP_MAX_OUTS, NCGP_INVALID_INPUT,
+                 "%d output buffers (1..%d)", n_out, NCGP_MAX_OUTS);
+  ncgp::OutSet o{};
+  for (int k = 0; k < n_out; ++k) o.p[k] = outs[k];
+  o.n = n_out;
+  return kop_apply_outs(op, V, ldv, w, o, ldo, row_begin, row_end, stream);
 }
 
 int ncgp_kop_impl(const ncgp_kop* op) { return op ? op->impl : -1; }

@@ -139,14 +139,16 @@ kop_simt_kernel(const T* __restrict__ Xr, int64_t nloc, const T* __restrict__ Xc
 
 template <typename T>
 __global__ void reduce_splits_kernel(const double* __restrict__ partial, int splits,
-                                     int64_t nloc, int w, T* __restrict__ out, int64_t ldo) {
+                                     int64_t nloc, int w, const ncgp::OutPtrs<T> out, int64_t ldo) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= nloc * w) return;
   const int64_t i = e / w;
   const int c = (int)(e % w);
   double s = 0.0;
   for (int p = 0; p < splits; ++p) s += partial[(int64_t)p * nloc * w + e];
-  out[i * ldo + c] = (T)s;
+#pragma unroll
+  for (int k = 0; k < NCGP_MAX_OUTS; ++k)
+    if (k < out.n) out.p[k][i * ldo + c] = (T)s;
 }
 
 int pick_wt(int w) { return w <= 1 ? 1 : (w <= 4 ? 4 : (w <= 16 ? 16 : 32)); }
@@ -166,7 +168,7 @@ int plan_splits(int64_t nloc, int64_t nc, int zs, int sms) {
 
 template <typename T, int FAM, int DMAX, int WT>
 int launch_t(ncgp_kop* op, const T* Xr, int64_t nloc, const T* V, int64_t ldv, int w,
-             T* out, int64_t ldo, cudaStream_t st) {
+             const ncgp::OutPtrs<T>& out, int64_t ldo, cudaStream_t st) {
   const int zs = (w + WT - 1) / WT;
   // planned on the full row count: row shards reduce in the same order
   const int splits = plan_splits(op->n_rows, op->n_cols, zs, op->sms);
@@ -197,7 +199,7 @@ int launch_t(ncgp_kop* op, const T* Xr, int64_t nloc, const T* V, int64_t ldv, i
 
 template <typename T, int FAM, int DMAX>
 int dispatch_wt(ncgp_kop* op, const T* Xr, int64_t nloc, const T* V, int64_t ldv, int w,
-                T* out, int64_t ldo, cudaStream_t st) {
+                const ncgp::OutPtrs<T>& out, int64_t ldo, cudaStream_t st) {
   switch (pick_wt(w)) {
     case 1: return launch_t<T, FAM, DMAX, 1>(op, Xr, nloc, V, ldv, w, out, ldo, st);
     case 4: return launch_t<T, FAM, DMAX, 4>(op, Xr, nloc, V, ldv, w, out, ldo, st);
@@ -208,7 +210,7 @@ int dispatch_wt(ncgp_kop* op, const T* Xr, int64_t nloc, const T* V, int64_t ldv
 
 template <typename T, int FAM>
 int dispatch_d(ncgp_kop* op, const T* Xr, int64_t nloc, const T* V, int64_t ldv, int w,
-               T* out, int64_t ldo, cudaStream_t st) {
+               const ncgp::OutPtrs<T>& out, int64_t ldo, cudaStream_t st) {
   switch (pick_dmax(op->d)) {
     case 8: return dispatch_wt<T, FAM, 8>(op, Xr, nloc, V, ldv, w, out, ldo, st);
     case 16: return dispatch_wt<T, FAM, 16>(op, Xr, nloc, V, ldv, w, out, ldo, st);
@@ -219,7 +221,7 @@ int dispatch_d(ncgp_kop* op, const T* Xr, int64_t nloc, const T* V, int64_t ldv,
 
 template <typename T>
 int dispatch_fam(ncgp_kop* op, const T* Xr, int64_t nloc, const T* V, int64_t ldv, int w,
-                 T* out, int64_t ldo, cudaStream_t st) {
+                 const ncgp::OutPtrs<T>& out, int64_t ldo, cudaStream_t st) {
   if (op->family == NCGP_RBF)
     return dispatch_d<T, NCGP_RBF>(op, Xr, nloc, V, ldv, w, out, ldo, st);
   return dispatch_d<T, NCGP_MATERN32>(op, Xr, nloc, V, ldv, w, out, ldo, st);
@@ -243,7 +245,7 @@ size_t simt_workspace_bytes(int dtype, int64_t n_rows, int64_t n_cols, int d, in
   return align_up(best, 256);
 }
 
-int simt_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, void* out, int64_t ldo,
+int simt_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out, int64_t ldo,
                int64_t r0, int64_t r1, cudaStream_t st) {
   NCGP_CHECK_ARG(op->d <= 64, NCGP_UNSUPPORTED, "CUDA-core operator supports d <= 64 (got %d)",
                  op->d);
@@ -252,11 +254,11 @@ int simt_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, void* out, int64
   if (op->dtype == NCGP_F64) {
     const double* Xr = static_cast<const double*>(op->Xr) + r0 * op->d;
     return dispatch_fam<double>(op, Xr, nloc, static_cast<const double*>(V), ldv, w,
-                                static_cast<double*>(out) + r0 * ldo, ldo, st);
+                                out_ptrs<double>(out, r0, ldo), ldo, st);
   }
   const float* Xr = static_cast<const float*>(op->Xr) + r0 * op->d;
   return dispatch_fam<float>(op, Xr, nloc, static_cast<const float*>(V), ldv, w,
-                             static_cast<float*>(out) + r0 * ldo, ldo, st);
+                             out_ptrs<float>(out, r0, ldo), ldo, st);
 }
 
 }  // namespace ncgp

@@ -313,7 +313,8 @@ struct TcParams {
   float L;               // log2(s2 * 2^s): Matern exponent offset
   const int* col_exp;    // per RHS column exponent e_c
   int s_exp;             // kernel prescale exponent s
-  void* out;
+  void* outs[NCGP_MAX_OUTS];  // destinations, offset to this launch's first row
+  int n_out;
   int64_t ldo;
   int out_f64;
   double* partial;       // [splits][nloc][w] when splits > 1
@@ -784,10 +785,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
               const double v = ldexp(acc[c * BM], -(p.s_exp + __ldg(&p.col_exp[c])));
               if (p.splits > 1)
                 p.partial[(sp * p.nloc + i) * p.w + c] = v;
-              else if (p.out_f64)
-                static_cast<double*>(p.out)[i * p.ldo + c] = v;
               else
-                static_cast<float*>(p.out)[i * p.ldo + c] = (float)v;
+#pragma unroll
+                for (int k = 0; k < NCGP_MAX_OUTS; ++k) {  // own output, then the peers'
+                  if (k >= p.n_out) break;
+                  if (p.out_f64)
+                    static_cast<double*>(p.outs[k])[i * p.ldo + c] = v;
+                  else
+                    static_cast<float*>(p.outs[k])[i * p.ldo + c] = (float)v;
+                }
             }
           }
 #pragma unroll
@@ -996,12 +1002,15 @@ __global__ void pack_v_kernel(const T* __restrict__ V, int64_t ldv, int64_t n, i
 
 template <typename T>
 __global__ void reduce_partial_kernel(const double* __restrict__ partial, int splits,
-                                      int64_t nloc, int w, T* __restrict__ out, int64_t ldo) {
+                                      int64_t nloc, int w, const ncgp::OutPtrs<T> out,
+                                      int64_t ldo) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= nloc * w) return;
   double s = 0.0;
   for (int p = 0; p < splits; ++p) s += partial[(int64_t)p * nloc * w + e];
-  out[(e / w) * ldo + (e % w)] = (T)s;
+#pragma unroll
+  for (int k = 0; k < NCGP_MAX_OUTS; ++k)
+    if (k < out.n) out.p[k][(e / w) * ldo + (e % w)] = (T)s;
 }
 
 // ------------------------------------------------------------------ host
@@ -1140,8 +1149,8 @@ int tc_prepare(ncgp_kop* op, cudaStream_t st) {
   return NCGP_OK;
 }
 
-int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, void* out, int64_t ldo, int64_t r0,
-             int64_t r1, cudaStream_t st) {
+int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out, int64_t ldo,
+             int64_t r0, int64_t r1, cudaStream_t st) {
   NCGP_CHECK_ARG(r0 % (2 * BM) == 0, NCGP_DIMENSION_MISMATCH,
                  "row_begin must be a multiple of %d for the tcgen05 operator", 2 * BM);
   const Layout L = layout_of(op->n_rows, op->n_cols, op->d, op->w_max, op->sms);
@@ -1191,7 +1200,9 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, void* out, int64_t
   p.L = (float)(log2(op->s2) + s_exp);  // RBF clamp / Matern exponent offset
   p.col_exp = col_exp;
   p.out_f64 = op->dtype == NCGP_F64;
-  p.out = static_cast<uint8_t*>(out) + r0 * ldo * (p.out_f64 ? 8 : 4);
+  p.n_out = out.n;
+  for (int k = 0; k < out.n; ++k)
+    p.outs[k] = static_cast<uint8_t*>(out.p[k]) + r0 * ldo * (p.out_f64 ? 8 : 4);
   p.ldo = ldo;
   p.partial = op->partial;
   p.trace = g_trace;
@@ -1245,10 +1256,10 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, void* out, int64_t
     const int64_t tot = p.nloc * w;
     if (p.out_f64)
       reduce_partial_kernel<double><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
-          p.partial, p.splits, p.nloc, w, static_cast<double*>(p.out), ldo);
+          p.partial, p.splits, p.nloc, w, ncgp::out_ptrs<double>(out, r0, ldo), ldo);
     else
       reduce_partial_kernel<float><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
-          p.partial, p.splits, p.nloc, w, static_cast<float*>(p.out), ldo);
+          p.partial, p.splits, p.nloc, w, ncgp::out_ptrs<float>(out, r0, ldo), ldo);
     NCGP_LAUNCHED();
   }
   return NCGP_OK;

@@ -16,7 +16,7 @@ from __future__ import annotations
 
 import enum
 from dataclasses import dataclass
-from typing import Dict, List, Optional, Tuple
+from typing import Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
 import torch
@@ -150,7 +150,11 @@ class PriorOperator:
         return self.groups[0][0].impl
 
     def apply(self, v: torch.Tensor, out: Optional[torch.Tensor] = None,
-              row_begin: int = 0, row_end: Optional[int] = None) -> torch.Tensor:
+              row_begin: int = 0, row_end: Optional[int] = None,
+              peers: Optional[Sequence[torch.Tensor]] = None) -> torch.Tensor:
+        """K v over rows [row_begin, row_end).  ``peers``: further (n_rows, C)
+        buffers (other ranks' gather buffers mapped into this process) that
+        receive the same rows; the K1 epilogue stores into all of them."""
         C = self.C
         flat = v.dim() == 1
         if (v.numel() != self.n_cols * C):
@@ -159,20 +163,23 @@ class PriorOperator:
         if out is None:
             out = torch.empty((self.n_rows, C), dtype=self.dtype, device=V.device)
         O = out.view(self.n_rows, C)
+        P = [p.view(self.n_rows, C) for p in peers] if peers else None
         with nvtx_range("K product"):
-            self._apply_groups(V, O, C, row_begin, row_end)
+            self._apply_groups(V, O, C, row_begin, row_end, P)
         self.matvecs += 1
         return out.reshape(-1) if flat else out
 
-    def _apply_groups(self, V, O, C, row_begin, row_end):
+    def _apply_groups(self, V, O, C, row_begin, row_end, peers=None):
+        r1 = self.n_rows if row_end is None else row_end
         for op, cols in self.groups:
             if len(cols) == C:
-                op.apply(V, out=O, row_begin=row_begin, row_end=row_end)
+                op.apply(V, out=O, row_begin=row_begin, row_end=row_end, peers=peers)
             else:
                 idx = torch.tensor(cols, device=V.device)
                 sub = op.apply(V.index_select(1, idx).contiguous(),
                                row_begin=row_begin, row_end=row_end)
-                O[:, cols] = sub
+                for dst in [O] + list(peers or ()):
+                    dst[row_begin:r1, cols] = sub[row_begin:r1]
 
     __call__ = apply
 

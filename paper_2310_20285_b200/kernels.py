@@ -8,6 +8,7 @@ contiguous (stride (ld, 1)); it is what the C ABI calls column b at
 
 from __future__ import annotations
 
+import ctypes
 from typing import Optional, Sequence, Tuple
 
 import torch
@@ -72,8 +73,13 @@ class KernelOperator:
             N.query("ncgp_kop_impl", h)]
 
     def apply(self, V: torch.Tensor, out: Optional[torch.Tensor] = None,
-              row_begin: int = 0, row_end: Optional[int] = None) -> torch.Tensor:
-        """K(X_rows[row_begin:row_end], X_cols) @ V for V of shape (n_cols, w)."""
+              row_begin: int = 0, row_end: Optional[int] = None,
+              peers: Optional[Sequence[torch.Tensor]] = None) -> torch.Tensor:
+        """K(X_rows[row_begin:row_end], X_cols) @ V for V of shape (n_cols, w).
+
+        ``peers``: further (n_rows, w) buffers with ``out``'s strides (other
+        ranks' gather buffers mapped into this process) that receive the same
+        rows from the same kernel (``ncgp_kop_apply_multi``)."""
         vec = V.dim() == 1
         if vec:
             V = V.unsqueeze(1)
@@ -91,11 +97,23 @@ class KernelOperator:
             out = out.view(-1, 1)
         ldv = V.stride(0) if V.shape[0] > 1 else w
         ldo = out.stride(0) if out.shape[0] > 1 else w
+        bases = [out.data_ptr()]
+        for p in peers or ():
+            p = p.view(-1, 1) if p.dim() == 1 else p
+            if tuple(p.shape) != tuple(out.shape) or p.stride() != out.stride() or \
+                    p.dtype != out.dtype:
+                raise N.DimensionMismatch("peer buffer shape / strides differ from the output")
+            bases.append(p.data_ptr())
+        es = V.element_size()
         for c0 in range(0, w, self.w_max):
             c1 = min(w, c0 + self.w_max)
-            es = V.element_size()
-            N.call("ncgp_kop_apply", self._h, V.data_ptr() + c0 * es, ldv, c1 - c0,
-                   out.data_ptr() + c0 * es, ldo, row_begin, row_end, stream())
+            if len(bases) == 1:
+                N.call("ncgp_kop_apply", self._h, V.data_ptr() + c0 * es, ldv, c1 - c0,
+                       out.data_ptr() + c0 * es, ldo, row_begin, row_end, stream())
+            else:
+                arr = (ctypes.c_void_p * len(bases))(*[b + c0 * es for b in bases])
+                N.call("ncgp_kop_apply_multi", self._h, V.data_ptr() + c0 * es, ldv, c1 - c0,
+                       arr, len(bases), ldo, row_begin, row_end, stream())
         return out[:, 0] if vec else out
 
     __call__ = apply

@@ -3,8 +3,10 @@
 SURVEY.md 8(e): output rows of K V are independent.  Each rank keeps the full
 inputs X (replicated, <= 200 MB at cfg5), computes a contiguous, 256-aligned
 block of output rows with the fused kernel-matmul directly into its slice of
-the gather buffer, and the blocks are all-gathered in place (NCCL over
-NVLink) so every rank holds the full product for the next solver step.  Solver state (v, r, s, z, d, Q, S, T) is replicated: the
+the gather buffer, and the blocks are exchanged so every rank holds the full
+product for the next solver step: either by the kernel itself, which stores
+each finished row into every rank's symmetric-memory gather buffer over
+NVLink (``gather="fused"``), or by an in-place NCCL all-gather after it.  Solver state (v, r, s, z, d, Q, S, T) is replicated: the
 vector work is O(N C R) against the O(N^2) operator, and replication keeps
 every rank's control flow (tolerance / breakdown exits) identical without
 extra collectives.
@@ -43,16 +45,50 @@ def row_partition(n: int, world: int, rank: int, align: int = ROW_ALIGN) -> Tupl
     return r0, r1, per
 
 
-class RowShardedOperator:
-    """y = K V with rows of K split across ranks and gathered with all_gather.
+class TorchSymmetricMemory:
+    """Peer-mapped gather buffers from ``torch.distributed._symmetric_memory``
+    (CUDA, NCCL process group): one buffer per rank, every rank's mapped into
+    every process over NVLink, plus a device-side cross-rank barrier."""
 
-    ``local_apply(V, out, row_begin, row_end)`` must write rows
-    [row_begin, row_end) of K V into ``out`` (an (n_rows, w) tensor); in
-    production it is :meth:`KernelOperator.apply` / :meth:`PriorOperator.apply`.
+    def __init__(self, group=None):
+        import torch.distributed._symmetric_memory as symm
+        self._symm = symm
+        self.group = group if group is not None else dist.group.WORLD
+
+    def alloc(self, shape, dtype, device):
+        """(own buffer, barrier(channel), [peer buffers in rank order, self excluded])."""
+        buf = self._symm.empty(shape, dtype=dtype, device=device)
+        hdl = self._symm.rendezvous(buf, self.group)
+        rank, world = dist.get_rank(self.group), dist.get_world_size(self.group)
+        peers = [hdl.get_buffer(r, shape, dtype) for r in range(world) if r != rank]
+        return buf, (lambda channel: hdl.barrier(channel=channel)), peers
+
+
+class RowShardedOperator:
+    """y = K V with rows of K split across ranks, every rank ending with all rows.
+
+    ``local_apply(V, out, row_begin, row_end, peers=None)`` must write rows
+    [row_begin, row_end) of K V into ``out`` (an (n_rows, w) tensor) and, when
+    ``peers`` is given, into each of those buffers too; in production it is
+    :meth:`KernelOperator.apply` / :meth:`PriorOperator.apply`.
+
+    Two exchange paths (``gather``):
+
+    - ``"nccl"`` (default): the rows land in this rank's slice of a gather
+      buffer and an in-place ``all_gather_into_tensor`` follows the kernel.
+    - ``"fused"``: the gather buffers are symmetric memory (``symm``; by
+      default :class:`TorchSymmetricMemory`), and the K1 epilogue stores each
+      finished row into every rank's buffer (``ncgp_kop_apply_multi``), so
+      the exchange overlaps the kernel instead of following it.  A barrier
+      before the kernel (the peers are done reading the previous product) and
+      one after it (every row has landed) replace the collective.
     """
 
     def __init__(self, n_rows: int, local_apply: Callable, group=None,
-                 dtype: torch.dtype = torch.float32, device=None):
+                 dtype: torch.dtype = torch.float32, device=None, gather: str = "nccl",
+                 symm=None):
+        if gather not in ("nccl", "fused"):
+            raise ValueError(f"gather must be 'nccl' or 'fused', got {gather!r}")
         self.n_rows = n_rows
         self.local_apply = local_apply
         self.group = group
@@ -61,7 +97,10 @@ class RowShardedOperator:
         self.r0, self.r1, self.per = row_partition(n_rows, self.world, self.rank)
         self.dtype = dtype
         self.device = device
+        self.gather = gather
+        self._symm_provider = symm
         self._bufs = {}
+        self._symm = {}
 
     def _buffer(self, w: int, device):
         key = (w, str(device))
@@ -71,24 +110,50 @@ class RowShardedOperator:
             self._bufs[key] = full
         return full
 
+    def symmetric(self, w: int, device):
+        """(own gather buffer, barrier, peers' buffers) for RHS width ``w``."""
+        key = (w, str(device))
+        hit = self._symm.get(key)
+        if hit is None:
+            if self._symm_provider is None:
+                self._symm_provider = TorchSymmetricMemory(self.group)
+            hit = self._symm_provider.alloc((self.per * self.world, w), self.dtype, device)
+            self._symm[key] = hit
+        return hit
+
+    def product(self, V2: torch.Tensor) -> torch.Tensor:
+        """All n_rows rows of K V2 as a view of the internal gather buffer
+        (valid until the next call)."""
+        w = V2.shape[1]
+        if self.gather == "fused":
+            full, barrier, peers = self.symmetric(w, V2.device)
+            barrier(0)   # every peer has consumed the previous product
+            self.local_apply(V2, full, self.r0, self.r1, peers=peers)
+            barrier(1)   # every rank's rows have landed everywhere
+        elif self.world == 1:
+            full = self._buffer(w, V2.device)
+            self.local_apply(V2, full, 0, self.n_rows)
+        else:
+            # rank r's rows [r0, r1) are rows [r * per, r * per + (r1 - r0)) of
+            # the gather buffer: the operator writes them in place and the
+            # gather runs in place (input = this rank's slice of the output)
+            full = self._buffer(w, V2.device)
+            self.local_apply(V2, full, self.r0, self.r1)
+            mine = full[self.rank * self.per:(self.rank + 1) * self.per]
+            dist.all_gather_into_tensor(full, mine, group=self.group)
+        return full[: self.n_rows]
+
     def apply(self, V: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         vec = V.dim() == 1
         V2 = V.view(-1, 1) if vec else V
         w = V2.shape[1]
-        if self.world == 1:
+        if self.world == 1 and self.gather == "nccl":
             dst = out.view(self.n_rows, w) if out is not None else torch.empty(
                 (self.n_rows, w), dtype=self.dtype, device=V2.device)
             self.local_apply(V2, dst, 0, self.n_rows)
             res = dst
         else:
-            # rank r's rows [r0, r1) are rows [r * per, r * per + (r1 - r0)) of the
-            # gather buffer: the operator writes them in place and the gather
-            # runs in place (input = this rank's slice of the output)
-            full = self._buffer(w, V2.device)
-            self.local_apply(V2, full, self.r0, self.r1)
-            mine = full[self.rank * self.per:(self.rank + 1) * self.per]
-            dist.all_gather_into_tensor(full, mine, group=self.group)
-            res = full[: self.n_rows]
+            res = self.product(V2)
             if out is not None:
                 out.view(self.n_rows, w).copy_(res)
                 res = out.view(self.n_rows, w)
@@ -104,7 +169,7 @@ class ShardedPriorOperator:
     the block-diagonal prior product on CN vectors, row-sharded across the
     ranks of ``group``."""
 
-    def __init__(self, prior, X, dtype=None, group=None):
+    def __init__(self, prior, X, dtype=None, group=None, gather: str = "nccl", symm=None):
         from .gp import PriorOperator
         self.inner = PriorOperator(prior, X, dtype=dtype)
         self.C = self.inner.C
@@ -113,14 +178,15 @@ class ShardedPriorOperator:
         self.matvecs = 0
         C = self.C
 
-        def local_apply(V, out, r0, r1):
+        def local_apply(V, out, r0, r1, peers=None):
             # ``out`` may be the (per * world)-row gather buffer: rows >= n_rows
             # are padding and never written
-            self.inner.apply(V.reshape(-1), out=out[: self.n_rows].reshape(-1),
-                             row_begin=r0, row_end=r1)
+            n = self.n_rows
+            self.inner.apply(V.reshape(-1), out=out[:n].reshape(-1), row_begin=r0, row_end=r1,
+                             peers=[p[:n].reshape(-1) for p in peers] if peers else None)
 
         self.sharded = RowShardedOperator(self.n_rows, local_apply, group=group,
-                                          dtype=self.dtype)
+                                          dtype=self.dtype, gather=gather, symm=symm)
         self._C = C
 
     @property

@@ -6,6 +6,8 @@ fp64 path within 1e-12 (it replays the reference arithmetic per entry and
 differs only in the order of the long j-sum).
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -228,3 +230,94 @@ def test_prior_matvec_cache_sees_in_place_updates():
     b = P.prior_matvec(prior, X, v, dtype=torch.float64)
     ref = O.prior_matvec([("rbf", 1.0, 1.0)] * 2, X, v)
     assert rel(b, ref) < 1e-12 and rel(a, ref) > 1e-3
+
+
+@pytest.mark.parametrize("impl", ["tcgen05", "simt"])
+@pytest.mark.parametrize("n,w", [(3000, 16), (40_000, 40)])
+def test_multi_destination_store_is_the_fused_gather(impl, n, w):
+    """ncgp_kop_apply_multi (the all-gather fused into K1's store): every
+    destination receives bitwise the rows a plain apply writes, each shard
+    only its own rows.  n=3000 takes the split-partial reduction path, n=40k
+    the in-kernel store; w=40 loops two RHS column blocks."""
+    rng = np.random.default_rng(5)
+    X = rng.standard_normal((n, 8))
+    V = torch.from_numpy(rng.standard_normal((n, w))).to("cuda", torch.float32)
+    op, _ = op_for(("rbf", 1.5, 1.0), X, torch.float32, impl=impl, w=32)
+    assert op.impl == impl
+    ref = op.apply(V)
+    bufs = [torch.full_like(ref, float("nan")) for _ in range(3)]
+    cuts = [0, (n // 3) // 256 * 256, (2 * n // 3) // 256 * 256, n]
+    for r0, r1 in zip(cuts[:-1], cuts[1:]):  # three "ranks", each storing to all buffers
+        op.apply(V, out=bufs[0], row_begin=r0, row_end=r1, peers=bufs[1:])
+    for b in bufs:
+        assert torch.equal(b, ref)
+    # one shard alone touches only its rows in every destination
+    fresh = [torch.full_like(ref, float("nan")) for _ in range(2)]
+    op.apply(V, out=fresh[0], row_begin=cuts[1], row_end=cuts[2], peers=fresh[1:])
+    for b in fresh:
+        assert torch.equal(b[cuts[1]:cuts[2]], ref[cuts[1]:cuts[2]])
+        assert bool(torch.isnan(b[:cuts[1]]).all()) and bool(torch.isnan(b[cuts[2]:]).all())
+
+
+def test_multi_destination_store_validates_peers():
+    X = np.random.default_rng(0).standard_normal((300, 4))
+    op, _ = op_for(("rbf", 1.0, 1.0), X, torch.float32)
+    V = torch.ones((300, 4), device="cuda")
+    out = torch.empty((300, 4), device="cuda")
+    with pytest.raises(P.DimensionMismatch):
+        op.apply(V, out=out, peers=[torch.empty((300, 5), device="cuda")])
+    with pytest.raises(P.InvalidInput):
+        op.apply(V, out=out, peers=[torch.empty_like(out) for _ in range(8)])  # 9 > 8 outputs
+
+
+def test_prior_operator_peers_with_per_class_specs():
+    """Mixed per-class specs go through the index_select path; peers still
+    receive exactly the shard's rows."""
+    g = golden("matvec_mixed")
+    specs = [P.KernelSpec(*s) for s in specs_from(g["specs"])]
+    prior = P.MultiOutputPrior(kernels=tuple(specs))
+    from paper_2310_20285_b200.gp import PriorOperator
+    op = PriorOperator(prior, g["X"], dtype=torch.float32)
+    v = torch.from_numpy(g["v"]).float().cuda()
+    ref = op.apply(v)
+    n = op.n_rows
+    out = torch.full_like(ref, float("nan"))
+    peer = torch.full_like(ref, float("nan"))
+    r1 = min(n, 256)
+    op.apply(v, out=out, row_begin=0, row_end=r1, peers=[peer])
+    op.apply(v, out=out, row_begin=r1, row_end=n, peers=[peer])
+    assert torch.equal(out, ref) and torch.equal(peer, ref)
+
+
+def test_fused_gather_symmetric_memory_single_rank(tmp_path):
+    """torchrun world=1, NCCL: ShardedPriorOperator(gather='fused') goes
+    through torch symmetric memory (rendezvous, peer mapping, device
+    barriers) and matches the unsharded product bitwise."""
+    import subprocess
+    import sys
+    script = tmp_path / "symm_run.py"
+    script.write_text(
+        "import os, sys, numpy as np, torch, torch.distributed as dist\n"
+        f"sys.path.insert(0, {repr(str(__import__('pathlib').Path(__file__).resolve().parents[1]))})\n"
+        "import paper_2310_20285_b200 as P\n"
+        "from paper_2310_20285_b200.parallel import ShardedPriorOperator\n"
+        "torch.cuda.set_device(0)\n"
+        "dist.init_process_group('nccl')\n"
+        "rng = np.random.default_rng(1)\n"
+        "X = rng.standard_normal((5000, 8)).astype(np.float32)\n"
+        "prior = P.MultiOutputPrior(kernels=(P.KernelSpec('rbf', 1.5, 1.0),) * 3)\n"
+        "v = torch.from_numpy(rng.standard_normal(5000 * 3)).float().cuda()\n"
+        "a = ShardedPriorOperator(prior, X, dtype=torch.float32, gather='fused')\n"
+        "b = ShardedPriorOperator(prior, X, dtype=torch.float32, gather='nccl')\n"
+        "ra = a(v); ra2 = a(2 * v); rb = b(v)\n"
+        "torch.cuda.synchronize()\n"
+        "assert torch.equal(ra, rb), float((ra - rb).abs().max())\n"
+        "assert torch.equal(ra2, b(2 * v))\n"
+        "dist.destroy_process_group()\n"
+        "print('SYMM_OK')\n")
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "1", "--master-addr", "127.0.0.1",
+                        "--master-port", "29631", str(script)],
+                       capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0 and "SYMM_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]

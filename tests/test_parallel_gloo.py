@@ -77,3 +77,82 @@ def test_two_rank_gather_matches_single_process(tmp_path, n):
         np.testing.assert_array_equal(got, ref)
         gv = np.load(tmp_path / f"v{r}.npy")
         np.testing.assert_array_equal(gv, ref[:, 0])
+
+
+class _FileSymmetricMemory:
+    """CPU stand-in for TorchSymmetricMemory: each rank's gather buffer is a
+    shared file mapping that every other rank maps too, so peer stores are
+    real cross-process writes; the barrier is a gloo barrier."""
+
+    def __init__(self, root):
+        self.root = root
+
+    def alloc(self, shape, dtype, device):
+        rank, world = dist.get_rank(), dist.get_world_size()
+        numel = int(np.prod(shape))
+
+        def mapped(r):
+            path = os.path.join(self.root, f"symm_{shape[1]}_{r}.bin")
+            return torch.from_file(path, shared=True, size=numel, dtype=dtype).view(shape)
+
+        own = mapped(rank)
+        own.fill_(float("nan"))  # every row must be written by some rank
+        dist.barrier()
+        peers = [mapped(r) for r in range(world) if r != rank]
+        return own, (lambda channel: dist.barrier()), peers
+
+
+def _fused_worker(rank, world, port, n, d, w, result_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import ncgp_oracle as O
+        rng = np.random.default_rng(0)
+        X = rng.standard_normal((n, d))
+        V = rng.standard_normal((n, w))
+        spec = ("rbf", 1.2, 1.0)
+        writes = []
+
+        def local_apply(Vt, out, r0, r1, peers=None):
+            writes.append((r0, r1, len(peers or ())))
+            if r1 > r0:
+                blk = torch.from_numpy(
+                    O.kernel_matmul_rows(spec, X[r0:r1], X, Vt.double().numpy())).to(out.dtype)
+                for dst in [out] + list(peers or ()):
+                    dst[r0:r1] = blk
+
+        op = RowShardedOperator(n, local_apply, dtype=torch.float64, gather="fused",
+                                symm=_FileSymmetricMemory(result_dir))
+        res = op.apply(torch.from_numpy(V))
+        np.save(os.path.join(result_dir, f"f{rank}.npy"), res.numpy())
+        # a second product reuses the mapped buffers (barrier before the stores)
+        res2 = op.apply(torch.from_numpy(2.0 * V))
+        np.save(os.path.join(result_dir, f"g{rank}.npy"), res2.numpy())
+        r0, r1, _ = row_partition(n, world, rank)
+        assert writes == [(r0, r1, world - 1)] * 2, writes
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [300, 1000])
+def test_two_rank_fused_peer_stores_match_single_process(tmp_path, n):
+    """gather='fused': each rank stores its rows into every rank's buffer; no
+    collective moves data, and every rank ends with the full product."""
+    from oracle import ncgp_oracle as O
+    d, w, world = 3, 4, 2
+    mp.spawn(_fused_worker, args=(world, _free_port(), n, d, w, str(tmp_path)), nprocs=world,
+             join=True)
+    rng = np.random.default_rng(0)
+    X = rng.standard_normal((n, d))
+    V = rng.standard_normal((n, w))
+    ref = O.kernel_matmul_rows(("rbf", 1.2, 1.0), X, X, V)
+    for r in range(world):
+        np.testing.assert_array_equal(np.load(tmp_path / f"f{r}.npy"), ref)
+        np.testing.assert_array_equal(np.load(tmp_path / f"g{r}.npy"),
+                                      O.kernel_matmul_rows(("rbf", 1.2, 1.0), X, X, 2.0 * V))
+
+
+def test_gather_mode_is_validated():
+    with pytest.raises(ValueError):
+        RowShardedOperator(10, lambda *a, **k: None, gather="bogus")

@@ -6,13 +6,21 @@ sys.path.insert(0, ".")
 from paper_2310_20285_b200 import _native
 from paper_2310_20285_b200.kernels import KernelOperator
 torch.cuda.set_device(0)
-n = 200_000
+import argparse
+ap = argparse.ArgumentParser()
+ap.add_argument("--n", type=int, default=200_000)
+ap.add_argument("--d", type=int, default=8)
+ap.add_argument("--w", type=int, default=32)
+ap.add_argument("--ell", type=float, default=1.5)
+ap.add_argument("--families", default="rbf,matern32")
+args = ap.parse_args()
+n = args.n
 lib = _native.load()
-for fam in ("rbf", "matern32"):
+for fam in args.families.split(","):
     rng = np.random.default_rng(0)
-    X = torch.from_numpy(rng.standard_normal((n, 8))).float().cuda()
-    S = torch.from_numpy(rng.standard_normal((n, 32))).float().cuda()
-    op = KernelOperator(fam, 1.5, 1.0, X, w_max=32, impl="tcgen05")
+    X = torch.from_numpy(rng.standard_normal((n, args.d))).float().cuda()
+    S = torch.from_numpy(rng.standard_normal((n, args.w))).float().cuda()
+    op = KernelOperator(fam, args.ell, 1.0, X, w_max=args.w, impl="tcgen05")
     for mode, name in ((0, "full"), (1, "no epilogue TMEM/MUFU"), (2, "no GEMM2"), (3, "no GEMM1"), (5, "no copies, no epilogue"), (6, "no GEMMs (sync + epilogue)")):
         lib.ncgp_debug_set_mode(mode)
         op.apply(S); torch.cuda.synchronize()
