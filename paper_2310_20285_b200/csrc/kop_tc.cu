@@ -3,7 +3,7 @@
 //
 // One CTA pair (cluster of 2, cta_group::2 MMAs with M = 256) per two SMs;
 // each CTA owns a 128-row tile and both sweep the same column tiles.
-// Roles per CTA (16 warps):
+// Roles per CTA (24 warps; registers rebalanced per warpgroup with setmaxnreg):
 //   warp 0 lane 0 producer: the CTA's row tile + its half of each XB column
 //                 tile (1-D bulk copies, cp.async.bulk -> UBLKCP).
 //   warp 3 lane 0 producer: the CTA's half of each V column tile.
@@ -18,11 +18,14 @@
 //                   GEMM2(t-3) completed (it overwrites that S/P buffer).
 //                 Two issuing warps because one thread issues a tcgen05.mma
 //                 only every ~46 cycles (tools/mma_queue_probe.cu).
-//   warps 4-11    two epilogue warpgroups, alternating column tiles:
-//                 TMEM -> regs, kernel transform (ex2 for RBF, sqrt + ex2 for
-//                 Matern), fp16 hi/lo split, regs -> TMEM over S (P aliases S).
-//   warps 12-15   correction warpgroup: drains O every CH column tiles into
-//                 fp64 shared-memory accumulators, scales, writes rows.
+//   warps 4-19    four epilogue warpgroups in two groups of 8 warps that
+//                 alternate column tiles (each warp: one TMEM lane quarter,
+//                 one 64-column half): TMEM -> regs, kernel transform (ex2 for
+//                 RBF, sqrt + ex2 for Matern), fp16 hi/lo split, regs -> TMEM
+//                 over S (P aliases S).  96 registers each.
+//   warps 20-23   correction warpgroup: drains O every CH column tiles into
+//                 fp64 shared-memory accumulators, scales, writes rows (to
+//                 every destination of a fused-gather launch).
 // cta_group::2 splits B by rows: CTA0 supplies B rows [0, N/2), CTA1 rows
 // [N/2, N), each at the same shared-memory offset (tools/mma2sm_layout.cu),
 // so CTA0 holds [XB rows 0-63 | Vhi | Vhi rows 0..WP/2) and CTA1

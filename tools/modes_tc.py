@@ -21,7 +21,8 @@ for fam in args.families.split(","):
     X = torch.from_numpy(rng.standard_normal((n, args.d))).float().cuda()
     S = torch.from_numpy(rng.standard_normal((n, args.w))).float().cuda()
     op = KernelOperator(fam, args.ell, 1.0, X, w_max=args.w, impl="tcgen05")
-    for mode, name in ((0, "full"), (1, "no epilogue TMEM/MUFU"), (2, "no GEMM2"), (3, "no GEMM1"), (5, "no copies, no epilogue"), (6, "no GEMMs (sync + epilogue)")):
+    for mode, name in ((0, "full"), (1, "no epilogue TMEM/MUFU"), (2, "no GEMM2"), (3, "no GEMM1"), (5, "no copies, no epilogue"), (6, "no GEMMs (sync + epilogue)"),
+                       (4, "no column copies"), (8, "no XB copies"), (9, "no V copies")):
         lib.ncgp_debug_set_mode(mode)
         op.apply(S); torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
