@@ -1030,11 +1030,30 @@ struct Layout {
   int64_t tile_stride, row_tiles, col_tiles;
 };
 
+// Column splits per row-tile pair.  Items (pair, column range) are dealt
+// round-robin to the persistent clusters, so the slowest cluster runs
+// ceil(items / clusters) of them; each item also restarts the pipeline (about
+// one tile).  Pick the split count that minimises that critical path: at
+// N = 1e5 one item per pair leaves the last wave 28 % full.  Depends only on
+// the operator's full shape, so every row shard reduces in the same order.
 int splits_for(int64_t pairs, int64_t col_tiles, int clusters) {
-  if (pairs >= 2 * clusters) return 1;
-  int64_t s = (2 * clusters + pairs - 1) / pairs;
-  if (s > col_tiles) s = col_tiles;
-  return (int)(s < 1 ? 1 : s);
+  auto cost = [&](int64_t s) {  // < 0: this s yields the same split as a smaller one
+    const int64_t tps = (col_tiles + s - 1) / s;
+    if ((col_tiles + tps - 1) / tps != s) return -1.0;
+    return (double)((pairs * s + clusters - 1) / clusters) * (double)(tps + 1);
+  };
+  const int64_t smax = std::min<int64_t>(col_tiles, 64);
+  double best = 1e300;
+  for (int64_t s = 1; s <= smax; ++s) {
+    const double c = cost(s);
+    if (c >= 0 && c < best) best = c;
+  }
+  // the fewest splits within 1 % of the best (fewer partial rows to reduce)
+  for (int64_t s = 1; s <= smax; ++s) {
+    const double c = cost(s);
+    if (c >= 0 && c <= best * 1.01) return (int)s;
+  }
+  return 1;
 }
 
 Layout layout_of(int64_t n_rows, int64_t n_cols, int d, int w_max, int sms) {
@@ -1060,8 +1079,10 @@ Layout layout_of(int64_t n_rows, int64_t n_cols, int d, int w_max, int sms) {
   L.bits = take(64 * sizeof(unsigned));
   L.xa = take((size_t)L.row_tiles * L.a_bytes);
   L.col = take((size_t)L.col_tiles * L.tile_stride);
-  // partial rows when splits > 1: splits * local rows <= 4 * sms * 128
-  L.partial = take((size_t)4 * sms * BM * w_max * sizeof(double));
+  // fp64 partial rows [splits][rows][w] when a pair's columns are split
+  const int sp = splits_for(L.row_tiles / 2, L.col_tiles, std::max(1, sms / 2));
+  L.partial = take((size_t)(sp > 1 ? sp : 0) * (size_t)(L.row_tiles * BM) * w_max *
+                   sizeof(double) + 256);
   L.total = off;
   return L;
 }

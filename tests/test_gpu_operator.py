@@ -141,10 +141,13 @@ def test_linearity_and_symmetry_fp32():
     Ka, Kb = op.apply(a), op.apply(b)
     Kab = op.apply(2.0 * a - 3.0 * b)
     assert float((Kab - (2 * Ka - 3 * Kb)).norm() / Kab.norm()) < 1e-5
-    # u'Kv = v'Ku
+    # u'Kv = v'Ku, up to the operator's per-entry error (<= 1e-6 of |K||v|,
+    # measured 6e-7: tools/sym_check.py), summed against |u|: the bound is
+    # 1e-6 |u|'K|v|.  uKv itself cancels heavily (|uKv| ~ 1e-3 |u|'K|v|).
     uKv = float((a.double() * Kb.double()).sum())
     vKu = float((b.double() * Ka.double()).sum())
-    assert abs(uKv - vKu) <= 1e-5 * (abs(uKv) + 1.0)
+    scale = float((a.abs().double() * op.apply(b.abs()).double()).sum())
+    assert abs(uKv - vKu) <= 1e-6 * scale, (uKv, vKu, scale)
 
 
 def test_errors_are_mapped():
