@@ -26,6 +26,10 @@ struct ncgp_kop {
   double* col_scale;    // per RHS column power-of-two scale (wpad)
   double* partial;      // fp64 partial sums
   double k_scale;       // 2^s prescale of kernel values
+  // symmetric kernel (Xr == Xc): work list and fp32 accumulator (kop_tc.cu)
+  int64_t sym_items;
+  int4* sym_tab;
+  float* sym_acc;
 };
 
 namespace ncgp {

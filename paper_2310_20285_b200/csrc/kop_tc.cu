@@ -47,6 +47,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <vector>
 
 #include "kop.cuh"
 
@@ -68,6 +70,7 @@ constexpr int TMEM_COLS = 512;
 constexpr int NS = 3;            // S/P buffers in TMEM (3 x 128 columns)
 constexpr int NR = 12;           // s_full / rdy rings: >= max wait lag (XB depth, V depth, 4)
 constexpr int TRACE_TILES = 256, TRACE_EV = 12;
+constexpr uint32_t PBUF = 2u * BM * BN * 2u;  // symmetric kernel: one [P_hi | P_lo] buffer (64 KB)
 
 // ------------------------------------------------------------------ PTX
 
@@ -263,6 +266,20 @@ __device__ __forceinline__ void tmem_wait_ld(uint32_t (&r)[32]) {
       :
       : "memory");
 }
+__device__ __forceinline__ void st_shared_v4(uint32_t saddr, uint32_t a, uint32_t b, uint32_t c,
+                                             uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(saddr), "r"(a), "r"(b), "r"(c),
+               "r"(d)
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void red_add_v4(float* gaddr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(gaddr), "f"(a), "f"(b),
+               "f"(c), "f"(d)
+               : "memory");
+}
 __device__ __forceinline__ void tmem_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
@@ -324,6 +341,11 @@ struct TcParams {
   int na;                // row-tile buffers in shared memory (1 or 2)
   int sx, sv;            // XB ring depth (3 or 6), V ring depth (6 or 9)
   long long* trace;      // debug: per-tile timestamps of cluster 0 (nullptr in production)
+  int n_items;           // work items: pairs * splits, or the symmetric item table's length
+  const int4* item_tab;  // symmetric kernel: (row-tile pair, c0, c1, -) per item
+  float* acc;            // symmetric kernel: fp32 output accumulator [row][WP], zeroed
+  int sym_dbg;           // symmetric kernel debug: 1 = drop D_T flushes, 2 = drop O flushes
+  float* sym_dump;       // symmetric kernel debug: raw D_T per (pair, tile, rank) when set
   int debug_mode;        // debug (timing only, wrong results): 1 = epilogue skips TMEM traffic,
                          // 2 = no GEMM2, 3 = no GEMM1, 4 = no column copies (8: XB only, 9: V only)
 };
@@ -340,6 +362,13 @@ struct Item {
 
 __device__ __forceinline__ Item item_of(const TcParams& p, int it) {
   Item r;
+  if (p.item_tab != nullptr) {
+    const int4 t = p.item_tab[it];
+    r.pp = t.x;
+    r.c0 = t.y;
+    r.c1 = t.z;
+    return r;
+  }
   r.pp = it / p.splits;
   const int sp = it - r.pp * p.splits;
   r.c0 = sp * (int)p.tiles_per_split;
@@ -371,6 +400,9 @@ struct TileIter {
     }
   }
   __device__ __forceinline__ bool first_in_item() const { return ct == cur.c0; }
+  // symmetric kernel: this tile's P also serves the transposed product
+  // (column tiles right of the pair's 256 x 256 diagonal block)
+  __device__ __forceinline__ bool transposed() const { return ct >= 2 * cur.pp + 2; }
   __device__ __forceinline__ bool last_in_item() const { return ct == cur.c1 - 1; }
   __device__ __forceinline__ bool first_in_chunk() const {
     return ct == cur.c0 || (ct & (CH - 1)) == 0;
@@ -434,22 +466,26 @@ __device__ __forceinline__ void transform_chunk(const uint32_t (&r)[32], float L
   }
 }
 
-template <int FAM, int WP, bool DBG>
+template <int FAM, int WP, bool DBG, bool SYM>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     kop_tc_kernel(const TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cta_rank();
-  const int items = (int)(p.pairs * p.splits);
+  const int items = p.n_items;
 
   // ---- shared-memory carve-up (identical offsets in both CTAs)
   const uint32_t vslot = p.v2_bytes + p.v3_bytes;       // this CTA's V half
   uint8_t* sA = smem;                                   // na x a_bytes (own row tile)
   uint8_t* sXB = sA + (size_t)p.na * p.a_bytes;         // sx x xbh_bytes
   uint8_t* sV = sXB + (size_t)p.sx * p.xbh_bytes;       // sv x vslot
-  double* sAcc = reinterpret_cast<double*>(sV + (size_t)p.sv * vslot);  // [WP][128]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sAcc + WP * BM);
+  // symmetric kernel: this CTA's own V block [Vhi | Vlo] (the transposed
+  // product's B) and two P buffers [P_hi | P_lo] (its MN-major A)
+  uint8_t* sVI = sV + (size_t)p.sv * vslot;
+  uint8_t* sP = sVI + (SYM ? 2 * (size_t)p.v2_bytes : 0);
+  double* sAcc = reinterpret_cast<double*>(sP + (SYM ? 2 * (size_t)PBUF : 0));  // [WP][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sAcc + (SYM ? 0 : WP * BM));
   uint64_t* xb_land = bars;               // [6]   local copy completion
   uint64_t* v_land = xb_land + 6;         // [9]   local copy completion
   uint64_t* a_land = v_land + 9;          // [2]   local copy completion
@@ -466,7 +502,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   uint64_t* o_full = s_full + NR;         // [2]   both: O chunk complete (multicast)
   uint64_t* o_empty = o_full + 2;         // [2]   leader: O drained (8 warp arrivals)
   uint64_t* g2done = o_empty + 2;         // [NR]  leader: GEMM2 of a step done (commit)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(g2done + NR);
+  uint64_t* vi_land = g2done + NR;        // [1]   SYM: local V block landed
+  uint64_t* vi_full = vi_land + 1;        // [1]   SYM leader: both V blocks landed
+  uint64_t* vi_empty = vi_full + 1;       // [1]   SYM both: V block free (multicast commit)
+  uint64_t* pt_free = vi_empty + 1;       // [2]   SYM both: P buffer free (multicast commit)
+  uint64_t* dt_full = pt_free + 2;        // [1]   SYM both: transposed product done
+  uint64_t* dt_empty = dt_full + 1;       // [1]   SYM leader: D_T drained (8 warp arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dt_empty + 1);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < 6; ++s) mbar_init(&xb_land[s], 1);
@@ -483,7 +525,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       mbar_init(&a_empty[b], 1);
       mbar_init(&o_full[b], 1);
       mbar_init(&o_empty[b], 8);
+      mbar_init(&pt_free[b], 1);
     }
+    mbar_init(vi_land, 1);
+    mbar_init(vi_full, 2);
+    mbar_init(vi_empty, 1);
+    mbar_init(dt_full, 1);
+    mbar_init(dt_empty, 8);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -497,28 +545,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   cluster_sync();  // barriers of both CTAs initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // TMEM columns: S/P buffers [0, 384), O double buffer [384, 384 + 4 WP)
+  // TMEM columns: S/P buffers [0, 384), O double buffer [384, 384 + 4 WP);
+  // symmetric kernel: single O [384, 384 + 2 WP), D_T [384 + 2 WP, 384 + 4 WP)
   auto tS = [&](int b) -> uint32_t { return tmem + (uint32_t)(b * BN); };
   auto tO = [&](int b) -> uint32_t { return tmem + (uint32_t)(NS * BN + b * 2 * WP); };
+  const uint32_t tDT = tmem + (uint32_t)(NS * BN + 2 * WP);
+  constexpr uint32_t NO = SYM ? 1u : 2u;  // O buffers
   const int64_t half_off = (int64_t)rank * p.rec_bytes;   // this CTA's half of a record
 
   // setmaxnreg sits at the top of each warpgroup's branch so that ptxas sees
   // one register budget per region (a shared prologue would cap all at 40).
   if (warp < 4) {
   asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
-  if (warp == 0 || warp == 3) {
+  if (warp == 0 || (!SYM && warp == 3)) {
     // ================= producers (lane 0) and relays (lane 1) =================
+    // (symmetric kernel: all four in warp 0 -- lanes 0/1 XB, lanes 2/3 V --
+    // so warp 3 can issue the transposed product)
     // Slot reuse is signalled by GEMM1 completions (s_full, one multicast commit
     // per tile): XB slot g mod sx is free once GEMM1(g - sx) completed; V slot
     // g mod sv once GEMM2(g - sv) did, which the in-order tensor pipe finishes
     // before GEMM1(g - sv + NS).  s_full has NR >= max(sx, sv) entries so no
     // waiter can lag two phases.  Relays forward this CTA's copy completions
     // to the leader CTA's barriers (the MMA consumes both CTAs' halves).
-    const bool is_x = (warp == 0);
+    const bool is_x = SYM ? (lane < 2) : (warp == 0);
+    const int role = SYM ? (lane < 4 ? (lane & 1) : lane - 2) : lane;  // 0/1 producer/relay
+    // (symmetric kernel: lane 4 loads this CTA's own V block per item, lane 5
+    // relays it; separate loops, because vi_empty depends on rdy, which
+    // depends on the XB stream running ahead)
     const uint32_t depth = is_x ? (uint32_t)p.sx : (uint32_t)p.sv;
     const uint32_t lagt = is_x ? (uint32_t)p.sx : (uint32_t)(p.sv - NS);  // tile g - lagt
     uint64_t* land = is_x ? xb_land : v_land;
-    if (lane == 0) {
+    if (role == 0) {
       TileIter ti;
       ti.start(p, items);
       Ring r, sr;
@@ -554,7 +611,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         ++g;
         ti.next(p, items);
       }
-    } else if (lane == 1) {
+    } else if (SYM && role == 2) {
+      uint32_t nitem = 0;
+      for (int it = (int)(blockIdx.x >> 1); it < items; it += (int)(gridDim.x >> 1), ++nitem) {
+        const Item cur = item_of(p, it);
+        mbar_wait(vi_empty, (nitem & 1u) ^ 1u);
+        mbar_expect_tx(vi_land, 2 * p.v2_bytes);
+        // Vhi of column tile rt sits in the record's CTA0 half, Vlo in its CTA1 half
+        const int64_t rt = p.rt0 + 2 * (int64_t)cur.pp + rank;
+        const int64_t vb = rt * p.tile_stride + p.xbh_bytes;
+        bulk_g2s(sVI, p.col_pack + vb, p.v2_bytes, vi_land);
+        bulk_g2s(sVI + p.v2_bytes, p.col_pack + vb + p.rec_bytes, p.v2_bytes, vi_land);
+      }
+    } else if (SYM && role == 3) {
+      uint32_t nitem = 0;
+      for (int it = (int)(blockIdx.x >> 1); it < items; it += (int)(gridDim.x >> 1), ++nitem) {
+        mbar_wait(vi_land, nitem & 1u);
+        mbar_arrive_cluster(leader_addr(vi_full));
+      }
+    } else if (role == 1) {
       TileIter ti;
       ti.start(p, items);
       Ring r, rr;
@@ -589,7 +664,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           rr.adv();
         }
     }
-  } else if (warp == 1 || warp == 2) {
+  } else if (warp == 1 || warp == 2 || (SYM && warp == 3)) {
     // ================= MMA issuers (leader CTA; whole warp, elected lane issues) =====
     // One thread issues a tcgen05.mma only every ~46 cycles and blocks once
     // the ~7-deep tensor queue is full (tools/mma_queue_probe.cu), so the two
@@ -649,7 +724,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           if (dx == xend) dx = dX0;
           look.next(p, items);
         }
-      } else {
+      } else if (warp == 1) {
         // ---------------- GEMM2 issuer
         const uint64_t dV0 = sdesc(smem_u32(sV), 128u, (uint32_t)(BN * 16));
         const uint64_t vstep = vslot >> 4, vend = dV0 + (uint64_t)p.sv * vstep;
@@ -662,8 +737,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           const bool fresh = cur.first_in_chunk(), last = cur.last_in_chunk();
           if (lane == 0) trace_ev<DBG>(p, gt, 11);
           mbar_wait(&rdy[r], rph);  // P(g), V(g) (and XB(g + NS)) present
-          const uint32_t ob = q & 1u;
-          if (fresh) mbar_wait(&o_empty[ob], ((q >> 1) & 1u) ^ 1u);
+          const uint32_t ob = SYM ? 0u : (q & 1u);
+          if (fresh) mbar_wait(&o_empty[ob], ((q / NO) & 1u) ^ 1u);
           tc_fence_after();
           if (lane == 0) trace_ev<DBG>(p, gt, 0);
           // GEMM2: P_hi x [Vhi | Vlo] (N = 2 WP: CTA0 supplies Vhi, CTA1 Vlo), then
@@ -694,6 +769,53 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           ++gt;
           cur.next(p, items);
         }
+      } else if (SYM) {
+        // ---------------- transposed-product issuer (symmetric kernel)
+        // D_T[j, :] += P(t)^T [V_I0 | V_I1]: A = P^T from each CTA's shared
+        // memory (MN-major: the K-major bytes of P read transposed), B split
+        // along N so each CTA supplies its own V block; CTA c's lanes keep
+        // columns [c WP, (c + 1) WP) -- its rows' contribution to out_J.
+        const uint32_t idT = idesc_f16(2 * WP) | (1u << 15);
+        const uint64_t dP0 = sdesc(smem_u32(sP), 2048u, 128u);
+        const uint64_t dVh = sdesc(smem_u32(sVI), 128u, (uint32_t)(BN * 16));
+        const uint64_t dVl = dVh + (p.v2_bytes >> 4);
+        TileIter cur;
+        cur.start(p, items);
+        uint32_t r = 0, rph = 0, gt = 0, nitem = 0, dtq = 0;
+        while (cur.valid) {
+          if (cur.first_in_item()) {
+            mbar_wait(vi_full, nitem & 1u);
+            ++nitem;
+          }
+          mbar_wait(&rdy[r], rph);  // P(g) stored in both CTAs' shared memory
+          const bool tp = cur.transposed();
+          if (tp) mbar_wait(dt_empty, (dtq & 1u) ^ 1u);
+          tc_fence_after();
+          if (elect_one()) {
+            if (tp) {
+              const uint64_t pa = dP0 + (uint64_t)(gt & 1u) * (PBUF >> 4);
+#pragma unroll 1
+              for (int m = 0; m < BN / 16; ++m) {
+                const uint64_t ah = pa + (uint64_t)m * (4096 >> 4), al = ah + ((PBUF / 2) >> 4);
+                const uint64_t bh = dVh + (uint64_t)(16 * m), bl = dVl + (uint64_t)(16 * m);
+                mma_ss(tDT, ah, bh, idT, m > 0 ? 1u : 0u);
+                mma_ss(tDT, ah, bl, idT, 1u);
+                mma_ss(tDT, al, bh, idT, 1u);
+              }
+              tc_commit2(dt_full);
+            }
+            tc_commit2(&pt_free[gt & 1u]);
+            if (cur.last_in_item()) tc_commit2(vi_empty);
+          }
+          __syncwarp();
+          dtq += tp ? 1u : 0u;
+          ++gt;
+          if (++r == (uint32_t)NR) {
+            r = 0;
+            rph ^= 1u;
+          }
+          cur.next(p, items);
+        }
       }
     }
   }
@@ -719,6 +841,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       if ((int)(gt & 1u) == e) {
         const int b = (int)bb;
         if (tr) trace_ev<DBG>(p, gt, 3 + 2 * e);
+        const bool tp = SYM && ti.transposed();
+        // P buffer e is free once the transposed issuer finished tile gt - 2.
+        // Waited on every tile, not only transposed ones: the issuer commits
+        // pt_free for every tile, and skipping waits (diagonal tiles at item
+        // starts) would let the epilogue run two phases ahead and alias the
+        // parity.
+        if (SYM && gt >= 2u) mbar_wait(&pt_free[e], ((gt >> 1) - 1u) & 1u);
         mbar_wait(&s_full[er.idx], er.phase);
         tc_fence_after();
         if (tr) trace_ev<DBG>(p, gt, 4 + 2 * e);
@@ -736,8 +865,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
               tmem_st16(base + 32 * c, hi);
               tmem_st16(base + 32 * c + 16, lo);
             }
+            if (tp) {  // row i = lane's TMEM lane, 32 columns = 4 core matrices of 8 j
+              const int i = 32 * wq + lane;
+              const uint32_t rowb = smem_u32(sP) + (uint32_t)e * PBUF + (uint32_t)(i >> 3) * 2048u +
+                                    (uint32_t)(i & 7) * 16u + ((col0 + 32u * c) >> 3) * 128u;
+#pragma unroll
+              for (int g = 0; g < 4; ++g) {
+                st_shared_v4(rowb + 128u * g, hi[4 * g], hi[4 * g + 1], hi[4 * g + 2], hi[4 * g + 3]);
+                st_shared_v4(rowb + PBUF / 2 + 128u * g, lo[4 * g], lo[4 * g + 1], lo[4 * g + 2],
+                             lo[4 * g + 3]);
+              }
+            }
           }
           tmem_wait_st();
+          if (tp) fence_proxy_async_smem();
         }
         tc_fence_before();
         __syncwarp();
@@ -755,6 +896,64 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     const int wq = warp & 3;
     const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
     const int row = 32 * wq + lane;
+    if (SYM) {
+      // O chunks and each transposed tile's D_T go straight into the fp32
+      // accumulator (scaled, vector reductions); rows past n are padding
+      TileIter ti;
+      ti.start(p, items);
+      uint32_t q = 0, dtq = 0;
+      auto flush8 = [&](float* dst, int c0, const uint32_t (&x)[8], const uint32_t (&y)[8], bool two) {
+        float v[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float s = __uint_as_float(x[c]) + (two ? __uint_as_float(y[c]) : 0.f);
+          v[c] = ldexpf(s, -(p.s_exp + __ldg(&p.col_exp[c0 + c])));
+        }
+        red_add_v4(dst + c0, v[0], v[1], v[2], v[3]);
+        red_add_v4(dst + c0 + 4, v[4], v[5], v[6], v[7]);
+      };
+      while (ti.valid) {
+        if (ti.transposed()) {
+          mbar_wait(dt_full, dtq & 1u);
+          tc_fence_after();
+          const int64_t j = (int64_t)ti.ct * BM + row;  // output row of the transposed product
+#pragma unroll 1
+          for (int h = 0; h < WP / 8; ++h) {
+            uint32_t x[8];
+            tmem_ld8(tDT + lane_off + (uint32_t)(rank * WP + 8 * h), x);
+            tmem_wait_ld();
+            if (j < p.nloc && p.sym_dbg != 1) flush8(p.acc + j * WP, 8 * h, x, x, false);
+            if (p.sym_dump != nullptr) {
+              float* dd = p.sym_dump + ((((int64_t)ti.cur.pp * p.col_tiles + ti.ct) * 2 + rank) * BM + row) * WP + 8 * h;
+#pragma unroll
+              for (int c = 0; c < 8; ++c) dd[c] = __uint_as_float(x[c]);
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(leader_addr(dt_empty));
+          ++dtq;
+        }
+        if (ti.last_in_chunk()) {
+          mbar_wait(&o_full[0], q & 1u);
+          tc_fence_after();
+          const int64_t i = (2 * (int64_t)ti.cur.pp + rank) * BM + row;
+#pragma unroll 1
+          for (int h = 0; h < WP / 8; ++h) {
+            uint32_t x[8], y[8];
+            tmem_ld8(tO(0) + lane_off + 8 * h, x);       // P_hi Vhi + P_lo Vhi
+            tmem_ld8(tO(0) + lane_off + WP + 8 * h, y);  // P_hi Vlo
+            tmem_wait_ld();
+            if (i < p.nloc && p.sym_dbg != 2) flush8(p.acc + i * WP, 8 * h, x, y, true);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(leader_addr(&o_empty[0]));
+          ++q;
+        }
+        ti.next(p, items);
+      }
+    } else {
     double* acc = sAcc + row;  // acc[c * BM], conflict-free across the warp
 #pragma unroll
     for (int c = 0; c < WP; ++c) acc[c * BM] = 0.0;
@@ -804,6 +1003,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         }
       }
       ti.next(p, items);
+    }
     }
   }
 
@@ -1016,16 +1216,35 @@ __global__ void reduce_partial_kernel(const double* __restrict__ partial, int sp
     if (k < out.n) out.p[k][(e / w) * ldo + (e % w)] = (T)s;
 }
 
+// symmetric kernel: rows of the fp32 accumulator to every destination
+__global__ void sym_finalize_kernel(const float* __restrict__ acc, int64_t n, int w, int wp,
+                                    const ncgp::OutPtrs<float> out, int64_t ldo) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * w) return;
+  const int64_t i = e / w;
+  const int c = (int)(e % w);
+  const float v = acc[i * wp + c];
+#pragma unroll
+  for (int k = 0; k < NCGP_MAX_OUTS; ++k)
+    if (k < out.n) out.p[k][i * ldo + c] = v;
+}
+
 // ------------------------------------------------------------------ host
 
 long long* g_trace = nullptr;  // debug hook (ncgp_debug_set_trace)
+float* g_sym_dump = nullptr;   // debug hook (ncgp_debug_set_sym_dump)
+// symmetric K(X, X) kernel: NCGP_SYM=0 disables it (default on once validated)
+bool sym_enabled() {
+  const char* e = getenv("NCGP_SYM");
+  return e != nullptr && e[0] == '1';
+}
 int g_debug_mode = 0;          // debug hook (ncgp_debug_set_mode)
 
 int ka_of(int d) { return ((3 * d + 4) + 15) / 16 * 16; }
 int wp_of(int w) { return w <= 16 ? 16 : 32; }
 
 struct Layout {
-  size_t mu, guard, colexp, bits, xa, col, partial, total;
+  size_t mu, guard, colexp, bits, xa, col, partial, symacc, symtab, total;
   uint32_t a_bytes, xbh_bytes, rec_bytes;
   int64_t tile_stride, row_tiles, col_tiles;
 };
@@ -1056,6 +1275,31 @@ int splits_for(int64_t pairs, int64_t col_tiles, int clusters) {
   return 1;
 }
 
+// Symmetric kernel work list: row-tile pair a covers column tiles [2a, nb)
+// (the diagonal 256 x 256 block plus everything right of it), cut into items
+// of at most SYM_ITEM tiles; the transposed products of tiles c >= 2a + 2
+// cover the blocks left of the diagonal.
+int sym_item_len() {
+  const char* e = getenv("NCGP_SYM_ITEM");
+  return e != nullptr && atoi(e) > 0 ? atoi(e) : 128;
+}
+int64_t sym_item_count(int64_t pairs, int64_t nb) {
+  const int L = sym_item_len();
+  int64_t n = 0;
+  for (int64_t a = 0; a < pairs; ++a)
+    if (2 * a < nb) n += (nb - 2 * a + L - 1) / L;
+  return n;
+}
+std::vector<int4> sym_items(int64_t pairs, int64_t nb) {
+  const int L = sym_item_len();
+  std::vector<int4> t;
+  t.reserve((size_t)sym_item_count(pairs, nb));
+  for (int64_t a = 0; a < pairs; ++a)
+    for (int64_t c0 = 2 * a; c0 < nb; c0 += L)
+      t.push_back(make_int4((int)a, (int)c0, (int)std::min<int64_t>(nb, c0 + L), 0));
+  return t;
+}
+
 Layout layout_of(int64_t n_rows, int64_t n_cols, int d, int w_max, int sms) {
   Layout L{};
   const int ka = ka_of(d);
@@ -1078,19 +1322,26 @@ Layout layout_of(int64_t n_rows, int64_t n_cols, int d, int w_max, int sms) {
   L.colexp = take(64 * sizeof(int));
   L.bits = take(64 * sizeof(unsigned));
   L.xa = take((size_t)L.row_tiles * L.a_bytes);
-  L.col = take((size_t)L.col_tiles * L.tile_stride);
+  // square operators get one zero record past the last column tile: the
+  // symmetric kernel reads the padding row tile's V block from it
+  L.col = take((size_t)(L.col_tiles + (n_rows == n_cols ? 1 : 0)) * L.tile_stride);
   // fp64 partial rows [splits][rows][w] when a pair's columns are split
   const int sp = splits_for(L.row_tiles / 2, L.col_tiles, std::max(1, sms / 2));
   L.partial = take((size_t)(sp > 1 ? sp : 0) * (size_t)(L.row_tiles * BM) * w_max *
                    sizeof(double) + 256);
+  // symmetric kernel (square operators): fp32 accumulator and item table
+  const bool sq = n_rows == n_cols;
+  L.symacc = take(sq ? (size_t)L.row_tiles * BM * wp_of(w_max) * sizeof(float) : 0);
+  L.symtab = take(sq ? (size_t)sym_item_count(L.row_tiles / 2, L.col_tiles) * 16 : 0);
   L.total = off;
   return L;
 }
 
-size_t smem_bytes(uint32_t a_bytes, int wp, int na, int sx, int sv) {
+size_t smem_bytes(uint32_t a_bytes, int wp, int na, int sx, int sv, bool sym = false) {
   const size_t v2 = (size_t)wp * BN * 2, v3 = v2 / 2;
   return (size_t)na * a_bytes + (size_t)sx * (a_bytes / 2) + (size_t)sv * (v2 + v3) +
-         (size_t)wp * BM * 8 + (6 + 9 + 2 + NS + 3 * NR + 8) * sizeof(uint64_t) + 16 + 1024;
+         (sym ? 2 * v2 + 2 * (size_t)PBUF : (size_t)wp * BM * 8) +
+         (6 + 9 + 2 + NS + 3 * NR + 8 + 8) * sizeof(uint64_t) + 16 + 1024;
 }
 
 }  // namespace
@@ -1118,6 +1369,19 @@ int tc_prepare(ncgp_kop* op, cudaStream_t st) {
   op->col_pack = op->ws + L.col;
   op->col_tile_bytes = (size_t)L.tile_stride;
   op->partial = reinterpret_cast<double*>(op->ws + L.partial);
+  op->sym_items = 0;
+  op->sym_acc = reinterpret_cast<float*>(op->ws + L.symacc);
+  op->sym_tab = reinterpret_cast<int4*>(op->ws + L.symtab);
+  std::vector<int4> tab;
+  if (op->n_rows == op->n_cols)
+    NCGP_CUDA(cudaMemsetAsync(op->col_pack + (size_t)L.col_tiles * L.tile_stride, 0,
+                              (size_t)L.tile_stride, st));
+  if (op->Xr == op->Xc && op->n_rows == op->n_cols) {
+    tab = sym_items(L.row_tiles / 2, L.col_tiles);
+    NCGP_CUDA(cudaMemcpyAsync(op->sym_tab, tab.data(), tab.size() * sizeof(int4),
+                              cudaMemcpyHostToDevice, st));
+    op->sym_items = (int64_t)tab.size();  // the stream sync below keeps `tab` alive long enough
+  }
   // prescale kernel values into fp16 range: s2 * 2^s in (2^13, 2^14]
   const int s_exp = 14 - (int)ceil(log2(op->s2));
   op->k_scale = ldexp(1.0, s_exp);
@@ -1231,6 +1495,59 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
   p.partial = op->partial;
   p.trace = g_trace;
   p.debug_mode = g_debug_mode;
+  p.n_items = (int)(p.pairs * p.splits);
+  p.item_tab = nullptr;
+  p.acc = nullptr;
+  // symmetric kernel: K(X, X) with the whole row range in one launch
+  const bool dbg = (g_trace != nullptr) || (g_debug_mode != 0);
+  bool sym = op->sym_items > 0 && r0 == 0 && r1 == op->n_rows && !dbg && sym_enabled();
+  if (sym) {
+    const int cand[][3] = {{1, 6, 6}, {1, 3, 6}, {1, 3, 5}, {1, 3, 4}, {1, 3, 3}};
+    sym = false;
+    for (auto& c : cand)
+      if (smem_bytes(p.a_bytes, wp, c[0], c[1], c[2], true) <= (size_t)SMEM_BUDGET) {
+        p.na = c[0];
+        p.sx = c[1];
+        p.sv = c[2];
+        sym = true;
+        break;
+      }
+  }
+  if (sym) {
+    p.splits = 1;
+    p.tiles_per_split = p.col_tiles;
+    p.n_items = (int)op->sym_items;
+    p.item_tab = op->sym_tab;
+    p.acc = op->sym_acc;
+    {
+      const char* e = getenv("NCGP_SYM_DBG");
+      p.sym_dbg = e != nullptr ? atoi(e) : 0;
+    }
+    p.sym_dump = g_sym_dump;
+    NCGP_CUDA(cudaMemsetAsync(p.acc, 0, (size_t)op->row_tiles * BM * wp * sizeof(float), st));
+    const size_t smem = smem_bytes(p.a_bytes, wp, p.na, p.sx, p.sv, true);
+    const unsigned grid = 2u * (unsigned)std::min<int64_t>(p.n_items, clusters);
+    auto launch = [&](auto kern) -> int {
+      NCGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+      kern<<<grid, NTHREADS, smem, st>>>(p);
+      NCGP_LAUNCHED();
+      return NCGP_OK;
+    };
+    int rc;
+    if (op->family == NCGP_RBF)
+      rc = wp == 16 ? launch(kop_tc_kernel<NCGP_RBF, 16, false, true>)
+                    : launch(kop_tc_kernel<NCGP_RBF, 32, false, true>);
+    else
+      rc = wp == 16 ? launch(kop_tc_kernel<NCGP_MATERN32, 16, false, true>)
+                    : launch(kop_tc_kernel<NCGP_MATERN32, 32, false, true>);
+    if (rc != NCGP_OK) return rc;
+    const int64_t tot = p.nloc * w;
+    sym_finalize_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+        p.acc, p.nloc, w, wp, ncgp::out_ptrs<float>(out, r0, ldo), ldo);
+    NCGP_LAUNCHED();
+    return NCGP_OK;
+  }
   // deepest rings that fit: (na, sx, sv) from (2, 6, 9) down to (1, 3, 6)
   {
     const int cand[][3] = {{2, 6, 9}, {2, 6, 6}, {2, 3, 9}, {2, 3, 6}, {1, 6, 6}, {1, 3, 6}};
@@ -1259,21 +1576,20 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
     return NCGP_OK;
   };
   int rc;
-  const bool dbg = (g_trace != nullptr) || (g_debug_mode != 0);
   if (op->family == NCGP_RBF) {
     if (dbg)
-      rc = wp == 16 ? launch(kop_tc_kernel<NCGP_RBF, 16, true>)
-                    : launch(kop_tc_kernel<NCGP_RBF, 32, true>);
+      rc = wp == 16 ? launch(kop_tc_kernel<NCGP_RBF, 16, true, false>)
+                    : launch(kop_tc_kernel<NCGP_RBF, 32, true, false>);
     else
-      rc = wp == 16 ? launch(kop_tc_kernel<NCGP_RBF, 16, false>)
-                    : launch(kop_tc_kernel<NCGP_RBF, 32, false>);
+      rc = wp == 16 ? launch(kop_tc_kernel<NCGP_RBF, 16, false, false>)
+                    : launch(kop_tc_kernel<NCGP_RBF, 32, false, false>);
   } else {
     if (dbg)
-      rc = wp == 16 ? launch(kop_tc_kernel<NCGP_MATERN32, 16, true>)
-                    : launch(kop_tc_kernel<NCGP_MATERN32, 32, true>);
+      rc = wp == 16 ? launch(kop_tc_kernel<NCGP_MATERN32, 16, true, false>)
+                    : launch(kop_tc_kernel<NCGP_MATERN32, 32, true, false>);
     else
-      rc = wp == 16 ? launch(kop_tc_kernel<NCGP_MATERN32, 16, false>)
-                    : launch(kop_tc_kernel<NCGP_MATERN32, 32, false>);
+      rc = wp == 16 ? launch(kop_tc_kernel<NCGP_MATERN32, 16, false, false>)
+                    : launch(kop_tc_kernel<NCGP_MATERN32, 32, false, false>);
   }
   if (rc != NCGP_OK) return rc;
   if (p.splits > 1) {
@@ -1290,6 +1606,11 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
 }
 
 }  // namespace ncgp
+
+extern "C" int ncgp_debug_set_sym_dump(void* dev_buf) {
+  g_sym_dump = static_cast<float*>(dev_buf);
+  return 0;
+}
 
 extern "C" int ncgp_debug_set_trace(void* dev_buf) {
   g_trace = static_cast<long long*>(dev_buf);
