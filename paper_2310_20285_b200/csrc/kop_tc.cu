@@ -275,10 +275,19 @@ __device__ __forceinline__ void st_shared_v4(uint32_t saddr, uint32_t a, uint32_
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-__device__ __forceinline__ void red_add_v4(float* gaddr, float a, float b, float c, float d) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(gaddr), "f"(a), "f"(b),
-               "f"(c), "f"(d)
-               : "memory");
+// TMA bulk reduction shared -> global (fp32 add), one bulk group per call
+__device__ __forceinline__ void bulk_reduce_add_f32(float* gdst, uint32_t ssrc, uint32_t bytes) {
+  asm volatile(
+      "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;\n\t"
+      "cp.async.bulk.commit_group;" ::"l"(gdst),
+      "r"(ssrc), "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 __device__ __forceinline__ void tmem_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -344,7 +353,9 @@ struct TcParams {
   int n_items;           // work items: pairs * splits, or the symmetric item table's length
   const int4* item_tab;  // symmetric kernel: (row-tile pair, c0, c1, -) per item
   float* acc;            // symmetric kernel: fp32 output accumulator [row][WP], zeroed
-  int sym_dbg;           // symmetric kernel debug: 1 = drop D_T flushes, 2 = drop O flushes
+  int sym_dbg;           // symmetric kernel debug bits (timing / diagnosis only): 1 = drop D_T
+                         // reductions, 2 = drop O reductions, 4 = no transposed MMAs,
+                         // 8 = no D_T loads, 16 = no P stores to shared memory
   float* sym_dump;       // symmetric kernel debug: raw D_T per (pair, tile, rank) when set
   int debug_mode;        // debug (timing only, wrong results): 1 = epilogue skips TMEM traffic,
                          // 2 = no GEMM2, 3 = no GEMM1, 4 = no column copies (8: XB only, 9: V only)
@@ -484,7 +495,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   // product's B) and two P buffers [P_hi | P_lo] (its MN-major A)
   uint8_t* sVI = sV + (size_t)p.sv * vslot;
   uint8_t* sP = sVI + (SYM ? 2 * (size_t)p.v2_bytes : 0);
-  double* sAcc = reinterpret_cast<double*>(sP + (SYM ? 2 * (size_t)PBUF : 0));  // [WP][128]
+  // symmetric kernel: fp32 staging rows [128][WP] for the bulk reductions
+  float* sStage = reinterpret_cast<float*>(sP + (SYM ? 2 * (size_t)PBUF : 0));
+  double* sAcc = reinterpret_cast<double*>(sStage + (SYM ? BM * WP : 0));  // [WP][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sAcc + (SYM ? 0 : WP * BM));
   uint64_t* xb_land = bars;               // [6]   local copy completion
   uint64_t* v_land = xb_land + 6;         // [9]   local copy completion
@@ -792,7 +805,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           if (tp) mbar_wait(dt_empty, (dtq & 1u) ^ 1u);
           tc_fence_after();
           if (elect_one()) {
-            if (tp) {
+            if (tp && !(p.sym_dbg & 4)) {
               const uint64_t pa = dP0 + (uint64_t)(gt & 1u) * (PBUF >> 4);
 #pragma unroll 1
               for (int m = 0; m < BN / 16; ++m) {
@@ -802,8 +815,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 mma_ss(tDT, ah, bl, idT, 1u);
                 mma_ss(tDT, al, bh, idT, 1u);
               }
-              tc_commit2(dt_full);
             }
+            if (tp) tc_commit2(dt_full);
             tc_commit2(&pt_free[gt & 1u]);
             if (cur.last_in_item()) tc_commit2(vi_empty);
           }
@@ -865,7 +878,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
               tmem_st16(base + 32 * c, hi);
               tmem_st16(base + 32 * c + 16, lo);
             }
-            if (tp) {  // row i = lane's TMEM lane, 32 columns = 4 core matrices of 8 j
+            if (tp && !(p.sym_dbg & 16)) {  // row i = TMEM lane, 32 columns = 4 core matrices of 8 j
               const int i = 32 * wq + lane;
               const uint32_t rowb = smem_u32(sP) + (uint32_t)e * PBUF + (uint32_t)(i >> 3) * 2048u +
                                     (uint32_t)(i & 7) * 16u + ((col0 + 32u * c) >> 3) * 128u;
@@ -891,7 +904,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       ti.next(p, items);
     }
   } else {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+    // (symmetric kernel: 56 -- 4 x 32 x 40 + 16 x 32 x 96 + 4 x 32 x 56 = the 61,440 pool)
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(SYM ? 56 : 40));
     // ================= correction warpgroup =================
     const int wq = warp & 3;
     const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
@@ -902,27 +916,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       TileIter ti;
       ti.start(p, items);
       uint32_t q = 0, dtq = 0;
-      auto flush8 = [&](float* dst, int c0, const uint32_t (&x)[8], const uint32_t (&y)[8], bool two) {
+      // Flushes go through shared memory and one TMA bulk reduction per warp
+      // (32 rows x WP floats, contiguous): 16 B chunk c of row r is stored at
+      // chunk c ^ (r mod C) (conflict-free stores), and the global accumulator
+      // keeps that swizzle (sym_finalize_kernel undoes it).
+      constexpr int C = WP / 4;
+      const uint32_t stg_warp = smem_u32(sStage) + (uint32_t)(32 * wq) * WP * 4u;
+      const uint32_t stg_row = stg_warp + (uint32_t)lane * WP * 4u;
+      auto stage8 = [&](int h, const uint32_t (&x)[8], const uint32_t (&y)[8], bool two) {
         float v[8];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
+          const int e = p.s_exp + __ldg(&p.col_exp[8 * h + c]);  // 2^-e, exact
           const float s = __uint_as_float(x[c]) + (two ? __uint_as_float(y[c]) : 0.f);
-          v[c] = ldexpf(s, -(p.s_exp + __ldg(&p.col_exp[c0 + c])));
+          v[c] = s * __int_as_float((127 - e) << 23);
         }
-        red_add_v4(dst + c0, v[0], v[1], v[2], v[3]);
-        red_add_v4(dst + c0 + 4, v[4], v[5], v[6], v[7]);
+        const uint32_t k0 = (uint32_t)((2 * h) ^ (lane & (C - 1))), k1 = (uint32_t)((2 * h + 1) ^ (lane & (C - 1)));
+        st_shared_v4(stg_row + 16u * k0, __float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]),
+                     __float_as_uint(v[3]));
+        st_shared_v4(stg_row + 16u * k1, __float_as_uint(v[4]), __float_as_uint(v[5]), __float_as_uint(v[6]),
+                     __float_as_uint(v[7]));
+      };
+      auto issue = [&](int64_t row0, bool skip) {  // after the stores of one flush
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0 && !skip) bulk_reduce_add_f32(p.acc + row0 * WP, stg_warp, 32u * WP * 4u);
+      };
+      auto reuse = [&]() {  // the staging rows may be rewritten once the last bulk op read them
+        if (lane == 0) bulk_wait_read();
+        __syncwarp();
       };
       while (ti.valid) {
         if (ti.transposed()) {
           mbar_wait(dt_full, dtq & 1u);
           tc_fence_after();
-          const int64_t j = (int64_t)ti.ct * BM + row;  // output row of the transposed product
-#pragma unroll 1
+          reuse();
+          const int64_t j0 = (int64_t)ti.ct * BM + 32 * wq;  // output rows of the transposed product
+          const bool ld = !(p.sym_dbg & 8);
+#pragma unroll
           for (int h = 0; h < WP / 8; ++h) {
             uint32_t x[8];
-            tmem_ld8(tDT + lane_off + (uint32_t)(rank * WP + 8 * h), x);
-            tmem_wait_ld();
-            if (j < p.nloc && p.sym_dbg != 1) flush8(p.acc + j * WP, 8 * h, x, x, false);
+            if (ld) {
+              tmem_ld8(tDT + lane_off + (uint32_t)(rank * WP + 8 * h), x);
+              tmem_wait_ld();
+            } else {
+#pragma unroll
+              for (int c = 0; c < 8; ++c) x[c] = 0u;
+            }
+            stage8(h, x, x, false);
             if (p.sym_dump != nullptr) {
               float* dd = p.sym_dump + ((((int64_t)ti.cur.pp * p.col_tiles + ti.ct) * 2 + rank) * BM + row) * WP + 8 * h;
 #pragma unroll
@@ -930,29 +971,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             }
           }
           tc_fence_before();
-          __syncwarp();
+          issue(j0, (p.sym_dbg & 1) != 0);
           if (lane == 0) mbar_arrive_cluster(leader_addr(dt_empty));
           ++dtq;
         }
         if (ti.last_in_chunk()) {
           mbar_wait(&o_full[0], q & 1u);
           tc_fence_after();
-          const int64_t i = (2 * (int64_t)ti.cur.pp + rank) * BM + row;
-#pragma unroll 1
+          reuse();
+          const int64_t i0 = (2 * (int64_t)ti.cur.pp + rank) * BM + 32 * wq;
+#pragma unroll
           for (int h = 0; h < WP / 8; ++h) {
             uint32_t x[8], y[8];
             tmem_ld8(tO(0) + lane_off + 8 * h, x);       // P_hi Vhi + P_lo Vhi
             tmem_ld8(tO(0) + lane_off + WP + 8 * h, y);  // P_hi Vlo
             tmem_wait_ld();
-            if (i < p.nloc && p.sym_dbg != 2) flush8(p.acc + i * WP, 8 * h, x, y, true);
+            stage8(h, x, y, true);
           }
           tc_fence_before();
-          __syncwarp();
+          issue(i0, (p.sym_dbg & 2) != 0);
           if (lane == 0) mbar_arrive_cluster(leader_addr(&o_empty[0]));
           ++q;
         }
         ti.next(p, items);
       }
+      if (lane == 0) bulk_wait_all();
     } else {
     double* acc = sAcc + row;  // acc[c * BM], conflict-free across the warp
 #pragma unroll
@@ -1223,7 +1266,8 @@ __global__ void sym_finalize_kernel(const float* __restrict__ acc, int64_t n, in
   if (e >= n * w) return;
   const int64_t i = e / w;
   const int c = (int)(e % w);
-  const float v = acc[i * wp + c];
+  const int cc = ((c >> 2) ^ (int)(i & (wp / 4 - 1))) * 4 + (c & 3);  // stored chunk swizzle
+  const float v = acc[i * wp + cc];
 #pragma unroll
   for (int k = 0; k < NCGP_MAX_OUTS; ++k)
     if (k < out.n) out.p[k][i * ldo + c] = v;
@@ -1233,10 +1277,16 @@ __global__ void sym_finalize_kernel(const float* __restrict__ acc, int64_t n, in
 
 long long* g_trace = nullptr;  // debug hook (ncgp_debug_set_trace)
 float* g_sym_dump = nullptr;   // debug hook (ncgp_debug_set_sym_dump)
-// symmetric K(X, X) kernel: NCGP_SYM=0 disables it (default on once validated)
-bool sym_enabled() {
+// Symmetric K(X, X) kernel policy.  It halves the transcendental work but
+// adds the transposed product to the tensor pipe: a clear win when the
+// epilogue is heavy (Matern: sqrt + ex2 per pair, 1.2-1.5x), break-even or
+// slower for RBF (one ex2 per pair).  NCGP_SYM=1 forces it on for any
+// family, NCGP_SYM=0 off (bitwise-reproducible plain kernel only).
+bool sym_enabled(int family) {
   const char* e = getenv("NCGP_SYM");
-  return e != nullptr && e[0] == '1';
+  if (e != nullptr && e[0] == '0') return false;
+  if (e != nullptr && e[0] == '1') return true;
+  return family == NCGP_MATERN32;
 }
 int g_debug_mode = 0;          // debug hook (ncgp_debug_set_mode)
 
@@ -1340,7 +1390,7 @@ Layout layout_of(int64_t n_rows, int64_t n_cols, int d, int w_max, int sms) {
 size_t smem_bytes(uint32_t a_bytes, int wp, int na, int sx, int sv, bool sym = false) {
   const size_t v2 = (size_t)wp * BN * 2, v3 = v2 / 2;
   return (size_t)na * a_bytes + (size_t)sx * (a_bytes / 2) + (size_t)sv * (v2 + v3) +
-         (sym ? 2 * v2 + 2 * (size_t)PBUF : (size_t)wp * BM * 8) +
+         (sym ? 2 * v2 + 2 * (size_t)PBUF + (size_t)BM * wp * 4 : (size_t)wp * BM * 8) +
          (6 + 9 + 2 + NS + 3 * NR + 8 + 8) * sizeof(uint64_t) + 16 + 1024;
 }
 
@@ -1500,7 +1550,7 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
   p.acc = nullptr;
   // symmetric kernel: K(X, X) with the whole row range in one launch
   const bool dbg = (g_trace != nullptr) || (g_debug_mode != 0);
-  bool sym = op->sym_items > 0 && r0 == 0 && r1 == op->n_rows && !dbg && sym_enabled();
+  bool sym = op->sym_items > 0 && r0 == 0 && r1 == op->n_rows && !dbg && sym_enabled(op->family);
   if (sym) {
     const int cand[][3] = {{1, 6, 6}, {1, 3, 6}, {1, 3, 5}, {1, 3, 4}, {1, 3, 3}};
     sym = false;

@@ -1,0 +1,102 @@
+"""Symmetric K(X, X) kernel (one P tile serves O_I += P V_J and O_J += P^T V_I)
+against the CPU oracle and the plain kernel.
+
+Tolerances (north_star): fp32 operator products within 1e-4 relative of
+|K||V| per entry.  The symmetric kernel accumulates through fp32 TMA
+reductions, so it is not bitwise reproducible; it is checked at 1e-5 of the
+entry scale (measured 1-4e-6) and against the plain kernel at 2e-5 in norm.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2310_20285_b200.kernels import KernelOperator  # noqa: E402
+from oracle import ncgp_oracle as O  # noqa: E402
+
+
+class _Env:
+    def __init__(self, **kw):
+        self.kw = kw
+
+    def __enter__(self):
+        self.old = {k: os.environ.get(k) for k in self.kw}
+        os.environ.update({k: str(v) for k, v in self.kw.items()})
+
+    def __exit__(self, *exc):
+        for k, v in self.old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def _case(n, d, w, spec, seed):
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((n, d))
+    V = rng.standard_normal((n, w))
+    op = KernelOperator(spec[0], spec[1], spec[2], torch.from_numpy(X).float().cuda(), w_max=32)
+    return X, V, op, torch.from_numpy(V).float().cuda()
+
+
+@pytest.mark.parametrize("n,d,w,spec", [
+    (300, 3, 4, ("matern32", 1.0, 1.0)),
+    (1000, 2, 1, ("matern32", 1.0, 2.0)),
+    (3000, 8, 32, ("matern32", 1.5, 1.0)),
+    (5000, 20, 10, ("matern32", 3.0, 1.0)),
+    (2561, 8, 7, ("rbf", 1.5, 1.0)),
+    (4096, 8, 32, ("rbf", 1.2, 0.7)),
+])
+def test_symmetric_kernel_matches_oracle(n, d, w, spec):
+    X, V, op, Vd = _case(n, d, w, spec, n + d)
+    with _Env(NCGP_SYM=1):
+        got = op.apply(Vd).double().cpu().numpy()
+    ref = O.kernel_matmul_rows(spec, X, X, V)
+    bound = O.kernel_matmul_rows(spec, X, X, np.abs(V))
+    assert np.all(np.abs(got - ref) <= 1e-5 * bound), float(np.max(np.abs(got - ref) / bound))
+
+
+@pytest.mark.parametrize("item", [3, 16, 128])
+def test_symmetric_kernel_item_transitions(item):
+    """Several work items per cluster (short items force many row-pair and
+    V-block switches): the result must not depend on the item length."""
+    X, V, op, Vd = _case(20000, 8, 16, ("matern32", 1.5, 1.0), 7)
+    with _Env(NCGP_SYM=0):
+        plain = op.apply(Vd).double()
+    with _Env(NCGP_SYM=1, NCGP_SYM_ITEM=item):
+        op2 = KernelOperator("matern32", 1.5, 1.0, op.X_rows, w_max=32)  # table built at creation
+        got = op2.apply(Vd).double()
+    assert float((got - plain).norm() / plain.norm()) < 2e-5
+
+
+def test_symmetric_kernel_only_on_full_square_launches():
+    """Row-range launches (shards) and rectangular operators use the plain
+    kernel, bitwise identical to NCGP_SYM=0."""
+    X, V, op, Vd = _case(3000, 8, 8, ("matern32", 1.5, 1.0), 3)
+    with _Env(NCGP_SYM=0):
+        plain = op.apply(Vd)
+    part = torch.empty_like(plain)
+    with _Env(NCGP_SYM=1):
+        for r0, r1 in ((0, 1280), (1280, 3000)):
+            op.apply(Vd, out=part, row_begin=r0, row_end=r1)
+        rect = KernelOperator("matern32", 1.5, 1.0, op.X_rows[:2000], op.X_rows, w_max=32)
+        rr = rect.apply(Vd)
+    with _Env(NCGP_SYM=0):
+        rr0 = rect.apply(Vd)
+    assert torch.equal(part, plain)
+    assert torch.equal(rr, rr0)
+
+
+def test_symmetric_default_policy_is_matern_only():
+    X, V, op, Vd = _case(3000, 8, 8, ("rbf", 1.5, 1.0), 4)
+    a = op.apply(Vd)
+    with _Env(NCGP_SYM=0):
+        b = op.apply(Vd)
+    assert torch.equal(a, b)  # RBF: plain kernel by default

@@ -55,6 +55,12 @@ for n, d, w, fam, ell in [(300, 3, 4, "rbf", 1.0), (3000, 8, 32, "rbf", 1.5), (5
                           (20000, 8, 32, "rbf", 1.5), (20000, 20, 10, "matern32", 3.0),
                           (12345, 8, 32, "matern32", 1.5)]:
     run(n, d, w, fam, ell)
+if timing and "--shapes" in sys.argv:
+    for n, d, w, fam, ell in [(200_000, 8, 10, "rbf", 1.5), (200_000, 20, 10, "rbf", 3.0),
+                              (200_000, 8, 16, "rbf", 1.5), (200_000, 20, 32, "rbf", 3.0),
+                              (200_000, 20, 10, "matern32", 3.0), (200_000, 32, 10, "rbf", 5.0)]:
+        run(n, d, w, fam, ell, True)
+    sys.exit(0)
 if timing:
     run(200_000, 8, 32, "rbf", 1.5, True)
     run(200_000, 8, 32, "matern32", 1.5, True)
