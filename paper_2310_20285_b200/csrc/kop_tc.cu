@@ -44,6 +44,7 @@
 // column boundaries (reduction order independent of row sharding).
 #include <cuda_fp16.h>
 #include <math.h>
+#include <stdio.h>
 #include <string.h>
 
 #include <algorithm>
@@ -67,9 +68,9 @@ constexpr int EPI_WARPS = 16;
 constexpr int NTHREADS = 32 * (4 + EPI_WARPS + 4);
 constexpr int SMEM_BUDGET = 225 * 1024;
 constexpr int TMEM_COLS = 512;
-constexpr int NS = 3;            // S/P buffers in TMEM (3 x 128 columns)
+constexpr int NS_MAX = 3;        // S/P buffers in TMEM (3 x 128 columns; symmetric kernel 2)
 constexpr int NR = 12;           // s_full / rdy rings: >= max wait lag (XB depth, V depth, 4)
-constexpr int TRACE_TILES = 256, TRACE_EV = 12;
+constexpr int TRACE_TILES = 256, TRACE_EV = 16;
 constexpr uint32_t PBUF = 2u * BM * BN * 2u;  // symmetric kernel: one [P_hi | P_lo] buffer (64 KB)
 
 // ------------------------------------------------------------------ PTX
@@ -355,7 +356,9 @@ struct TcParams {
   float* acc;            // symmetric kernel: fp32 output accumulator [row][WP], zeroed
   int sym_dbg;           // symmetric kernel debug bits (timing / diagnosis only): 1 = drop D_T
                          // reductions, 2 = drop O reductions, 4 = no transposed MMAs,
-                         // 8 = no D_T loads, 16 = no P stores to shared memory
+                         // 8 = no D_T loads, 16 = no P stores to shared memory;
+                         // variants (correct results): 32 = P stored per chunk, not
+                         // in a burst, 64 = flip whether T(g) is held back behind GEMM1(g + NS)
   float* sym_dump;       // symmetric kernel debug: raw D_T per (pair, tile, rank) when set
   int debug_mode;        // debug (timing only, wrong results): 1 = epilogue skips TMEM traffic,
                          // 2 = no GEMM2, 3 = no GEMM1, 4 = no column copies (8: XB only, 9: V only)
@@ -485,6 +488,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cta_rank();
   const int items = p.n_items;
+  // S/P buffers in TMEM.  The symmetric kernel double-buffers its O and D_T
+  // accumulators (2 x 2 WP columns each): with WP = 32 that leaves room for
+  // two S/P buffers only, with WP = 16 for three.
+  constexpr int NS = (SYM && WP == 32) ? 2 : NS_MAX;
 
   // ---- shared-memory carve-up (identical offsets in both CTAs)
   const uint32_t vslot = p.v2_bytes + p.v3_bytes;       // this CTA's V half
@@ -519,9 +526,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   uint64_t* vi_full = vi_land + 1;        // [1]   SYM leader: both V blocks landed
   uint64_t* vi_empty = vi_full + 1;       // [1]   SYM both: V block free (multicast commit)
   uint64_t* pt_free = vi_empty + 1;       // [2]   SYM both: P buffer free (multicast commit)
-  uint64_t* dt_full = pt_free + 2;        // [1]   SYM both: transposed product done
-  uint64_t* dt_empty = dt_full + 1;       // [1]   SYM leader: D_T drained (8 warp arrivals)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dt_empty + 1);
+  uint64_t* dt_full = pt_free + 2;        // [2]   SYM both: transposed product done
+  uint64_t* dt_empty = dt_full + 2;       // [2]   SYM leader: D_T drained (8 warp arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dt_empty + 2);
+  // SYM leader: GEMM1 tiles issued so far (the transposed issuer queues T(g)
+  // behind GEMM1(g + NS) in the in-order tensor pipe)
+  volatile uint32_t* g1_cnt = tmem_slot + 1;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < 6; ++s) mbar_init(&xb_land[s], 1);
@@ -539,12 +549,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       mbar_init(&o_full[b], 1);
       mbar_init(&o_empty[b], 8);
       mbar_init(&pt_free[b], 1);
+      mbar_init(&dt_full[b], 1);
+      mbar_init(&dt_empty[b], 8);
     }
     mbar_init(vi_land, 1);
     mbar_init(vi_full, 2);
     mbar_init(vi_empty, 1);
-    mbar_init(dt_full, 1);
-    mbar_init(dt_empty, 8);
+    *g1_cnt = 0u;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -556,14 +567,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   tc_fence_before();
   __syncthreads();
   cluster_sync();  // barriers of both CTAs initialised before any remote arrive
+  if (DBG && p.trace != nullptr && threadIdx.x == 0) {  // per-CTA span (global timer, ns)
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[TRACE_TILES * TRACE_EV + 4 * blockIdx.x] = (long long)t;
+  }
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   // TMEM columns: S/P buffers [0, 384), O double buffer [384, 384 + 4 WP);
-  // symmetric kernel: single O [384, 384 + 2 WP), D_T [384 + 2 WP, 384 + 4 WP)
+  // symmetric kernel: S/P [0, 256), O double buffer [256, 256 + 4 WP),
+  // D_T double buffer [256 + 4 WP, 256 + 8 WP)
   auto tS = [&](int b) -> uint32_t { return tmem + (uint32_t)(b * BN); };
   auto tO = [&](int b) -> uint32_t { return tmem + (uint32_t)(NS * BN + b * 2 * WP); };
-  const uint32_t tDT = tmem + (uint32_t)(NS * BN + 2 * WP);
-  constexpr uint32_t NO = SYM ? 1u : 2u;  // O buffers
+  auto tDT = [&](uint32_t b) -> uint32_t { return tmem + (uint32_t)(NS * BN + 4 * WP) + b * 2u * WP; };
+  constexpr uint32_t NO = 2u;  // O buffers
   const int64_t half_off = (int64_t)rank * p.rec_bytes;   // this CTA's half of a record
 
   // setmaxnreg sits at the top of each warpgroup's branch so that ptxas sees
@@ -730,6 +747,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           }
           __syncwarp();
           if (lane == 0) trace_ev<DBG>(p, g1n, 2);
+          if (SYM && lane == 0) *g1_cnt = g1n + 1u;
           ++g1n;
           c1 = (c1 + 1u == (uint32_t)NR) ? 0u : c1 + 1u;
           s1 = (s1 + 1u == (uint32_t)NS) ? 0u : s1 + 1u;
@@ -737,6 +755,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           if (dx == xend) dx = dX0;
           look.next(p, items);
         }
+        if (SYM && lane == 0) *g1_cnt = 0xFFFFFFFFu;
       } else if (warp == 1) {
         // ---------------- GEMM2 issuer
         const uint64_t dV0 = sdesc(smem_u32(sV), 128u, (uint32_t)(BN * 16));
@@ -750,7 +769,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           const bool fresh = cur.first_in_chunk(), last = cur.last_in_chunk();
           if (lane == 0) trace_ev<DBG>(p, gt, 11);
           mbar_wait(&rdy[r], rph);  // P(g), V(g) (and XB(g + NS)) present
-          const uint32_t ob = SYM ? 0u : (q & 1u);
+          const uint32_t ob = q & 1u;
           if (fresh) mbar_wait(&o_empty[ob], ((q / NO) & 1u) ^ 1u);
           tc_fence_after();
           if (lane == 0) trace_ev<DBG>(p, gt, 0);
@@ -801,9 +820,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             ++nitem;
           }
           mbar_wait(&rdy[r], rph);  // P(g) stored in both CTAs' shared memory
+          if (lane == 0) trace_ev<DBG>(p, gt, 12);
           const bool tp = cur.transposed();
-          if (tp) mbar_wait(dt_empty, (dtq & 1u) ^ 1u);
+          if (tp) mbar_wait(&dt_empty[dtq & 1u], ((dtq >> 1) & 1u) ^ 1u);
+          // With two S buffers, T(g) enters the tensor pipe after GEMM1(g + 2):
+          // the GEMM2 -> GEMM1 -> epilogue chain must not queue behind the
+          // transposed product (three buffers leave enough slack without it)
+          if ((NS == 2) != ((p.sym_dbg & 64) != 0))
+            while (*g1_cnt < gt + (uint32_t)NS + 1u) {
+            }
           tc_fence_after();
+          if (lane == 0) trace_ev<DBG>(p, gt, 13);
           if (elect_one()) {
             if (tp && !(p.sym_dbg & 4)) {
               const uint64_t pa = dP0 + (uint64_t)(gt & 1u) * (PBUF >> 4);
@@ -811,16 +838,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
               for (int m = 0; m < BN / 16; ++m) {
                 const uint64_t ah = pa + (uint64_t)m * (4096 >> 4), al = ah + ((PBUF / 2) >> 4);
                 const uint64_t bh = dVh + (uint64_t)(16 * m), bl = dVl + (uint64_t)(16 * m);
-                mma_ss(tDT, ah, bh, idT, m > 0 ? 1u : 0u);
-                mma_ss(tDT, ah, bl, idT, 1u);
-                mma_ss(tDT, al, bh, idT, 1u);
+                const uint32_t dt = tDT(dtq & 1u);
+                mma_ss(dt, ah, bh, idT, m > 0 ? 1u : 0u);
+                mma_ss(dt, ah, bl, idT, 1u);
+                mma_ss(dt, al, bh, idT, 1u);
               }
             }
-            if (tp) tc_commit2(dt_full);
+            if (tp) tc_commit2(&dt_full[dtq & 1u]);
             tc_commit2(&pt_free[gt & 1u]);
             if (cur.last_in_item()) tc_commit2(vi_empty);
           }
           __syncwarp();
+          if (lane == 0) trace_ev<DBG>(p, gt, 14);
           dtq += tp ? 1u : 0u;
           ++gt;
           if (++r == (uint32_t)NR) {
@@ -859,8 +888,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         // Waited on every tile, not only transposed ones: the issuer commits
         // pt_free for every tile, and skipping waits (diagonal tiles at item
         // starts) would let the epilogue run two phases ahead and alias the
-        // parity.
-        if (SYM && gt >= 2u) mbar_wait(&pt_free[e], ((gt >> 1) - 1u) & 1u);
+        // parity.  By default (burst) P is copied TMEM -> shared memory after
+        // the whole tile is transformed, so T(gt - 2) has the tile's epilogue
+        // time to finish; sym_dbg bit 32 stores each chunk as it is made
+        // (the wait then sits before the first store).
+        const bool burst = SYM && !(p.sym_dbg & 32);
+        bool pt_wait = SYM && gt >= 2u;
         mbar_wait(&s_full[er.idx], er.phase);
         tc_fence_after();
         if (tr) trace_ev<DBG>(p, gt, 4 + 2 * e);
@@ -878,6 +911,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
               tmem_st16(base + 32 * c, hi);
               tmem_st16(base + 32 * c + 16, lo);
             }
+            if (burst) continue;
+            if (SYM && pt_wait) {
+              mbar_wait(&pt_free[e], ((gt >> 1) - 1u) & 1u);
+              pt_wait = false;
+              if (tr) trace_ev<DBG>(p, gt, 8);
+            }
             if (tp && !(p.sym_dbg & 16)) {  // row i = TMEM lane, 32 columns = 4 core matrices of 8 j
               const int i = 32 * wq + lane;
               const uint32_t rowb = smem_u32(sP) + (uint32_t)e * PBUF + (uint32_t)(i >> 3) * 2048u +
@@ -891,6 +930,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             }
           }
           tmem_wait_st();
+          if (burst) {
+            if (pt_wait) mbar_wait(&pt_free[e], ((gt >> 1) - 1u) & 1u);
+            if (tr) trace_ev<DBG>(p, gt, 8);
+            if (tp && !(p.sym_dbg & 16)) {
+              const int i = 32 * wq + lane;
+              const uint32_t rowb0 = smem_u32(sP) + (uint32_t)e * PBUF + (uint32_t)(i >> 3) * 2048u +
+                                     (uint32_t)(i & 7) * 16u + (col0 >> 3) * 128u;
+#pragma unroll
+              for (int c = 0; c < BN / 64; ++c) {
+                tmem_ld32(base + 32 * c, ra);  // [P_hi 16 | P_lo 16] packed pairs
+                tmem_wait_ld(ra);
+                const uint32_t rowb = rowb0 + 4u * 128u * c;
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                  st_shared_v4(rowb + 128u * g, ra[4 * g], ra[4 * g + 1], ra[4 * g + 2], ra[4 * g + 3]);
+                  st_shared_v4(rowb + PBUF / 2 + 128u * g, ra[16 + 4 * g], ra[16 + 4 * g + 1],
+                               ra[16 + 4 * g + 2], ra[16 + 4 * g + 3]);
+                }
+              }
+            }
+          }
           if (tp) fence_proxy_async_smem();
         }
         tc_fence_before();
@@ -948,7 +1008,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       };
       while (ti.valid) {
         if (ti.transposed()) {
-          mbar_wait(dt_full, dtq & 1u);
+          mbar_wait(&dt_full[dtq & 1u], (dtq >> 1) & 1u);
           tc_fence_after();
           reuse();
           const int64_t j0 = (int64_t)ti.ct * BM + 32 * wq;  // output rows of the transposed product
@@ -957,7 +1017,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           for (int h = 0; h < WP / 8; ++h) {
             uint32_t x[8];
             if (ld) {
-              tmem_ld8(tDT + lane_off + (uint32_t)(rank * WP + 8 * h), x);
+              tmem_ld8(tDT(dtq & 1u) + lane_off + (uint32_t)(rank * WP + 8 * h), x);
               tmem_wait_ld();
             } else {
 #pragma unroll
@@ -972,25 +1032,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           }
           tc_fence_before();
           issue(j0, (p.sym_dbg & 1) != 0);
-          if (lane == 0) mbar_arrive_cluster(leader_addr(dt_empty));
+          if (lane == 0) mbar_arrive_cluster(leader_addr(&dt_empty[dtq & 1u]));
+          if (lane == 0 && wq == 0 && ti.it == (int)(blockIdx.x >> 1)) trace_ev<DBG>(p, ti.ct - ti.cur.c0, 15);
           ++dtq;
         }
         if (ti.last_in_chunk()) {
-          mbar_wait(&o_full[0], q & 1u);
+          mbar_wait(&o_full[q & 1u], (q >> 1) & 1u);
           tc_fence_after();
           reuse();
           const int64_t i0 = (2 * (int64_t)ti.cur.pp + rank) * BM + 32 * wq;
 #pragma unroll
           for (int h = 0; h < WP / 8; ++h) {
             uint32_t x[8], y[8];
-            tmem_ld8(tO(0) + lane_off + 8 * h, x);       // P_hi Vhi + P_lo Vhi
-            tmem_ld8(tO(0) + lane_off + WP + 8 * h, y);  // P_hi Vlo
+            tmem_ld8(tO(q & 1u) + lane_off + 8 * h, x);       // P_hi Vhi + P_lo Vhi
+            tmem_ld8(tO(q & 1u) + lane_off + WP + 8 * h, y);  // P_hi Vlo
             tmem_wait_ld();
             stage8(h, x, y, true);
           }
           tc_fence_before();
           issue(i0, (p.sym_dbg & 2) != 0);
-          if (lane == 0) mbar_arrive_cluster(leader_addr(&o_empty[0]));
+          if (lane == 0) mbar_arrive_cluster(leader_addr(&o_empty[q & 1u]));
           ++q;
         }
         ti.next(p, items);
@@ -1053,6 +1114,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   __syncwarp();
   tc_fence_before();
   __syncthreads();
+  if (DBG && p.trace != nullptr && threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[TRACE_TILES * TRACE_EV + 4 * blockIdx.x + 1] = (long long)t;
+  }
   cluster_sync();  // both CTAs done with TMEM / remote barriers
   tc_fence_after();
   if (warp == 2) {
@@ -1278,15 +1344,21 @@ __global__ void sym_finalize_kernel(const float* __restrict__ acc, int64_t n, in
 long long* g_trace = nullptr;  // debug hook (ncgp_debug_set_trace)
 float* g_sym_dump = nullptr;   // debug hook (ncgp_debug_set_sym_dump)
 // Symmetric K(X, X) kernel policy.  It halves the transcendental work but
-// adds the transposed product to the tensor pipe: a clear win when the
-// epilogue is heavy (Matern: sqrt + ex2 per pair, 1.2-1.5x), break-even or
-// slower for RBF (one ex2 per pair).  NCGP_SYM=1 forces it on for any
-// family, NCGP_SYM=0 off (bitwise-reproducible plain kernel only).
-bool sym_enabled(int family) {
+// adds the transposed product (half of it wasted by the pair's shared B) to
+// the tensor pipe and an fp32 reduction of every transposed tile.  Measured
+// on one B200 (tools/sym_exp.py, n = 1e5 - 2e5): Matern-3/2 (sqrt + ex2 per
+// pair) 1.3-1.5x faster at any width; RBF (one ex2 per pair) 1.1-1.2x faster
+// at WP = 16 (three S buffers next to double-buffered O / D_T), 1.2x slower
+// at WP = 32 (only two S buffers fit in TMEM).  Below ~500 column tiles the
+// triangular work list balances poorly over the clusters and the plain
+// kernel wins.  NCGP_SYM=1 forces it on, NCGP_SYM=0 off (the plain kernel's
+// results are bitwise reproducible across row shardings; the symmetric
+// kernel's fp32 reductions are not).
+bool sym_enabled(int family, int wp, int64_t col_tiles) {
   const char* e = getenv("NCGP_SYM");
   if (e != nullptr && e[0] == '0') return false;
   if (e != nullptr && e[0] == '1') return true;
-  return family == NCGP_MATERN32;
+  return col_tiles >= 512 && (family == NCGP_MATERN32 || wp == 16);
 }
 int g_debug_mode = 0;          // debug hook (ncgp_debug_set_mode)
 
@@ -1391,7 +1463,7 @@ size_t smem_bytes(uint32_t a_bytes, int wp, int na, int sx, int sv, bool sym = f
   const size_t v2 = (size_t)wp * BN * 2, v3 = v2 / 2;
   return (size_t)na * a_bytes + (size_t)sx * (a_bytes / 2) + (size_t)sv * (v2 + v3) +
          (sym ? 2 * v2 + 2 * (size_t)PBUF + (size_t)BM * wp * 4 : (size_t)wp * BM * 8) +
-         (6 + 9 + 2 + NS + 3 * NR + 8 + 8) * sizeof(uint64_t) + 16 + 1024;
+         (6 + 9 + 2 + NS_MAX + 3 * NR + 8 + 12) * sizeof(uint64_t) + 16 + 1024;
 }
 
 }  // namespace
@@ -1550,7 +1622,8 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
   p.acc = nullptr;
   // symmetric kernel: K(X, X) with the whole row range in one launch
   const bool dbg = (g_trace != nullptr) || (g_debug_mode != 0);
-  bool sym = op->sym_items > 0 && r0 == 0 && r1 == op->n_rows && !dbg && sym_enabled(op->family);
+  bool sym = op->sym_items > 0 && r0 == 0 && r1 == op->n_rows && g_debug_mode == 0 &&
+             sym_enabled(op->family, wp, op->col_tiles);
   if (sym) {
     const int cand[][3] = {{1, 6, 6}, {1, 3, 6}, {1, 3, 5}, {1, 3, 4}, {1, 3, 3}};
     sym = false;
@@ -1585,7 +1658,13 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
       return NCGP_OK;
     };
     int rc;
-    if (op->family == NCGP_RBF)
+    if (dbg)  // per-tile trace of cluster 0 (tools/trace_sym.py)
+      rc = op->family == NCGP_RBF
+               ? (wp == 16 ? launch(kop_tc_kernel<NCGP_RBF, 16, true, true>)
+                           : launch(kop_tc_kernel<NCGP_RBF, 32, true, true>))
+               : (wp == 16 ? launch(kop_tc_kernel<NCGP_MATERN32, 16, true, true>)
+                           : launch(kop_tc_kernel<NCGP_MATERN32, 32, true, true>));
+    else if (op->family == NCGP_RBF)
       rc = wp == 16 ? launch(kop_tc_kernel<NCGP_RBF, 16, false, true>)
                     : launch(kop_tc_kernel<NCGP_RBF, 32, false, true>);
     else
@@ -1611,6 +1690,14 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
         break;
       }
     NCGP_CHECK_ARG(ok, NCGP_UNSUPPORTED, "shared memory too small for d=%d", op->d);
+    const char* e = getenv("NCGP_RINGS");  // timing experiments: "na,sx,sv"
+    int na, sx, sv;
+    if (e != nullptr && sscanf(e, "%d,%d,%d", &na, &sx, &sv) == 3 &&
+        smem_bytes(p.a_bytes, wp, na, sx, sv) <= (size_t)SMEM_BUDGET) {
+      p.na = na;
+      p.sx = sx;
+      p.sv = sv;
+    }
   }
   NCGP_CHECK_ARG((int64_t)p.splits * p.nloc * w * 8 <= (int64_t)(L.total - L.partial) ||
                      p.splits == 1,

@@ -1,14 +1,15 @@
 """Timing of the symmetric kernel with parts removed (NCGP_SYM_DBG bits; wrong
-results, timing only).  usage: python tools/sym_modes.py [n]"""
+results, timing only).  usage: python tools/sym_modes.py [n] [family]"""
 import os, sys, numpy as np, torch
 sys.path.insert(0, ".")
 from paper_2310_20285_b200.kernels import KernelOperator
 torch.cuda.set_device(0)
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 200_000
+fam = sys.argv[2] if len(sys.argv) > 2 else "rbf"
 rng = np.random.default_rng(0)
 X = torch.from_numpy(rng.standard_normal((n, 8))).float().cuda()
 V = torch.from_numpy(rng.standard_normal((n, 32))).float().cuda()
-op = KernelOperator("rbf", 1.5, 1.0, X, w_max=32)
+op = KernelOperator(fam, 1.5, 1.0, X, w_max=32)
 for sym, dbg, name in (("0", "0", "plain"), ("1", "0", "sym"), ("1", "1", "no D_T red"), ("1", "3", "no red at all"),
                        ("1", "9", "no D_T ld/red"), ("1", "4", "no transposed MMAs"), ("1", "13", "no T MMA, no D_T ld/red"),
                        ("1", "16", "no P smem stores"), ("1", "29", "no T path at all")):

@@ -9,6 +9,7 @@ Events (clock64 of CTA 0, one row per tile step g):
   7/10 eN_done epilogue WG N arrived p_full(g)
 """
 import ctypes
+import os
 import sys
 
 import numpy as np
@@ -22,13 +23,14 @@ torch.cuda.set_device(0)
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 200_000
 fam = sys.argv[2] if len(sys.argv) > 2 else "rbf"
 mode = int(sys.argv[3]) if len(sys.argv) > 3 else 0
-EV = 12
+EV = 16
 rng = np.random.default_rng(0)
 X = torch.from_numpy(rng.standard_normal((n, 8))).float().cuda()
-S = torch.from_numpy(rng.standard_normal((n, 32))).float().cuda()
+W = int(os.environ.get("TRACE_W", "32"))
+S = torch.from_numpy(rng.standard_normal((n, W))).float().cuda()
 op = KernelOperator(fam, 1.5, 1.0, X, w_max=32, impl="tcgen05")
 op.apply(S)
-buf = torch.zeros(256 * EV, dtype=torch.int64, device="cuda")
+buf = torch.zeros(256 * EV + 4 * 4096, dtype=torch.int64, device="cuda")
 lib = _native.load()
 lib.ncgp_debug_set_trace.argtypes = [ctypes.c_void_p]
 lib.ncgp_debug_set_trace(buf.data_ptr())
@@ -37,7 +39,13 @@ op.apply(S)
 torch.cuda.synchronize()
 lib.ncgp_debug_set_trace(None)
 lib.ncgp_debug_set_mode(0)
-t = buf.view(256, EV).cpu().numpy().astype(np.int64)
+allb = buf.cpu().numpy().astype(np.int64)
+t = allb[:256 * EV].reshape(256, EV)
+span = allb[256 * EV:].reshape(4096, 4)
+span = span[span[:, 0] > 0]
+t0 = span[:, 0].min()
+ends = (span[:, 1] - t0) / 1e3
+print(f"CTAs {len(span)}: end min {ends.min():.1f} / median {np.median(ends):.1f} / max {ends.max():.1f} us")
 lo, hi = 40, 200
 e = t[lo:hi]
 
