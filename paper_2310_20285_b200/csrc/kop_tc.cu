@@ -357,8 +357,8 @@ struct TcParams {
   int sym_dbg;           // symmetric kernel debug bits (timing / diagnosis only): 1 = drop D_T
                          // reductions, 2 = drop O reductions, 4 = no transposed MMAs,
                          // 8 = no D_T loads, 16 = no P stores to shared memory;
-                         // variants (correct results): 32 = P stored per chunk, not
-                         // in a burst, 64 = flip whether T(g) is held back behind GEMM1(g + NS)
+                         // variant (correct results): 64 = flip whether T(g) is held
+                         // back behind GEMM1(g + NS)
   float* sym_dump;       // symmetric kernel debug: raw D_T per (pair, tile, rank) when set
   int debug_mode;        // debug (timing only, wrong results): 1 = epilogue skips TMEM traffic,
                          // 2 = no GEMM2, 3 = no GEMM1, 4 = no column copies (8: XB only, 9: V only)
@@ -528,7 +528,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   uint64_t* pt_free = vi_empty + 1;       // [2]   SYM both: P buffer free (multicast commit)
   uint64_t* dt_full = pt_free + 2;        // [2]   SYM both: transposed product done
   uint64_t* dt_empty = dt_full + 2;       // [2]   SYM leader: D_T drained (8 warp arrivals)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dt_empty + 2);
+  uint64_t* s_free = dt_empty + 2;        // [NR]  SYM leader: S(g) loaded by the epilogue (16 warps)
+  uint64_t* xb_full = s_free + NR;        // [NR]  SYM leader: XB(g) landed (2 halves)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xb_full + NR);
   // SYM leader: GEMM1 tiles issued so far (the transposed issuer queues T(g)
   // behind GEMM1(g + NS) in the in-order tensor pipe)
   volatile uint32_t* g1_cnt = tmem_slot + 1;
@@ -540,7 +542,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     for (int s = 0; s < NR; ++s) {
       mbar_init(&s_full[s], 1);
       mbar_init(&g2done[s], 1);
-      mbar_init(&rdy[s], 16 + 2 + 2);  // epilogue group (8 warps x 2 CTAs), V, XB
+      // epilogue group (8 warps x 2 CTAs), V, XB (symmetric kernel: XB has its own ring)
+      mbar_init(&rdy[s], SYM ? 16 + 2 : 16 + 2 + 2);
+      mbar_init(&s_free[s], 16);
+      mbar_init(&xb_full[s], 2);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&a_land[b], 1);
@@ -548,7 +553,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       mbar_init(&a_empty[b], 1);
       mbar_init(&o_full[b], 1);
       mbar_init(&o_empty[b], 8);
-      mbar_init(&pt_free[b], 1);
+      mbar_init(&pt_free[b], SYM ? 2 : 1);  // SYM: GEMM2(g) and T(g) both read P(g)
       mbar_init(&dt_full[b], 1);
       mbar_init(&dt_empty[b], 8);
     }
@@ -603,7 +608,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     // relays it; separate loops, because vi_empty depends on rdy, which
     // depends on the XB stream running ahead)
     const uint32_t depth = is_x ? (uint32_t)p.sx : (uint32_t)p.sv;
-    const uint32_t lagt = is_x ? (uint32_t)p.sx : (uint32_t)(p.sv - NS);  // tile g - lagt
+    // symmetric kernel: GEMM1 no longer waits for GEMM2, so V slots are
+    // released by GEMM2's own completion (g2done, multicast)
+    const uint32_t lagt = is_x ? (uint32_t)p.sx : (SYM ? depth : (uint32_t)(p.sv - NS));  // tile g - lagt
+    uint64_t* rel = (SYM && !is_x) ? g2done : s_full;
     uint64_t* land = is_x ? xb_land : v_land;
     if (role == 0) {
       TileIter ti;
@@ -623,7 +631,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                    &a_land[ab]);
           ++nitem;
         }
-        if (g >= depth) mbar_wait(&s_full[sr.idx], sr.phase);
+        if (g >= depth) mbar_wait(&rel[sr.idx], sr.phase);
         const int64_t src = (int64_t)ti.ct * p.tile_stride + half_off;
         if (DBG && (p.debug_mode == 4 || p.debug_mode == 5 || p.debug_mode == (is_x ? 8 : 9))) {
           mbar_expect_tx(&land[r.idx], 0);  // timing only: no copy
@@ -678,17 +686,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         // V(g) -> rdy[g]; XB(t) -> rdy[t - NS] (prologue tiles: xb_pro[t])
         if (!is_x)
           mbar_arrive_cluster(leader_addr(&rdy[rr.idx]));
+        else if (SYM)
+          mbar_arrive_cluster(leader_addr(&xb_full[rr.idx]));
         else if (g < (uint32_t)NS)
           mbar_arrive_cluster(leader_addr(&xb_pro[g]));
         else
           mbar_arrive_cluster(leader_addr(&rdy[rr.idx]));
-        if (!is_x || g >= (uint32_t)NS) rr.adv();
+        if (!is_x || SYM || g >= (uint32_t)NS) rr.adv();
         r.adv();
         ++g;
         ti.next(p, items);
       }
       // the last NS steps have no XB(g + NS): stand in for those arrivals
-      if (is_x)
+      if (is_x && !SYM)
         for (uint32_t t = g < (uint32_t)NS ? (uint32_t)NS : g; t < g + (uint32_t)NS; ++t) {
           mbar_arrive_cluster(leader_addr(&rdy[rr.idx]));
           rr.adv();
@@ -724,7 +734,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
               mbar_wait(&a_full[0], item1 & 1u);
             ++item1;
           }
-          if (g1n < (uint32_t)NS) {
+          if (SYM) {  // XB(t) landed; S buffer free once the epilogue loaded S(t - NS)
+            mbar_wait(&xb_full[c1], (g1n / (uint32_t)NR) & 1u);
+            if (g1n >= (uint32_t)NS) {
+              mbar_wait(&s_free[gd], gdph);
+              if (++gd == (uint32_t)NR) {
+                gd = 0;
+                gdph ^= 1u;
+              }
+            }
+          } else if (g1n < (uint32_t)NS) {
             mbar_wait(&xb_pro[g1n], 0);
           } else {  // S buffer free; XB(t) landed (it is part of rdy(t - NS))
             mbar_wait(&g2done[gd], gdph);
@@ -777,15 +796,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           // P_lo x Vhi (N = WP: each CTA supplies half of Vhi's rows).
           const uint32_t a0 = tmem + s2 * (uint32_t)BN, dO = tO((int)ob);
           if (elect_one()) {
-            if (!(DBG && (p.debug_mode == 2 || p.debug_mode == 6))) {
+            if (SYM) {
+              // symmetric kernel: P(g) from shared-memory buffer g mod 2 (K-major
+              // canonical layout, the same bytes the transposed product reads)
+              const uint64_t ph = sdesc(smem_u32(sP) + (gt & 1u) * PBUF, 128u, 2048u);
+              const uint64_t pl = ph + ((PBUF / 2) >> 4);
 #pragma unroll
               for (int m = 0; m < BN / 16; ++m) {
-                const uint32_t ahi = a0 + 32u * (m >> 1) + 8u * (m & 1);
-                mma_ts(dO, ahi, dv + (uint64_t)(16 * m), id2, (fresh && m == 0) ? 0u : 1u);
-                mma_ts(dO, ahi + 16u, dv + v3off + (uint64_t)(16 * m), id2h, 1u);
+                mma_ss(dO, ph + (uint64_t)(16 * m), dv + (uint64_t)(16 * m), id2, (fresh && m == 0) ? 0u : 1u);
+                mma_ss(dO, pl + (uint64_t)(16 * m), dv + v3off + (uint64_t)(16 * m), id2h, 1u);
               }
+              tc_commit2(&g2done[r]);           // V slot g free (both CTAs)
+              tc_commit2(&pt_free[gt & 1u]);    // with T(g): P buffer g mod 2 free
+            } else {
+              if (!(DBG && (p.debug_mode == 2 || p.debug_mode == 6))) {
+#pragma unroll
+                for (int m = 0; m < BN / 16; ++m) {
+                  const uint32_t ahi = a0 + 32u * (m >> 1) + 8u * (m & 1);
+                  mma_ts(dO, ahi, dv + (uint64_t)(16 * m), id2, (fresh && m == 0) ? 0u : 1u);
+                  mma_ts(dO, ahi + 16u, dv + v3off + (uint64_t)(16 * m), id2h, 1u);
+                }
+              }
+              tc_commit2_leader(&g2done[r]);  // frees S buffer g for GEMM1(g + NS)
             }
-            tc_commit2_leader(&g2done[r]);  // frees S buffer g for GEMM1(g + NS)
             if (last) tc_commit2(&o_full[ob]);
           }
           __syncwarp();
@@ -883,16 +916,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       if ((int)(gt & 1u) == e) {
         const int b = (int)bb;
         if (tr) trace_ev<DBG>(p, gt, 3 + 2 * e);
-        const bool tp = SYM && ti.transposed();
-        // P buffer e is free once the transposed issuer finished tile gt - 2.
-        // Waited on every tile, not only transposed ones: the issuer commits
-        // pt_free for every tile, and skipping waits (diagonal tiles at item
-        // starts) would let the epilogue run two phases ahead and alias the
-        // parity.  By default (burst) P is copied TMEM -> shared memory after
-        // the whole tile is transformed, so T(gt - 2) has the tile's epilogue
-        // time to finish; sym_dbg bit 32 stores each chunk as it is made
-        // (the wait then sits before the first store).
-        const bool burst = SYM && !(p.sym_dbg & 32);
+        // symmetric kernel: P buffer e is free once GEMM2(gt - 2) and T(gt - 2)
+        // completed.  Waited on every tile (both commit pt_free for every
+        // tile), just before the first shared-memory store, so the first
+        // chunk's TMEM load and transform overlap them.
         bool pt_wait = SYM && gt >= 2u;
         mbar_wait(&s_full[er.idx], er.phase);
         tc_fence_after();
@@ -900,58 +927,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         if (!(DBG && (p.debug_mode == 1 || p.debug_mode == 5))) {
           const uint32_t base = tS(b) + lane_off + col0;
           uint32_t ra[32], hi[16], lo[16];
+          if constexpr (SYM) {
+            // P goes to shared memory only (row i = TMEM lane, 8 consecutive j
+            // per 16 B): the K-major A of GEMM2 and the MN-major A of T.  S(g)
+            // is released to GEMM1(g + NS) as soon as it is loaded.
+            const int i = 32 * wq + lane;
+            const uint32_t rowb0 = smem_u32(sP) + (uint32_t)e * PBUF + (uint32_t)(i >> 3) * 2048u +
+                                   (uint32_t)(i & 7) * 16u + (col0 >> 3) * 128u;
 #pragma unroll
-          for (int c = 0; c < BN / 64; ++c) {
-            tmem_ld32(base + 32 * c, ra);
-            tmem_wait_ld(ra);
-            transform_chunk<FAM>(ra, L, hi, lo);
-            if (FAM == NCGP_RBF) {
-              tmem_st_hilo(base + 32 * c, hi, lo);
-            } else {
-              tmem_st16(base + 32 * c, hi);
-              tmem_st16(base + 32 * c + 16, lo);
-            }
-            if (burst) continue;
-            if (SYM && pt_wait) {
-              mbar_wait(&pt_free[e], ((gt >> 1) - 1u) & 1u);
-              pt_wait = false;
-              if (tr) trace_ev<DBG>(p, gt, 8);
-            }
-            if (tp && !(p.sym_dbg & 16)) {  // row i = TMEM lane, 32 columns = 4 core matrices of 8 j
-              const int i = 32 * wq + lane;
-              const uint32_t rowb = smem_u32(sP) + (uint32_t)e * PBUF + (uint32_t)(i >> 3) * 2048u +
-                                    (uint32_t)(i & 7) * 16u + ((col0 + 32u * c) >> 3) * 128u;
-#pragma unroll
-              for (int g = 0; g < 4; ++g) {
-                st_shared_v4(rowb + 128u * g, hi[4 * g], hi[4 * g + 1], hi[4 * g + 2], hi[4 * g + 3]);
-                st_shared_v4(rowb + PBUF / 2 + 128u * g, lo[4 * g], lo[4 * g + 1], lo[4 * g + 2],
-                             lo[4 * g + 3]);
+            for (int c = 0; c < BN / 64; ++c) {
+              tmem_ld32(base + 32 * c, ra);
+              tmem_wait_ld(ra);
+              if (c == BN / 64 - 1) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(leader_addr(&s_free[er.idx]));
               }
-            }
-          }
-          tmem_wait_st();
-          if (burst) {
-            if (pt_wait) mbar_wait(&pt_free[e], ((gt >> 1) - 1u) & 1u);
-            if (tr) trace_ev<DBG>(p, gt, 8);
-            if (tp && !(p.sym_dbg & 16)) {
-              const int i = 32 * wq + lane;
-              const uint32_t rowb0 = smem_u32(sP) + (uint32_t)e * PBUF + (uint32_t)(i >> 3) * 2048u +
-                                     (uint32_t)(i & 7) * 16u + (col0 >> 3) * 128u;
-#pragma unroll
-              for (int c = 0; c < BN / 64; ++c) {
-                tmem_ld32(base + 32 * c, ra);  // [P_hi 16 | P_lo 16] packed pairs
-                tmem_wait_ld(ra);
-                const uint32_t rowb = rowb0 + 4u * 128u * c;
+              transform_chunk<FAM>(ra, L, hi, lo);
+              if (pt_wait) {
+                mbar_wait(&pt_free[e], ((gt >> 1) - 1u) & 1u);
+                pt_wait = false;
+                if (tr) trace_ev<DBG>(p, gt, 8);
+              }
+              if (!(p.sym_dbg & 16)) {
+                const uint32_t rowb = rowb0 + 512u * c;
 #pragma unroll
                 for (int g = 0; g < 4; ++g) {
-                  st_shared_v4(rowb + 128u * g, ra[4 * g], ra[4 * g + 1], ra[4 * g + 2], ra[4 * g + 3]);
-                  st_shared_v4(rowb + PBUF / 2 + 128u * g, ra[16 + 4 * g], ra[16 + 4 * g + 1],
-                               ra[16 + 4 * g + 2], ra[16 + 4 * g + 3]);
+                  st_shared_v4(rowb + 128u * g, hi[4 * g], hi[4 * g + 1], hi[4 * g + 2], hi[4 * g + 3]);
+                  st_shared_v4(rowb + PBUF / 2 + 128u * g, lo[4 * g], lo[4 * g + 1], lo[4 * g + 2],
+                               lo[4 * g + 3]);
                 }
               }
             }
+            fence_proxy_async_smem();
+          } else {
+#pragma unroll
+            for (int c = 0; c < BN / 64; ++c) {
+              tmem_ld32(base + 32 * c, ra);
+              tmem_wait_ld(ra);
+              transform_chunk<FAM>(ra, L, hi, lo);
+              if (FAM == NCGP_RBF) {
+                tmem_st_hilo(base + 32 * c, hi, lo);
+              } else {
+                tmem_st16(base + 32 * c, hi);
+                tmem_st16(base + 32 * c + 16, lo);
+              }
+            }
+            tmem_wait_st();
           }
-          if (tp) fence_proxy_async_smem();
         }
         tc_fence_before();
         __syncwarp();
@@ -1463,7 +1486,7 @@ size_t smem_bytes(uint32_t a_bytes, int wp, int na, int sx, int sv, bool sym = f
   const size_t v2 = (size_t)wp * BN * 2, v3 = v2 / 2;
   return (size_t)na * a_bytes + (size_t)sx * (a_bytes / 2) + (size_t)sv * (v2 + v3) +
          (sym ? 2 * v2 + 2 * (size_t)PBUF + (size_t)BM * wp * 4 : (size_t)wp * BM * 8) +
-         (6 + 9 + 2 + NS_MAX + 3 * NR + 8 + 12) * sizeof(uint64_t) + 16 + 1024;
+         (6 + 9 + 2 + NS_MAX + 5 * NR + 8 + 12) * sizeof(uint64_t) + 16 + 1024;
 }
 
 }  // namespace
