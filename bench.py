@@ -313,7 +313,18 @@ def run_ours(args, rank, world, local_rank):
                 "peak_basis": f"min({pk['source']} bf16 {pk['bf16']}/2 TF/s, "
                               f"{sms} SM x {P_MUFU_PER_SM_CLK} ex2/clk x "
                               f"{pk['sm_max_mhz']} MHz x F/E={F}/{E})",
-                "kernel_ms": round(1e3 * t_kernel, 3), "impl": op.impl}
+                "kernel_ms": round(1e3 * t_kernel, 3), "impl": op.impl,
+                "variant": op.last_variant}
+    if op.last_variant == "symmetric":
+        # each off-diagonal 128 x 128 tile is evaluated once and serves both
+        # K V and K^T V; `achieved` / `frac` count the algorithmic n^2 pairs
+        nb = -(-n // 128)
+        ev = sum(2 * (nb - 2 * a) for a in range((nb + 1) // 2)) / float(nb * nb)
+        roofline["evaluated_pair_fraction"] = round(ev, 4)
+        roofline["frac_executed"] = round(achieved * ev / peak_tflops, 4)
+        roofline["note"] = ("symmetric K(X,X) kernel: evaluated_pair_fraction of the n^2 kernel "
+                            "values are computed; frac_executed is the executed exp rate "
+                            "against the MUFU peak")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

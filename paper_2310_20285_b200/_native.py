@@ -51,6 +51,7 @@ _SIGS = {
     "ncgp_kop_apply_multi": (_i32, [_vp, _vp, _i64, _i32, ctypes.POINTER(_vp), _i32, _i64, _i64,
                                     _i64, _vp]),
     "ncgp_kop_impl": (_i32, [_vp]),
+    "ncgp_kop_last_variant": (_i32, [_vp]),
     "ncgp_kop_destroy": (_i32, [_vp]),
     "ncgp_softmax_stats": (_i32, [_i32, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp]),
     "ncgp_softmax_winv": (_i32, [_i32, _vp, _i64, _i32, _vp, _i64, _i32, _vp, _i64, _f64, _f64,

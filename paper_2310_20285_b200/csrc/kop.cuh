@@ -30,6 +30,7 @@ struct ncgp_kop {
   int64_t sym_items;
   int4* sym_tab;
   float* sym_acc;
+  int last_variant = -1;  // 0 plain, 1 symmetric (ncgp_kop_last_variant)
 };
 
 namespace ncgp {

@@ -111,6 +111,7 @@ static int kop_apply_outs(ncgp_kop* op, const void* V, int64_t ldv, int w,
   }
   if (op->impl == NCGP_KOP_TCGEN05)
     return ncgp::tc_apply(op, V, ldv, w, outs, ldo, row_begin, row_end, ncgp::as_stream(stream));
+  op->last_variant = 0;
   return ncgp::simt_apply(op, V, ldv, w, outs, ldo, row_begin, row_end, ncgp::as_stream(stream));
 }
 
@@ -135,6 +136,8 @@ int ncgp_kop_apply_multi(ncgp_kop* op, const void* V, int64_t ldv, int w, void* 
 }
 
 int ncgp_kop_impl(const ncgp_kop* op) { return op ? op->impl : -1; }
+
+int ncgp_kop_last_variant(const ncgp_kop* op) { return op ? op->last_variant : -1; }
 
 int ncgp_kop_destroy(ncgp_kop* op) {
   delete op;

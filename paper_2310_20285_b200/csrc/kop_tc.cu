@@ -1421,27 +1421,43 @@ int splits_for(int64_t pairs, int64_t col_tiles, int clusters) {
 }
 
 // Symmetric kernel work list: row-tile pair a covers column tiles [2a, nb)
-// (the diagonal 256 x 256 block plus everything right of it), cut into items
-// of at most SYM_ITEM tiles; the transposed products of tiles c >= 2a + 2
-// cover the blocks left of the diagonal.
+// (the diagonal 256 x 256 block plus everything right of it); the transposed
+// products of tiles c >= 2a + 2 cover the blocks left of the diagonal.  The
+// columns are cut into global blocks of SYM_ITEM tiles, and the list is
+// block-major: (block 0: pairs 0, 1, ...), (block 1: ...), ...  The clusters
+// running at the same time then share one block's column records and the
+// fp32 accumulator rows its transposed products reduce into, both L2-sized
+// (at N = 1e6 a pair-major list streamed all 192 MB of records and 128 MB of
+// accumulator rows through L2 at once).
 int sym_item_len() {
   const char* e = getenv("NCGP_SYM_ITEM");
   return e != nullptr && atoi(e) > 0 ? atoi(e) : 128;
 }
+template <typename F>
+void sym_walk(int64_t pairs, int64_t nb, F&& f) {
+  const int64_t L = sym_item_len();
+  const char* e = getenv("NCGP_SYM_ORDER");  // "pair": the pair-major list (experiments)
+  if (e != nullptr && e[0] == 'p') {
+    for (int64_t a = 0; a < pairs; ++a)
+      for (int64_t c0 = 2 * a; c0 < nb; c0 += L) f(a, c0, std::min<int64_t>(nb, c0 + L));
+    return;
+  }
+  for (int64_t b0 = 0; b0 < nb; b0 += L) {
+    const int64_t b1 = std::min<int64_t>(nb, b0 + L);
+    for (int64_t a = 0; a < pairs && 2 * a < b1; ++a) f(a, std::max<int64_t>(b0, 2 * a), b1);
+  }
+}
 int64_t sym_item_count(int64_t pairs, int64_t nb) {
-  const int L = sym_item_len();
   int64_t n = 0;
-  for (int64_t a = 0; a < pairs; ++a)
-    if (2 * a < nb) n += (nb - 2 * a + L - 1) / L;
+  sym_walk(pairs, nb, [&](int64_t, int64_t, int64_t) { ++n; });
   return n;
 }
 std::vector<int4> sym_items(int64_t pairs, int64_t nb) {
-  const int L = sym_item_len();
   std::vector<int4> t;
   t.reserve((size_t)sym_item_count(pairs, nb));
-  for (int64_t a = 0; a < pairs; ++a)
-    for (int64_t c0 = 2 * a; c0 < nb; c0 += L)
-      t.push_back(make_int4((int)a, (int)c0, (int)std::min<int64_t>(nb, c0 + L), 0));
+  sym_walk(pairs, nb, [&](int64_t a, int64_t c0, int64_t c1) {
+    t.push_back(make_int4((int)a, (int)c0, (int)c1, 0));
+  });
   return t;
 }
 
@@ -1680,6 +1696,7 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
       NCGP_LAUNCHED();
       return NCGP_OK;
     };
+    op->last_variant = 1;
     int rc;
     if (dbg)  // per-tile trace of cluster 0 (tools/trace_sym.py)
       rc = op->family == NCGP_RBF
@@ -1727,6 +1744,7 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
                  NCGP_INVALID_INPUT, "partial workspace too small");
   const size_t smem = smem_bytes(p.a_bytes, wp, p.na, p.sx, p.sv);
   const int64_t items = p.pairs * p.splits;
+  op->last_variant = 0;
   const unsigned grid = 2u * (unsigned)std::min<int64_t>(items, clusters);
   auto launch = [&](auto kern) -> int {
     NCGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -72,6 +72,11 @@ class KernelOperator:
         self.impl = {N.KOP_TCGEN05: "tcgen05", N.KOP_SIMT: "simt"}[
             N.query("ncgp_kop_impl", h)]
 
+    @property
+    def last_variant(self) -> str:
+        """Kernel variant of the last apply: "plain", "symmetric" or "none"."""
+        return {0: "plain", 1: "symmetric"}.get(N.query("ncgp_kop_last_variant", self._h), "none")
+
     def apply(self, V: torch.Tensor, out: Optional[torch.Tensor] = None,
               row_begin: int = 0, row_end: Optional[int] = None,
               peers: Optional[Sequence[torch.Tensor]] = None) -> torch.Tensor:
