@@ -94,9 +94,47 @@ def test_symmetric_kernel_only_on_full_square_launches():
     assert torch.equal(rr, rr0)
 
 
-def test_symmetric_default_policy_is_matern_only():
-    X, V, op, Vd = _case(3000, 8, 8, ("rbf", 1.5, 1.0), 4)
-    a = op.apply(Vd)
+@pytest.mark.parametrize("n,w,fam,variant", [
+    (3000, 8, "rbf", "plain"),             # small: the triangular list balances poorly
+    (3000, 8, "matern32", "plain"),
+    (70001, 32, "rbf", "plain"),           # RBF at WP = 32: the plain kernel is faster
+    (70001, 10, "rbf", "symmetric"),       # RBF at WP = 16
+    (70001, 32, "matern32", "symmetric"),
+])
+def test_symmetric_default_policy(n, w, fam, variant):
+    """Default kernel choice (kop_tc.cu sym_enabled) and, for the symmetric
+    kernel, agreement with the plain kernel and with fp64 on a row block."""
+    X, V, op, Vd = _case(n, 8, w, (fam, 1.5, 1.0), 11)
+    got = op.apply(Vd)
+    assert op.last_variant == variant
+    if variant == "plain":
+        with _Env(NCGP_SYM=0):
+            assert torch.equal(got, op.apply(Vd))
+        return
     with _Env(NCGP_SYM=0):
-        b = op.apply(Vd)
-    assert torch.equal(a, b)  # RBF: plain kernel by default
+        plain = op.apply(Vd)
+    assert op.last_variant == "plain"
+    assert float((got.double() - plain.double()).norm() / plain.double().norm()) < 2e-5
+    # fp64 CUDA-core reference on the first and last row blocks (ragged tail)
+    op64 = KernelOperator(fam, 1.5, 1.0, op.X_rows.double(), w_max=32, impl="simt")
+    Vd64, Va64 = Vd.double(), Vd.double().abs()
+    for r0, r1 in ((0, 512), (n - 300, n)):
+        ref = torch.zeros((n, w), dtype=torch.float64, device=Vd.device)
+        sc = torch.zeros_like(ref)
+        op64.apply(Vd64, out=ref, row_begin=r0, row_end=r1)
+        op64.apply(Va64, out=sc, row_begin=r0, row_end=r1)
+        err = (got[r0:r1].double() - ref[r0:r1]).abs() / sc[r0:r1]
+        assert float(err.max()) < 1e-5
+
+
+def test_symmetric_work_list_order_invariant():
+    """Block-major (default) and pair-major work lists give the same product
+    up to fp32 reduction order."""
+    X, V, op, Vd = _case(40000, 8, 10, ("rbf", 1.5, 1.0), 5)
+    outs = []
+    for order in ("block", "pair"):
+        with _Env(NCGP_SYM=1, NCGP_SYM_ORDER=order):
+            o = KernelOperator("rbf", 1.5, 1.0, op.X_rows, w_max=32)  # table built at creation
+            outs.append(o.apply(Vd).double())
+            assert o.last_variant == "symmetric"
+    assert float((outs[0] - outs[1]).norm() / outs[1].norm()) < 5e-6
