@@ -360,6 +360,7 @@ struct TcParams {
                          // variant (correct results): 64 = flip whether T(g) is held
                          // back behind GEMM1(g + NS)
   float* sym_dump;       // symmetric kernel debug: raw D_T per (pair, tile, rank) when set
+  int npb;               // symmetric kernel: P buffers in shared memory (2, or 1 for large D)
   int debug_mode;        // debug (timing only, wrong results): 1 = epilogue skips TMEM traffic,
                          // 2 = no GEMM2, 3 = no GEMM1, 4 = no column copies (8: XB only, 9: V only)
 };
@@ -503,7 +504,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   uint8_t* sVI = sV + (size_t)p.sv * vslot;
   uint8_t* sP = sVI + (SYM ? 2 * (size_t)p.v2_bytes : 0);
   // symmetric kernel: fp32 staging rows [128][WP] for the bulk reductions
-  float* sStage = reinterpret_cast<float*>(sP + (SYM ? 2 * (size_t)PBUF : 0));
+  float* sStage = reinterpret_cast<float*>(sP + (SYM ? (size_t)p.npb * PBUF : 0));
+  // symmetric kernel: P buffer of tile g (two alternate by tile parity; one
+  // when shared memory is short).  GEMM2(g) and T(g) always commit to
+  // pt_free[g & 1], whose phases then advance once per two tiles; the
+  // epilogue of tile g waits for tile g - npb's phase, which with one buffer
+  // is the other group's barrier.  A single barrier would let a group, which
+  // only sees every other phase, alias a phase two behind as complete.
+  auto pbuf = [&](uint32_t g) -> uint32_t { return p.npb == 2 ? (g & 1u) : 0u; };
   double* sAcc = reinterpret_cast<double*>(sStage + (SYM ? BM * WP : 0));  // [WP][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sAcc + (SYM ? 0 : WP * BM));
   uint64_t* xb_land = bars;               // [6]   local copy completion
@@ -799,7 +807,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             if (SYM) {
               // symmetric kernel: P(g) from shared-memory buffer g mod 2 (K-major
               // canonical layout, the same bytes the transposed product reads)
-              const uint64_t ph = sdesc(smem_u32(sP) + (gt & 1u) * PBUF, 128u, 2048u);
+              const uint64_t ph = sdesc(smem_u32(sP) + pbuf(gt) * PBUF, 128u, 2048u);
               const uint64_t pl = ph + ((PBUF / 2) >> 4);
 #pragma unroll
               for (int m = 0; m < BN / 16; ++m) {
@@ -807,7 +815,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 mma_ss(dO, pl + (uint64_t)(16 * m), dv + v3off + (uint64_t)(16 * m), id2h, 1u);
               }
               tc_commit2(&g2done[r]);           // V slot g free (both CTAs)
-              tc_commit2(&pt_free[gt & 1u]);    // with T(g): P buffer g mod 2 free
+              tc_commit2(&pt_free[gt & 1u]);    // with T(g): P(g)'s buffer free
             } else {
               if (!(DBG && (p.debug_mode == 2 || p.debug_mode == 6))) {
 #pragma unroll
@@ -866,7 +874,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           if (lane == 0) trace_ev<DBG>(p, gt, 13);
           if (elect_one()) {
             if (tp && !(p.sym_dbg & 4)) {
-              const uint64_t pa = dP0 + (uint64_t)(gt & 1u) * (PBUF >> 4);
+              const uint64_t pa = dP0 + (uint64_t)pbuf(gt) * (PBUF >> 4);
 #pragma unroll 1
               for (int m = 0; m < BN / 16; ++m) {
                 const uint64_t ah = pa + (uint64_t)m * (4096 >> 4), al = ah + ((PBUF / 2) >> 4);
@@ -920,7 +928,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         // completed.  Waited on every tile (both commit pt_free for every
         // tile), just before the first shared-memory store, so the first
         // chunk's TMEM load and transform overlap them.
-        bool pt_wait = SYM && gt >= 2u;
+        bool pt_wait = SYM && gt >= (uint32_t)p.npb;
         mbar_wait(&s_full[er.idx], er.phase);
         tc_fence_after();
         if (tr) trace_ev<DBG>(p, gt, 4 + 2 * e);
@@ -932,7 +940,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             // per 16 B): the K-major A of GEMM2 and the MN-major A of T.  S(g)
             // is released to GEMM1(g + NS) as soon as it is loaded.
             const int i = 32 * wq + lane;
-            const uint32_t rowb0 = smem_u32(sP) + (uint32_t)e * PBUF + (uint32_t)(i >> 3) * 2048u +
+            const uint32_t rowb0 = smem_u32(sP) + pbuf(gt) * PBUF + (uint32_t)(i >> 3) * 2048u +
                                    (uint32_t)(i & 7) * 16u + (col0 >> 3) * 128u;
 #pragma unroll
             for (int c = 0; c < BN / 64; ++c) {
@@ -945,7 +953,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
               }
               transform_chunk<FAM>(ra, L, hi, lo);
               if (pt_wait) {
-                mbar_wait(&pt_free[e], ((gt >> 1) - 1u) & 1u);
+                const uint32_t t = gt - (uint32_t)p.npb;
+                mbar_wait(&pt_free[t & 1u], (t >> 1) & 1u);
                 pt_wait = false;
                 if (tr) trace_ev<DBG>(p, gt, 8);
               }
@@ -1498,10 +1507,10 @@ Layout layout_of(int64_t n_rows, int64_t n_cols, int d, int w_max, int sms) {
   return L;
 }
 
-size_t smem_bytes(uint32_t a_bytes, int wp, int na, int sx, int sv, bool sym = false) {
+size_t smem_bytes(uint32_t a_bytes, int wp, int na, int sx, int sv, int sym_npb = 0) {
   const size_t v2 = (size_t)wp * BN * 2, v3 = v2 / 2;
   return (size_t)na * a_bytes + (size_t)sx * (a_bytes / 2) + (size_t)sv * (v2 + v3) +
-         (sym ? 2 * v2 + 2 * (size_t)PBUF + (size_t)BM * wp * 4 : (size_t)wp * BM * 8) +
+         (sym_npb ? 2 * v2 + sym_npb * (size_t)PBUF + (size_t)BM * wp * 4 : (size_t)wp * BM * 8) +
          (6 + 9 + 2 + NS_MAX + 5 * NR + 8 + 12) * sizeof(uint64_t) + 16 + 1024;
 }
 
@@ -1664,13 +1673,22 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
   bool sym = op->sym_items > 0 && r0 == 0 && r1 == op->n_rows && g_debug_mode == 0 &&
              sym_enabled(op->family, wp, op->col_tiles);
   if (sym) {
-    const int cand[][3] = {{1, 6, 6}, {1, 3, 6}, {1, 3, 5}, {1, 3, 4}, {1, 3, 3}};
+    // two P buffers with the deepest rings that fit, else one P buffer
+    // (large D: the row tile and XB ring outgrow the 227 KB)
+    const int cand[][4] = {{2, 1, 6, 6}, {2, 1, 3, 6}, {2, 1, 3, 5}, {2, 1, 3, 4}, {2, 1, 3, 3},
+                           {1, 1, 3, 6}, {1, 1, 3, 4}, {1, 1, 3, 3}};
+    const char* e = getenv("NCGP_SYM_NPB");  // experiments: force 1 or 2 P buffers
+    const int force = e != nullptr ? atoi(e) : 0;
     sym = false;
     for (auto& c : cand)
-      if (smem_bytes(p.a_bytes, wp, c[0], c[1], c[2], true) <= (size_t)SMEM_BUDGET) {
-        p.na = c[0];
-        p.sx = c[1];
-        p.sv = c[2];
+      // one P buffer serialises the two epilogue groups on it: a 1.15x gain
+      // for Matern-3/2 at D = 50 but a loss for RBF (tools/sym_exp.py)
+      if ((force == c[0] || (force == 0 && (c[0] == 2 || op->family == NCGP_MATERN32))) &&
+          smem_bytes(p.a_bytes, wp, c[1], c[2], c[3], c[0]) <= (size_t)SMEM_BUDGET) {
+        p.npb = c[0];
+        p.na = c[1];
+        p.sx = c[2];
+        p.sv = c[3];
         sym = true;
         break;
       }
@@ -1687,7 +1705,7 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
     }
     p.sym_dump = g_sym_dump;
     NCGP_CUDA(cudaMemsetAsync(p.acc, 0, (size_t)op->row_tiles * BM * wp * sizeof(float), st));
-    const size_t smem = smem_bytes(p.a_bytes, wp, p.na, p.sx, p.sv, true);
+    const size_t smem = smem_bytes(p.a_bytes, wp, p.na, p.sx, p.sv, p.npb);
     const unsigned grid = 2u * (unsigned)std::min<int64_t>(p.n_items, clusters);
     auto launch = [&](auto kern) -> int {
       NCGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
