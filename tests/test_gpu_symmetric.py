@@ -138,3 +138,21 @@ def test_symmetric_work_list_order_invariant():
             outs.append(o.apply(Vd).double())
             assert o.last_variant == "symmetric"
     assert float((outs[0] - outs[1]).norm() / outs[1].norm()) < 5e-6
+
+
+@pytest.mark.parametrize("n,d,w,fam,force", [
+    (70001, 50, 10, "matern32", None),   # default: one P buffer (D = 50 outgrows two)
+    (3000, 8, 8, "rbf", "1"),            # forced one buffer on a small RBF case
+    (20000, 8, 32, "matern32", "1"),
+])
+def test_symmetric_kernel_single_p_buffer(n, d, w, fam, force):
+    """One shared P buffer: each epilogue group waits for the other group's
+    previous tile (pt_free barriers alternate by tile parity)."""
+    X, V, op, Vd = _case(n, d, w, (fam, 3.0, 1.0), 13)
+    env = {"NCGP_SYM": 1, "NCGP_SYM_NPB": force} if force else {}
+    with _Env(**env):
+        got = op.apply(Vd).double()
+    assert op.last_variant == "symmetric"
+    with _Env(NCGP_SYM=0):
+        plain = op.apply(Vd).double()
+    assert float((got - plain).norm() / plain.norm()) < 2e-5
