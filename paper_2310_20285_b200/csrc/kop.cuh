@@ -30,7 +30,8 @@ struct ncgp_kop {
   int64_t sym_items;
   int4* sym_tab;
   float* sym_acc;
-  int last_variant = -1;  // 0 plain, 1 symmetric (ncgp_kop_last_variant)
+  int sym_cg = 2;         // symmetric kernel flavour the work list was built for (1 or 2)
+  int last_variant = -1;  // 0 plain, 1 symmetric pair kernel, 2 symmetric single-CTA kernel
 };
 
 namespace ncgp {

@@ -1159,6 +1159,461 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   }
 }
 
+// ------------------------------------------------------------------ single-CTA symmetric kernel
+// K1-sym1: the symmetric K(X, X) kernel with cta_group::1 MMAs.  One CTA per
+// SM owns a 128-row tile I and sweeps column tiles J >= I; each P(I, J) tile
+// serves O_I += P V_J (GEMM2, A = P K-major) and D_T = P^T V_I (T, A = P
+// MN-major), both read from the same shared-memory copy of P.  Against the
+// pair kernel: the transposed product has no wasted half (B = [Vhi_I | Vlo_I]
+// is this CTA's own block), at the price of one MMA issue per SM instead of
+// per pair and full (not half) column records per CTA.
+// Roles (24 warps): warp 0 lane 0 producer (row tile per item, XB and V per
+// column tile); warp 1 GEMM2; warp 2 TMEM allocation + GEMM1; warp 3 the
+// transposed product (and this row tile's V block per item); warps 4-19 the
+// epilogue (as in the pair kernel's symmetric mode); warps 20-23 the O / D_T
+// drains into the fp32 accumulator.
+__device__ __forceinline__ void mma1_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit1(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+// kind::f16, A/B F16, D F32, M = 128; bit 15: A MN-major (transposed)
+__host__ __device__ constexpr uint32_t idesc1_f16(int n, bool a_mn = false) {
+  return (1u << 4) | (a_mn ? (1u << 15) : 0u) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(128 >> 4) << 24);
+}
+
+struct Tile1 {  // the CTA's global column-tile sequence across its items
+  int it, ct, r, c0, c1;
+  bool valid;
+  __device__ __forceinline__ void load(const TcParams& p) {
+    const int4 t = p.item_tab[it];
+    r = t.x;
+    c0 = t.y;
+    c1 = t.z;
+    ct = c0;
+  }
+  __device__ __forceinline__ void start(const TcParams& p) {
+    it = (int)blockIdx.x;
+    valid = it < p.n_items;
+    if (valid) load(p);
+  }
+  __device__ __forceinline__ void next(const TcParams& p) {
+    if (++ct >= c1) {
+      it += (int)gridDim.x;
+      valid = it < p.n_items;
+      if (valid) load(p);
+    }
+  }
+  __device__ __forceinline__ bool first_in_item() const { return ct == c0; }
+  __device__ __forceinline__ bool last_in_item() const { return ct == c1 - 1; }
+  __device__ __forceinline__ bool transposed() const { return ct > r; }
+  __device__ __forceinline__ bool first_in_chunk() const { return ct == c0 || (ct & (CH - 1)) == 0; }
+  __device__ __forceinline__ bool last_in_chunk() const {
+    return ct == c1 - 1 || (ct & (CH - 1)) == CH - 1;
+  }
+};
+
+template <int FAM, int WP, bool DBG>
+__global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  constexpr int NS1 = 2;  // S buffers: 2 x 128 + O 2 x 2 WP + D_T 2 x 2 WP columns
+  const uint32_t xb_bytes = 2u * p.xbh_bytes;  // 128 XB rows
+  const uint32_t vb_bytes = 2u * p.v2_bytes;   // [Vhi | Vlo]: 2 WP rows
+  uint8_t* sA = smem;
+  uint8_t* sXB = sA + p.a_bytes;
+  uint8_t* sV = sXB + (size_t)p.sx * xb_bytes;
+  uint8_t* sVI = sV + (size_t)p.sv * vb_bytes;
+  uint8_t* sP = sVI + vb_bytes;
+  float* sStage = reinterpret_cast<float*>(sP + 2 * (size_t)PBUF);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStage + BM * WP);
+  uint64_t* xb_full = bars;            // [6]
+  uint64_t* v_full = xb_full + 6;      // [9]
+  uint64_t* a_full = v_full + 9;       // [1]
+  uint64_t* a_empty = a_full + 1;      // [1]
+  uint64_t* vi_full = a_empty + 1;     // [1]
+  uint64_t* vi_empty = vi_full + 1;    // [1]
+  uint64_t* s_full = vi_empty + 1;     // [NR] GEMM1(g) done
+  uint64_t* s_free = s_full + NR;      // [NR] S(g) loaded by the epilogue group (8 warps)
+  uint64_t* rdy = s_free + NR;         // [NR] P(g) stored (8 warps)
+  uint64_t* g2done = rdy + NR;         // [NR] GEMM2(g) done
+  uint64_t* pt_free = g2done + NR;     // [2]  GEMM2(g) and T(g) done with P buffer g & 1
+  uint64_t* o_full = pt_free + 2;      // [2]
+  uint64_t* o_empty = o_full + 2;      // [2]  4 drain warps
+  uint64_t* dt_full = o_empty + 2;     // [2]
+  uint64_t* dt_empty = dt_full + 2;    // [2]  4 drain warps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dt_empty + 2);
+  volatile uint32_t* g1_cnt = tmem_slot + 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 6; ++s) mbar_init(&xb_full[s], 1);
+    for (int s = 0; s < 9; ++s) mbar_init(&v_full[s], 1);
+    mbar_init(a_full, 1);
+    mbar_init(a_empty, 1);
+    mbar_init(vi_full, 1);
+    mbar_init(vi_empty, 1);
+    for (int s = 0; s < NR; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&s_free[s], 8);
+      mbar_init(&rdy[s], 8);
+      mbar_init(&g2done[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&pt_free[b], 2);
+      mbar_init(&o_full[b], 1);
+      mbar_init(&o_empty[b], 4);
+      mbar_init(&dt_full[b], 1);
+      mbar_init(&dt_empty[b], 4);
+    }
+    *g1_cnt = 0u;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (DBG && p.trace != nullptr && threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[TRACE_TILES * TRACE_EV + 4 * blockIdx.x] = (long long)t;
+  }
+  const uint32_t tmem = *tmem_slot;
+  auto tS = [&](uint32_t b) -> uint32_t { return tmem + b * (uint32_t)BN; };
+  auto tO = [&](uint32_t b) -> uint32_t { return tmem + (uint32_t)(NS1 * BN) + b * 2u * WP; };
+  auto tDT = [&](uint32_t b) -> uint32_t { return tmem + (uint32_t)(NS1 * BN + 4 * WP) + b * 2u * WP; };
+
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+    if (warp == 0) {
+      // ================= producer (lane 0) =================
+      if (lane == 0) {
+        Tile1 ti;
+        ti.start(p);
+        Ring xr, vr, xs, vs;  // slot rings; release rings (s_full for XB, g2done for V)
+        xr.init((uint32_t)p.sx);
+        vr.init((uint32_t)p.sv);
+        xs.init(NR);
+        vs.init(NR);
+        uint32_t g = 0, nitem = 0;
+        while (ti.valid) {
+          if (ti.first_in_item()) {
+            mbar_wait(a_empty, (nitem & 1u) ^ 1u);
+            mbar_expect_tx(a_full, p.a_bytes);
+            bulk_g2s(sA, p.xa_pack + (int64_t)ti.r * p.a_bytes, p.a_bytes, a_full);
+            ++nitem;
+          }
+          const uint8_t* rec = p.col_pack + (int64_t)ti.ct * p.tile_stride;
+          if (g >= (uint32_t)p.sx) {
+            mbar_wait(&s_full[xs.idx], xs.phase);
+            xs.adv();
+          }
+          mbar_expect_tx(&xb_full[xr.idx], xb_bytes);
+          uint8_t* dx = sXB + (size_t)xr.idx * xb_bytes;
+          bulk_g2s(dx, rec, p.xbh_bytes, &xb_full[xr.idx]);
+          bulk_g2s(dx + p.xbh_bytes, rec + p.rec_bytes, p.xbh_bytes, &xb_full[xr.idx]);
+          xr.adv();
+          if (g >= (uint32_t)p.sv) {
+            mbar_wait(&g2done[vs.idx], vs.phase);
+            vs.adv();
+          }
+          mbar_expect_tx(&v_full[vr.idx], vb_bytes);
+          uint8_t* dv = sV + (size_t)vr.idx * vb_bytes;
+          bulk_g2s(dv, rec + p.xbh_bytes, p.v2_bytes, &v_full[vr.idx]);                    // Vhi
+          bulk_g2s(dv + p.v2_bytes, rec + p.rec_bytes + p.xbh_bytes, p.v2_bytes, &v_full[vr.idx]);  // Vlo
+          vr.adv();
+          ++g;
+          ti.next(p);
+        }
+      }
+    } else if (warp == 2) {
+      // ================= GEMM1: S(g) = XA . XB(g)^T =================
+      const uint32_t sbo_x = (uint32_t)(p.ka / 8) * 128u;
+      const int ksteps1 = p.ka / 16;
+      const uint64_t dA = sdesc(smem_u32(sA), 128u, sbo_x);
+      const uint64_t dX0 = sdesc(smem_u32(sXB), 128u, sbo_x);
+      const uint32_t id1 = idesc1_f16(BN);
+      Tile1 ti;
+      ti.start(p);
+      Ring xr, sf;
+      xr.init((uint32_t)p.sx);
+      sf.init(NR);
+      uint32_t g = 0, c1 = 0, nitem = 0;
+      while (ti.valid) {
+        const bool li = ti.last_in_item();
+        if (ti.first_in_item()) {
+          mbar_wait(a_full, nitem & 1u);
+          ++nitem;
+        }
+        mbar_wait(&xb_full[xr.idx], xr.phase);
+        if (g >= (uint32_t)NS1) {  // S buffer free once the epilogue loaded S(g - NS1)
+          mbar_wait(&s_free[sf.idx], sf.phase);
+          sf.adv();
+        }
+        tc_fence_after();
+        if (lane == 0) trace_ev<DBG>(p, g, 9);
+        const uint64_t dx = dX0 + (uint64_t)xr.idx * (xb_bytes >> 4);
+        const uint32_t d = tS(g & 1u);
+        if (elect_one()) {
+          for (int k = 0; k < ksteps1; ++k)
+            mma1_ss(d, dA + (uint64_t)(16 * k), dx + (uint64_t)(16 * k), id1, k > 0);
+          tc_commit1(&s_full[c1]);  // also frees XB slot g (producer)
+          if (li) tc_commit1(a_empty);
+        }
+        __syncwarp();
+        if (lane == 0) trace_ev<DBG>(p, g, 2);
+        if (lane == 0) *g1_cnt = g + 1u;
+        xr.adv();
+        c1 = (c1 + 1u == (uint32_t)NR) ? 0u : c1 + 1u;
+        ++g;
+        ti.next(p);
+      }
+      if (lane == 0) *g1_cnt = 0xFFFFFFFFu;
+    } else if (warp == 1) {
+      // ================= GEMM2: O_I += P(g) [Vhi | Vlo] + P_lo Vhi =================
+      const uint32_t id2 = idesc1_f16(2 * WP), id2h = idesc1_f16(WP);
+      const uint64_t dV0 = sdesc(smem_u32(sV), 128u, (uint32_t)(BN * 16));
+      Tile1 ti;
+      ti.start(p);
+      Ring vr, rr;
+      vr.init((uint32_t)p.sv);
+      rr.init(NR);
+      uint32_t g = 0, q = 0;
+      while (ti.valid) {
+        const bool fresh = ti.first_in_chunk(), last = ti.last_in_chunk();
+        if (lane == 0) trace_ev<DBG>(p, g, 11);
+        mbar_wait(&rdy[rr.idx], rr.phase);
+        mbar_wait(&v_full[vr.idx], vr.phase);
+        const uint32_t ob = q & 1u;
+        if (fresh) mbar_wait(&o_empty[ob], ((q >> 1) & 1u) ^ 1u);
+        tc_fence_after();
+        if (lane == 0) trace_ev<DBG>(p, g, 0);
+        const uint64_t dv = dV0 + (uint64_t)vr.idx * (vb_bytes >> 4);
+        const uint64_t ph = sdesc(smem_u32(sP) + (g & 1u) * PBUF, 128u, 2048u);
+        const uint64_t pl = ph + ((PBUF / 2) >> 4);
+        const uint32_t dO = tO(ob);
+        if (elect_one()) {
+#pragma unroll
+          for (int m = 0; m < BN / 16; ++m) {
+            mma1_ss(dO, ph + (uint64_t)(16 * m), dv + (uint64_t)(16 * m), id2, (fresh && m == 0) ? 0u : 1u);
+            mma1_ss(dO, pl + (uint64_t)(16 * m), dv + (uint64_t)(16 * m), id2h, 1u);
+          }
+          tc_commit1(&g2done[rr.idx]);  // V slot g free
+          tc_commit1(&pt_free[g & 1u]);
+          if (last) tc_commit1(&o_full[ob]);
+        }
+        __syncwarp();
+        if (lane == 0) trace_ev<DBG>(p, g, 1);
+        q += last ? 1u : 0u;
+        vr.adv();
+        rr.adv();
+        ++g;
+        ti.next(p);
+      }
+    } else {
+      // ================= T: D_T(J) = P(g)^T [Vhi_I | Vlo_I] + P_lo^T Vhi_I =================
+      const uint32_t idT = idesc1_f16(2 * WP, true), idTh = idesc1_f16(WP, true);
+      const uint64_t dP0 = sdesc(smem_u32(sP), 2048u, 128u);
+      const uint64_t dVI = sdesc(smem_u32(sVI), 128u, (uint32_t)(BN * 16));
+      Tile1 ti;
+      ti.start(p);
+      Ring rr;
+      rr.init(NR);
+      uint32_t g = 0, nitem = 0, dtq = 0;
+      const bool hold = !(p.sym_dbg & 64);
+      while (ti.valid) {
+        if (ti.first_in_item()) {  // this row tile's V block (the transposed product's B)
+          mbar_wait(vi_empty, (nitem & 1u) ^ 1u);
+          if (elect_one()) {
+            mbar_expect_tx(vi_full, vb_bytes);
+            const uint8_t* rec = p.col_pack + (int64_t)ti.r * p.tile_stride;
+            bulk_g2s(sVI, rec + p.xbh_bytes, p.v2_bytes, vi_full);
+            bulk_g2s(sVI + p.v2_bytes, rec + p.rec_bytes + p.xbh_bytes, p.v2_bytes, vi_full);
+          }
+          __syncwarp();
+          mbar_wait(vi_full, nitem & 1u);
+          ++nitem;
+        }
+        mbar_wait(&rdy[rr.idx], rr.phase);
+        if (lane == 0) trace_ev<DBG>(p, g, 12);
+        const bool tp = ti.transposed();
+        if (tp) mbar_wait(&dt_empty[dtq & 1u], ((dtq >> 1) & 1u) ^ 1u);
+        if (hold)  // T(g) behind GEMM1(g + 2) in the in-order tensor pipe
+          while (*g1_cnt < g + (uint32_t)NS1 + 1u) {
+          }
+        tc_fence_after();
+        if (lane == 0) trace_ev<DBG>(p, g, 13);
+        if (elect_one()) {
+          if (tp && !(p.sym_dbg & 4)) {
+            const uint64_t pa = dP0 + (uint64_t)(g & 1u) * (PBUF >> 4);
+            const uint32_t dt = tDT(dtq & 1u);
+#pragma unroll 1
+            for (int m = 0; m < BN / 16; ++m) {
+              const uint64_t ah = pa + (uint64_t)m * (4096 >> 4), al = ah + ((PBUF / 2) >> 4);
+              mma1_ss(dt, ah, dVI + (uint64_t)(16 * m), idT, m > 0 ? 1u : 0u);
+              mma1_ss(dt, al, dVI + (uint64_t)(16 * m), idTh, 1u);
+            }
+          }
+          if (tp) tc_commit1(&dt_full[dtq & 1u]);
+          tc_commit1(&pt_free[g & 1u]);
+          if (ti.last_in_item()) tc_commit1(vi_empty);
+        }
+        __syncwarp();
+        if (lane == 0) trace_ev<DBG>(p, g, 14);
+        dtq += tp ? 1u : 0u;
+        rr.adv();
+        ++g;
+        ti.next(p);
+      }
+    }
+  } else if (warp < 4 + EPI_WARPS) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 96;");
+    // ================= epilogue: two groups of 8 warps alternate tiles =================
+    const int e = (warp - 4) / 8;
+    const int hc = ((warp - 4) % 8) / 4;
+    const int wq = warp & 3;
+    const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
+    const uint32_t col0 = (uint32_t)(hc * (BN / 2));
+    const int i = 32 * wq + lane;
+    const uint32_t rowb_base = (uint32_t)(i >> 3) * 2048u + (uint32_t)(i & 7) * 16u + (col0 >> 3) * 128u;
+    Tile1 ti;
+    ti.start(p);
+    Ring er;
+    er.init(NR);
+    const float L = p.L;
+    uint32_t g = 0;
+    const bool tr = (wq == 0 && hc == 0 && lane == 0);
+    while (ti.valid) {
+      if ((int)(g & 1u) == e) {
+        if (tr) trace_ev<DBG>(p, g, 3 + 2 * e);
+        bool pt_wait = g >= 2u;
+        mbar_wait(&s_full[er.idx], er.phase);
+        tc_fence_after();
+        if (tr) trace_ev<DBG>(p, g, 4 + 2 * e);
+        const uint32_t base = tS(g & 1u) + lane_off + col0;
+        const uint32_t rowb0 = smem_u32(sP) + (g & 1u) * PBUF + rowb_base;
+        uint32_t ra[32], hi[16], lo[16];
+#pragma unroll
+        for (int c = 0; c < BN / 64; ++c) {
+          tmem_ld32(base + 32 * c, ra);
+          tmem_wait_ld(ra);
+          if (c == BN / 64 - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_free[er.idx]);
+          }
+          transform_chunk<FAM>(ra, L, hi, lo);
+          if (pt_wait) {
+            const uint32_t t = g - 2u;
+            mbar_wait(&pt_free[t & 1u], (t >> 1) & 1u);
+            pt_wait = false;
+            if (tr) trace_ev<DBG>(p, g, 8);
+          }
+          const uint32_t rowb = rowb0 + 512u * c;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            st_shared_v4(rowb + 128u * k, hi[4 * k], hi[4 * k + 1], hi[4 * k + 2], hi[4 * k + 3]);
+            st_shared_v4(rowb + PBUF / 2 + 128u * k, lo[4 * k], lo[4 * k + 1], lo[4 * k + 2], lo[4 * k + 3]);
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&rdy[er.idx]);
+        if (tr) trace_ev<DBG>(p, g, e == 0 ? 7 : 10);
+      }
+      ++g;
+      er.adv();
+      ti.next(p);
+    }
+  } else {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    // ================= drains: O every CH tiles, D_T every transposed tile =================
+    const int wq = warp & 3;
+    const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
+    constexpr int C = WP / 4;
+    const uint32_t stg_warp = smem_u32(sStage) + (uint32_t)(32 * wq) * WP * 4u;
+    const uint32_t stg_row = stg_warp + (uint32_t)lane * WP * 4u;
+    auto stage8 = [&](int h, const uint32_t (&x)[8], const uint32_t (&y)[8]) {
+      float v[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int ex = p.s_exp + __ldg(&p.col_exp[8 * h + c]);  // 2^-e, exact
+        v[c] = (__uint_as_float(x[c]) + __uint_as_float(y[c])) * __int_as_float((127 - ex) << 23);
+      }
+      const uint32_t k0 = (uint32_t)((2 * h) ^ (lane & (C - 1))), k1 = (uint32_t)((2 * h + 1) ^ (lane & (C - 1)));
+      st_shared_v4(stg_row + 16u * k0, __float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]),
+                   __float_as_uint(v[3]));
+      st_shared_v4(stg_row + 16u * k1, __float_as_uint(v[4]), __float_as_uint(v[5]), __float_as_uint(v[6]),
+                   __float_as_uint(v[7]));
+    };
+    auto drain = [&](uint32_t tacc, int64_t row0, bool skip) {
+      if (lane == 0) bulk_wait_read();  // staging rows free again
+      __syncwarp();
+#pragma unroll
+      for (int h = 0; h < WP / 8; ++h) {
+        uint32_t x[8], y[8];
+        tmem_ld8(tacc + lane_off + 8 * h, x);       // [0, WP): hi Vhi + lo Vhi
+        tmem_ld8(tacc + lane_off + WP + 8 * h, y);  // [WP, 2 WP): hi Vlo
+        tmem_wait_ld();
+        stage8(h, x, y);
+      }
+      tc_fence_before();
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0 && !skip) bulk_reduce_add_f32(p.acc + row0 * WP, stg_warp, 32u * WP * 4u);
+    };
+    Tile1 ti;
+    ti.start(p);
+    uint32_t q = 0, dtq = 0;
+    while (ti.valid) {
+      if (ti.transposed()) {
+        mbar_wait(&dt_full[dtq & 1u], (dtq >> 1) & 1u);
+        tc_fence_after();
+        drain(tDT(dtq & 1u), (int64_t)ti.ct * BM + 32 * wq, (p.sym_dbg & 1) != 0);
+        if (lane == 0) mbar_arrive(&dt_empty[dtq & 1u]);
+        ++dtq;
+      }
+      if (ti.last_in_chunk()) {
+        mbar_wait(&o_full[q & 1u], (q >> 1) & 1u);
+        tc_fence_after();
+        drain(tO(q & 1u), (int64_t)ti.r * BM + 32 * wq, (p.sym_dbg & 2) != 0);
+        if (lane == 0) mbar_arrive(&o_empty[q & 1u]);
+        ++q;
+      }
+      ti.next(p);
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+
+  if (DBG && p.trace != nullptr && threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[TRACE_TILES * TRACE_EV + 4 * blockIdx.x + 1] = (long long)t;
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
 // ------------------------------------------------------------------ packing
 
 // column means of Xc in fp64 (single block, fixed order)
@@ -1470,6 +1925,32 @@ std::vector<int4> sym_items(int64_t pairs, int64_t nb) {
   return t;
 }
 
+// Single-CTA symmetric kernel (K1-sym1): row tile r covers column tiles
+// [r, nb); same block-major order.
+int sym_cg() {  // NCGP_SYM_CG=1: cta_group::1 symmetric kernel, 2: the pair kernel
+  const char* e = getenv("NCGP_SYM_CG");
+  return (e != nullptr && e[0] == '1') ? 1 : 2;
+}
+template <typename F>
+void sym1_walk(int64_t nb, F&& f) {
+  const int64_t L = sym_item_len();
+  for (int64_t b0 = 0; b0 < nb; b0 += L) {
+    const int64_t b1 = std::min<int64_t>(nb, b0 + L);
+    for (int64_t r = 0; r < b1; ++r) f(r, std::max<int64_t>(b0, r), b1);
+  }
+}
+int64_t sym1_item_count(int64_t nb) {
+  int64_t n = 0;
+  sym1_walk(nb, [&](int64_t, int64_t, int64_t) { ++n; });
+  return n;
+}
+constexpr size_t SMEM_MAX = 232448;  // sm_100 opt-in maximum per block
+size_t smem1_bytes(uint32_t a_bytes, int wp, int sx, int sv) {
+  const size_t v2 = (size_t)wp * BN * 2;
+  return (size_t)a_bytes + (size_t)sx * a_bytes + (size_t)sv * 2 * v2 + 2 * v2 + 2 * (size_t)PBUF +
+         (size_t)BM * wp * 4 + (6 + 9 + 4 + 4 * NR + 10) * sizeof(uint64_t) + 16 + 1024;
+}
+
 Layout layout_of(int64_t n_rows, int64_t n_cols, int d, int w_max, int sms) {
   Layout L{};
   const int ka = ka_of(d);
@@ -1502,7 +1983,9 @@ Layout layout_of(int64_t n_rows, int64_t n_cols, int d, int w_max, int sms) {
   // symmetric kernel (square operators): fp32 accumulator and item table
   const bool sq = n_rows == n_cols;
   L.symacc = take(sq ? (size_t)L.row_tiles * BM * wp_of(w_max) * sizeof(float) : 0);
-  L.symtab = take(sq ? (size_t)sym_item_count(L.row_tiles / 2, L.col_tiles) * 16 : 0);
+  L.symtab = take(sq ? (size_t)std::max(sym_item_count(L.row_tiles / 2, L.col_tiles),
+                                         sym1_item_count(L.col_tiles)) * 16
+                     : 0);
   L.total = off;
   return L;
 }
@@ -1547,7 +2030,13 @@ int tc_prepare(ncgp_kop* op, cudaStream_t st) {
     NCGP_CUDA(cudaMemsetAsync(op->col_pack + (size_t)L.col_tiles * L.tile_stride, 0,
                               (size_t)L.tile_stride, st));
   if (op->Xr == op->Xc && op->n_rows == op->n_cols) {
-    tab = sym_items(L.row_tiles / 2, L.col_tiles);
+    op->sym_cg = sym_cg();
+    if (op->sym_cg == 1)
+      sym1_walk(L.col_tiles, [&](int64_t r, int64_t c0, int64_t c1) {
+        tab.push_back(make_int4((int)r, (int)c0, (int)c1, 0));
+      });
+    else
+      tab = sym_items(L.row_tiles / 2, L.col_tiles);
     NCGP_CUDA(cudaMemcpyAsync(op->sym_tab, tab.data(), tab.size() * sizeof(int4),
                               cudaMemcpyHostToDevice, st));
     op->sym_items = (int64_t)tab.size();  // the stream sync below keeps `tab` alive long enough
@@ -1672,6 +2161,54 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
   const bool dbg = (g_trace != nullptr) || (g_debug_mode != 0);
   bool sym = op->sym_items > 0 && r0 == 0 && r1 == op->n_rows && g_debug_mode == 0 &&
              sym_enabled(op->family, wp, op->col_tiles);
+  if (sym && op->sym_cg == 1) {
+    const int cand[][2] = {{3, 6}, {3, 4}, {3, 3}, {2, 4}, {3, 2}, {2, 3}, {2, 2}};
+    bool fit = false;
+    for (auto& c : cand)
+      if (smem1_bytes(p.a_bytes, wp, c[0], c[1]) <= SMEM_MAX) {
+        p.sx = c[0];
+        p.sv = c[1];
+        fit = true;
+        break;
+      }
+    if (fit) {
+      p.na = 1;
+      p.npb = 2;
+      p.splits = 1;
+      p.tiles_per_split = p.col_tiles;
+      p.n_items = (int)op->sym_items;
+      p.item_tab = op->sym_tab;
+      p.acc = op->sym_acc;
+      const char* e = getenv("NCGP_SYM_DBG");
+      p.sym_dbg = e != nullptr ? atoi(e) : 0;
+      NCGP_CUDA(cudaMemsetAsync(p.acc, 0, (size_t)op->row_tiles * BM * wp * sizeof(float), st));
+      const size_t smem = smem1_bytes(p.a_bytes, wp, p.sx, p.sv);
+      const unsigned grid = (unsigned)std::min<int64_t>(p.n_items, op->sms);
+      auto launch = [&](auto kern) -> int {
+        NCGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<grid, NTHREADS, smem, st>>>(p);
+        NCGP_LAUNCHED();
+        return NCGP_OK;
+      };
+      op->last_variant = 2;
+      int rc;
+      if (op->family == NCGP_RBF)
+        rc = dbg ? (wp == 16 ? launch(kop_sym1_kernel<NCGP_RBF, 16, true>) : launch(kop_sym1_kernel<NCGP_RBF, 32, true>))
+                 : (wp == 16 ? launch(kop_sym1_kernel<NCGP_RBF, 16, false>) : launch(kop_sym1_kernel<NCGP_RBF, 32, false>));
+      else
+        rc = dbg ? (wp == 16 ? launch(kop_sym1_kernel<NCGP_MATERN32, 16, true>)
+                             : launch(kop_sym1_kernel<NCGP_MATERN32, 32, true>))
+                 : (wp == 16 ? launch(kop_sym1_kernel<NCGP_MATERN32, 16, false>)
+                             : launch(kop_sym1_kernel<NCGP_MATERN32, 32, false>));
+      if (rc != NCGP_OK) return rc;
+      const int64_t tot = p.nloc * w;
+      sym_finalize_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+          p.acc, p.nloc, w, wp, ncgp::out_ptrs<float>(out, r0, ldo), ldo);
+      NCGP_LAUNCHED();
+      return NCGP_OK;
+    }
+    sym = false;
+  }
   if (sym) {
     // two P buffers with the deepest rings that fit, else one P buffer
     // (large D: the row tile and XB ring outgrow the 227 KB)

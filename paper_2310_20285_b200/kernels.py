@@ -75,7 +75,8 @@ class KernelOperator:
     @property
     def last_variant(self) -> str:
         """Kernel variant of the last apply: "plain", "symmetric" or "none"."""
-        return {0: "plain", 1: "symmetric"}.get(N.query("ncgp_kop_last_variant", self._h), "none")
+        return {0: "plain", 1: "symmetric", 2: "symmetric"}.get(
+            N.query("ncgp_kop_last_variant", self._h), "none")
 
     def apply(self, V: torch.Tensor, out: Optional[torch.Tensor] = None,
               row_begin: int = 0, row_end: Optional[int] = None,
