@@ -314,12 +314,16 @@ def run_ours(args, rank, world, local_rank):
                               f"{sms} SM x {P_MUFU_PER_SM_CLK} ex2/clk x "
                               f"{pk['sm_max_mhz']} MHz x F/E={F}/{E})",
                 "kernel_ms": round(1e3 * t_kernel, 3), "impl": op.impl,
-                "variant": op.last_variant}
-    if op.last_variant == "symmetric":
+                "variant": {0: "plain", 1: "symmetric (CTA pairs)",
+                            2: "symmetric (single CTA)"}.get(op.last_variant_code, "none")}
+    if op.last_variant_code in (1, 2):
         # each off-diagonal 128 x 128 tile is evaluated once and serves both
         # K V and K^T V; `achieved` / `frac` count the algorithmic n^2 pairs
         nb = -(-n // 128)
-        ev = sum(2 * (nb - 2 * a) for a in range((nb + 1) // 2)) / float(nb * nb)
+        if op.last_variant_code == 2:  # single-CTA kernel: row tile r covers [r, nb)
+            ev = (nb + 1) / (2.0 * nb)
+        else:                          # pair kernel: row-tile pair a covers [2a, nb)
+            ev = sum(2 * (nb - 2 * a) for a in range((nb + 1) // 2)) / float(nb * nb)
         roofline["evaluated_pair_fraction"] = round(ev, 4)
         roofline["frac_executed"] = round(achieved * ev / peak_tflops, 4)
         roofline["note"] = ("symmetric K(X,X) kernel: evaluated_pair_fraction of the n^2 kernel "

@@ -110,8 +110,9 @@ int ncgp_kop_apply_multi(ncgp_kop* op, const void* V, int64_t ldv, int w,
 /* Actual implementation chosen (NCGP_KOP_TCGEN05 or NCGP_KOP_SIMT). */
 int ncgp_kop_impl(const ncgp_kop* op);
 /* Kernel variant of the last apply (telemetry, no reference counterpart):
- * 0 = plain tiled product, 1 = symmetric K(X, X) kernel (each off-diagonal
- * tile pair evaluated once, serving both K V and K^T V), -1 = none yet. */
+ * 0 = plain tiled product, 1 = symmetric K(X, X) kernel on CTA pairs, 2 =
+ * symmetric K(X, X) kernel on single CTAs (each off-diagonal tile evaluated
+ * once, serving both K V and K^T V), -1 = none yet. */
 int ncgp_kop_last_variant(const ncgp_kop* op);
 int ncgp_kop_destroy(ncgp_kop* op);
 

@@ -1830,21 +1830,24 @@ __global__ void sym_finalize_kernel(const float* __restrict__ acc, int64_t n, in
 
 long long* g_trace = nullptr;  // debug hook (ncgp_debug_set_trace)
 float* g_sym_dump = nullptr;   // debug hook (ncgp_debug_set_sym_dump)
-// Symmetric K(X, X) kernel policy.  It halves the transcendental work but
-// adds the transposed product (half of it wasted by the pair's shared B) to
-// the tensor pipe and an fp32 reduction of every transposed tile.  Measured
-// on one B200 (tools/sym_exp.py, n = 1e5 - 2e5): Matern-3/2 (sqrt + ex2 per
-// pair) 1.3-1.5x faster at any width; RBF (one ex2 per pair) 1.1-1.2x faster
-// at WP = 16 (three S buffers next to double-buffered O / D_T), 1.2x slower
-// at WP = 32 (only two S buffers fit in TMEM).  Below ~500 column tiles the
-// triangular work list balances poorly over the clusters and the plain
-// kernel wins.  NCGP_SYM=1 forces it on, NCGP_SYM=0 off (the plain kernel's
-// results are bitwise reproducible across row shardings; the symmetric
-// kernel's fp32 reductions are not).
-bool sym_enabled(int family, int wp, int64_t col_tiles) {
+// Symmetric K(X, X) kernel policy.  Evaluating only the tiles on and right
+// of the diagonal halves the transcendental work (the bound of the plain
+// kernel) but adds the transposed product and an fp32 reduction of every
+// transposed tile.  Two flavours:
+//   K1-sym1 (cta_group::1, default where its shared memory fits, D <= ~24):
+//     one B200, CUDA events: cfg3 RBF 316 -> 296 ms, cfg3 Matern 542 -> 356
+//     ms, RBF w = 10 at n = 1e6 281 -> 209 ms; it loses below ~300 column
+//     tiles (the triangular list balances poorly over 148 CTAs);
+//   K1-sym (the pair kernel): larger D; wins for Matern-3/2 at any width and
+//     for RBF at WP = 16 from ~512 column tiles.
+// NCGP_SYM=1 forces it on, NCGP_SYM=0 off (the plain kernel's results are
+// bitwise reproducible across row shardings; the symmetric kernels' fp32
+// reductions are not).
+bool sym_enabled(int family, int wp, int64_t col_tiles, int cg) {
   const char* e = getenv("NCGP_SYM");
   if (e != nullptr && e[0] == '0') return false;
   if (e != nullptr && e[0] == '1') return true;
+  if (cg == 1) return col_tiles >= 300;
   return col_tiles >= 512 && (family == NCGP_MATERN32 || wp == 16);
 }
 int g_debug_mode = 0;          // debug hook (ncgp_debug_set_mode)
@@ -1927,9 +1930,15 @@ std::vector<int4> sym_items(int64_t pairs, int64_t nb) {
 
 // Single-CTA symmetric kernel (K1-sym1): row tile r covers column tiles
 // [r, nb); same block-major order.
-int sym_cg() {  // NCGP_SYM_CG=1: cta_group::1 symmetric kernel, 2: the pair kernel
+constexpr size_t SMEM_MAX = 232448;  // sm_100 opt-in maximum per block
+size_t smem1_bytes(uint32_t a_bytes, int wp, int sx, int sv);
+// Flavour of the symmetric kernel an operator's work list is built for: the
+// single-CTA kernel where its shared memory fits the widest RHS (full column
+// records plus two P buffers), else the pair kernel.  NCGP_SYM_CG=1 / 2 forces.
+int sym_cg(int d, int w_max) {
   const char* e = getenv("NCGP_SYM_CG");
-  return (e != nullptr && e[0] == '1') ? 1 : 2;
+  if (e != nullptr && (e[0] == '1' || e[0] == '2')) return e[0] - '0';
+  return smem1_bytes((uint32_t)(BM * ka_of(d) * 2), wp_of(w_max), 2, 2) <= SMEM_MAX ? 1 : 2;
 }
 template <typename F>
 void sym1_walk(int64_t nb, F&& f) {
@@ -1944,7 +1953,6 @@ int64_t sym1_item_count(int64_t nb) {
   sym1_walk(nb, [&](int64_t, int64_t, int64_t) { ++n; });
   return n;
 }
-constexpr size_t SMEM_MAX = 232448;  // sm_100 opt-in maximum per block
 size_t smem1_bytes(uint32_t a_bytes, int wp, int sx, int sv) {
   const size_t v2 = (size_t)wp * BN * 2;
   return (size_t)a_bytes + (size_t)sx * a_bytes + (size_t)sv * 2 * v2 + 2 * v2 + 2 * (size_t)PBUF +
@@ -2030,7 +2038,7 @@ int tc_prepare(ncgp_kop* op, cudaStream_t st) {
     NCGP_CUDA(cudaMemsetAsync(op->col_pack + (size_t)L.col_tiles * L.tile_stride, 0,
                               (size_t)L.tile_stride, st));
   if (op->Xr == op->Xc && op->n_rows == op->n_cols) {
-    op->sym_cg = sym_cg();
+    op->sym_cg = sym_cg(op->d, op->w_max);
     if (op->sym_cg == 1)
       sym1_walk(L.col_tiles, [&](int64_t r, int64_t c0, int64_t c1) {
         tab.push_back(make_int4((int)r, (int)c0, (int)c1, 0));
@@ -2160,7 +2168,7 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
   // symmetric kernel: K(X, X) with the whole row range in one launch
   const bool dbg = (g_trace != nullptr) || (g_debug_mode != 0);
   bool sym = op->sym_items > 0 && r0 == 0 && r1 == op->n_rows && g_debug_mode == 0 &&
-             sym_enabled(op->family, wp, op->col_tiles);
+             sym_enabled(op->family, wp, op->col_tiles, op->sym_cg);
   if (sym && op->sym_cg == 1) {
     const int cand[][2] = {{3, 6}, {3, 4}, {3, 3}, {2, 4}, {3, 2}, {2, 3}, {2, 2}};
     bool fit = false;

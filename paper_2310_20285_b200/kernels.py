@@ -75,8 +75,13 @@ class KernelOperator:
     @property
     def last_variant(self) -> str:
         """Kernel variant of the last apply: "plain", "symmetric" or "none"."""
-        return {0: "plain", 1: "symmetric", 2: "symmetric"}.get(
-            N.query("ncgp_kop_last_variant", self._h), "none")
+        return {0: "plain", 1: "symmetric", 2: "symmetric"}.get(self.last_variant_code, "none")
+
+    @property
+    def last_variant_code(self) -> int:
+        """ncgp_kop_last_variant: 0 plain, 1 symmetric pair kernel, 2 symmetric
+        single-CTA kernel, -1 none yet."""
+        return int(N.query("ncgp_kop_last_variant", self._h))
 
     def apply(self, V: torch.Tensor, out: Optional[torch.Tensor] = None,
               row_begin: int = 0, row_end: Optional[int] = None,

@@ -38,11 +38,14 @@ class _Env:
                 os.environ[k] = v
 
 
-def _case(n, d, w, spec, seed):
+def _case(n, d, w, spec, seed, cg=None):
+    """cg: symmetric kernel flavour the operator's work list is built for
+    (1 single-CTA, 2 CTA pairs; None = the default choice)."""
     rng = np.random.default_rng(seed)
     X = rng.standard_normal((n, d))
     V = rng.standard_normal((n, w))
-    op = KernelOperator(spec[0], spec[1], spec[2], torch.from_numpy(X).float().cuda(), w_max=32)
+    with _Env(**({"NCGP_SYM_CG": cg} if cg else {})):
+        op = KernelOperator(spec[0], spec[1], spec[2], torch.from_numpy(X).float().cuda(), w_max=32)
     return X, V, op, torch.from_numpy(V).float().cuda()
 
 
@@ -54,10 +57,12 @@ def _case(n, d, w, spec, seed):
     (2561, 8, 7, ("rbf", 1.5, 1.0)),
     (4096, 8, 32, ("rbf", 1.2, 0.7)),
 ])
-def test_symmetric_kernel_matches_oracle(n, d, w, spec):
-    X, V, op, Vd = _case(n, d, w, spec, n + d)
+@pytest.mark.parametrize("cg", [1, 2])
+def test_symmetric_kernel_matches_oracle(n, d, w, spec, cg):
+    X, V, op, Vd = _case(n, d, w, spec, n + d, cg)
     with _Env(NCGP_SYM=1):
         got = op.apply(Vd).double().cpu().numpy()
+    assert op.last_variant_code == (2 if cg == 1 else 1)
     ref = O.kernel_matmul_rows(spec, X, X, V)
     bound = O.kernel_matmul_rows(spec, X, X, np.abs(V))
     assert np.all(np.abs(got - ref) <= 1e-5 * bound), float(np.max(np.abs(got - ref) / bound))
@@ -70,10 +75,12 @@ def test_symmetric_kernel_item_transitions(item):
     X, V, op, Vd = _case(20000, 8, 16, ("matern32", 1.5, 1.0), 7)
     with _Env(NCGP_SYM=0):
         plain = op.apply(Vd).double()
-    with _Env(NCGP_SYM=1, NCGP_SYM_ITEM=item):
-        op2 = KernelOperator("matern32", 1.5, 1.0, op.X_rows, w_max=32)  # table built at creation
-        got = op2.apply(Vd).double()
-    assert float((got - plain).norm() / plain.norm()) < 2e-5
+    for cg in (1, 2):
+        with _Env(NCGP_SYM=1, NCGP_SYM_ITEM=item, NCGP_SYM_CG=cg):
+            op2 = KernelOperator("matern32", 1.5, 1.0, op.X_rows, w_max=32)  # table built at creation
+            got = op2.apply(Vd).double()
+        assert op2.last_variant_code == (2 if cg == 1 else 1)
+        assert float((got - plain).norm() / plain.norm()) < 2e-5
 
 
 def test_symmetric_kernel_only_on_full_square_launches():
@@ -97,8 +104,8 @@ def test_symmetric_kernel_only_on_full_square_launches():
 @pytest.mark.parametrize("n,w,fam,variant", [
     (3000, 8, "rbf", "plain"),             # small: the triangular list balances poorly
     (3000, 8, "matern32", "plain"),
-    (70001, 32, "rbf", "plain"),           # RBF at WP = 32: the plain kernel is faster
-    (70001, 10, "rbf", "symmetric"),       # RBF at WP = 16
+    (70001, 32, "rbf", "symmetric"),       # single-CTA symmetric kernel (D = 8)
+    (70001, 10, "rbf", "symmetric"),
     (70001, 32, "matern32", "symmetric"),
 ])
 def test_symmetric_default_policy(n, w, fam, variant):
@@ -133,7 +140,7 @@ def test_symmetric_work_list_order_invariant():
     X, V, op, Vd = _case(40000, 8, 10, ("rbf", 1.5, 1.0), 5)
     outs = []
     for order in ("block", "pair"):
-        with _Env(NCGP_SYM=1, NCGP_SYM_ORDER=order):
+        with _Env(NCGP_SYM=1, NCGP_SYM_ORDER=order, NCGP_SYM_CG=2):
             o = KernelOperator("rbf", 1.5, 1.0, op.X_rows, w_max=32)  # table built at creation
             outs.append(o.apply(Vd).double())
             assert o.last_variant == "symmetric"
@@ -148,11 +155,11 @@ def test_symmetric_work_list_order_invariant():
 def test_symmetric_kernel_single_p_buffer(n, d, w, fam, force):
     """One shared P buffer: each epilogue group waits for the other group's
     previous tile (pt_free barriers alternate by tile parity)."""
-    X, V, op, Vd = _case(n, d, w, (fam, 3.0, 1.0), 13)
+    X, V, op, Vd = _case(n, d, w, (fam, 3.0, 1.0), 13, cg=2)
     env = {"NCGP_SYM": 1, "NCGP_SYM_NPB": force} if force else {}
     with _Env(**env):
         got = op.apply(Vd).double()
-    assert op.last_variant == "symmetric"
+    assert op.last_variant_code == 1
     with _Env(NCGP_SYM=0):
         plain = op.apply(Vd).double()
     assert float((got - plain).norm() / plain.norm()) < 2e-5
