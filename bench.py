@@ -300,16 +300,19 @@ def run_ours(args, rank, world, local_rank):
     t_kernel = kern_total / args.steps / 1e3
     achieved = F * local_pairs / t_kernel / 1e12
     peak_tflops = min(tensor_tflops, F * mufu_rate / E / 1e12)
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "r01e_summary.json")
-    if os.path.exists(prof) and c["name"] == "cfg3" and world == 1:
-        with open(prof) as fh:
+    # DRAM traffic of the same kernel variant on the same workload, from the
+    # committed ncu --set full capture (profiles/*_summary.json)
+    traffic, traffic_src = None, None
+    captures = {("cfg3", 2): "r01g_summary.json", ("cfg3", 0): "r01e_summary.json"}
+    prof = captures.get((c["name"], op.last_variant_code))
+    if prof and world == 1 and os.path.exists(os.path.join(ROOT, "profiles", prof)):
+        with open(os.path.join(ROOT, "profiles", prof)) as fh:
             traffic = json.load(fh).get("traffic_bytes_per_launch")
+        traffic_src = f"profiles/{prof} (ncu --set full, dram read+write)"
     roofline = {"bound": "tensor", "limiter": "MUFU ex2" if peak_tflops < tensor_tflops
                 else "tensor pipe", "achieved": round(achieved, 3), "peak": round(peak_tflops, 3),
                 "unit": "TFLOP/s", "frac": round(achieved / peak_tflops, 4), "traffic": traffic,
-                "traffic_source": "profiles/r01e_summary.json (ncu --set full, dram read+write)"
-                if traffic else None,
+                "traffic_source": traffic_src,
                 "peak_basis": f"min({pk['source']} bf16 {pk['bf16']}/2 TF/s, "
                               f"{sms} SM x {P_MUFU_PER_SM_CLK} ex2/clk x "
                               f"{pk['sm_max_mhz']} MHz x F/E={F}/{E})",
