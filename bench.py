@@ -186,7 +186,15 @@ def run_ours(args, rank, world, local_rank):
     # buffer and the all-gather runs in place.  fused: the gather buffers are
     # symmetric memory and K1 stores every row into all ranks' buffers
     # (parallel.RowShardedOperator implements both).
-    fused = world > 1 and args.gather == "fused"
+    # reduce: the symmetric kernel's triangular work list is split across the
+    # ranks and an NCCL all-reduce sums the fp32 accumulators
+    # (parallel.SymmetricSplitOperator); auto takes it when available.
+    gather = args.gather
+    if gather == "auto":
+        gather = "reduce" if world > 1 and op.sym_acc_elems(w) > 0 else "nccl"
+    reduce_ = world > 1 and gather == "reduce"
+    acc = torch.empty(max(1, op.sym_acc_elems(w)), dtype=torch.float32, device=dev) if reduce_ else None
+    fused = world > 1 and gather == "fused"
     peer_rows = None
     if fused:
         from paper_2310_20285_b200.parallel import TorchSymmetricMemory
@@ -207,12 +215,21 @@ def run_ours(args, rank, world, local_rank):
     def post():
         if fused:
             barrier(1)
+        elif reduce_:
+            dist.all_reduce(acc)
+            op.sym_finalize(acc, w, out_rows)
         elif world > 1:
             dist.all_gather_into_tensor(out_full, mine)
 
+    def kernel():
+        if reduce_:
+            op.sym_partial(Sd, rank, world, acc)
+        else:
+            op.apply(Sd, out=out_rows, row_begin=r0, row_end=r1, peers=peer_rows)
+
     def step():
         pre()
-        op.apply(Sd, out=out_rows, row_begin=r0, row_end=r1, peers=peer_rows)
+        kernel()
         post()
 
     for _ in range(args.warmup):
@@ -235,7 +252,7 @@ def run_ours(args, rank, world, local_rank):
         starts[k].record(stream)
         pre()
         kstarts[k].record(stream)
-        op.apply(Sd, out=out_rows, row_begin=r0, row_end=r1, peers=peer_rows)
+        kernel()
         kends[k].record(stream)
         post()
         ends[k].record(stream)
@@ -267,9 +284,13 @@ def run_ours(args, rank, world, local_rank):
     else:
         from paper_2310_20285_b200.parallel import ShardedPriorOperator
         sop = ShardedPriorOperator(prior, X.astype(np.float32), dtype=torch.float32,
-                                   gather=args.gather)
+                                   gather=gather)
         call = lambda: to_host_tensor(sop(Sh.view(-1).to(dev, non_blocking=True)))  # noqa: E731
-    res = call()  # builds + caches the operator
+    # builds + caches the operator; two results alive at once so the pinned
+    # host allocator holds the blocks the timed calls cycle through
+    warm = [call(), call()]
+    del warm
+    res = call()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -290,13 +311,17 @@ def run_ours(args, rank, world, local_rank):
                                           "operator, " + ("rows stored into every rank's "
                                                           "symmetric-memory buffer by K1)"
                                                           if fused else "in-place all-gather)"))}
+    if reduce_:
+        e2e["note"] = ("X resident in the cached operator; S (pinned fp32) uploaded and the product "
+                       f"downloaded every step on each of the {world} ranks (symmetric kernel's work "
+                       "list split across ranks, fp32 accumulators summed by an NCCL all-reduce)")
 
     # ---- roofline of the dominant kernel (the fused kernel-matmul)
     pk = peaks()
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     mufu_rate = sms * P_MUFU_PER_SM_CLK * pk["sm_max_mhz"] * 1e6   # ex2 / s
     tensor_tflops = pk["bf16"] / 2.0                                 # tf32-class dense
-    local_pairs = float(r1 - r0) * n
+    local_pairs = float(n) * n / world if reduce_ else float(r1 - r0) * n
     t_kernel = kern_total / args.steps / 1e3
     achieved = F * local_pairs / t_kernel / 1e12
     peak_tflops = min(tensor_tflops, F * mufu_rate / E / 1e12)
@@ -352,7 +377,7 @@ def run_ours(args, rank, world, local_rank):
                            "flops_per_pair": F, "exp_per_pair": E,
                            "l2": "flushed (256 MiB write) before every timed step",
                            "parallelism": f"row-sharded x{world}",
-                           "gather": args.gather if world > 1 else None},
+                           "gather": gather if world > 1 else None},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clocks}
         print(json.dumps(line), flush=True)
@@ -429,7 +454,7 @@ def run_fit(args, rank, world, local_rank):
                        "kernel": list(c["kernel"]), "schedule": [c["steps"], c["inner"]],
                        "rank": c["rank"], "residual": args.residual,
                        "parallelism": f"row-sharded x{world}",
-                       "gather": args.gather if world > 1 else None},
+                       "gather": op.gather if op is not None else None},
             "kernel_matvecs": trace.total_kernel_matvecs,
             "inner_iters": [s.inner_iterations for s in trace.steps],
             "posterior": post,
@@ -457,9 +482,11 @@ def main():
     ap.add_argument("--residual", default="explicit", choices=["explicit", "recurrence"],
                     help="fit workloads: inner residual mode (recurrence is opt-in)")
     ap.add_argument("--kop", default="auto", choices=["auto", "tcgen05", "simt"])
-    ap.add_argument("--gather", default="nccl", choices=["nccl", "fused"],
-                    help="N>1 row exchange: in-place NCCL all-gather after K1, or K1 storing "
-                         "each row into every rank's symmetric-memory buffer")
+    ap.add_argument("--gather", default="auto", choices=["auto", "reduce", "nccl", "fused"],
+                    help="N>1 exchange: reduce = the symmetric kernel's work list split across "
+                         "ranks + NCCL all-reduce of the accumulators; nccl = row blocks + in-place "
+                         "all-gather; fused = row blocks stored by K1 into every rank's "
+                         "symmetric-memory buffer; auto = reduce when available, else nccl")
     ap.add_argument("--cpu-rows", type=int, default=24)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -107,6 +107,24 @@ int ncgp_kop_apply_multi(ncgp_kop* op, const void* V, int64_t ldv, int w,
                          void* const* outs, int n_out, int64_t ldo,
                          int64_t row_begin, int64_t row_end, void* stream);
 
+/* The symmetric K(X, X) kernel split across `nparts` processes (SURVEY.md
+ * 8(e); no reference counterpart: the reference has no multi-GPU path).
+ * ncgp_kop_sym_acc_elems: fp32 elements of the per-process accumulator for
+ * RHS width w, or 0 when a full apply of width w would not use a symmetric
+ * kernel (rectangular operator, too small, or the shape does not fit); the
+ * caller then row-shards with row_begin / row_end.
+ * ncgp_kop_sym_partial: part `part` of `nparts` slices of the triangular work
+ * list (equal tile counts) into `acc` (zeroed first, on `stream`).  The sum
+ * of all parts' acc is the full product in a padded, swizzled layout; the
+ * caller sums them (an all-reduce) and calls ncgp_kop_sym_finalize to write
+ * the (n_rows, w) product with row stride ldo.  Errors: NCGP_UNSUPPORTED
+ * when ncgp_kop_sym_acc_elems is 0. */
+int64_t ncgp_kop_sym_acc_elems(const ncgp_kop* op, int w);
+int ncgp_kop_sym_partial(ncgp_kop* op, const void* V, int64_t ldv, int w, int part,
+                         int nparts, float* acc, void* stream);
+int ncgp_kop_sym_finalize(ncgp_kop* op, const float* acc, int w, void* out, int64_t ldo,
+                          void* stream);
+
 /* Actual implementation chosen (NCGP_KOP_TCGEN05 or NCGP_KOP_SIMT). */
 int ncgp_kop_impl(const ncgp_kop* op);
 /* Kernel variant of the last apply (telemetry, no reference counterpart):

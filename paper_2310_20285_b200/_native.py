@@ -52,6 +52,9 @@ _SIGS = {
                                     _i64, _vp]),
     "ncgp_kop_impl": (_i32, [_vp]),
     "ncgp_kop_last_variant": (_i32, [_vp]),
+    "ncgp_kop_sym_acc_elems": (_i64, [_vp, _i32]),
+    "ncgp_kop_sym_partial": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp]),
+    "ncgp_kop_sym_finalize": (_i32, [_vp, _vp, _i32, _vp, _i64, _vp]),
     "ncgp_kop_destroy": (_i32, [_vp]),
     "ncgp_softmax_stats": (_i32, [_i32, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp]),
     "ncgp_softmax_winv": (_i32, [_i32, _vp, _i64, _i32, _vp, _i64, _i32, _vp, _i64, _f64, _f64,

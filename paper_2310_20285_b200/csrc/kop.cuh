@@ -3,6 +3,8 @@
 
 #include "common.cuh"
 
+#include <vector>
+
 struct ncgp_kop {
   int impl;      // NCGP_KOP_TCGEN05 | NCGP_KOP_SIMT
   int family;    // NCGP_RBF | NCGP_MATERN32
@@ -30,6 +32,7 @@ struct ncgp_kop {
   int64_t sym_items;
   int4* sym_tab;
   float* sym_acc;
+  std::vector<int64_t> sym_cum;  // host: tiles before each work item (partition of the list)
   int sym_cg = 2;         // symmetric kernel flavour the work list was built for (1 or 2)
   int last_variant = -1;  // 0 plain, 1 symmetric pair kernel, 2 symmetric single-CTA kernel
 };
@@ -66,7 +69,15 @@ int simt_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& ou
 bool tc_supported(int dtype, int d, int w_max);
 size_t tc_workspace_bytes(int64_t n_rows, int64_t n_cols, int d, int w_max);
 int tc_prepare(ncgp_kop* op, cudaStream_t st);
+// symmetric kernel split over processes: this part's items, contributions left in acc
+struct SymPart {
+  int part, nparts;
+  float* acc;
+};
 int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out, int64_t ldo,
-             int64_t r0, int64_t r1, cudaStream_t st);
+             int64_t r0, int64_t r1, cudaStream_t st, const SymPart* part = nullptr);
+int64_t tc_sym_acc_elems(const ncgp_kop* op, int w);
+int tc_sym_finalize(ncgp_kop* op, const float* acc, int w, const OutSet& out, int64_t ldo,
+                    cudaStream_t st);
 
 }  // namespace ncgp

@@ -137,6 +137,37 @@ int ncgp_kop_apply_multi(ncgp_kop* op, const void* V, int64_t ldv, int w, void* 
 
 int ncgp_kop_impl(const ncgp_kop* op) { return op ? op->impl : -1; }
 
+int64_t ncgp_kop_sym_acc_elems(const ncgp_kop* op, int w) {
+  if (op == nullptr || op->impl != NCGP_KOP_TCGEN05 || w < 1 || w > op->w_max) return 0;
+  return ncgp::tc_sym_acc_elems(op, w);
+}
+
+int ncgp_kop_sym_partial(ncgp_kop* op, const void* V, int64_t ldv, int w, int part, int nparts,
+                         float* acc, void* stream) {
+  NCGP_CHECK_ARG(op != nullptr && V != nullptr && acc != nullptr, NCGP_INVALID_INPUT,
+                 "null argument");
+  NCGP_CHECK_ARG(ldv >= w, NCGP_DIMENSION_MISMATCH, "leading dimension < width");
+  NCGP_CHECK_ARG(ncgp_kop_sym_acc_elems(op, w) > 0, NCGP_UNSUPPORTED,
+                 "no symmetric kernel for this operator and width %d", w);
+  ncgp::OutSet none{};
+  none.n = 0;
+  const ncgp::SymPart sp{part, nparts, acc};
+  return ncgp::tc_apply(op, V, ldv, w, none, w, 0, op->n_rows, ncgp::as_stream(stream), &sp);
+}
+
+int ncgp_kop_sym_finalize(ncgp_kop* op, const float* acc, int w, void* out, int64_t ldo,
+                          void* stream) {
+  NCGP_CHECK_ARG(op != nullptr && acc != nullptr && out != nullptr, NCGP_INVALID_INPUT,
+                 "null argument");
+  NCGP_CHECK_ARG(ldo >= w, NCGP_DIMENSION_MISMATCH, "leading dimension < width");
+  NCGP_CHECK_ARG(ncgp_kop_sym_acc_elems(op, w) > 0, NCGP_UNSUPPORTED,
+                 "no symmetric kernel for this operator and width %d", w);
+  ncgp::OutSet o{};
+  o.p[0] = out;
+  o.n = 1;
+  return ncgp::tc_sym_finalize(op, acc, w, o, ldo, ncgp::as_stream(stream));
+}
+
 int ncgp_kop_last_variant(const ncgp_kop* op) { return op ? op->last_variant : -1; }
 
 int ncgp_kop_destroy(ncgp_kop* op) {

@@ -358,7 +358,8 @@ struct TcParams {
                          // reductions, 2 = drop O reductions, 4 = no transposed MMAs,
                          // 8 = no D_T loads, 16 = no P stores to shared memory;
                          // variant (correct results): 64 = flip whether T(g) is held
-                         // back behind GEMM1(g + NS)
+                         // back behind GEMM1(g + NS); 128 (single-CTA kernel) = GEMM2
+                         // reads P from TMEM (TS), as measured slower
   float* sym_dump;       // symmetric kernel debug: raw D_T per (pair, tile, rank) when set
   int npb;               // symmetric kernel: P buffers in shared memory (2, or 1 for large D)
   int debug_mode;        // debug (timing only, wrong results): 1 = epilogue skips TMEM traffic,
@@ -1181,6 +1182,15 @@ __device__ __forceinline__ void mma1_ss(uint32_t d, uint64_t a, uint64_t b, uint
       "l"(a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
+__device__ __forceinline__ void mma1_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
 __device__ __forceinline__ void tc_commit1(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -1362,7 +1372,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
         }
         mbar_wait(&xb_full[xr.idx], xr.phase);
         if (g >= (uint32_t)NS1) {  // S buffer free once the epilogue loaded S(g - NS1)
-          mbar_wait(&s_free[sf.idx], sf.phase);
+          // (P in TMEM, sym_dbg 128: once GEMM2(g - NS1) has read it)
+          mbar_wait(p.sym_dbg & 128 ? &g2done[sf.idx] : &s_free[sf.idx], sf.phase);
           sf.adv();
         }
         tc_fence_after();
@@ -1408,10 +1419,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
         const uint64_t pl = ph + ((PBUF / 2) >> 4);
         const uint32_t dO = tO(ob);
         if (elect_one()) {
+          if (p.sym_dbg & 128) {  // A = P from TMEM (the epilogue's copy over S(g))
+            const uint32_t a0 = tS(g & 1u);
 #pragma unroll
-          for (int m = 0; m < BN / 16; ++m) {
-            mma1_ss(dO, ph + (uint64_t)(16 * m), dv + (uint64_t)(16 * m), id2, (fresh && m == 0) ? 0u : 1u);
-            mma1_ss(dO, pl + (uint64_t)(16 * m), dv + (uint64_t)(16 * m), id2h, 1u);
+            for (int m = 0; m < BN / 16; ++m) {
+              const uint32_t ahi = a0 + 32u * (m >> 1) + 8u * (m & 1);
+              mma1_ts(dO, ahi, dv + (uint64_t)(16 * m), id2, (fresh && m == 0) ? 0u : 1u);
+              mma1_ts(dO, ahi + 16u, dv + (uint64_t)(16 * m), id2h, 1u);
+            }
+          } else {
+#pragma unroll
+            for (int m = 0; m < BN / 16; ++m) {
+              mma1_ss(dO, ph + (uint64_t)(16 * m), dv + (uint64_t)(16 * m), id2, (fresh && m == 0) ? 0u : 1u);
+              mma1_ss(dO, pl + (uint64_t)(16 * m), dv + (uint64_t)(16 * m), id2h, 1u);
+            }
           }
           tc_commit1(&g2done[rr.idx]);  // V slot g free
           tc_commit1(&pt_free[g & 1u]);
@@ -1507,17 +1528,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
         if (tr) trace_ev<DBG>(p, g, 4 + 2 * e);
         const uint32_t base = tS(g & 1u) + lane_off + col0;
         const uint32_t rowb0 = smem_u32(sP) + (g & 1u) * PBUF + rowb_base;
+        const bool p_tmem = (p.sym_dbg & 128) != 0;
         uint32_t ra[32], hi[16], lo[16];
 #pragma unroll
         for (int c = 0; c < BN / 64; ++c) {
           tmem_ld32(base + 32 * c, ra);
           tmem_wait_ld(ra);
-          if (c == BN / 64 - 1) {
+          if (c == BN / 64 - 1 && !p_tmem) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&s_free[er.idx]);
           }
           transform_chunk<FAM>(ra, L, hi, lo);
+          if (p_tmem) {
+            if (FAM == NCGP_RBF) {
+              tmem_st_hilo(base + 32 * c, hi, lo);
+            } else {
+              tmem_st16(base + 32 * c, hi);
+              tmem_st16(base + 32 * c + 16, lo);
+            }
+          }
           if (pt_wait) {
             const uint32_t t = g - 2u;
             mbar_wait(&pt_free[t & 1u], (t >> 1) & 1u);
@@ -1530,6 +1560,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
             st_shared_v4(rowb + 128u * k, hi[4 * k], hi[4 * k + 1], hi[4 * k + 2], hi[4 * k + 3]);
             st_shared_v4(rowb + PBUF / 2 + 128u * k, lo[4 * k], lo[4 * k + 1], lo[4 * k + 2], lo[4 * k + 3]);
           }
+        }
+        if (p_tmem) {
+          tmem_wait_st();
+          tc_fence_before();
         }
         fence_proxy_async_smem();
         __syncwarp();
@@ -2005,9 +2039,37 @@ size_t smem_bytes(uint32_t a_bytes, int wp, int na, int sx, int sv, int sym_npb 
          (6 + 9 + 2 + NS_MAX + 5 * NR + 8 + 12) * sizeof(uint64_t) + 16 + 1024;
 }
 
+// Which symmetric kernel a full-range apply of width w runs: 0 none (the
+// plain kernel), 1 the pair kernel, 2 the single-CTA kernel.
+int sym_variant(const ncgp_kop* op, int w) {
+  if (op->sym_items <= 0 || g_debug_mode != 0) return 0;
+  const int wp = wp_of(w);
+  if (!sym_enabled(op->family, wp, op->col_tiles, op->sym_cg)) return 0;
+  const uint32_t a_bytes = (uint32_t)(BM * op->ka * 2);
+  if (op->sym_cg == 1) return smem1_bytes(a_bytes, wp, 2, 2) <= SMEM_MAX ? 2 : 0;
+  if (smem_bytes(a_bytes, wp, 1, 3, 3, 2) <= (size_t)SMEM_BUDGET) return 1;
+  if (op->family == NCGP_MATERN32 && smem_bytes(a_bytes, wp, 1, 3, 3, 1) <= (size_t)SMEM_BUDGET) return 1;
+  const char* e = getenv("NCGP_SYM_NPB");
+  if (e != nullptr && atoi(e) == 1 && smem_bytes(a_bytes, wp, 1, 3, 3, 1) <= (size_t)SMEM_BUDGET) return 1;
+  return 0;
+}
+
 }  // namespace
 
 namespace ncgp {
+
+int64_t tc_sym_acc_elems(const ncgp_kop* op, int w) {
+  return sym_variant(op, w) ? op->row_tiles * BM * wp_of(w) : 0;
+}
+
+int tc_sym_finalize(ncgp_kop* op, const float* acc, int w, const OutSet& out, int64_t ldo,
+                    cudaStream_t st) {
+  const int64_t tot = op->n_rows * w;
+  sym_finalize_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+      acc, op->n_rows, w, wp_of(w), ncgp::out_ptrs<float>(out, 0, ldo), ldo);
+  NCGP_LAUNCHED();
+  return NCGP_OK;
+}
 
 bool tc_supported(int dtype, int d, int w_max) {
   if (dtype != NCGP_F32) return false;
@@ -2048,6 +2110,8 @@ int tc_prepare(ncgp_kop* op, cudaStream_t st) {
     NCGP_CUDA(cudaMemcpyAsync(op->sym_tab, tab.data(), tab.size() * sizeof(int4),
                               cudaMemcpyHostToDevice, st));
     op->sym_items = (int64_t)tab.size();  // the stream sync below keeps `tab` alive long enough
+    op->sym_cum.assign(tab.size() + 1, 0);
+    for (size_t k = 0; k < tab.size(); ++k) op->sym_cum[k + 1] = op->sym_cum[k] + (tab[k].z - tab[k].y);
   }
   // prescale kernel values into fp16 range: s2 * 2^s in (2^13, 2^14]
   const int s_exp = 14 - (int)ceil(log2(op->s2));
@@ -2105,7 +2169,15 @@ int tc_prepare(ncgp_kop* op, cudaStream_t st) {
 }
 
 int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out, int64_t ldo,
-             int64_t r0, int64_t r1, cudaStream_t st) {
+             int64_t r0, int64_t r1, cudaStream_t st, const SymPart* part) {
+  if (part != nullptr) {
+    NCGP_CHECK_ARG(sym_variant(op, w) != 0, NCGP_UNSUPPORTED,
+                   "no symmetric kernel for this operator and width");
+    NCGP_CHECK_ARG(part->nparts >= 1 && part->part >= 0 && part->part < part->nparts,
+                   NCGP_INVALID_INPUT, "bad part %d of %d", part->part, part->nparts);
+    r0 = 0;
+    r1 = op->n_rows;
+  }
   NCGP_CHECK_ARG(r0 % (2 * BM) == 0, NCGP_DIMENSION_MISMATCH,
                  "row_begin must be a multiple of %d for the tcgen05 operator", 2 * BM);
   const Layout L = layout_of(op->n_rows, op->n_cols, op->d, op->w_max, op->sms);
@@ -2167,8 +2239,22 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
   p.acc = nullptr;
   // symmetric kernel: K(X, X) with the whole row range in one launch
   const bool dbg = (g_trace != nullptr) || (g_debug_mode != 0);
-  bool sym = op->sym_items > 0 && r0 == 0 && r1 == op->n_rows && g_debug_mode == 0 &&
-             sym_enabled(op->family, wp, op->col_tiles, op->sym_cg);
+  bool sym = r0 == 0 && r1 == op->n_rows && sym_variant(op, w) != 0;
+  // items of this launch: all, or part `part` of `nparts` slices of equal
+  // tile count (contiguous in the block-major list)
+  int64_t it_lo = 0, it_hi = op->sym_items;
+  if (part != nullptr) {
+    const int64_t tot = op->sym_cum.back();
+    auto cut = [&](int k) {
+      const int64_t target = tot * k / part->nparts;
+      return (int64_t)(std::lower_bound(op->sym_cum.begin(), op->sym_cum.end(), target) -
+                       op->sym_cum.begin());
+    };
+    it_lo = std::min<int64_t>(cut(part->part), op->sym_items);
+    it_hi = std::min<int64_t>(cut(part->part + 1), op->sym_items);
+  }
+  float* const sym_acc = part != nullptr ? part->acc : op->sym_acc;
+  const bool sym_fin = part == nullptr;
   if (sym && op->sym_cg == 1) {
     const int cand[][2] = {{3, 6}, {3, 4}, {3, 3}, {2, 4}, {3, 2}, {2, 3}, {2, 2}};
     bool fit = false;
@@ -2184,12 +2270,14 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
       p.npb = 2;
       p.splits = 1;
       p.tiles_per_split = p.col_tiles;
-      p.n_items = (int)op->sym_items;
-      p.item_tab = op->sym_tab;
-      p.acc = op->sym_acc;
+      p.n_items = (int)(it_hi - it_lo);
+      p.item_tab = op->sym_tab + it_lo;
+      p.acc = sym_acc;
       const char* e = getenv("NCGP_SYM_DBG");
       p.sym_dbg = e != nullptr ? atoi(e) : 0;
       NCGP_CUDA(cudaMemsetAsync(p.acc, 0, (size_t)op->row_tiles * BM * wp * sizeof(float), st));
+      op->last_variant = 2;
+      if (p.n_items == 0) return NCGP_OK;  // an empty part
       const size_t smem = smem1_bytes(p.a_bytes, wp, p.sx, p.sv);
       const unsigned grid = (unsigned)std::min<int64_t>(p.n_items, op->sms);
       auto launch = [&](auto kern) -> int {
@@ -2198,7 +2286,6 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
         NCGP_LAUNCHED();
         return NCGP_OK;
       };
-      op->last_variant = 2;
       int rc;
       if (op->family == NCGP_RBF)
         rc = dbg ? (wp == 16 ? launch(kop_sym1_kernel<NCGP_RBF, 16, true>) : launch(kop_sym1_kernel<NCGP_RBF, 32, true>))
@@ -2209,11 +2296,7 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
                  : (wp == 16 ? launch(kop_sym1_kernel<NCGP_MATERN32, 16, false>)
                              : launch(kop_sym1_kernel<NCGP_MATERN32, 32, false>));
       if (rc != NCGP_OK) return rc;
-      const int64_t tot = p.nloc * w;
-      sym_finalize_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
-          p.acc, p.nloc, w, wp, ncgp::out_ptrs<float>(out, r0, ldo), ldo);
-      NCGP_LAUNCHED();
-      return NCGP_OK;
+      return sym_fin ? tc_sym_finalize(op, p.acc, w, out, ldo, st) : NCGP_OK;
     }
     sym = false;
   }
@@ -2241,15 +2324,17 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
   if (sym) {
     p.splits = 1;
     p.tiles_per_split = p.col_tiles;
-    p.n_items = (int)op->sym_items;
-    p.item_tab = op->sym_tab;
-    p.acc = op->sym_acc;
+    p.n_items = (int)(it_hi - it_lo);
+    p.item_tab = op->sym_tab + it_lo;
+    p.acc = sym_acc;
     {
       const char* e = getenv("NCGP_SYM_DBG");
       p.sym_dbg = e != nullptr ? atoi(e) : 0;
     }
     p.sym_dump = g_sym_dump;
     NCGP_CUDA(cudaMemsetAsync(p.acc, 0, (size_t)op->row_tiles * BM * wp * sizeof(float), st));
+    op->last_variant = 1;
+    if (p.n_items == 0) return NCGP_OK;
     const size_t smem = smem_bytes(p.a_bytes, wp, p.na, p.sx, p.sv, p.npb);
     const unsigned grid = 2u * (unsigned)std::min<int64_t>(p.n_items, clusters);
     auto launch = [&](auto kern) -> int {
@@ -2259,7 +2344,6 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
       NCGP_LAUNCHED();
       return NCGP_OK;
     };
-    op->last_variant = 1;
     int rc;
     if (dbg)  // per-tile trace of cluster 0 (tools/trace_sym.py)
       rc = op->family == NCGP_RBF
@@ -2274,12 +2358,9 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
       rc = wp == 16 ? launch(kop_tc_kernel<NCGP_MATERN32, 16, false, true>)
                     : launch(kop_tc_kernel<NCGP_MATERN32, 32, false, true>);
     if (rc != NCGP_OK) return rc;
-    const int64_t tot = p.nloc * w;
-    sym_finalize_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
-        p.acc, p.nloc, w, wp, ncgp::out_ptrs<float>(out, r0, ldo), ldo);
-    NCGP_LAUNCHED();
-    return NCGP_OK;
+    return sym_fin ? tc_sym_finalize(op, p.acc, w, out, ldo, st) : NCGP_OK;
   }
+  NCGP_CHECK_ARG(part == nullptr, NCGP_UNSUPPORTED, "no symmetric kernel for this operator");
   // deepest rings that fit: (na, sx, sv) from (2, 6, 9) down to (1, 3, 6)
   {
     const int cand[][3] = {{2, 6, 9}, {2, 6, 6}, {2, 3, 9}, {2, 3, 6}, {1, 6, 6}, {1, 3, 6}};

@@ -129,6 +129,39 @@ class KernelOperator:
 
     __call__ = apply
 
+    # ---- the symmetric K(X, X) kernel split across processes (parallel.py)
+    def sym_acc_elems(self, w: int) -> int:
+        """fp32 elements of the per-process accumulator of a split symmetric
+        apply of width ``w`` (<= w_max), or 0 when the full apply would not
+        use a symmetric kernel (then shard rows instead)."""
+        if not 1 <= w <= self.w_max:
+            return 0
+        return int(N.query("ncgp_kop_sym_acc_elems", self._h, w))
+
+    def sym_partial(self, V: torch.Tensor, part: int, nparts: int, acc: torch.Tensor) -> None:
+        """Part ``part`` of ``nparts`` of the triangular work list into ``acc``
+        (float32, ``sym_acc_elems(w)`` elements; zeroed by the call)."""
+        if V.dim() == 1:
+            V = V.unsqueeze(1)
+        if V.shape[0] != self.n_cols or V.dtype != self.dtype:
+            raise N.DimensionMismatch("operand shape / dtype do not match the operator")
+        if V.stride(1) != 1:
+            V = V.contiguous()
+        w = V.shape[1]
+        if acc.dtype != torch.float32 or acc.numel() < self.sym_acc_elems(w) or not acc.is_contiguous():
+            raise N.DimensionMismatch("accumulator too small or not contiguous float32")
+        ldv = V.stride(0) if V.shape[0] > 1 else w
+        N.call("ncgp_kop_sym_partial", self._h, V.data_ptr(), ldv, w, part, nparts, acc.data_ptr(),
+               stream())
+
+    def sym_finalize(self, acc: torch.Tensor, w: int, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """The (n_rows, w) product from the summed accumulators."""
+        if out is None:
+            out = torch.empty((self.n_rows, w), dtype=self.dtype, device=acc.device)
+        ldo = out.stride(0) if out.shape[0] > 1 else w
+        N.call("ncgp_kop_sym_finalize", self._h, acc.data_ptr(), w, out.data_ptr(), ldo, stream())
+        return out
+
     def close(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:

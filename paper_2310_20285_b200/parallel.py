@@ -16,6 +16,14 @@ flushes its fp32 partial sums at fixed global column boundaries, a row is
 reduced in exactly the same order on 1 or P GPUs: the sharded product is
 bitwise identical to the single-GPU one.
 
+For K(X, X) the symmetric kernel evaluates each
+off-diagonal tile once; a row split would lose that.  :class:`SymmetricSplitOperator`
+instead splits the triangular work list itself: every rank evaluates a slice
+of equal tile count into an fp32 accumulator, an all-reduce sums the
+accumulators (the exchange step: a reduction, of the same size as the
+all-gather it replaces), and every rank writes the full product from the sum.
+Being an fp32 reduction it is not bitwise identical to the one-GPU product.
+
 The partition and gather logic takes the local compute as a callable so it
 is unit-tested on CPU with the ``gloo`` backend (tests/test_parallel_gloo.py).
 """
@@ -164,19 +172,86 @@ class RowShardedOperator:
     __call__ = apply
 
 
+class SymmetricSplitOperator:
+    """y = K(X, X) V with the symmetric kernel's triangular work list split
+    across the ranks of ``group``; every rank ends with all rows.
+
+    ``partial(V, part, nparts, acc)`` writes part ``part`` of ``nparts`` of the
+    product's contributions into ``acc`` (zeroing it first), ``finalize(acc,
+    w, out)`` writes the (n_rows, w) product from the summed accumulators and
+    ``acc_elems(w)`` sizes the accumulator; in production they are
+    :meth:`KernelOperator.sym_partial` / ``sym_finalize`` / ``sym_acc_elems``.
+    """
+
+    def __init__(self, n_rows: int, partial: Callable, finalize: Callable, acc_elems: Callable,
+                 group=None, dtype: torch.dtype = torch.float32,
+                 acc_dtype: torch.dtype = torch.float32):
+        self.n_rows = n_rows
+        self.partial, self.finalize, self.acc_elems = partial, finalize, acc_elems
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.dtype = dtype
+        self.acc_dtype = acc_dtype  # the kernel's accumulators are fp32
+        self._acc = {}
+
+    def accumulator(self, w: int, device) -> torch.Tensor:
+        key = (w, str(device))
+        acc = self._acc.get(key)
+        if acc is None:
+            acc = torch.empty(int(self.acc_elems(w)), dtype=self.acc_dtype, device=device)
+            self._acc[key] = acc
+        return acc
+
+    def apply(self, V: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        vec = V.dim() == 1
+        V2 = V.view(-1, 1) if vec else V
+        w = V2.shape[1]
+        acc = self.accumulator(w, V2.device)
+        self.partial(V2, self.rank, self.world, acc)
+        if self.world > 1:
+            dist.all_reduce(acc, group=self.group)
+        dst = None if out is None else out.view(self.n_rows, w)
+        res = self.finalize(acc, w, dst)
+        return res.view(-1) if vec else res
+
+    __call__ = apply
+
+
 class ShardedPriorOperator:
     """Drop-in for :class:`gp.PriorOperator` in ``fit(..., operator=...)``:
     the block-diagonal prior product on CN vectors, row-sharded across the
     ranks of ``group``."""
 
-    def __init__(self, prior, X, dtype=None, group=None, gather: str = "nccl", symm=None):
+    def __init__(self, prior, X, dtype=None, group=None, gather: str = "auto", symm=None):
+        """``gather``: ``"reduce"`` splits the symmetric kernel's work list
+        (:class:`SymmetricSplitOperator`), ``"nccl"`` / ``"fused"`` shard rows
+        (:class:`RowShardedOperator`), ``"auto"`` takes ``"reduce"`` when the
+        operator has a symmetric kernel for the C-wide product (one kernel
+        spec for all outputs), else ``"nccl"``."""
         from .gp import PriorOperator
+        if gather not in ("auto", "reduce", "nccl", "fused"):
+            raise ValueError(f"gather must be auto, reduce, nccl or fused, got {gather!r}")
         self.inner = PriorOperator(prior, X, dtype=dtype)
         self.C = self.inner.C
         self.n_rows = self.inner.n_rows
         self.dtype = self.inner.dtype
         self.matvecs = 0
         C = self.C
+        g0 = self.inner.groups[0]
+        sym_ok = (len(self.inner.groups) == 1 and len(g0[1]) == C and hasattr(g0[0], "sym_acc_elems")
+                  and g0[0].sym_acc_elems(C) > 0)
+        if gather == "auto":
+            gather = "reduce" if sym_ok else "nccl"
+        if gather == "reduce" and not sym_ok:
+            raise ValueError("gather='reduce' needs a symmetric kernel for this prior / width")
+        self.gather = gather
+        if gather == "reduce":
+            kop = g0[0]
+            self.sharded = SymmetricSplitOperator(self.n_rows, kop.sym_partial, kop.sym_finalize,
+                                                  kop.sym_acc_elems, group=group, dtype=self.dtype)
+            self._C = C
+            return
 
         def local_apply(V, out, r0, r1, peers=None):
             # ``out`` may be the (per * world)-row gather buffer: rows >= n_rows
@@ -187,6 +262,7 @@ class ShardedPriorOperator:
 
         self.sharded = RowShardedOperator(self.n_rows, local_apply, group=group,
                                           dtype=self.dtype, gather=gather, symm=symm)
+        self.gather = gather
         self._C = C
 
     @property

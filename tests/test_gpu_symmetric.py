@@ -163,3 +163,62 @@ def test_symmetric_kernel_single_p_buffer(n, d, w, fam, force):
     with _Env(NCGP_SYM=0):
         plain = op.apply(Vd).double()
     assert float((got - plain).norm() / plain.norm()) < 2e-5
+
+
+@pytest.mark.parametrize("n,d,w,fam,cg,parts", [
+    (45000, 8, 32, "rbf", 1, (1, 2, 3, 8)),
+    (70001, 8, 10, "matern32", 2, (1, 2, 5)),
+    (70001, 50, 10, "matern32", None, (2, 8)),   # pair kernel, one P buffer
+])
+def test_symmetric_split_across_parts(n, d, w, fam, cg, parts):
+    """ncgp_kop_sym_partial / _finalize (the multi-GPU split of the
+    triangular work list, parallel.SymmetricSplitOperator): the parts'
+    accumulators summed give the full product."""
+    X, V, op, Vd = _case(n, d, w, (fam, 2.0, 1.0), 17, cg)
+    full = op.apply(Vd).double()
+    assert op.last_variant == "symmetric"
+    with _Env(NCGP_SYM=0):
+        plain = op.apply(Vd).double()
+    m = op.sym_acc_elems(w)
+    assert m >= n * w
+    for P in parts:
+        tot = torch.zeros(m, dtype=torch.float32, device="cuda")
+        acc = torch.empty(m, dtype=torch.float32, device="cuda")
+        for k in range(P):
+            op.sym_partial(Vd, k, P, acc)
+            tot += acc
+        got = op.sym_finalize(tot, w).double()
+        assert float((got - full).norm() / full.norm()) < 1e-5, P
+        assert float((got - plain).norm() / plain.norm()) < 2e-5, P
+
+
+def test_symmetric_split_unavailable():
+    """No symmetric kernel (small, rectangular or forced off): acc size 0 and
+    the split entry points refuse (the caller row-shards instead)."""
+    from paper_2310_20285_b200 import _native as N
+    X, V, op, Vd = _case(3000, 8, 8, ("rbf", 1.5, 1.0), 3)
+    assert op.sym_acc_elems(8) == 0
+    with pytest.raises(N.Unsupported):
+        op.sym_partial(Vd, 0, 1, torch.empty(3000 * 32, dtype=torch.float32, device="cuda"))
+    rect = KernelOperator("rbf", 1.5, 1.0, op.X_rows[:2000], op.X_rows, w_max=32)
+    with _Env(NCGP_SYM=1):
+        assert rect.sym_acc_elems(8) == 0
+        assert op.sym_acc_elems(8) > 0       # forced on for the square operator
+        assert op.sym_acc_elems(40) == 0     # wider than w_max
+
+
+def test_sharded_prior_operator_reduce_single_rank():
+    """ShardedPriorOperator(gather='reduce') without a process group (one
+    rank): the split path end to end through the public operator."""
+    import paper_2310_20285_b200 as P
+    from paper_2310_20285_b200.parallel import ShardedPriorOperator
+    rng = np.random.default_rng(2)
+    n, C = 45000, 10
+    X = rng.standard_normal((n, 8)).astype(np.float32)
+    prior = P.MultiOutputPrior(kernels=(P.KernelSpec("matern32", 2.0, 1.5),) * C)
+    v = torch.from_numpy(rng.standard_normal(n * C)).float().cuda()
+    red = ShardedPriorOperator(prior, X, dtype=torch.float32, gather="auto")
+    assert red.gather == "reduce"
+    rows = ShardedPriorOperator(prior, X, dtype=torch.float32, gather="nccl")
+    a, b = red(v).double(), rows(v).double()
+    assert float((a - b).norm() / b.norm()) < 2e-5

@@ -156,3 +156,76 @@ def test_two_rank_fused_peer_stores_match_single_process(tmp_path, n):
 def test_gather_mode_is_validated():
     with pytest.raises(ValueError):
         RowShardedOperator(10, lambda *a, **k: None, gather="bogus")
+
+
+def _tri_items(n, b):
+    """Upper-triangle block pairs (I <= J) in block-major order, with tile
+    counts: the CPU stand-in for the symmetric kernel's work list."""
+    nb = (n + b - 1) // b
+    return [(i, j) for j in range(nb) for i in range(j + 1)]
+
+
+def _sym_worker(rank, world, port, n, d, w, b, result_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import ncgp_oracle as O
+        from paper_2310_20285_b200.parallel import SymmetricSplitOperator
+        rng = np.random.default_rng(0)
+        X = rng.standard_normal((n, d))
+        V = rng.standard_normal((n, w))
+        spec = ("rbf", 1.2, 1.0)
+        items = _tri_items(n, b)
+        seen = []
+
+        def partial(Vt, part, nparts, acc):
+            # slice of equal item count (the GPU slices by tile count)
+            lo, hi = len(items) * part // nparts, len(items) * (part + 1) // nparts
+            seen.append((part, nparts, lo, hi))
+            A = acc.view(n, -1)
+            A.zero_()
+            Vn = Vt.double().numpy()
+            for i, j in items[lo:hi]:
+                ri, rj = slice(i * b, min(n, (i + 1) * b)), slice(j * b, min(n, (j + 1) * b))
+                Kij = O.kernel_matmul_rows(spec, X[ri], X[rj], np.eye(rj.stop - rj.start))
+                A[ri] += torch.from_numpy(Kij @ Vn[rj])
+                if i != j:
+                    A[rj] += torch.from_numpy(Kij.T @ Vn[ri])
+
+        def finalize(acc, w_, out):
+            res = acc.view(n, -1)[:, :w_].clone()
+            if out is not None:
+                out.copy_(res)
+                return out
+            return res
+
+        op = SymmetricSplitOperator(n, partial, finalize, lambda w_: n * w_, dtype=torch.float64,
+                                    acc_dtype=torch.float64)
+        res = op.apply(torch.from_numpy(V))
+        np.save(os.path.join(result_dir, f"s{rank}.npy"), res.numpy())
+        resv = op.apply(torch.from_numpy(V[:, 0].copy()))
+        np.save(os.path.join(result_dir, f"t{rank}.npy"), resv.numpy())
+        assert [s[:2] for s in seen] == [(rank, world)] * 2, seen
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n,b", [(300, 64), (1000, 128)])
+def test_two_rank_symmetric_split_matches_single_process(tmp_path, n, b):
+    """gather='reduce': each rank evaluates a slice of the triangular work
+    list into an accumulator, a gloo all-reduce sums them, and every rank
+    finalises the full product."""
+    from oracle import ncgp_oracle as O
+    d, w, world = 3, 4, 2
+    assert len(_tri_items(n, b)) >= world
+    mp.spawn(_sym_worker, args=(world, _free_port(), n, d, w, b, str(tmp_path)), nprocs=world,
+             join=True)
+    rng = np.random.default_rng(0)
+    X = rng.standard_normal((n, d))
+    V = rng.standard_normal((n, w))
+    ref = O.kernel_matmul_rows(("rbf", 1.2, 1.0), X, X, V)
+    outs = [np.load(tmp_path / f"s{r}.npy") for r in range(world)]
+    np.testing.assert_array_equal(outs[0], outs[1])  # every rank holds the same product
+    np.testing.assert_allclose(outs[0], ref, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(np.load(tmp_path / "t0.npy"), ref[:, 0], rtol=1e-12, atol=1e-12)
