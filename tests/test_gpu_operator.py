@@ -298,7 +298,8 @@ def test_prior_operator_peers_with_per_class_specs():
 def test_fused_gather_symmetric_memory_single_rank(tmp_path):
     """torchrun world=1, NCCL: ShardedPriorOperator(gather='fused') goes
     through torch symmetric memory (rendezvous, peer mapping, device
-    barriers) and matches the unsharded product bitwise."""
+    barriers) and matches the unsharded product bitwise; gather='reduce'
+    (the symmetric kernel's split with an NCCL all-reduce) within 2e-5."""
     import subprocess
     import sys
     script = tmp_path / "symm_run.py"
@@ -319,6 +320,10 @@ def test_fused_gather_symmetric_memory_single_rank(tmp_path):
         "torch.cuda.synchronize()\n"
         "assert torch.equal(ra, rb), float((ra - rb).abs().max())\n"
         "assert torch.equal(ra2, b(2 * v))\n"
+        "os.environ['NCGP_SYM'] = '1'  # the symmetric kernel at this small n\n"
+        "c = ShardedPriorOperator(prior, X, dtype=torch.float32, gather='reduce')\n"
+        "rc = c(v)\n"
+        "assert float((rc - rb).norm() / rb.norm()) < 2e-5\n"
         "dist.destroy_process_group()\n"
         "print('SYMM_OK')\n")
     env = dict(os.environ, MASTER_ADDR="127.0.0.1")
