@@ -358,7 +358,8 @@ struct TcParams {
                          // reductions, 2 = drop O reductions, 4 = no transposed MMAs,
                          // 8 = no D_T loads, 16 = no P stores to shared memory;
                          // variant (correct results): 64 = flip whether T(g) is held
-                         // back behind GEMM1(g + NS); 128 (single-CTA kernel) = GEMM2
+                         // back behind GEMM1(g + NS); 256 (single-CTA kernel) = drains by
+                         // red.global.add.v4 from registers; 128 (single-CTA kernel) = GEMM2
                          // reads P from TMEM (TS), as measured slower
   float* sym_dump;       // symmetric kernel debug: raw D_T per (pair, tile, rank) when set
   int npb;               // symmetric kernel: P buffers in shared memory (2, or 1 for large D)
@@ -1555,10 +1556,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
             if (tr) trace_ev<DBG>(p, g, 8);
           }
           const uint32_t rowb = rowb0 + 512u * c;
+          if (!(p.sym_dbg & 16)) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            st_shared_v4(rowb + 128u * k, hi[4 * k], hi[4 * k + 1], hi[4 * k + 2], hi[4 * k + 3]);
-            st_shared_v4(rowb + PBUF / 2 + 128u * k, lo[4 * k], lo[4 * k + 1], lo[4 * k + 2], lo[4 * k + 3]);
+            for (int k = 0; k < 4; ++k) {
+              st_shared_v4(rowb + 128u * k, hi[4 * k], hi[4 * k + 1], hi[4 * k + 2], hi[4 * k + 3]);
+              st_shared_v4(rowb + PBUF / 2 + 128u * k, lo[4 * k], lo[4 * k + 1], lo[4 * k + 2], lo[4 * k + 3]);
+            }
           }
         }
         if (p_tmem) {
@@ -1596,6 +1599,32 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
                    __float_as_uint(v[7]));
     };
     auto drain = [&](uint32_t tacc, int64_t row0, bool skip) {
+      if (p.sym_dbg & 256) {  // variant: vector reductions straight from registers
+        float* dst = p.acc + (row0 + lane) * WP;
+#pragma unroll
+        for (int h = 0; h < WP / 8; ++h) {
+          uint32_t x[8], y[8];
+          tmem_ld8(tacc + lane_off + 8 * h, x);
+          tmem_ld8(tacc + lane_off + WP + 8 * h, y);
+          tmem_wait_ld();
+          float v[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const int ex = p.s_exp + __ldg(&p.col_exp[8 * h + c]);
+            v[c] = (__uint_as_float(x[c]) + __uint_as_float(y[c])) * __int_as_float((127 - ex) << 23);
+          }
+          const int k0 = (2 * h) ^ (lane & (C - 1)), k1 = (2 * h + 1) ^ (lane & (C - 1));
+          if (!skip) {
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * k0), "f"(v[0]),
+                         "f"(v[1]), "f"(v[2]), "f"(v[3]) : "memory");
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * k1), "f"(v[4]),
+                         "f"(v[5]), "f"(v[6]), "f"(v[7]) : "memory");
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        return;
+      }
       if (lane == 0) bulk_wait_read();  // staging rows free again
       __syncwarp();
 #pragma unroll
@@ -1618,7 +1647,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
       if (ti.transposed()) {
         mbar_wait(&dt_full[dtq & 1u], (dtq >> 1) & 1u);
         tc_fence_after();
-        drain(tDT(dtq & 1u), (int64_t)ti.ct * BM + 32 * wq, (p.sym_dbg & 1) != 0);
+        if (!(p.sym_dbg & 8)) drain(tDT(dtq & 1u), (int64_t)ti.ct * BM + 32 * wq, (p.sym_dbg & 1) != 0);
+        else tc_fence_before();
         if (lane == 0) mbar_arrive(&dt_empty[dtq & 1u]);
         ++dtq;
       }
