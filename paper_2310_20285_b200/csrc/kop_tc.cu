@@ -1247,7 +1247,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
   uint8_t* sV = sXB + (size_t)p.sx * xb_bytes;
   uint8_t* sVI = sV + (size_t)p.sv * vb_bytes;
   uint8_t* sP = sVI + vb_bytes;
-  float* sStage = reinterpret_cast<float*>(sP + 2 * (size_t)PBUF);
+  float* sStage = reinterpret_cast<float*>(sP + (size_t)p.npb * PBUF);
+  // P buffer of tile g: two alternating, or one when shared memory is short
+  auto pbuf = [&](uint32_t g) -> uint32_t { return p.npb == 2 ? (g & 1u) : 0u; };
   uint64_t* bars = reinterpret_cast<uint64_t*>(sStage + BM * WP);
   uint64_t* xb_full = bars;            // [6]
   uint64_t* v_full = xb_full + 6;      // [9]
@@ -1416,7 +1418,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
         tc_fence_after();
         if (lane == 0) trace_ev<DBG>(p, g, 0);
         const uint64_t dv = dV0 + (uint64_t)vr.idx * (vb_bytes >> 4);
-        const uint64_t ph = sdesc(smem_u32(sP) + (g & 1u) * PBUF, 128u, 2048u);
+        const uint64_t ph = sdesc(smem_u32(sP) + pbuf(g) * PBUF, 128u, 2048u);
         const uint64_t pl = ph + ((PBUF / 2) >> 4);
         const uint32_t dO = tO(ob);
         if (elect_one()) {
@@ -1482,7 +1484,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
         if (lane == 0) trace_ev<DBG>(p, g, 13);
         if (elect_one()) {
           if (tp && !(p.sym_dbg & 4)) {
-            const uint64_t pa = dP0 + (uint64_t)(g & 1u) * (PBUF >> 4);
+            const uint64_t pa = dP0 + (uint64_t)pbuf(g) * (PBUF >> 4);
             const uint32_t dt = tDT(dtq & 1u);
 #pragma unroll 1
             for (int m = 0; m < BN / 16; ++m) {
@@ -1523,12 +1525,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
     while (ti.valid) {
       if ((int)(g & 1u) == e) {
         if (tr) trace_ev<DBG>(p, g, 3 + 2 * e);
-        bool pt_wait = g >= 2u;
+        bool pt_wait = g >= (uint32_t)p.npb;
         mbar_wait(&s_full[er.idx], er.phase);
         tc_fence_after();
         if (tr) trace_ev<DBG>(p, g, 4 + 2 * e);
         const uint32_t base = tS(g & 1u) + lane_off + col0;
-        const uint32_t rowb0 = smem_u32(sP) + (g & 1u) * PBUF + rowb_base;
+        const uint32_t rowb0 = smem_u32(sP) + pbuf(g) * PBUF + rowb_base;
         const bool p_tmem = (p.sym_dbg & 128) != 0;
         uint32_t ra[32], hi[16], lo[16];
 #pragma unroll
@@ -1549,8 +1551,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
               tmem_st16(base + 32 * c + 16, lo);
             }
           }
-          if (pt_wait) {
-            const uint32_t t = g - 2u;
+          if (pt_wait) {  // tile g - npb's GEMM2 and T are done with the buffer
+            const uint32_t t = g - (uint32_t)p.npb;
             mbar_wait(&pt_free[t & 1u], (t >> 1) & 1u);
             pt_wait = false;
             if (tr) trace_ev<DBG>(p, g, 8);
@@ -1995,14 +1997,18 @@ std::vector<int4> sym_items(int64_t pairs, int64_t nb) {
 // Single-CTA symmetric kernel (K1-sym1): row tile r covers column tiles
 // [r, nb); same block-major order.
 constexpr size_t SMEM_MAX = 232448;  // sm_100 opt-in maximum per block
-size_t smem1_bytes(uint32_t a_bytes, int wp, int sx, int sv);
+size_t smem1_bytes(uint32_t a_bytes, int wp, int sx, int sv, int npb = 2);
 // Flavour of the symmetric kernel an operator's work list is built for: the
 // single-CTA kernel where its shared memory fits the widest RHS (full column
 // records plus two P buffers), else the pair kernel.  NCGP_SYM_CG=1 / 2 forces.
 int sym_cg(int d, int w_max) {
   const char* e = getenv("NCGP_SYM_CG");
   if (e != nullptr && (e[0] == '1' || e[0] == '2')) return e[0] - '0';
-  return smem1_bytes((uint32_t)(BM * ka_of(d) * 2), wp_of(w_max), 2, 2) <= SMEM_MAX ? 1 : 2;
+  const uint32_t a = (uint32_t)(BM * ka_of(d) * 2);
+  if (smem1_bytes(a, wp_of(w_max), 2, 2, 2) <= SMEM_MAX) return 1;
+  const char* f = getenv("NCGP_SYM1_NPB");  // experiments: one-P-buffer single-CTA kernel
+  if (f != nullptr && f[0] == '1' && smem1_bytes(a, wp_of(w_max), 2, 2, 1) <= SMEM_MAX) return 1;
+  return 2;
 }
 template <typename F>
 void sym1_walk(int64_t nb, F&& f) {
@@ -2017,9 +2023,9 @@ int64_t sym1_item_count(int64_t nb) {
   sym1_walk(nb, [&](int64_t, int64_t, int64_t) { ++n; });
   return n;
 }
-size_t smem1_bytes(uint32_t a_bytes, int wp, int sx, int sv) {
+size_t smem1_bytes(uint32_t a_bytes, int wp, int sx, int sv, int npb) {
   const size_t v2 = (size_t)wp * BN * 2;
-  return (size_t)a_bytes + (size_t)sx * a_bytes + (size_t)sv * 2 * v2 + 2 * v2 + 2 * (size_t)PBUF +
+  return (size_t)a_bytes + (size_t)sx * a_bytes + (size_t)sv * 2 * v2 + 2 * v2 + npb * (size_t)PBUF +
          (size_t)BM * wp * 4 + (6 + 9 + 4 + 4 * NR + 10) * sizeof(uint64_t) + 16 + 1024;
 }
 
@@ -2076,7 +2082,7 @@ int sym_variant(const ncgp_kop* op, int w) {
   const int wp = wp_of(w);
   if (!sym_enabled(op->family, wp, op->col_tiles, op->sym_cg)) return 0;
   const uint32_t a_bytes = (uint32_t)(BM * op->ka * 2);
-  if (op->sym_cg == 1) return smem1_bytes(a_bytes, wp, 2, 2) <= SMEM_MAX ? 2 : 0;
+  if (op->sym_cg == 1) return smem1_bytes(a_bytes, wp, 2, 2, 1) <= SMEM_MAX ? 2 : 0;
   if (smem_bytes(a_bytes, wp, 1, 3, 3, 2) <= (size_t)SMEM_BUDGET) return 1;
   if (op->family == NCGP_MATERN32 && smem_bytes(a_bytes, wp, 1, 3, 3, 1) <= (size_t)SMEM_BUDGET) return 1;
   const char* e = getenv("NCGP_SYM_NPB");
@@ -2288,16 +2294,17 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
   if (sym && op->sym_cg == 1) {
     const int cand[][2] = {{3, 6}, {3, 4}, {3, 3}, {2, 4}, {3, 2}, {2, 3}, {2, 2}};
     bool fit = false;
-    for (auto& c : cand)
-      if (smem1_bytes(p.a_bytes, wp, c[0], c[1]) <= SMEM_MAX) {
-        p.sx = c[0];
-        p.sv = c[1];
-        fit = true;
-        break;
-      }
+    for (int npb = 2; npb >= 1 && !fit; --npb)
+      for (auto& c : cand)
+        if (smem1_bytes(p.a_bytes, wp, c[0], c[1], npb) <= SMEM_MAX) {
+          p.sx = c[0];
+          p.sv = c[1];
+          p.npb = npb;
+          fit = true;
+          break;
+        }
     if (fit) {
       p.na = 1;
-      p.npb = 2;
       p.splits = 1;
       p.tiles_per_split = p.col_tiles;
       p.n_items = (int)(it_hi - it_lo);
@@ -2308,7 +2315,7 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
       NCGP_CUDA(cudaMemsetAsync(p.acc, 0, (size_t)op->row_tiles * BM * wp * sizeof(float), st));
       op->last_variant = 2;
       if (p.n_items == 0) return NCGP_OK;  // an empty part
-      const size_t smem = smem1_bytes(p.a_bytes, wp, p.sx, p.sv);
+      const size_t smem = smem1_bytes(p.a_bytes, wp, p.sx, p.sv, p.npb);
       const unsigned grid = (unsigned)std::min<int64_t>(p.n_items, op->sms);
       auto launch = [&](auto kern) -> int {
         NCGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
