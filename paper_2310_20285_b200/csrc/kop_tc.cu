@@ -1239,7 +1239,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  constexpr int NS1 = 2;  // S buffers: 2 x 128 + O 2 x 2 WP + D_T 2 x 2 WP columns
+  // S buffers next to double-buffered O and D_T (2 x 2 WP columns each):
+  // two at WP = 32, three at WP = 16
+  constexpr int NS1 = WP == 16 ? 3 : 2;
   const uint32_t xb_bytes = 2u * p.xbh_bytes;  // 128 XB rows
   const uint32_t vb_bytes = 2u * p.v2_bytes;   // [Vhi | Vlo]: 2 WP rows
   uint8_t* sA = smem;
@@ -1366,7 +1368,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
       Ring xr, sf;
       xr.init((uint32_t)p.sx);
       sf.init(NR);
-      uint32_t g = 0, c1 = 0, nitem = 0;
+      uint32_t g = 0, c1 = 0, nitem = 0, sb = 0;
       while (ti.valid) {
         const bool li = ti.last_in_item();
         if (ti.first_in_item()) {
@@ -1382,7 +1384,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
         tc_fence_after();
         if (lane == 0) trace_ev<DBG>(p, g, 9);
         const uint64_t dx = dX0 + (uint64_t)xr.idx * (xb_bytes >> 4);
-        const uint32_t d = tS(g & 1u);
+        const uint32_t d = tS(sb);
         if (elect_one()) {
           for (int k = 0; k < ksteps1; ++k)
             mma1_ss(d, dA + (uint64_t)(16 * k), dx + (uint64_t)(16 * k), id1, k > 0);
@@ -1392,6 +1394,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
         __syncwarp();
         if (lane == 0) trace_ev<DBG>(p, g, 2);
         if (lane == 0) *g1_cnt = g + 1u;
+        sb = sb + 1u == (uint32_t)NS1 ? 0u : sb + 1u;
         xr.adv();
         c1 = (c1 + 1u == (uint32_t)NR) ? 0u : c1 + 1u;
         ++g;
@@ -1407,7 +1410,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
       Ring vr, rr;
       vr.init((uint32_t)p.sv);
       rr.init(NR);
-      uint32_t g = 0, q = 0;
+      uint32_t g = 0, q = 0, sb = 0;
       while (ti.valid) {
         const bool fresh = ti.first_in_chunk(), last = ti.last_in_chunk();
         if (lane == 0) trace_ev<DBG>(p, g, 11);
@@ -1423,7 +1426,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
         const uint32_t dO = tO(ob);
         if (elect_one()) {
           if (p.sym_dbg & 128) {  // A = P from TMEM (the epilogue's copy over S(g))
-            const uint32_t a0 = tS(g & 1u);
+            const uint32_t a0 = tS(sb);
 #pragma unroll
             for (int m = 0; m < BN / 16; ++m) {
               const uint32_t ahi = a0 + 32u * (m >> 1) + 8u * (m & 1);
@@ -1444,6 +1447,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
         __syncwarp();
         if (lane == 0) trace_ev<DBG>(p, g, 1);
         q += last ? 1u : 0u;
+        sb = sb + 1u == (uint32_t)NS1 ? 0u : sb + 1u;
         vr.adv();
         rr.adv();
         ++g;
@@ -1520,7 +1524,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
     Ring er;
     er.init(NR);
     const float L = p.L;
-    uint32_t g = 0;
+    uint32_t g = 0, sb = 0;
     const bool tr = (wq == 0 && hc == 0 && lane == 0);
     while (ti.valid) {
       if ((int)(g & 1u) == e) {
@@ -1529,7 +1533,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
         mbar_wait(&s_full[er.idx], er.phase);
         tc_fence_after();
         if (tr) trace_ev<DBG>(p, g, 4 + 2 * e);
-        const uint32_t base = tS(g & 1u) + lane_off + col0;
+        const uint32_t base = tS(sb) + lane_off + col0;
         const uint32_t rowb0 = smem_u32(sP) + pbuf(g) * PBUF + rowb_base;
         const bool p_tmem = (p.sym_dbg & 128) != 0;
         uint32_t ra[32], hi[16], lo[16];
@@ -1576,6 +1580,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
         if (tr) trace_ev<DBG>(p, g, e == 0 ? 7 : 10);
       }
       ++g;
+      sb = sb + 1u == (uint32_t)NS1 ? 0u : sb + 1u;
       er.adv();
       ti.next(p);
     }
@@ -2005,7 +2010,9 @@ int sym_cg(int d, int w_max) {
   const char* e = getenv("NCGP_SYM_CG");
   if (e != nullptr && (e[0] == '1' || e[0] == '2')) return e[0] - '0';
   const uint32_t a = (uint32_t)(BM * ka_of(d) * 2);
-  if (smem1_bytes(a, wp_of(w_max), 2, 2, 2) <= SMEM_MAX) return 1;
+  // at least a 3-deep XB ring (D = 24 with a 2-deep one ran slower than the
+  // plain kernel; the pair kernel keeps 3)
+  if (smem1_bytes(a, wp_of(w_max), 3, 2, 2) <= SMEM_MAX) return 1;
   const char* f = getenv("NCGP_SYM1_NPB");  // experiments: one-P-buffer single-CTA kernel
   if (f != nullptr && f[0] == '1' && smem1_bytes(a, wp_of(w_max), 2, 2, 1) <= SMEM_MAX) return 1;
   return 2;
@@ -2292,7 +2299,7 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
   float* const sym_acc = part != nullptr ? part->acc : op->sym_acc;
   const bool sym_fin = part == nullptr;
   if (sym && op->sym_cg == 1) {
-    const int cand[][2] = {{3, 6}, {3, 4}, {3, 3}, {2, 4}, {3, 2}, {2, 3}, {2, 2}};
+    const int cand[][2] = {{3, 6}, {3, 4}, {3, 3}, {3, 2}, {2, 4}, {2, 3}, {2, 2}};
     bool fit = false;
     for (int npb = 2; npb >= 1 && !fit; --npb)
       for (auto& c : cand)
