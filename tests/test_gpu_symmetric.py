@@ -222,3 +222,23 @@ def test_sharded_prior_operator_reduce_single_rank():
     rows = ShardedPriorOperator(prior, X, dtype=torch.float32, gather="nccl")
     a, b = red(v).double(), rows(v).double()
     assert float((a - b).norm() / b.norm()) < 2e-5
+
+
+@pytest.mark.parametrize("n,d,w,fam", [
+    (38401, 1, 1, "rbf"),          # just above the default threshold, D = 1, w = 1
+    (38529, 8, 17, "matern32"),    # ragged last tile, WP = 32 with 15 padding columns
+    (70000, 24, 16, "rbf"),        # D = 24: pair kernel (sym1 lacks a 3-deep XB ring)
+    (70000, 20, 32, "matern32"),   # WP = 32, D = 20: pair kernel
+    (39000, 3, 5, "rbf"),
+])
+def test_symmetric_default_shapes_sweep(n, d, w, fam):
+    """Default policy at the edges of the symmetric kernels' ranges: whichever
+    flavour runs, it agrees with the plain kernel."""
+    X, V, op, Vd = _case(n, d, w, (fam, 1.7, 1.3), n + w)
+    got = op.apply(Vd).double()
+    assert op.last_variant == "symmetric"
+    with _Env(NCGP_SYM=0):
+        plain = op.apply(Vd).double()
+        scale = op.apply(Vd.abs()).double()  # K |V|: the entry scale
+    assert float((got - plain).norm() / plain.norm()) < 2e-5
+    assert float(((got - plain).abs() / scale).max()) < 1e-5
