@@ -70,6 +70,44 @@ __global__ void gemv_t_partial_kernel(const T* __restrict__ Q, int64_t ldq, int 
   if (threadIdx.x == 0) partial[(int64_t)r * gridDim.x + blockIdx.x] = s;
 }
 
+// fp32 with 16-byte alignment: RPB rows of Q per block share each float4 of
+// z, so z is read from L2 once per RPB rows and every thread keeps RPB * 4
+// independent loads in flight.  chunk is a multiple of 4 * RB.
+template <int RPB>
+__global__ void gemv_t_partial_v4_kernel(const float* __restrict__ Q, int64_t ldq, int k,
+                                         const float* __restrict__ z, int64_t n, int64_t chunk,
+                                         double* __restrict__ partial) {
+  __shared__ double sm[32];
+  const int r0 = blockIdx.y * RPB;
+  const int64_t lo = (int64_t)blockIdx.x * chunk;
+  const int64_t hi = min(n, lo + chunk);
+  const int64_t hi4 = lo + (hi - lo) / 4 * 4;
+  double acc[RPB];
+#pragma unroll
+  for (int rr = 0; rr < RPB; ++rr) acc[rr] = 0.0;
+  for (int64_t i = lo + 4 * (int64_t)threadIdx.x; i < hi4; i += 4 * RB) {
+    const float4 zv = __ldg(reinterpret_cast<const float4*>(z + i));
+#pragma unroll
+    for (int rr = 0; rr < RPB; ++rr) {
+      if (r0 + rr < k) {
+        const float4 qv = __ldcs(reinterpret_cast<const float4*>(Q + (int64_t)(r0 + rr) * ldq + i));
+        acc[rr] += (double)qv.x * (double)zv.x + (double)qv.y * (double)zv.y +
+                   (double)qv.z * (double)zv.z + (double)qv.w * (double)zv.w;
+      }
+    }
+  }
+  for (int64_t i = hi4 + threadIdx.x; i < hi; i += RB) {  // ragged tail of the last chunk
+#pragma unroll
+    for (int rr = 0; rr < RPB; ++rr)
+      if (r0 + rr < k) acc[rr] += (double)Q[(int64_t)(r0 + rr) * ldq + i] * (double)z[i];
+  }
+#pragma unroll
+  for (int rr = 0; rr < RPB; ++rr) {
+    const double t = ncgp::block_sum(acc[rr], sm);
+    if (threadIdx.x == 0 && r0 + rr < k) partial[(int64_t)(r0 + rr) * gridDim.x + blockIdx.x] = t;
+  }
+}
+
 template <typename T>
 __global__ void gemv_n_kernel(const T* __restrict__ Q, int64_t ldq, int k,
                               const double* __restrict__ y, const T* __restrict__ s, double alpha,
@@ -294,8 +332,28 @@ int ncgp_gemv_t(int dtype, const void* Q, int64_t ldq, int k, const void* z, int
   if (G > per) G = per < 1 ? 1 : per;
   NCGP_CHECK_ARG(ws_bytes >= (size_t)G * k * sizeof(double), NCGP_INVALID_INPUT,
                  "reduce workspace too small");
-  const int64_t chunk = (n + G - 1) / G;
   double* part = static_cast<double*>(workspace);
+  constexpr int RPB = 8;
+  if (dtype == NCGP_F32 && ldq % 4 == 0 && ((uintptr_t)Q & 15) == 0 && ((uintptr_t)z & 15) == 0) {
+    // vector path: Gv blocks per group of RPB rows, ~16 blocks per SM in
+    // total (a few resident blocks per SM would leave the SMs that got one
+    // more block finishing last)
+    const int groups = (k + RPB - 1) / RPB;
+    int64_t Gv = (n + 4 * RB * 8 - 1) / (4 * RB * 8);  // >= 8 vector sweeps per thread
+    const int64_t perv = ((int64_t)sms * 16 + groups - 1) / groups;
+    if (Gv > perv) Gv = perv < 1 ? 1 : perv;
+    const int64_t gws = (int64_t)(ws_bytes / ((size_t)k * sizeof(double)));
+    if (Gv > gws) Gv = gws;  // the workspace holds gws * k partials
+    const int64_t chunk = ((n + Gv - 1) / Gv + 4 * RB - 1) / (4 * RB) * (4 * RB);
+    Gv = (n + chunk - 1) / chunk;
+    gemv_t_partial_v4_kernel<RPB><<<dim3((unsigned)Gv, (unsigned)groups), RB, 0, st>>>(
+        (const float*)Q, ldq, k, (const float*)z, n, chunk, part);
+    NCGP_LAUNCHED();
+    sum_partials_kernel<<<(k + 7) / 8, 256, 0, st>>>(part, Gv, k, out);
+    NCGP_LAUNCHED();
+    return NCGP_OK;
+  }
+  const int64_t chunk = (n + G - 1) / G;
   dim3 grid((unsigned)G, (unsigned)k);
   if (dtype == NCGP_F64)
     gemv_t_partial_kernel<double><<<grid, RB, 0, st>>>((const double*)Q, ldq, k,
