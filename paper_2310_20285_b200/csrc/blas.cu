@@ -42,6 +42,39 @@ __global__ void dots_partial_kernel(int64_t n, int npairs, const T* x0, const T*
   }
 }
 
+// fp32, 16-byte aligned operands: float4 loads, chunk a multiple of 4 * RB
+__global__ void dots_partial_v4_kernel(int64_t n, int npairs, const float* x0, const float* y0,
+                                       const float* x1, const float* y1, const float* x2,
+                                       const float* y2, const float* x3, const float* y3,
+                                       int64_t chunk, double* __restrict__ partial) {
+  __shared__ double sm[32];
+  const int64_t lo = (int64_t)blockIdx.x * chunk;
+  const int64_t hi = min(n, lo + chunk);
+  const int64_t hi4 = lo + (hi - lo) / 4 * 4;
+  const float* xs[4] = {x0, x1, x2, x3};
+  const float* ys[4] = {y0, y1, y2, y3};
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t i = lo + 4 * (int64_t)threadIdx.x; i < hi4; i += 4 * RB) {
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+      if (p < npairs) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(xs[p] + i));
+        const float4 b = __ldg(reinterpret_cast<const float4*>(ys[p] + i));
+        acc[p] += (double)a.x * (double)b.x + (double)a.y * (double)b.y + (double)a.z * (double)b.z +
+                  (double)a.w * (double)b.w;
+      }
+  }
+  for (int64_t i = hi4 + threadIdx.x; i < hi; i += RB) {
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+      if (p < npairs) acc[p] += (double)xs[p][i] * (double)ys[p][i];
+  }
+  for (int p = 0; p < npairs; ++p) {
+    const double t = ncgp::block_sum(acc[p], sm);
+    if (threadIdx.x == 0) partial[(int64_t)p * gridDim.x + blockIdx.x] = t;
+  }
+}
+
 __global__ void sum_partials_kernel(const double* __restrict__ partial, int64_t nblk, int nvec,
                                     double* __restrict__ out) {
   // one warp per output vector entry; lanes stride then a fixed-order warp tree
@@ -301,6 +334,20 @@ int ncgp_dots(int dtype, int64_t n, int npairs, const void* const* xs, const voi
                       npairs > 3 ? xs[3] : xs[0]};
   const void* y[4] = {ys[0], npairs > 1 ? ys[1] : ys[0], npairs > 2 ? ys[2] : ys[0],
                       npairs > 3 ? ys[3] : ys[0]};
+  bool aligned = true;
+  for (int p = 0; p < 4; ++p)
+    aligned = aligned && (((uintptr_t)x[p] | (uintptr_t)y[p]) & 15) == 0;
+  if (dtype == NCGP_F32 && aligned) {
+    const int64_t chunk4 = (chunk + 4 * RB - 1) / (4 * RB) * (4 * RB);
+    const int64_t G4 = (n + chunk4 - 1) / chunk4;  // <= G
+    dots_partial_v4_kernel<<<(unsigned)G4, RB, 0, st>>>(
+        n, npairs, (const float*)x[0], (const float*)y[0], (const float*)x[1], (const float*)y[1],
+        (const float*)x[2], (const float*)y[2], (const float*)x[3], (const float*)y[3], chunk4, part);
+    NCGP_LAUNCHED();
+    sum_partials_kernel<<<(npairs + 7) / 8, 256, 0, st>>>(part, G4, npairs, out);
+    NCGP_LAUNCHED();
+    return NCGP_OK;
+  }
   if (dtype == NCGP_F64)
     dots_partial_kernel<double><<<(unsigned)G, RB, 0, st>>>(
         n, npairs, (const double*)x[0], (const double*)y[0], (const double*)x[1],

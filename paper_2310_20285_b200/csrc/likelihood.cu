@@ -68,6 +68,85 @@ __global__ void softmax_stats_kernel(const T* __restrict__ f, const int64_t* __r
     if (c < C) yhat_out[p * C + c] = fp[c] + (g[c] - um);
 }
 
+// The same per point, with the block's 128 points x C values moved through
+// shared memory: the (n, C) row-major rows of a block are one contiguous
+// range, so every global load and store is a coalesced sweep instead of a
+// C-strided access per thread.
+template <typename T, int CMAX>
+__global__ void softmax_stats_tiled_kernel(const T* __restrict__ f, const int64_t* __restrict__ y,
+                                           int64_t n, int C, T* __restrict__ pi_out,
+                                           T* __restrict__ grad_out, T* __restrict__ yhat_out) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T* tile = reinterpret_cast<T*>(smraw);  // [128][C]
+  const int64_t p0 = (int64_t)blockIdx.x * 128;
+  const int np = n - p0 < 128 ? (int)(n - p0) : 128;
+  const int m = np * C;
+  const T* src = f + p0 * C;
+  for (int j = threadIdx.x; j < m; j += blockDim.x) tile[j] = src[j];
+  __syncthreads();
+  const int t = threadIdx.x;
+  const bool live = t < np;
+  T fv[CMAX], e[CMAX], g[CMAX];
+  T sum = 0, gm = 0;
+  if (live) {
+    T mx = tile[t * C];
+#pragma unroll
+    for (int c = 0; c < CMAX; ++c)
+      if (c < C) {
+        fv[c] = tile[t * C + c];
+        mx = fv[c] > mx ? fv[c] : mx;
+      }
+#pragma unroll
+    for (int c = 0; c < CMAX; ++c)
+      if (c < C) { e[c] = dev_exp<T>(fv[c] - mx); sum += e[c]; }
+    const int64_t lab = y ? y[p0 + t] : -1;
+#pragma unroll
+    for (int c = 0; c < CMAX; ++c)
+      if (c < C) {
+        e[c] = e[c] / sum;  // pi
+        g[c] = (c == lab ? T(1) : T(0)) - e[c];
+        gm += g[c];
+      }
+  }
+  // one coalesced store sweep per requested output, staged through the tile
+  auto store = [&](T* dst, int which) {
+    __syncthreads();
+    if (live) {
+      if (which == 0) {
+#pragma unroll
+        for (int c = 0; c < CMAX; ++c)
+          if (c < C) tile[t * C + c] = e[c];
+      } else if (which == 1) {
+#pragma unroll
+        for (int c = 0; c < CMAX; ++c)
+          if (c < C) tile[t * C + c] = g[c];
+      } else {
+        // W^+ g = P diag(1/max(pi, floor)) P g  (likelihoods.py:298-301)
+        const T gmean = gm / T(C);
+        T u[CMAX];
+        T um = 0;
+#pragma unroll
+        for (int c = 0; c < CMAX; ++c)
+          if (c < C) {
+            const T pc = e[c] > T(kProbFloor) ? e[c] : T(kProbFloor);
+            u[c] = (g[c] - gmean) * (T(1) / pc);
+            um += u[c];
+          }
+        um /= T(C);
+#pragma unroll
+        for (int c = 0; c < CMAX; ++c)
+          if (c < C) tile[t * C + c] = fv[c] + (u[c] - um);
+      }
+    }
+    __syncthreads();
+    T* d = dst + p0 * C;
+    for (int j = threadIdx.x; j < m; j += blockDim.x) d[j] = tile[j];
+  };
+  if (pi_out) store(pi_out, 0);
+  if (grad_out) store(grad_out, 1);
+  if (yhat_out) store(yhat_out, 2);
+}
+
 // out = beta*base + alpha*W^+ V, column blocks (likelihoods.py:291-310)
 template <typename T, int CMAX>
 __global__ void softmax_winv_kernel(const T* __restrict__ pi, int64_t n, int C,
@@ -172,8 +251,12 @@ __global__ void diag_apply_kernel(const T* __restrict__ d, int64_t n, const T* _
 template <int CMAX, typename T>
 int launch_stats(const T* f, const int64_t* y, int64_t n, int C, T* pi, T* g, T* yh,
                  cudaStream_t st) {
-  softmax_stats_kernel<T, CMAX><<<(unsigned)((n + 127) / 128), 128, 0, st>>>(f, y, n, C, pi, g,
-                                                                               yh);
+  if constexpr (CMAX <= 16)  // tiles of <= 16 KB; wider C keeps the per-thread kernel (registers)
+    softmax_stats_tiled_kernel<T, CMAX><<<(unsigned)((n + 127) / 128), 128,
+                                         (size_t)128 * C * sizeof(T), st>>>(f, y, n, C, pi, g, yh);
+  else
+    softmax_stats_kernel<T, CMAX><<<(unsigned)((n + 127) / 128), 128, 0, st>>>(f, y, n, C, pi, g,
+                                                                                 yh);
   NCGP_LAUNCHED();
   return NCGP_OK;
 }
