@@ -483,9 +483,13 @@ __device__ __forceinline__ void transform_chunk(const uint32_t (&r)[32], float L
   }
 }
 
-template <int FAM, int WP, bool DBG, bool SYM>
+// ATM (symmetric kernel, WP = 16, large D): the row tile lives in TMEM (the
+// drain warps load it per item; GEMM1 becomes a TS MMA), which frees its
+// shared memory for the two P buffers.
+template <int FAM, int WP, bool DBG, bool SYM, bool ATM = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     kop_tc_kernel(const TcParams p) {
+  static_assert(!ATM || (SYM && WP == 16), "row tile in TMEM: symmetric kernel, WP = 16");
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -494,7 +498,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   // S/P buffers in TMEM.  The symmetric kernel double-buffers its O and D_T
   // accumulators (2 x 2 WP columns each): with WP = 32 that leaves room for
   // two S/P buffers only, with WP = 16 for three.
-  constexpr int NS = (SYM && WP == 32) ? 2 : NS_MAX;
+  constexpr int NS = (SYM && (WP == 32 || ATM)) ? 2 : NS_MAX;
 
   // ---- shared-memory carve-up (identical offsets in both CTAs)
   const uint32_t vslot = p.v2_bytes + p.v3_bytes;       // this CTA's V half
@@ -559,7 +563,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&a_land[b], 1);
-      mbar_init(&a_full[b], 2);
+      mbar_init(&a_full[b], ATM ? 8 : 2);  // ATM: 4 drain warps x 2 CTAs
       mbar_init(&a_empty[b], 1);
       mbar_init(&o_full[b], 1);
       mbar_init(&o_empty[b], 8);
@@ -595,6 +599,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   auto tS = [&](int b) -> uint32_t { return tmem + (uint32_t)(b * BN); };
   auto tO = [&](int b) -> uint32_t { return tmem + (uint32_t)(NS * BN + b * 2 * WP); };
   auto tDT = [&](uint32_t b) -> uint32_t { return tmem + (uint32_t)(NS * BN + 4 * WP) + b * 2u * WP; };
+  const uint32_t tA = tmem + (uint32_t)(NS * BN + 8 * WP);  // ATM: row tile, ka / 2 columns
   constexpr uint32_t NO = 2u;  // O buffers
   const int64_t half_off = (int64_t)rank * p.rec_bytes;   // this CTA's half of a record
 
@@ -631,7 +636,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       sr.init(NR);
       uint32_t nitem = 0, g = 0;
       while (ti.valid) {
-        if (is_x && ti.first_in_item()) {
+        if (!ATM && is_x && ti.first_in_item()) {
           const uint32_t ab = p.na == 2 ? (nitem & 1u) : 0u;
           const uint32_t aph = p.na == 2 ? ((nitem >> 1) & 1u) : (nitem & 1u);
           mbar_wait(&a_empty[ab], aph ^ 1u);
@@ -685,7 +690,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       rr.init(NR);
       uint32_t nitem = 0, g = 0;
       while (ti.valid) {
-        if (is_x && ti.first_in_item()) {
+        if (!ATM && is_x && ti.first_in_item()) {
           const uint32_t ab = p.na == 2 ? (nitem & 1u) : 0u;
           const uint32_t aph = p.na == 2 ? ((nitem >> 1) & 1u) : (nitem & 1u);
           mbar_wait(&a_land[ab], aph);
@@ -768,7 +773,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           const uint64_t da = dA0 + ab * astep;
           const uint32_t d = tmem + s1 * (uint32_t)BN;
           if (elect_one()) {
-            if (!(DBG && (p.debug_mode == 3 || p.debug_mode == 6)))
+            if (ATM)  // A = this CTA's row tile in TMEM (8 columns per K step of 16)
+              for (int k = 0; k < ksteps1; ++k)
+                mma_ts(d, tA + 8u * k, dx + (uint64_t)(16 * k), id1, k > 0);
+            else if (!(DBG && (p.debug_mode == 3 || p.debug_mode == 6)))
               for (int k = 0; k < ksteps1; ++k)
                 mma_ss(d, da + (uint64_t)(16 * k), dx + (uint64_t)(16 * k), id1, k > 0);
             tc_commit2(&s_full[c1]);  // also releases XB / V slots (see producers)
@@ -869,7 +877,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           // With two S buffers, T(g) enters the tensor pipe after GEMM1(g + 2):
           // the GEMM2 -> GEMM1 -> epilogue chain must not queue behind the
           // transposed product (three buffers leave enough slack without it)
-          if ((NS == 2) != ((p.sym_dbg & 64) != 0))
+          // (not with the row tile in TMEM: GEMM1 of an item's first tile
+          // waits for the drain warps' A load, which comes after they drained
+          // this tile's D_T -- holding T(g) for it would close a cycle)
+          if (!ATM && (NS == 2) != ((p.sym_dbg & 64) != 0))
             while (*g1_cnt < gt + (uint32_t)NS + 1u) {
             }
           tc_fence_after();
@@ -1040,7 +1051,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         if (lane == 0) bulk_wait_read();
         __syncwarp();
       };
+      uint32_t aitem = 0;
       while (ti.valid) {
+        if (ATM && ti.first_in_item()) {
+          // this CTA's row tile into TMEM: row = lane, 16-byte K chunk q of the
+          // canonical K-major pack -> columns 4q .. 4q + 3; once GEMM1 of the
+          // previous item is done with it (a_empty), then a_full on the leader
+          mbar_wait(&a_empty[0], (aitem & 1u) ^ 1u);
+          tc_fence_after();
+          const int64_t rt = p.rt0 + 2 * (int64_t)ti.cur.pp + rank;
+          const int r = 32 * wq + lane;
+          const uint8_t* src = p.xa_pack + rt * (int64_t)p.a_bytes + (size_t)(r >> 3) * (p.ka / 8) * 128 +
+                               (size_t)(r & 7) * 16;
+          for (int q = 0; q < p.ka / 8; ++q) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + (size_t)q * 128));
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                             tA + lane_off + 4u * q),
+                         "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w));
+          }
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(leader_addr(&a_full[0]));
+          ++aitem;
+        }
         if (ti.transposed()) {
           mbar_wait(&dt_full[dtq & 1u], (dtq >> 1) & 1u);
           tc_fence_after();
@@ -2082,6 +2116,13 @@ size_t smem_bytes(uint32_t a_bytes, int wp, int na, int sx, int sv, int sym_npb 
          (6 + 9 + 2 + NS_MAX + 5 * NR + 8 + 12) * sizeof(uint64_t) + 16 + 1024;
 }
 
+// The pair kernel with its row tile in TMEM (large D, WP = 16).  NCGP_SYM_ATM=0
+// disables it.
+bool atm_allowed() {
+  const char* e = getenv("NCGP_SYM_ATM");
+  return !(e != nullptr && e[0] == '0');
+}
+
 // Which symmetric kernel a full-range apply of width w runs: 0 none (the
 // plain kernel), 1 the pair kernel, 2 the single-CTA kernel.
 int sym_variant(const ncgp_kop* op, int w) {
@@ -2091,6 +2132,9 @@ int sym_variant(const ncgp_kop* op, int w) {
   const uint32_t a_bytes = (uint32_t)(BM * op->ka * 2);
   if (op->sym_cg == 1) return smem1_bytes(a_bytes, wp, 2, 2, 1) <= SMEM_MAX ? 2 : 0;
   if (smem_bytes(a_bytes, wp, 1, 3, 3, 2) <= (size_t)SMEM_BUDGET) return 1;
+  if (wp == 16 && atm_allowed() && op->ka <= 2 * 128 &&
+      smem_bytes(a_bytes, wp, 0, 3, 3, 2) <= (size_t)SMEM_BUDGET)
+    return 1;
   if (op->family == NCGP_MATERN32 && smem_bytes(a_bytes, wp, 1, 3, 3, 1) <= (size_t)SMEM_BUDGET) return 1;
   const char* e = getenv("NCGP_SYM_NPB");
   if (e != nullptr && atoi(e) == 1 && smem_bytes(a_bytes, wp, 1, 3, 3, 1) <= (size_t)SMEM_BUDGET) return 1;
@@ -2347,7 +2391,9 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
   if (sym) {
     // two P buffers with the deepest rings that fit, else one P buffer
     // (large D: the row tile and XB ring outgrow the 227 KB)
+    // (npb, na, sx, sv); na = 0: the row tile lives in TMEM (ATM, WP = 16)
     const int cand[][4] = {{2, 1, 6, 6}, {2, 1, 3, 6}, {2, 1, 3, 5}, {2, 1, 3, 4}, {2, 1, 3, 3},
+                           {2, 0, 3, 6}, {2, 0, 3, 4}, {2, 0, 3, 3},
                            {1, 1, 3, 6}, {1, 1, 3, 4}, {1, 1, 3, 3}};
     const char* e = getenv("NCGP_SYM_NPB");  // experiments: force 1 or 2 P buffers
     const int force = e != nullptr ? atoi(e) : 0;
@@ -2356,6 +2402,7 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
       // one P buffer serialises the two epilogue groups on it: a 1.15x gain
       // for Matern-3/2 at D = 50 but a loss for RBF (tools/sym_exp.py)
       if ((force == c[0] || (force == 0 && (c[0] == 2 || op->family == NCGP_MATERN32))) &&
+          (c[1] > 0 || (wp == 16 && atm_allowed())) &&
           smem_bytes(p.a_bytes, wp, c[1], c[2], c[3], c[0]) <= (size_t)SMEM_BUDGET) {
         p.npb = c[0];
         p.na = c[1];
@@ -2389,7 +2436,10 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
       return NCGP_OK;
     };
     int rc;
-    if (dbg)  // per-tile trace of cluster 0 (tools/trace_sym.py)
+    if (p.na == 0)  // row tile in TMEM
+      rc = op->family == NCGP_RBF ? launch(kop_tc_kernel<NCGP_RBF, 16, false, true, true>)
+                                  : launch(kop_tc_kernel<NCGP_MATERN32, 16, false, true, true>);
+    else if (dbg)  // per-tile trace of cluster 0 (tools/trace_sym.py)
       rc = op->family == NCGP_RBF
                ? (wp == 16 ? launch(kop_tc_kernel<NCGP_RBF, 16, true, true>)
                            : launch(kop_tc_kernel<NCGP_RBF, 32, true, true>))

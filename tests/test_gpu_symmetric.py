@@ -156,7 +156,8 @@ def test_symmetric_kernel_single_p_buffer(n, d, w, fam, force):
     """One shared P buffer: each epilogue group waits for the other group's
     previous tile (pt_free barriers alternate by tile parity)."""
     X, V, op, Vd = _case(n, d, w, (fam, 3.0, 1.0), 13, cg=2)
-    env = {"NCGP_SYM": 1, "NCGP_SYM_NPB": force} if force else {}
+    # (at D = 50 the default is the row tile in TMEM with two P buffers)
+    env = {"NCGP_SYM": 1, "NCGP_SYM_NPB": force} if force else {"NCGP_SYM_ATM": 0}
     with _Env(**env):
         got = op.apply(Vd).double()
     assert op.last_variant_code == 1
@@ -240,5 +241,29 @@ def test_symmetric_default_shapes_sweep(n, d, w, fam):
     with _Env(NCGP_SYM=0):
         plain = op.apply(Vd).double()
         scale = op.apply(Vd.abs()).double()  # K |V|: the entry scale
+    assert float((got - plain).norm() / plain.norm()) < 2e-5
+    assert float(((got - plain).abs() / scale).max()) < 1e-5
+
+
+@pytest.mark.parametrize("n,d,w,fam,item", [
+    (70001, 50, 10, "rbf", None),
+    (70001, 50, 10, "matern32", None),
+    (70001, 40, 3, "rbf", None),
+    (3000, 50, 16, "rbf", 3),      # many items per cluster: the row tile is reloaded into TMEM
+    (9000, 52, 7, "matern32", 5),  # D = 52: K = 160, 80 TMEM columns (D >= 56 does not fit)
+])
+def test_symmetric_row_tile_in_tmem(n, d, w, fam, item):
+    """Pair kernel with its row tile in TMEM (large D, WP = 16): GEMM1 reads
+    A from TMEM, the drain warps load it per item."""
+    env = {"NCGP_SYM": 1}
+    if item:
+        env["NCGP_SYM_ITEM"] = item
+    with _Env(**env):
+        X, V, op, Vd = _case(n, d, w, (fam, 4.0, 1.0), n + d, cg=2)
+        got = op.apply(Vd).double()
+        assert op.last_variant_code == 1
+    with _Env(NCGP_SYM=0):
+        plain = op.apply(Vd).double()
+        scale = op.apply(Vd.abs()).double()
     assert float((got - plain).norm() / plain.norm()) < 2e-5
     assert float(((got - plain).abs() / scale).max()) < 1e-5
