@@ -376,7 +376,8 @@ def run_ours(args, rank, world, local_rank):
                 "config": {"workload": c["name"], "n": n, "d": d, "w": w, "kernel": list(spec),
                            "flops_per_pair": F, "exp_per_pair": E,
                            "l2": "flushed (256 MiB write) before every timed step",
-                           "parallelism": f"row-sharded x{world}",
+                           "parallelism": (f"symmetric work list split x{world}" if reduce_
+                                           else f"row-sharded x{world}"),
                            "gather": gather if world > 1 else None},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clocks}
@@ -453,7 +454,9 @@ def run_fit(args, rank, world, local_rank):
             "config": {"workload": args.workload, "n": int(c["X"].shape[0]), "C": C,
                        "kernel": list(c["kernel"]), "schedule": [c["steps"], c["inner"]],
                        "rank": c["rank"], "residual": args.residual,
-                       "parallelism": f"row-sharded x{world}",
+                       "parallelism": (f"symmetric work list split x{world}"
+                                       if op is not None and op.gather == "reduce"
+                                       else f"row-sharded x{world}"),
                        "gather": op.gather if op is not None else None},
             "kernel_matvecs": trace.total_kernel_matvecs,
             "inner_iters": [s.inner_iterations for s in trace.steps],
