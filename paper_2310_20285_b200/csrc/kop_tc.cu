@@ -2044,9 +2044,11 @@ int sym_cg(int d, int w_max) {
   const char* e = getenv("NCGP_SYM_CG");
   if (e != nullptr && (e[0] == '1' || e[0] == '2')) return e[0] - '0';
   const uint32_t a = (uint32_t)(BM * ka_of(d) * 2);
-  // at least a 3-deep XB ring (D = 24 with a 2-deep one ran slower than the
-  // plain kernel; the pair kernel keeps 3)
-  if (smem1_bytes(a, wp_of(w_max), 3, 2, 2) <= SMEM_MAX) return 1;
+  // rings no shallower than (XB 2, V 4) or (XB 3, V 2): D = 24 at WP = 16
+  // only fits (2, 3), which ran slower than the plain kernel; the pair kernel
+  // keeps 3-deep rings there
+  const int wpm = wp_of(w_max);
+  if (smem1_bytes(a, wpm, 2, 4, 2) <= SMEM_MAX || smem1_bytes(a, wpm, 3, 2, 2) <= SMEM_MAX) return 1;
   const char* f = getenv("NCGP_SYM1_NPB");  // experiments: one-P-buffer single-CTA kernel
   if (f != nullptr && f[0] == '1' && smem1_bytes(a, wp_of(w_max), 2, 2, 1) <= SMEM_MAX) return 1;
   return 2;
@@ -2343,7 +2345,7 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
   float* const sym_acc = part != nullptr ? part->acc : op->sym_acc;
   const bool sym_fin = part == nullptr;
   if (sym && op->sym_cg == 1) {
-    const int cand[][2] = {{3, 6}, {3, 4}, {3, 3}, {3, 2}, {2, 4}, {2, 3}, {2, 2}};
+    const int cand[][2] = {{3, 6}, {3, 4}, {3, 3}, {2, 4}, {3, 2}, {2, 3}, {2, 2}};
     bool fit = false;
     for (int npb = 2; npb >= 1 && !fit; --npb)
       for (auto& c : cand)
