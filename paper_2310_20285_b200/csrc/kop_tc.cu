@@ -1497,7 +1497,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
       Ring rr;
       rr.init(NR);
       uint32_t g = 0, nitem = 0, dtq = 0;
-      const bool hold = !(p.sym_dbg & 64);
+      // Holding T(g) behind GEMM1(g + 2) (as the pair kernel does at WP = 32)
+      // costs 5 % at cfg3 here (one box, interleaved: 316 vs 300 ms) and is
+      // neutral for Matern and at WP = 16: off unless sym_dbg bit 64.
+      const bool hold = (p.sym_dbg & 64) != 0;
       while (ti.valid) {
         if (ti.first_in_item()) {  // this row tile's V block (the transposed product's B)
           mbar_wait(vi_empty, (nitem & 1u) ^ 1u);
@@ -1515,7 +1518,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
         if (lane == 0) trace_ev<DBG>(p, g, 12);
         const bool tp = ti.transposed();
         if (tp) mbar_wait(&dt_empty[dtq & 1u], ((dtq >> 1) & 1u) ^ 1u);
-        if (hold)  // T(g) behind GEMM1(g + 2) in the in-order tensor pipe
+        if (hold)  // T(g) behind GEMM1(g + NS1) in the in-order tensor pipe
           while (*g1_cnt < g + (uint32_t)NS1 + 1u) {
           }
         tc_fence_after();
