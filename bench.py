@@ -268,6 +268,9 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms, kern_total = float(t[0]), float(t[1])
+    if os.environ.get("NCGP_BENCH_RANK_REPORT"):  # per-rank kernel time (tools/fake_dist_bench.py)
+        print(json.dumps({"rank": rank, "kernel_ms": round(kern_total / args.steps, 3)}),
+              file=sys.stderr, flush=True)
     pairs = float(n) * float(n)
     value = F * pairs * args.steps / (total_ms / 1e3) / 1e9
 
