@@ -89,6 +89,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifndef NCGP_SYM1_NS16
+#define NCGP_SYM1_NS16 3  // K1-sym1 S buffers at WP = 16 (build-time A/B: 2 or 3)
+#endif
 #ifndef NCGP_WAIT_MODE
 #define NCGP_WAIT_MODE 0  // 0: try_wait + suspend hint, 1: try_wait (default limit), 2: test_wait spin
 #endif
@@ -1275,7 +1278,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
   const int lane = threadIdx.x & 31;
   // S buffers next to double-buffered O and D_T (2 x 2 WP columns each):
   // two at WP = 32, three at WP = 16
-  constexpr int NS1 = WP == 16 ? 3 : 2;
+  constexpr int NS1 = WP == 16 ? NCGP_SYM1_NS16 : 2;
   const uint32_t xb_bytes = 2u * p.xbh_bytes;  // 128 XB rows
   const uint32_t vb_bytes = 2u * p.v2_bytes;   // [Vhi | Vlo]: 2 WP rows
   uint8_t* sA = smem;
