@@ -331,7 +331,7 @@ def run_ours(args, rank, world, local_rank):
     # DRAM traffic of the same kernel variant on the same workload, from the
     # committed ncu --set full capture (profiles/*_summary.json)
     traffic, traffic_src = None, None
-    captures = {("cfg3", 2): "r01g_summary.json", ("cfg3", 0): "r01e_summary.json"}
+    captures = {("cfg3", 2): "r01i_summary.json", ("cfg3", 0): "r01e_summary.json"}
     prof = captures.get((c["name"], op.last_variant_code))
     if prof and world == 1 and os.path.exists(os.path.join(ROOT, "profiles", prof)):
         with open(os.path.join(ROOT, "profiles", prof)) as fh:
