@@ -107,23 +107,81 @@ int ncgp_kop_apply_multi(ncgp_kop* op, const void* V, int64_t ldv, int w,
                          void* const* outs, int n_out, int64_t ldo,
                          int64_t row_begin, int64_t row_end, void* stream);
 
+/* Fused epilogue of an apply (SURVEY.md 2.3, K1 "optional epilogues"):
+ *
+ *   out  = alpha * (K V) + beta * base + gamma * (W^-1 V)
+ *   out2 = K V                                   (optional raw product)
+ *
+ * evaluated per output row inside K1's reduction pass, so the Newton-step
+ * operator K^ = K + W^-1 (W^+ for softmax) is applied without a second pass
+ * over K V.  It replaces, in one call,
+ *   - t = apply_kernel(s); z = t + apply_noise(s)          solver.py:262,265
+ *     (alpha 1, gamma 1, out2 = t),
+ *   - r = rhs - apply_kernel(v) - apply_noise(v)            solver.py:249
+ *     (alpha -1, beta 1, base = rhs, gamma -1),
+ *   - f = prior_matvec(w) + m                               outer.py:134-137
+ *     (alpha 1, beta 1, base = m, out2 = g = K w).
+ * noise = NCGP_NOISE_SOFTMAX: W^+ from the cached probabilities pi (n_rows,
+ * w) row-major (softmax_pinv_apply, likelihoods.py:291-310; w = C);
+ * NCGP_NOISE_DIAG: diagonal W^-1 d (n_rows * w, CN), e.g. Bernoulli
+ * (likelihoods.py:210-212) or Gaussian noise variances (likelihoods.py:109).
+ * The noise term needs V's row i next to output row i, so it is only valid
+ * for square operators (K(X, X)).  base / out2 / noise_state are indexed by
+ * the apply's global rows with strides ldb / ld2 (noise_state dense).
+ * A NULL epilogue is the plain product (alpha 1, nothing else). */
+enum { NCGP_NOISE_NONE = 0, NCGP_NOISE_SOFTMAX = 1, NCGP_NOISE_DIAG = 2 };
+typedef struct ncgp_kop_epilogue {
+  double alpha, beta, gamma;
+  const void* base;        /* NULL: beta ignored */
+  int64_t ldb;
+  int noise;               /* NCGP_NOISE_*; NONE: gamma ignored */
+  const void* noise_state; /* pi (softmax) or d (diagonal) */
+  void* out2;              /* NULL: no raw copy */
+  int64_t ld2;
+} ncgp_kop_epilogue;
+
+int ncgp_kop_apply_ex(ncgp_kop* op, const void* V, int64_t ldv, int w,
+                      void* out, int64_t ldo, int64_t row_begin,
+                      int64_t row_end, const ncgp_kop_epilogue* epi,
+                      void* stream);
+
 /* The symmetric K(X, X) kernel split across `nparts` processes (SURVEY.md
  * 8(e); no reference counterpart: the reference has no multi-GPU path).
- * ncgp_kop_sym_acc_elems: fp32 elements of the per-process accumulator for
+ *
+ * The symmetric kernels accumulate in int64 fixed point (2^-F resolution in
+ * the kernel's scaled domain, F fixed by n): integer addition is associative,
+ * so the product is bitwise identical run to run, for any CTA schedule and
+ * for any number of parts -- the property the reference pins with its
+ * tile-size invariance (gp.py:144-172 "bit-identical for any tile size",
+ * test_gp.py:106-110).
+ *
+ * ncgp_kop_sym_acc_elems: int64 elements of the per-process accumulator for
  * RHS width w, or 0 when a full apply of width w would not use a symmetric
  * kernel (rectangular operator, too small, or the shape does not fit); the
  * caller then row-shards with row_begin / row_end.
  * ncgp_kop_sym_partial: part `part` of `nparts` slices of the triangular work
- * list (equal tile counts) into `acc` (zeroed first, on `stream`).  The sum
- * of all parts' acc is the full product in a padded, swizzled layout; the
- * caller sums them (an all-reduce) and calls ncgp_kop_sym_finalize to write
- * the (n_rows, w) product with row stride ldo.  Errors: NCGP_UNSUPPORTED
- * when ncgp_kop_sym_acc_elems is 0. */
+ * list (equal tile counts) into `acc` (acc_elems >= ncgp_kop_sym_acc_elems;
+ * zeroed first, on `stream`).  The integer sum of all parts' acc (an
+ * all-reduce with int64 SUM) is the full product in a padded, swizzled
+ * layout; ncgp_kop_sym_finalize writes the (n_rows, w) product with row
+ * stride ldo through the epilogue (V: the operand, needed only for a noise
+ * term; epi may be NULL).  Errors: NCGP_UNSUPPORTED when
+ * ncgp_kop_sym_acc_elems is 0, NCGP_DIMENSION_MISMATCH when acc_elems is
+ * too small. */
 int64_t ncgp_kop_sym_acc_elems(const ncgp_kop* op, int w);
 int ncgp_kop_sym_partial(ncgp_kop* op, const void* V, int64_t ldv, int w, int part,
-                         int nparts, float* acc, void* stream);
-int ncgp_kop_sym_finalize(ncgp_kop* op, const float* acc, int w, void* out, int64_t ldo,
-                          void* stream);
+                         int nparts, int64_t* acc, int64_t acc_elems, void* stream);
+int ncgp_kop_sym_finalize(ncgp_kop* op, const int64_t* acc, int64_t acc_elems,
+                          const void* V, int64_t ldv, int w, void* out, int64_t ldo,
+                          const ncgp_kop_epilogue* epi, void* stream);
+
+/* Symmetric-kernel policy of an operator (no reference counterpart): -1 the
+ * default size policy, 0 always the plain tiled kernel, 1 a symmetric kernel
+ * whenever one fits (K(X, X) launches over all rows).  Both give correct
+ * products; the plain kernel's fp64-flushed rows and the symmetric kernels'
+ * int64 sums are each bitwise reproducible, but they differ from each other
+ * in the last bits.  The initial mode comes from NCGP_SYM (read at creation). */
+int ncgp_kop_set_sym(ncgp_kop* op, int mode);
 
 /* Actual implementation chosen (NCGP_KOP_TCGEN05 or NCGP_KOP_SIMT). */
 int ncgp_kop_impl(const ncgp_kop* op);
@@ -166,6 +224,13 @@ int ncgp_softmax_w(int dtype, const void* pi, int64_t n, int C,
 int ncgp_bernoulli_stats(int dtype, const void* f, const int64_t* labels,
                          int64_t n, void* winv, void* w, void* grad,
                          void* yhat, void* stream);
+
+/* Poisson log-link statistics (likelihoods.py:174-182, outer.py:129-131):
+ * w = exp(f), winv = exp(-f), grad = y - exp(f), yhat = f + winv * grad;
+ * counts in the working dtype.  Any output may be NULL. */
+int ncgp_poisson_stats(int dtype, const void* f, const void* counts, int64_t n,
+                       void* winv, void* w, void* grad, void* yhat,
+                       void* stream);
 
 /* out[:, b] = beta * base[:, b] + alpha * diag(dvec) V[:, b]
  * (_apply_diag likelihoods.py:149-153). */

@@ -21,6 +21,19 @@ RBF, MATERN32 = 0, 1
 KOP_AUTO, KOP_TCGEN05, KOP_SIMT = 0, 1, 2
 
 
+NOISE_NONE, NOISE_SOFTMAX, NOISE_DIAG = 0, 1, 2
+
+
+class Epilogue(ctypes.Structure):
+    """``ncgp_kop_epilogue`` (include/ncgp_b200.h)."""
+
+    _fields_ = [("alpha", ctypes.c_double), ("beta", ctypes.c_double),
+                ("gamma", ctypes.c_double), ("base", ctypes.c_void_p),
+                ("ldb", ctypes.c_int64), ("noise", ctypes.c_int),
+                ("noise_state", ctypes.c_void_p), ("out2", ctypes.c_void_p),
+                ("ld2", ctypes.c_int64)]
+
+
 class NativeUnavailable(NcgpError, RuntimeError):
     """The CUDA library could not be loaded (not built, or no GPU)."""
 
@@ -50,17 +63,22 @@ _SIGS = {
     "ncgp_kop_apply": (_i32, [_vp, _vp, _i64, _i32, _vp, _i64, _i64, _i64, _vp]),
     "ncgp_kop_apply_multi": (_i32, [_vp, _vp, _i64, _i32, ctypes.POINTER(_vp), _i32, _i64, _i64,
                                     _i64, _vp]),
+    "ncgp_kop_apply_ex": (_i32, [_vp, _vp, _i64, _i32, _vp, _i64, _i64, _i64,
+                                 ctypes.POINTER(Epilogue), _vp]),
     "ncgp_kop_impl": (_i32, [_vp]),
+    "ncgp_kop_set_sym": (_i32, [_vp, _i32]),
     "ncgp_kop_last_variant": (_i32, [_vp]),
     "ncgp_kop_sym_acc_elems": (_i64, [_vp, _i32]),
-    "ncgp_kop_sym_partial": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp]),
-    "ncgp_kop_sym_finalize": (_i32, [_vp, _vp, _i32, _vp, _i64, _vp]),
+    "ncgp_kop_sym_partial": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _i64, _vp]),
+    "ncgp_kop_sym_finalize": (_i32, [_vp, _vp, _i64, _vp, _i64, _i32, _vp, _i64,
+                                     ctypes.POINTER(Epilogue), _vp]),
     "ncgp_kop_destroy": (_i32, [_vp]),
     "ncgp_softmax_stats": (_i32, [_i32, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp]),
     "ncgp_softmax_winv": (_i32, [_i32, _vp, _i64, _i32, _vp, _i64, _i32, _vp, _i64, _f64, _f64,
                                  _vp, _i64, _vp]),
     "ncgp_softmax_w": (_i32, [_i32, _vp, _i64, _i32, _vp, _i64, _i32, _vp, _i64, _vp]),
     "ncgp_bernoulli_stats": (_i32, [_i32, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
+    "ncgp_poisson_stats": (_i32, [_i32, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
     "ncgp_diag_apply": (_i32, [_i32, _vp, _i64, _vp, _i64, _i32, _vp, _i64, _f64, _f64, _vp,
                                _i64, _vp]),
     "ncgp_reduce_workspace_bytes": (_sz, [_i64, _i32]),

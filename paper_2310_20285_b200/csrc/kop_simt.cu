@@ -151,6 +151,21 @@ __global__ void reduce_splits_kernel(const double* __restrict__ partial, int spl
     if (k < out.n) out.p[k][i * ldo + c] = (T)s;
 }
 
+// the same fixed-order split sum, one thread per row, through the epilogue
+template <typename T>
+__global__ void reduce_splits_epi_kernel(const double* __restrict__ partial, int splits,
+                                         int64_t nloc, int w, const EpiDev e,
+                                         const ncgp::OutPtrs<T> out, int64_t ldo) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nloc) return;
+  auto kv = [&](int c) -> double {
+    double s = 0.0;
+    for (int p = 0; p < splits; ++p) s += partial[((int64_t)p * nloc + i) * w + c];
+    return s;
+  };
+  ncgp::epi_row<T, NCGP_MAX_OUTS>(e, i, w, kv, out.p, out.n, ldo);
+}
+
 int pick_wt(int w) { return w <= 1 ? 1 : (w <= 4 ? 4 : (w <= 16 ? 16 : 32)); }
 int pick_dmax(int d) { return d <= 8 ? 8 : (d <= 16 ? 16 : (d <= 32 ? 32 : 64)); }
 
@@ -168,7 +183,7 @@ int plan_splits(int64_t nloc, int64_t nc, int zs, int sms) {
 
 template <typename T, int FAM, int DMAX, int WT>
 int launch_t(ncgp_kop* op, const T* Xr, int64_t nloc, const T* V, int64_t ldv, int w,
-             const ncgp::OutPtrs<T>& out, int64_t ldo, cudaStream_t st) {
+             const ncgp::OutPtrs<T>& out, int64_t ldo, cudaStream_t st, const EpiDev& epi) {
   const int zs = (w + WT - 1) / WT;
   // planned on the full row count: row shards reduce in the same order
   const int splits = plan_splits(op->n_rows, op->n_cols, zs, op->sms);
@@ -190,41 +205,46 @@ int launch_t(ncgp_kop* op, const T* Xr, int64_t nloc, const T* V, int64_t ldv, i
   kop_simt_kernel<T, FAM, DMAX, WT><<<grid, BR, 0, st>>>(
       Xr, nloc, static_cast<const T*>(op->Xc), op->n_cols, op->d, V, ldv, w, cps, partial, kf);
   NCGP_LAUNCHED();
-  const int64_t tot = nloc * w;
-  reduce_splits_kernel<T><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(partial, splits, nloc,
-                                                                           w, out, ldo);
+  if (epi.active) {
+    reduce_splits_epi_kernel<T><<<(unsigned)((nloc + 127) / 128), 128, 0, st>>>(
+        partial, splits, nloc, w, epi, out, ldo);
+  } else {
+    const int64_t tot = nloc * w;
+    reduce_splits_kernel<T><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(partial, splits,
+                                                                             nloc, w, out, ldo);
+  }
   NCGP_LAUNCHED();
   return NCGP_OK;
 }
 
 template <typename T, int FAM, int DMAX>
 int dispatch_wt(ncgp_kop* op, const T* Xr, int64_t nloc, const T* V, int64_t ldv, int w,
-                const ncgp::OutPtrs<T>& out, int64_t ldo, cudaStream_t st) {
+                const ncgp::OutPtrs<T>& out, int64_t ldo, cudaStream_t st, const EpiDev& e) {
   switch (pick_wt(w)) {
-    case 1: return launch_t<T, FAM, DMAX, 1>(op, Xr, nloc, V, ldv, w, out, ldo, st);
-    case 4: return launch_t<T, FAM, DMAX, 4>(op, Xr, nloc, V, ldv, w, out, ldo, st);
-    case 16: return launch_t<T, FAM, DMAX, 16>(op, Xr, nloc, V, ldv, w, out, ldo, st);
-    default: return launch_t<T, FAM, DMAX, 32>(op, Xr, nloc, V, ldv, w, out, ldo, st);
+    case 1: return launch_t<T, FAM, DMAX, 1>(op, Xr, nloc, V, ldv, w, out, ldo, st, e);
+    case 4: return launch_t<T, FAM, DMAX, 4>(op, Xr, nloc, V, ldv, w, out, ldo, st, e);
+    case 16: return launch_t<T, FAM, DMAX, 16>(op, Xr, nloc, V, ldv, w, out, ldo, st, e);
+    default: return launch_t<T, FAM, DMAX, 32>(op, Xr, nloc, V, ldv, w, out, ldo, st, e);
   }
 }
 
 template <typename T, int FAM>
 int dispatch_d(ncgp_kop* op, const T* Xr, int64_t nloc, const T* V, int64_t ldv, int w,
-               const ncgp::OutPtrs<T>& out, int64_t ldo, cudaStream_t st) {
+               const ncgp::OutPtrs<T>& out, int64_t ldo, cudaStream_t st, const EpiDev& e) {
   switch (pick_dmax(op->d)) {
-    case 8: return dispatch_wt<T, FAM, 8>(op, Xr, nloc, V, ldv, w, out, ldo, st);
-    case 16: return dispatch_wt<T, FAM, 16>(op, Xr, nloc, V, ldv, w, out, ldo, st);
-    case 32: return dispatch_wt<T, FAM, 32>(op, Xr, nloc, V, ldv, w, out, ldo, st);
-    default: return dispatch_wt<T, FAM, 64>(op, Xr, nloc, V, ldv, w, out, ldo, st);
+    case 8: return dispatch_wt<T, FAM, 8>(op, Xr, nloc, V, ldv, w, out, ldo, st, e);
+    case 16: return dispatch_wt<T, FAM, 16>(op, Xr, nloc, V, ldv, w, out, ldo, st, e);
+    case 32: return dispatch_wt<T, FAM, 32>(op, Xr, nloc, V, ldv, w, out, ldo, st, e);
+    default: return dispatch_wt<T, FAM, 64>(op, Xr, nloc, V, ldv, w, out, ldo, st, e);
   }
 }
 
 template <typename T>
 int dispatch_fam(ncgp_kop* op, const T* Xr, int64_t nloc, const T* V, int64_t ldv, int w,
-                 const ncgp::OutPtrs<T>& out, int64_t ldo, cudaStream_t st) {
+                 const ncgp::OutPtrs<T>& out, int64_t ldo, cudaStream_t st, const EpiDev& e) {
   if (op->family == NCGP_RBF)
-    return dispatch_d<T, NCGP_RBF>(op, Xr, nloc, V, ldv, w, out, ldo, st);
-  return dispatch_d<T, NCGP_MATERN32>(op, Xr, nloc, V, ldv, w, out, ldo, st);
+    return dispatch_d<T, NCGP_RBF>(op, Xr, nloc, V, ldv, w, out, ldo, st, e);
+  return dispatch_d<T, NCGP_MATERN32>(op, Xr, nloc, V, ldv, w, out, ldo, st, e);
 }
 
 }  // namespace
@@ -246,7 +266,7 @@ size_t simt_workspace_bytes(int dtype, int64_t n_rows, int64_t n_cols, int d, in
 }
 
 int simt_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out, int64_t ldo,
-               int64_t r0, int64_t r1, cudaStream_t st) {
+               int64_t r0, int64_t r1, cudaStream_t st, const EpiDev& epi) {
   NCGP_CHECK_ARG(op->d <= 64, NCGP_UNSUPPORTED, "CUDA-core operator supports d <= 64 (got %d)",
                  op->d);
   const int64_t nloc = r1 - r0;
@@ -254,11 +274,11 @@ int simt_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& ou
   if (op->dtype == NCGP_F64) {
     const double* Xr = static_cast<const double*>(op->Xr) + r0 * op->d;
     return dispatch_fam<double>(op, Xr, nloc, static_cast<const double*>(V), ldv, w,
-                                out_ptrs<double>(out, r0, ldo), ldo, st);
+                                out_ptrs<double>(out, r0, ldo), ldo, st, epi);
   }
   const float* Xr = static_cast<const float*>(op->Xr) + r0 * op->d;
   return dispatch_fam<float>(op, Xr, nloc, static_cast<const float*>(V), ldv, w,
-                             out_ptrs<float>(out, r0, ldo), ldo, st);
+                             out_ptrs<float>(out, r0, ldo), ldo, st, epi);
 }
 
 }  // namespace ncgp

@@ -290,6 +290,19 @@ __device__ __forceinline__ void bulk_reduce_add_f32(float* gdst, uint32_t ssrc, 
 __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
+// all but the most recent bulk group have finished reading shared memory
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+// TMA bulk reduction shared -> global (u64 add: two's-complement int64 sums)
+__device__ __forceinline__ void bulk_reduce_add_u64(unsigned long long* gdst, uint32_t ssrc,
+                                                    uint32_t bytes) {
+  asm volatile(
+      "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.u64 [%0], [%1], %2;\n\t"
+      "cp.async.bulk.commit_group;" ::"l"(gdst),
+      "r"(ssrc), "r"(bytes)
+      : "memory");
+}
 __device__ __forceinline__ void bulk_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
@@ -356,14 +369,19 @@ struct TcParams {
   long long* trace;      // debug: per-tile timestamps of cluster 0 (nullptr in production)
   int n_items;           // work items: pairs * splits, or the symmetric item table's length
   const int4* item_tab;  // symmetric kernel: (row-tile pair, c0, c1, -) per item
-  float* acc;            // symmetric kernel: fp32 output accumulator [row][WP], zeroed
-  int sym_dbg;           // symmetric kernel debug bits (timing / diagnosis only): 1 = drop D_T
-                         // reductions, 2 = drop O reductions, 4 = no transposed MMAs,
-                         // 8 = no D_T loads, 16 = no P stores to shared memory;
-                         // variant (correct results): 64 = flip whether T(g) is held
-                         // back behind GEMM1(g + NS); 256 (single-CTA kernel) = drains by
-                         // red.global.add.v4 from registers; 128 (single-CTA kernel) = GEMM2
-                         // reads P from TMEM (TS), as measured slower
+  // symmetric kernel: int64 fixed-point accumulator [WP/8][acc_rows][8] (zeroed), the
+  // 8-column groups of 32 rows contiguous (2 KB, one bulk reduction each); an fp32
+  // partial x (kernel's scaled domain) adds round(x * fx), fx = 2^F
+  unsigned long long* acc;
+  int64_t acc_rows;
+  float fx;
+  int sym_dbg;           // symmetric kernel variant bits (correct results): 64 = flip whether
+                         // T(g) is held back behind GEMM1(g + NS); 128 (single-CTA kernel) =
+                         // GEMM2 reads P from TMEM (TS), as measured slower.  Debug
+                         // instantiations only (timing / diagnosis, wrong results): 1 = drop
+                         // D_T reductions, 2 = drop O reductions, 4 = no transposed MMAs,
+                         // 8 = no D_T loads, 16 = no P stores to shared memory
+  EpiDev epi;            // plain kernel, splits == 1: the apply's epilogue at the row store
   float* sym_dump;       // symmetric kernel debug: raw D_T per (pair, tile, rank) when set
   int npb;               // symmetric kernel: P buffers in shared memory (2, or 1 for large D)
   int debug_mode;        // debug (timing only, wrong results): 1 = epilogue skips TMEM traffic,
@@ -484,6 +502,45 @@ __device__ __forceinline__ void transform_chunk(const uint32_t (&r)[32], float L
     hi[i] = pack_h2(h0, h1);
     lo[i] = pack_h2(k0 - h0, k1 - h1);
   }
+}
+
+// Deterministic accumulation of the symmetric kernels.  Every flushed fp32
+// partial (O chunk or transposed tile, in the kernel's scaled domain) is
+// rounded to an int64 multiple of 2^-F and added to the global accumulator
+// with an integer bulk reduction.  Integer addition is associative and
+// commutative, so the sums do not depend on the order in which CTAs flush,
+// on the number of CTAs, or on how the work list is split across processes:
+// the product is bitwise reproducible (hard part 5) and 1-GPU
+// and N-GPU results are identical.  F = 33 - ceil(log2 n) keeps |sum| < 2^62
+// (|P V| < 2^28 per pair after the fp16 prescaling).
+// One call adds 8 columns (group h) of the warp's 32 rows (one per lane)
+// through a 2 KB staging block (row r at 64 r, 16-byte chunk k at
+// k ^ ((r >> 1) & 3): conflict-free stores); NBLK blocks per warp rotate.
+template <uint32_t NBLK>
+__device__ __forceinline__ void fx_flush8(const TcParams& p, uint32_t stg_warp, uint32_t& nst,
+                                          int lane, int h, const float (&v)[8], int64_t row0,
+                                          bool skip) {
+  if (lane == 0) {
+    if (NBLK == 2)
+      bulk_wait_read1();  // the block written two flushes ago has been read
+    else
+      bulk_wait_read();
+  }
+  __syncwarp();
+  const uint32_t blk = stg_warp + (nst & (NBLK - 1u)) * 2048u;
+  ++nst;
+  const uint32_t rowa = blk + (uint32_t)lane * 64u;
+  const uint32_t swz = (uint32_t)((lane >> 1) & 3);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const long long q0 = __float2ll_rn(v[2 * k] * p.fx);
+    const long long q1 = __float2ll_rn(v[2 * k + 1] * p.fx);
+    st_shared_v4(rowa + 16u * ((uint32_t)k ^ swz), (uint32_t)q0, (uint32_t)((unsigned long long)q0 >> 32),
+                 (uint32_t)q1, (uint32_t)((unsigned long long)q1 >> 32));
+  }
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0 && !skip) bulk_reduce_add_u64(p.acc + ((int64_t)h * p.acc_rows + row0) * 8, blk, 2048u);
 }
 
 // ATM (symmetric kernel, WP = 16, large D): the row tile lives in TMEM (the
@@ -889,7 +946,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           tc_fence_after();
           if (lane == 0) trace_ev<DBG>(p, gt, 13);
           if (elect_one()) {
-            if (tp && !(p.sym_dbg & 4)) {
+            if (tp && !(DBG && (p.sym_dbg & 4))) {
               const uint64_t pa = dP0 + (uint64_t)pbuf(gt) * (PBUF >> 4);
 #pragma unroll 1
               for (int m = 0; m < BN / 16; ++m) {
@@ -974,7 +1031,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 pt_wait = false;
                 if (tr) trace_ev<DBG>(p, gt, 8);
               }
-              if (!(p.sym_dbg & 16)) {
+              if (!(DBG && (p.sym_dbg & 16))) {
                 const uint32_t rowb = rowb0 + 512u * c;
 #pragma unroll
                 for (int g = 0; g < 4; ++g) {
@@ -1019,41 +1076,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
     const int row = 32 * wq + lane;
     if (SYM) {
-      // O chunks and each transposed tile's D_T go straight into the fp32
-      // accumulator (scaled, vector reductions); rows past n are padding
+      // O chunks and each transposed tile's D_T go into the int64 fixed-point
+      // accumulator (fx_flush8: one 2 KB bulk reduction per 8 columns of the
+      // warp's 32 rows); rows past n are padding
       TileIter ti;
       ti.start(p, items);
-      uint32_t q = 0, dtq = 0;
-      // Flushes go through shared memory and one TMA bulk reduction per warp
-      // (32 rows x WP floats, contiguous): 16 B chunk c of row r is stored at
-      // chunk c ^ (r mod C) (conflict-free stores), and the global accumulator
-      // keeps that swizzle (sym_finalize_kernel undoes it).
-      constexpr int C = WP / 4;
-      const uint32_t stg_warp = smem_u32(sStage) + (uint32_t)(32 * wq) * WP * 4u;
-      const uint32_t stg_row = stg_warp + (uint32_t)lane * WP * 4u;
-      auto stage8 = [&](int h, const uint32_t (&x)[8], const uint32_t (&y)[8], bool two) {
-        float v[8];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const int e = p.s_exp + __ldg(&p.col_exp[8 * h + c]);  // 2^-e, exact
-          const float s = __uint_as_float(x[c]) + (two ? __uint_as_float(y[c]) : 0.f);
-          v[c] = s * __int_as_float((127 - e) << 23);
-        }
-        const uint32_t k0 = (uint32_t)((2 * h) ^ (lane & (C - 1))), k1 = (uint32_t)((2 * h + 1) ^ (lane & (C - 1)));
-        st_shared_v4(stg_row + 16u * k0, __float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]),
-                     __float_as_uint(v[3]));
-        st_shared_v4(stg_row + 16u * k1, __float_as_uint(v[4]), __float_as_uint(v[5]), __float_as_uint(v[6]),
-                     __float_as_uint(v[7]));
-      };
-      auto issue = [&](int64_t row0, bool skip) {  // after the stores of one flush
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0 && !skip) bulk_reduce_add_f32(p.acc + row0 * WP, stg_warp, 32u * WP * 4u);
-      };
-      auto reuse = [&]() {  // the staging rows may be rewritten once the last bulk op read them
-        if (lane == 0) bulk_wait_read();
-        __syncwarp();
-      };
+      uint32_t q = 0, dtq = 0, nst = 0;
+      constexpr uint32_t NBLK = WP == 32 ? 2u : 1u;  // staging blocks per warp (BM x WP x 4 bytes)
+      const uint32_t stg_warp = smem_u32(sStage) + (uint32_t)wq * NBLK * 2048u;
       uint32_t aitem = 0;
       while (ti.valid) {
         if (ATM && ti.first_in_item()) {
@@ -1081,9 +1111,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         if (ti.transposed()) {
           mbar_wait(&dt_full[dtq & 1u], (dtq >> 1) & 1u);
           tc_fence_after();
-          reuse();
           const int64_t j0 = (int64_t)ti.ct * BM + 32 * wq;  // output rows of the transposed product
-          const bool ld = !(p.sym_dbg & 8);
+          const bool ld = !(DBG && (p.sym_dbg & 8));
 #pragma unroll
           for (int h = 0; h < WP / 8; ++h) {
             uint32_t x[8];
@@ -1094,15 +1123,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 #pragma unroll
               for (int c = 0; c < 8; ++c) x[c] = 0u;
             }
-            stage8(h, x, x, false);
-            if (p.sym_dump != nullptr) {
+            float v[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) v[c] = __uint_as_float(x[c]);
+            if (DBG && p.sym_dump != nullptr) {
               float* dd = p.sym_dump + ((((int64_t)ti.cur.pp * p.col_tiles + ti.ct) * 2 + rank) * BM + row) * WP + 8 * h;
 #pragma unroll
-              for (int c = 0; c < 8; ++c) dd[c] = __uint_as_float(x[c]);
+              for (int c = 0; c < 8; ++c) dd[c] = v[c];
             }
+            fx_flush8<NBLK>(p, stg_warp, nst, lane, h, v, j0, DBG && (p.sym_dbg & 1));
           }
           tc_fence_before();
-          issue(j0, (p.sym_dbg & 1) != 0);
           if (lane == 0) mbar_arrive_cluster(leader_addr(&dt_empty[dtq & 1u]));
           if (lane == 0 && wq == 0 && ti.it == (int)(blockIdx.x >> 1)) trace_ev<DBG>(p, ti.ct - ti.cur.c0, 15);
           ++dtq;
@@ -1110,7 +1141,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         if (ti.last_in_chunk()) {
           mbar_wait(&o_full[q & 1u], (q >> 1) & 1u);
           tc_fence_after();
-          reuse();
           const int64_t i0 = (2 * (int64_t)ti.cur.pp + rank) * BM + 32 * wq;
 #pragma unroll
           for (int h = 0; h < WP / 8; ++h) {
@@ -1118,10 +1148,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             tmem_ld8(tO(q & 1u) + lane_off + 8 * h, x);       // P_hi Vhi + P_lo Vhi
             tmem_ld8(tO(q & 1u) + lane_off + WP + 8 * h, y);  // P_hi Vlo
             tmem_wait_ld();
-            stage8(h, x, y, true);
+            float v[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) v[c] = __uint_as_float(x[c]) + __uint_as_float(y[c]);
+            fx_flush8<NBLK>(p, stg_warp, nst, lane, h, v, i0, DBG && (p.sym_dbg & 2));
           }
           tc_fence_before();
-          issue(i0, (p.sym_dbg & 2) != 0);
           if (lane == 0) mbar_arrive_cluster(leader_addr(&o_empty[q & 1u]));
           ++q;
         }
@@ -1158,19 +1190,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           const int64_t i = (2 * (int64_t)ti.cur.pp + rank) * BM + row;  // local row
           if (i < p.nloc) {
             const int64_t sp = ti.it % p.splits;  // once per item
-            for (int c = 0; c < p.w; ++c) {
-              const double v = ldexp(acc[c * BM], -(p.s_exp + __ldg(&p.col_exp[c])));
-              if (p.splits > 1)
-                p.partial[(sp * p.nloc + i) * p.w + c] = v;
-              else
-#pragma unroll
-                for (int k = 0; k < NCGP_MAX_OUTS; ++k) {  // own output, then the peers'
-                  if (k >= p.n_out) break;
-                  if (p.out_f64)
-                    static_cast<double*>(p.outs[k])[i * p.ldo + c] = v;
-                  else
-                    static_cast<float*>(p.outs[k])[i * p.ldo + c] = (float)v;
-                }
+            auto kv = [&](int c) -> double {
+              return ldexp(acc[c * BM], -(p.s_exp + __ldg(&p.col_exp[c])));
+            };
+            if (p.splits > 1) {
+              for (int c = 0; c < p.w; ++c) p.partial[(sp * p.nloc + i) * p.w + c] = kv(c);
+            } else if (p.out_f64) {  // own output, then the peers', through the epilogue
+              ncgp::epi_row<double, NCGP_MAX_OUTS>(p.epi, i, p.w, kv,
+                                                   reinterpret_cast<double* const*>(p.outs), p.n_out, p.ldo);
+            } else {
+              ncgp::epi_row<float, NCGP_MAX_OUTS>(p.epi, i, p.w, kv,
+                                                  reinterpret_cast<float* const*>(p.outs), p.n_out, p.ldo);
             }
           }
 #pragma unroll
@@ -1527,7 +1557,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
         tc_fence_after();
         if (lane == 0) trace_ev<DBG>(p, g, 13);
         if (elect_one()) {
-          if (tp && !(p.sym_dbg & 4)) {
+          if (tp && !(DBG && (p.sym_dbg & 4))) {
             const uint64_t pa = dP0 + (uint64_t)pbuf(g) * (PBUF >> 4);
             const uint32_t dt = tDT(dtq & 1u);
 #pragma unroll 1
@@ -1602,7 +1632,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
             if (tr) trace_ev<DBG>(p, g, 8);
           }
           const uint32_t rowb = rowb0 + 512u * c;
-          if (!(p.sym_dbg & 16)) {
+          if (!(DBG && (p.sym_dbg & 16))) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               st_shared_v4(rowb + 128u * k, hi[4 * k], hi[4 * k + 1], hi[4 * k + 2], hi[4 * k + 3]);
@@ -1627,65 +1657,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
   } else {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
     // ================= drains: O every CH tiles, D_T every transposed tile =================
+    // into the int64 fixed-point accumulator (fx_flush8, deterministic)
     const int wq = warp & 3;
     const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
-    constexpr int C = WP / 4;
-    const uint32_t stg_warp = smem_u32(sStage) + (uint32_t)(32 * wq) * WP * 4u;
-    const uint32_t stg_row = stg_warp + (uint32_t)lane * WP * 4u;
-    auto stage8 = [&](int h, const uint32_t (&x)[8], const uint32_t (&y)[8]) {
-      float v[8];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const int ex = p.s_exp + __ldg(&p.col_exp[8 * h + c]);  // 2^-e, exact
-        v[c] = (__uint_as_float(x[c]) + __uint_as_float(y[c])) * __int_as_float((127 - ex) << 23);
-      }
-      const uint32_t k0 = (uint32_t)((2 * h) ^ (lane & (C - 1))), k1 = (uint32_t)((2 * h + 1) ^ (lane & (C - 1)));
-      st_shared_v4(stg_row + 16u * k0, __float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]),
-                   __float_as_uint(v[3]));
-      st_shared_v4(stg_row + 16u * k1, __float_as_uint(v[4]), __float_as_uint(v[5]), __float_as_uint(v[6]),
-                   __float_as_uint(v[7]));
-    };
+    constexpr uint32_t NBLK = WP == 32 ? 2u : 1u;  // staging blocks per warp (BM x WP x 4 bytes)
+    const uint32_t stg_warp = smem_u32(sStage) + (uint32_t)wq * NBLK * 2048u;
+    uint32_t nst = 0;
     auto drain = [&](uint32_t tacc, int64_t row0, bool skip) {
-      if (p.sym_dbg & 256) {  // variant: vector reductions straight from registers
-        float* dst = p.acc + (row0 + lane) * WP;
-#pragma unroll
-        for (int h = 0; h < WP / 8; ++h) {
-          uint32_t x[8], y[8];
-          tmem_ld8(tacc + lane_off + 8 * h, x);
-          tmem_ld8(tacc + lane_off + WP + 8 * h, y);
-          tmem_wait_ld();
-          float v[8];
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const int ex = p.s_exp + __ldg(&p.col_exp[8 * h + c]);
-            v[c] = (__uint_as_float(x[c]) + __uint_as_float(y[c])) * __int_as_float((127 - ex) << 23);
-          }
-          const int k0 = (2 * h) ^ (lane & (C - 1)), k1 = (2 * h + 1) ^ (lane & (C - 1));
-          if (!skip) {
-            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * k0), "f"(v[0]),
-                         "f"(v[1]), "f"(v[2]), "f"(v[3]) : "memory");
-            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * k1), "f"(v[4]),
-                         "f"(v[5]), "f"(v[6]), "f"(v[7]) : "memory");
-          }
-        }
-        tc_fence_before();
-        __syncwarp();
-        return;
-      }
-      if (lane == 0) bulk_wait_read();  // staging rows free again
-      __syncwarp();
 #pragma unroll
       for (int h = 0; h < WP / 8; ++h) {
         uint32_t x[8], y[8];
         tmem_ld8(tacc + lane_off + 8 * h, x);       // [0, WP): hi Vhi + lo Vhi
         tmem_ld8(tacc + lane_off + WP + 8 * h, y);  // [WP, 2 WP): hi Vlo
         tmem_wait_ld();
-        stage8(h, x, y);
+        float v[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) v[c] = __uint_as_float(x[c]) + __uint_as_float(y[c]);
+        fx_flush8<NBLK>(p, stg_warp, nst, lane, h, v, row0, skip);
       }
       tc_fence_before();
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0 && !skip) bulk_reduce_add_f32(p.acc + row0 * WP, stg_warp, 32u * WP * 4u);
     };
     Tile1 ti;
     ti.start(p);
@@ -1694,7 +1684,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
       if (ti.transposed()) {
         mbar_wait(&dt_full[dtq & 1u], (dtq >> 1) & 1u);
         tc_fence_after();
-        if (!(p.sym_dbg & 8)) drain(tDT(dtq & 1u), (int64_t)ti.ct * BM + 32 * wq, (p.sym_dbg & 1) != 0);
+        if (!(DBG && (p.sym_dbg & 8))) drain(tDT(dtq & 1u), (int64_t)ti.ct * BM + 32 * wq, DBG && (p.sym_dbg & 1));
         else tc_fence_before();
         if (lane == 0) mbar_arrive(&dt_empty[dtq & 1u]);
         ++dtq;
@@ -1702,7 +1692,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
       if (ti.last_in_chunk()) {
         mbar_wait(&o_full[q & 1u], (q >> 1) & 1u);
         tc_fence_after();
-        drain(tO(q & 1u), (int64_t)ti.r * BM + 32 * wq, (p.sym_dbg & 2) != 0);
+        drain(tO(q & 1u), (int64_t)ti.r * BM + 32 * wq, DBG && (p.sym_dbg & 2));
         if (lane == 0) mbar_arrive(&o_empty[q & 1u]);
         ++q;
       }
@@ -1923,18 +1913,38 @@ __global__ void reduce_partial_kernel(const double* __restrict__ partial, int sp
     if (k < out.n) out.p[k][(e / w) * ldo + (e % w)] = (T)s;
 }
 
-// symmetric kernel: rows of the fp32 accumulator to every destination
-__global__ void sym_finalize_kernel(const float* __restrict__ acc, int64_t n, int w, int wp,
+// split columns: the fixed-order fp64 sum of the partial rows, one thread per
+// row, through the apply's epilogue
+template <typename T>
+__global__ void reduce_partial_epi_kernel(const double* __restrict__ partial, int splits,
+                                          int64_t nloc, int w, const EpiDev e,
+                                          const ncgp::OutPtrs<T> out, int64_t ldo) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nloc) return;
+  auto kv = [&](int c) -> double {
+    double s = 0.0;
+    for (int p = 0; p < splits; ++p) s += partial[((int64_t)p * nloc + i) * w + c];
+    return s;
+  };
+  ncgp::epi_row<T, NCGP_MAX_OUTS>(e, i, w, kv, out.p, out.n, ldo);
+}
+
+// symmetric kernel: rows of the int64 fixed-point accumulator (layout of
+// fx_flush8) scaled back by 2^-(F + s + e_c) in fp64, through the epilogue,
+// to every destination; one thread per row
+__global__ void sym_finalize_kernel(const unsigned long long* __restrict__ acc, int64_t acc_rows,
+                                    int64_t n, int w, int fx_exp, int s_exp,
+                                    const int* __restrict__ col_exp, const EpiDev e,
                                     const ncgp::OutPtrs<float> out, int64_t ldo) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= n * w) return;
-  const int64_t i = e / w;
-  const int c = (int)(e % w);
-  const int cc = ((c >> 2) ^ (int)(i & (wp / 4 - 1))) * 4 + (c & 3);  // stored chunk swizzle
-  const float v = acc[i * wp + cc];
-#pragma unroll
-  for (int k = 0; k < NCGP_MAX_OUTS; ++k)
-    if (k < out.n) out.p[k][i * ldo + c] = v;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int swz = (int)((i >> 1) & 3);
+  auto kv = [&](int c) -> double {
+    const int h = c >> 3, cc = c & 7;
+    const int64_t idx = ((int64_t)h * acc_rows + i) * 8 + (((cc >> 1) ^ swz) << 1) + (cc & 1);
+    return ldexp((double)(long long)acc[idx], -(fx_exp + s_exp + __ldg(&col_exp[c])));
+  };
+  ncgp::epi_row<float, NCGP_MAX_OUTS>(e, i, w, kv, out.p, out.n, ldo);
 }
 
 // ------------------------------------------------------------------ host
@@ -1954,10 +1964,9 @@ float* g_sym_dump = nullptr;   // debug hook (ncgp_debug_set_sym_dump)
 // NCGP_SYM=1 forces it on, NCGP_SYM=0 off (the plain kernel's results are
 // bitwise reproducible across row shardings; the symmetric kernels' fp32
 // reductions are not).
-bool sym_enabled(int family, int wp, int64_t col_tiles, int cg) {
-  const char* e = getenv("NCGP_SYM");
-  if (e != nullptr && e[0] == '0') return false;
-  if (e != nullptr && e[0] == '1') return true;
+bool sym_enabled(const ncgp_kop* op, int family, int wp, int64_t col_tiles, int cg) {
+  if (op->knob_sym == 0) return false;
+  if (op->knob_sym == 1) return true;
   if (cg == 1) return col_tiles >= 300;
   return col_tiles >= 512 && (family == NCGP_MATERN32 || wp == 16);
 }
@@ -2007,15 +2016,14 @@ int splits_for(int64_t pairs, int64_t col_tiles, int clusters) {
 // fp32 accumulator rows its transposed products reduce into, both L2-sized
 // (at N = 1e6 a pair-major list streamed all 192 MB of records and 128 MB of
 // accumulator rows through L2 at once).
-int sym_item_len() {
-  const char* e = getenv("NCGP_SYM_ITEM");
-  return e != nullptr && atoi(e) > 0 ? atoi(e) : 128;
-}
+// (The item length is a creation-time knob, NCGP_SYM_ITEM, default 128; the
+// workspace's item table is sized for the shortest allowed length, 16, and
+// longer items only shorten the list.)
+constexpr int SYM_ITEM_MIN = 16;
 template <typename F>
-void sym_walk(int64_t pairs, int64_t nb, F&& f) {
-  const int64_t L = sym_item_len();
-  const char* e = getenv("NCGP_SYM_ORDER");  // "pair": the pair-major list (experiments)
-  if (e != nullptr && e[0] == 'p') {
+void sym_walk(int64_t pairs, int64_t nb, F&& f, int item = SYM_ITEM_MIN, bool pair_order = false) {
+  const int64_t L = std::max(item, SYM_ITEM_MIN);
+  if (pair_order) {  // NCGP_SYM_ORDER=pair: the pair-major list (experiments)
     for (int64_t a = 0; a < pairs; ++a)
       for (int64_t c0 = 2 * a; c0 < nb; c0 += L) f(a, c0, std::min<int64_t>(nb, c0 + L));
     return;
@@ -2030,12 +2038,12 @@ int64_t sym_item_count(int64_t pairs, int64_t nb) {
   sym_walk(pairs, nb, [&](int64_t, int64_t, int64_t) { ++n; });
   return n;
 }
-std::vector<int4> sym_items(int64_t pairs, int64_t nb) {
+std::vector<int4> sym_items(int64_t pairs, int64_t nb, int item, bool pair_order) {
   std::vector<int4> t;
   t.reserve((size_t)sym_item_count(pairs, nb));
   sym_walk(pairs, nb, [&](int64_t a, int64_t c0, int64_t c1) {
     t.push_back(make_int4((int)a, (int)c0, (int)c1, 0));
-  });
+  }, item, pair_order);
   return t;
 }
 
@@ -2046,22 +2054,21 @@ size_t smem1_bytes(uint32_t a_bytes, int wp, int sx, int sv, int npb = 2);
 // Flavour of the symmetric kernel an operator's work list is built for: the
 // single-CTA kernel where its shared memory fits the widest RHS (full column
 // records plus two P buffers), else the pair kernel.  NCGP_SYM_CG=1 / 2 forces.
-int sym_cg(int d, int w_max) {
-  const char* e = getenv("NCGP_SYM_CG");
-  if (e != nullptr && (e[0] == '1' || e[0] == '2')) return e[0] - '0';
+int sym_cg(const ncgp_kop* op, int d, int w_max) {
+  if (op->knob_sym_cg == 1 || op->knob_sym_cg == 2) return op->knob_sym_cg;
   const uint32_t a = (uint32_t)(BM * ka_of(d) * 2);
   // rings no shallower than (XB 2, V 4) or (XB 3, V 2): D = 24 at WP = 16
   // only fits (2, 3), which ran slower than the plain kernel; the pair kernel
   // keeps 3-deep rings there
   const int wpm = wp_of(w_max);
   if (smem1_bytes(a, wpm, 2, 4, 2) <= SMEM_MAX || smem1_bytes(a, wpm, 3, 2, 2) <= SMEM_MAX) return 1;
-  const char* f = getenv("NCGP_SYM1_NPB");  // experiments: one-P-buffer single-CTA kernel
-  if (f != nullptr && f[0] == '1' && smem1_bytes(a, wp_of(w_max), 2, 2, 1) <= SMEM_MAX) return 1;
+  // experiments (NCGP_SYM1_NPB=1): one-P-buffer single-CTA kernel
+  if (op->knob_npb1 && smem1_bytes(a, wp_of(w_max), 2, 2, 1) <= SMEM_MAX) return 1;
   return 2;
 }
 template <typename F>
-void sym1_walk(int64_t nb, F&& f) {
-  const int64_t L = sym_item_len();
+void sym1_walk(int64_t nb, F&& f, int item = SYM_ITEM_MIN) {
+  const int64_t L = std::max(item, SYM_ITEM_MIN);
   for (int64_t b0 = 0; b0 < nb; b0 += L) {
     const int64_t b1 = std::min<int64_t>(nb, b0 + L);
     for (int64_t r = 0; r < b1; ++r) f(r, std::max<int64_t>(b0, r), b1);
@@ -2107,9 +2114,9 @@ Layout layout_of(int64_t n_rows, int64_t n_cols, int d, int w_max, int sms) {
   const int sp = splits_for(L.row_tiles / 2, L.col_tiles, std::max(1, sms / 2));
   L.partial = take((size_t)(sp > 1 ? sp : 0) * (size_t)(L.row_tiles * BM) * w_max *
                    sizeof(double) + 256);
-  // symmetric kernel (square operators): fp32 accumulator and item table
+  // symmetric kernel (square operators): int64 accumulator and item table
   const bool sq = n_rows == n_cols;
-  L.symacc = take(sq ? (size_t)L.row_tiles * BM * wp_of(w_max) * sizeof(float) : 0);
+  L.symacc = take(sq ? (size_t)L.row_tiles * BM * wp_of(w_max) * sizeof(unsigned long long) : 0);
   L.symtab = take(sq ? (size_t)std::max(sym_item_count(L.row_tiles / 2, L.col_tiles),
                                          sym1_item_count(L.col_tiles)) * 16
                      : 0);
@@ -2126,26 +2133,22 @@ size_t smem_bytes(uint32_t a_bytes, int wp, int na, int sx, int sv, int sym_npb 
 
 // The pair kernel with its row tile in TMEM (large D, WP = 16).  NCGP_SYM_ATM=0
 // disables it.
-bool atm_allowed() {
-  const char* e = getenv("NCGP_SYM_ATM");
-  return !(e != nullptr && e[0] == '0');
-}
+bool atm_allowed(const ncgp_kop* op) { return op->knob_atm; }
 
 // Which symmetric kernel a full-range apply of width w runs: 0 none (the
 // plain kernel), 1 the pair kernel, 2 the single-CTA kernel.
 int sym_variant(const ncgp_kop* op, int w) {
   if (op->sym_items <= 0 || g_debug_mode != 0) return 0;
   const int wp = wp_of(w);
-  if (!sym_enabled(op->family, wp, op->col_tiles, op->sym_cg)) return 0;
+  if (!sym_enabled(op, op->family, wp, op->col_tiles, op->sym_cg)) return 0;
   const uint32_t a_bytes = (uint32_t)(BM * op->ka * 2);
   if (op->sym_cg == 1) return smem1_bytes(a_bytes, wp, 2, 2, 1) <= SMEM_MAX ? 2 : 0;
   if (smem_bytes(a_bytes, wp, 1, 3, 3, 2) <= (size_t)SMEM_BUDGET) return 1;
-  if (wp == 16 && atm_allowed() && op->ka <= 2 * 128 &&
+  if (wp == 16 && atm_allowed(op) && op->ka <= 2 * 128 &&
       smem_bytes(a_bytes, wp, 0, 3, 3, 2) <= (size_t)SMEM_BUDGET)
     return 1;
   if (op->family == NCGP_MATERN32 && smem_bytes(a_bytes, wp, 1, 3, 3, 1) <= (size_t)SMEM_BUDGET) return 1;
-  const char* e = getenv("NCGP_SYM_NPB");
-  if (e != nullptr && atoi(e) == 1 && smem_bytes(a_bytes, wp, 1, 3, 3, 1) <= (size_t)SMEM_BUDGET) return 1;
+  if (op->knob_npb == 1 && smem_bytes(a_bytes, wp, 1, 3, 3, 1) <= (size_t)SMEM_BUDGET) return 1;
   return 0;
 }
 
@@ -2157,11 +2160,14 @@ int64_t tc_sym_acc_elems(const ncgp_kop* op, int w) {
   return sym_variant(op, w) ? op->row_tiles * BM * wp_of(w) : 0;
 }
 
-int tc_sym_finalize(ncgp_kop* op, const float* acc, int w, const OutSet& out, int64_t ldo,
-                    cudaStream_t st) {
-  const int64_t tot = op->n_rows * w;
-  sym_finalize_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
-      acc, op->n_rows, w, wp_of(w), ncgp::out_ptrs<float>(out, 0, ldo), ldo);
+int tc_sym_finalize(ncgp_kop* op, const unsigned long long* acc, int w, const OutSet& out,
+                    int64_t ldo, cudaStream_t st, const EpiDev& epi) {
+  const Layout L = layout_of(op->n_rows, op->n_cols, op->d, op->w_max, op->sms);
+  const int* col_exp = reinterpret_cast<const int*>(op->ws + L.colexp);
+  const int s_exp = (int)lround(log2(op->k_scale));
+  sym_finalize_kernel<<<(unsigned)((op->n_rows + 127) / 128), 128, 0, st>>>(
+      acc, op->row_tiles * BM, op->n_rows, w, op->sym_fx, s_exp, col_exp, epi,
+      ncgp::out_ptrs<float>(out, 0, ldo), ldo);
   NCGP_LAUNCHED();
   return NCGP_OK;
 }
@@ -2188,20 +2194,22 @@ int tc_prepare(ncgp_kop* op, cudaStream_t st) {
   op->col_tile_bytes = (size_t)L.tile_stride;
   op->partial = reinterpret_cast<double*>(op->ws + L.partial);
   op->sym_items = 0;
-  op->sym_acc = reinterpret_cast<float*>(op->ws + L.symacc);
+  op->sym_acc = reinterpret_cast<unsigned long long*>(op->ws + L.symacc);
+  // fixed-point fraction bits of the symmetric accumulator: |sum| < n 2^28 2^F < 2^62
+  op->sym_fx = 33 - (int)ceil(log2((double)std::max<int64_t>(op->n_cols, 2)));
   op->sym_tab = reinterpret_cast<int4*>(op->ws + L.symtab);
   std::vector<int4> tab;
   if (op->n_rows == op->n_cols)
     NCGP_CUDA(cudaMemsetAsync(op->col_pack + (size_t)L.col_tiles * L.tile_stride, 0,
                               (size_t)L.tile_stride, st));
   if (op->Xr == op->Xc && op->n_rows == op->n_cols) {
-    op->sym_cg = sym_cg(op->d, op->w_max);
+    op->sym_cg = sym_cg(op, op->d, op->w_max);
     if (op->sym_cg == 1)
       sym1_walk(L.col_tiles, [&](int64_t r, int64_t c0, int64_t c1) {
         tab.push_back(make_int4((int)r, (int)c0, (int)c1, 0));
-      });
+      }, op->knob_item);
     else
-      tab = sym_items(L.row_tiles / 2, L.col_tiles);
+      tab = sym_items(L.row_tiles / 2, L.col_tiles, op->knob_item, op->knob_pair_order);
     NCGP_CUDA(cudaMemcpyAsync(op->sym_tab, tab.data(), tab.size() * sizeof(int4),
                               cudaMemcpyHostToDevice, st));
     op->sym_items = (int64_t)tab.size();  // the stream sync below keeps `tab` alive long enough
@@ -2264,7 +2272,7 @@ int tc_prepare(ncgp_kop* op, cudaStream_t st) {
 }
 
 int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out, int64_t ldo,
-             int64_t r0, int64_t r1, cudaStream_t st, const SymPart* part) {
+             int64_t r0, int64_t r1, cudaStream_t st, const EpiDev& epi, const SymPart* part) {
   if (part != nullptr) {
     NCGP_CHECK_ARG(sym_variant(op, w) != 0, NCGP_UNSUPPORTED,
                    "no symmetric kernel for this operator and width");
@@ -2332,6 +2340,9 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
   p.n_items = (int)(p.pairs * p.splits);
   p.item_tab = nullptr;
   p.acc = nullptr;
+  p.acc_rows = op->row_tiles * BM;
+  p.fx = ldexpf(1.f, op->sym_fx);
+  p.epi = epi;
   // symmetric kernel: K(X, X) with the whole row range in one launch
   const bool dbg = (g_trace != nullptr) || (g_debug_mode != 0);
   bool sym = r0 == 0 && r1 == op->n_rows && sym_variant(op, w) != 0;
@@ -2348,7 +2359,13 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
     it_lo = std::min<int64_t>(cut(part->part), op->sym_items);
     it_hi = std::min<int64_t>(cut(part->part + 1), op->sym_items);
   }
-  float* const sym_acc = part != nullptr ? part->acc : op->sym_acc;
+  unsigned long long* const sym_acc = part != nullptr ? part->acc : op->sym_acc;
+  const size_t acc_bytes = (size_t)op->row_tiles * BM * wp * sizeof(unsigned long long);
+  // variant bits always; the result-changing debug bits only with a debug hook set
+  const int sym_dbg = op->knob_sym_var | (dbg ? [] {
+    const char* e = getenv("NCGP_SYM_DBG");
+    return e != nullptr ? atoi(e) : 0;
+  }() : 0);
   const bool sym_fin = part == nullptr;
   if (sym && op->sym_cg == 1) {
     const int cand[][2] = {{3, 6}, {3, 4}, {3, 3}, {2, 4}, {3, 2}, {2, 3}, {2, 2}};
@@ -2369,9 +2386,8 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
       p.n_items = (int)(it_hi - it_lo);
       p.item_tab = op->sym_tab + it_lo;
       p.acc = sym_acc;
-      const char* e = getenv("NCGP_SYM_DBG");
-      p.sym_dbg = e != nullptr ? atoi(e) : 0;
-      NCGP_CUDA(cudaMemsetAsync(p.acc, 0, (size_t)op->row_tiles * BM * wp * sizeof(float), st));
+      p.sym_dbg = sym_dbg;
+      NCGP_CUDA(cudaMemsetAsync(p.acc, 0, acc_bytes, st));
       op->last_variant = 2;
       if (p.n_items == 0) return NCGP_OK;  // an empty part
       const size_t smem = smem1_bytes(p.a_bytes, wp, p.sx, p.sv, p.npb);
@@ -2392,7 +2408,7 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
                  : (wp == 16 ? launch(kop_sym1_kernel<NCGP_MATERN32, 16, false>)
                              : launch(kop_sym1_kernel<NCGP_MATERN32, 32, false>));
       if (rc != NCGP_OK) return rc;
-      return sym_fin ? tc_sym_finalize(op, p.acc, w, out, ldo, st) : NCGP_OK;
+      return sym_fin ? tc_sym_finalize(op, p.acc, w, out, ldo, st, epi) : NCGP_OK;
     }
     sym = false;
   }
@@ -2403,14 +2419,13 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
     const int cand[][4] = {{2, 1, 6, 6}, {2, 1, 3, 6}, {2, 1, 3, 5}, {2, 1, 3, 4}, {2, 1, 3, 3},
                            {2, 0, 3, 6}, {2, 0, 3, 4}, {2, 0, 3, 3},
                            {1, 1, 3, 6}, {1, 1, 3, 4}, {1, 1, 3, 3}};
-    const char* e = getenv("NCGP_SYM_NPB");  // experiments: force 1 or 2 P buffers
-    const int force = e != nullptr ? atoi(e) : 0;
+    const int force = op->knob_npb;  // NCGP_SYM_NPB experiments: force 1 or 2 P buffers
     sym = false;
     for (auto& c : cand)
       // one P buffer serialises the two epilogue groups on it: a 1.15x gain
       // for Matern-3/2 at D = 50 but a loss for RBF (tools/sym_exp.py)
       if ((force == c[0] || (force == 0 && (c[0] == 2 || op->family == NCGP_MATERN32))) &&
-          (c[1] > 0 || (wp == 16 && atm_allowed())) &&
+          (c[1] > 0 || (wp == 16 && atm_allowed(op))) &&
           smem_bytes(p.a_bytes, wp, c[1], c[2], c[3], c[0]) <= (size_t)SMEM_BUDGET) {
         p.npb = c[0];
         p.na = c[1];
@@ -2426,12 +2441,9 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
     p.n_items = (int)(it_hi - it_lo);
     p.item_tab = op->sym_tab + it_lo;
     p.acc = sym_acc;
-    {
-      const char* e = getenv("NCGP_SYM_DBG");
-      p.sym_dbg = e != nullptr ? atoi(e) : 0;
-    }
+    p.sym_dbg = sym_dbg;
     p.sym_dump = g_sym_dump;
-    NCGP_CUDA(cudaMemsetAsync(p.acc, 0, (size_t)op->row_tiles * BM * wp * sizeof(float), st));
+    NCGP_CUDA(cudaMemsetAsync(p.acc, 0, acc_bytes, st));
     op->last_variant = 1;
     if (p.n_items == 0) return NCGP_OK;
     const size_t smem = smem_bytes(p.a_bytes, wp, p.na, p.sx, p.sv, p.npb);
@@ -2460,7 +2472,7 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
       rc = wp == 16 ? launch(kop_tc_kernel<NCGP_MATERN32, 16, false, true>)
                     : launch(kop_tc_kernel<NCGP_MATERN32, 32, false, true>);
     if (rc != NCGP_OK) return rc;
-    return sym_fin ? tc_sym_finalize(op, p.acc, w, out, ldo, st) : NCGP_OK;
+    return sym_fin ? tc_sym_finalize(op, p.acc, w, out, ldo, st, epi) : NCGP_OK;
   }
   NCGP_CHECK_ARG(part == nullptr, NCGP_UNSUPPORTED, "no symmetric kernel for this operator");
   // deepest rings that fit: (na, sx, sv) from (2, 6, 9) down to (1, 3, 6)
@@ -2476,10 +2488,9 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
         break;
       }
     NCGP_CHECK_ARG(ok, NCGP_UNSUPPORTED, "shared memory too small for d=%d", op->d);
-    const char* e = getenv("NCGP_RINGS");  // timing experiments: "na,sx,sv"
-    int na, sx, sv;
-    if (e != nullptr && sscanf(e, "%d,%d,%d", &na, &sx, &sv) == 3 &&
-        smem_bytes(p.a_bytes, wp, na, sx, sv) <= (size_t)SMEM_BUDGET) {
+    // timing experiments: NCGP_RINGS "na,sx,sv"
+    const int na = op->knob_rings[0], sx = op->knob_rings[1], sv = op->knob_rings[2];
+    if (na > 0 && smem_bytes(p.a_bytes, wp, na, sx, sv) <= (size_t)SMEM_BUDGET) {
       p.na = na;
       p.sx = sx;
       p.sv = sv;
@@ -2518,7 +2529,14 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
   if (rc != NCGP_OK) return rc;
   if (p.splits > 1) {
     const int64_t tot = p.nloc * w;
-    if (p.out_f64)
+    const unsigned rb = (unsigned)((p.nloc + 127) / 128);
+    if (epi.active && p.out_f64)
+      reduce_partial_epi_kernel<double><<<rb, 128, 0, st>>>(
+          p.partial, p.splits, p.nloc, w, epi, ncgp::out_ptrs<double>(out, r0, ldo), ldo);
+    else if (epi.active)
+      reduce_partial_epi_kernel<float><<<rb, 128, 0, st>>>(
+          p.partial, p.splits, p.nloc, w, epi, ncgp::out_ptrs<float>(out, r0, ldo), ldo);
+    else if (p.out_f64)
       reduce_partial_kernel<double><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
           p.partial, p.splits, p.nloc, w, ncgp::out_ptrs<double>(out, r0, ldo), ldo);
     else

@@ -236,6 +236,24 @@ __global__ void bernoulli_stats_kernel(const T* __restrict__ f, const int64_t* _
   if (yhat) yhat[i] = fi + wi * g;
 }
 
+// Poisson, log link (likelihoods.py:174-182, outer.py:129-131): w = e^f,
+// winv = e^-f, grad = y - e^f, yhat = f + winv * grad
+template <typename T>
+__global__ void poisson_stats_kernel(const T* __restrict__ f, const T* __restrict__ y, int64_t n,
+                                     T* __restrict__ winv, T* __restrict__ w, T* __restrict__ grad,
+                                     T* __restrict__ yhat) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const T fi = f[i];
+  const T wv = dev_exp<T>(fi);
+  const T wi = dev_exp<T>(-fi);
+  const T g = (y ? y[i] : T(0)) - wv;
+  if (winv) winv[i] = wi;
+  if (w) w[i] = wv;
+  if (grad) grad[i] = g;
+  if (yhat) yhat[i] = fi + wi * g;
+}
+
 template <typename T>
 __global__ void diag_apply_kernel(const T* __restrict__ d, int64_t n, const T* __restrict__ V,
                                   int64_t ldv, int k, const T* __restrict__ base, int64_t ldb,
@@ -359,6 +377,26 @@ int ncgp_bernoulli_stats(int dtype, const void* f, const int64_t* labels, int64_
   else
     bernoulli_stats_kernel<float><<<g, 256, 0, st>>>((const float*)f, labels, n, (float*)winv,
                                                      (float*)w, (float*)grad, (float*)yhat);
+  NCGP_LAUNCHED();
+  return NCGP_OK;
+}
+
+int ncgp_poisson_stats(int dtype, const void* f, const void* counts, int64_t n, void* winv,
+                       void* w, void* grad, void* yhat, void* stream) {
+  NCGP_CHECK_ARG(n >= 0, NCGP_DIMENSION_MISMATCH, "negative n");
+  if (n == 0) return NCGP_OK;
+  NCGP_CHECK_ARG(f != nullptr, NCGP_INVALID_INPUT, "null latent");
+  NCGP_CHECK_ARG(!(grad || yhat) || counts, NCGP_INVALID_INPUT, "counts required");
+  cudaStream_t st = ncgp::as_stream(stream);
+  const unsigned g = (unsigned)((n + 255) / 256);
+  if (dtype == NCGP_F64)
+    poisson_stats_kernel<double><<<g, 256, 0, st>>>((const double*)f, (const double*)counts, n,
+                                                    (double*)winv, (double*)w, (double*)grad,
+                                                    (double*)yhat);
+  else
+    poisson_stats_kernel<float><<<g, 256, 0, st>>>((const float*)f, (const float*)counts, n,
+                                                   (float*)winv, (float*)w, (float*)grad,
+                                                   (float*)yhat);
   NCGP_LAUNCHED();
   return NCGP_OK;
 }

@@ -149,6 +149,39 @@ class PriorOperator:
     def impl(self) -> str:
         return self.groups[0][0].impl
 
+    @property
+    def supports_fused(self) -> bool:
+        """One kernel spec for all outputs and the whole CN row in one K1
+        block: the Newton-step epilogues fuse into the product."""
+        op, cols = self.groups[0]
+        return len(self.groups) == 1 and len(cols) == self.C and self.C <= op.w_max
+
+    def apply_fused(self, v: torch.Tensor, epi, out: Optional[torch.Tensor] = None,
+                    row_begin: int = 0, row_end: Optional[int] = None) -> torch.Tensor:
+        """``epi.alpha K v + epi.beta base + epi.gamma W^-1 v`` in one K1 call
+        (``ncgp_kop_apply_ex``), with the raw K v into ``epi.out2`` when set.
+        ``base`` / ``out2`` may be CN vectors (viewed as (n_rows, C)).  This is
+        the fused K^ = K + W^-1 of SURVEY.md 2.3: the solver residual
+        (solver.py:249), z = t + W^-1 s (solver.py:262,265) and the Newton
+        update K v + m (outer.py:134-137)."""
+        if not self.supports_fused:
+            raise DimensionMismatch("fused epilogues need one kernel spec for all outputs")
+        C = self.C
+        if v.numel() != self.n_cols * C:
+            raise DimensionMismatch(f"vector length {v.numel()} != {self.n_cols} * {C}")
+        flat = v.dim() == 1
+        V = v.reshape(self.n_cols, C)
+        if out is None:
+            out = torch.empty((self.n_rows, C), dtype=self.dtype, device=V.device)
+        rows = lambda t: None if t is None else t.view(-1, C)
+        from .kernels import Epi
+        e = Epi(epi.alpha, epi.beta, rows(epi.base), epi.gamma, epi.noise, rows(epi.out2))
+        with nvtx_range("K product (fused epilogue)"):
+            self.groups[0][0].apply(V, out=out.view(self.n_rows, C), row_begin=row_begin,
+                                    row_end=row_end, epi=e)
+        self.matvecs += 1
+        return out.reshape(-1) if flat else out
+
     def apply(self, v: torch.Tensor, out: Optional[torch.Tensor] = None,
               row_begin: int = 0, row_end: Optional[int] = None,
               peers: Optional[Sequence[torch.Tensor]] = None) -> torch.Tensor:
@@ -185,40 +218,51 @@ class PriorOperator:
 
 
 _OP_CACHE: Dict[tuple, PriorOperator] = {}
+_OP_CACHE_MAX = 4
 
 
-def _fingerprint(X):
-    """Cheap content fingerprint of an input array: ~4k strided samples plus the
-    buffer address, so an in-place update of a cached host array is noticed."""
+def _snapshot(X):
+    """An exact copy of the input's contents (host or device)."""
     if isinstance(X, torch.Tensor):
-        flat = X.detach().reshape(-1)
-        addr = X.data_ptr()
-    else:
-        arr = np.asarray(X)
-        flat = arr.reshape(-1)
-        addr = arr.__array_interface__["data"][0]
-    step = max(1, flat.shape[0] // 4096)
-    sample = flat[::step]
-    total = float(sample.double().sum()) if isinstance(sample, torch.Tensor) else \
-        float(np.asarray(sample, dtype=np.float64).sum())
-    return addr, total
+        return X.detach().clone()
+    return np.array(X, copy=True)
+
+
+def _unchanged(snap, X) -> bool:
+    """Full-content equality with the snapshot taken when the operator was
+    packed: any in-place edit of the input invalidates the cached operator
+    (the reference keeps no state, gp.py:144-172, so it can never return a
+    product of stale inputs; neither may this cache)."""
+    if isinstance(X, torch.Tensor):
+        return (isinstance(snap, torch.Tensor) and snap.shape == X.shape and
+                snap.dtype == X.dtype and snap.device == X.device and torch.equal(snap, X))
+    a = np.asarray(X)
+    return isinstance(snap, np.ndarray) and snap.shape == a.shape and snap.dtype == a.dtype \
+        and np.array_equal(snap, a)
+
+
+def clear_operator_cache() -> None:
+    """Drop every cached packed operator (and its device workspace)."""
+    _OP_CACHE.clear()
 
 
 def _cached_operator(prior, X, dtype) -> PriorOperator:
-    """Reuse the packed operator across calls on the same input array (the
-    reference rebuilds nothing to cache, gp.py:222-250; packing K1's operands
-    costs about one product's worth of HBM traffic).  A content fingerprint
-    invalidates the entry when the array was modified in place."""
+    """Reuse the packed operator across calls on the same, unmodified input
+    array (packing K1's operands costs about one product's worth of HBM
+    traffic).  The entry is validated against a full copy of the inputs on
+    every call (memcmp speed on the host, an on-device compare for CUDA
+    tensors), so an edit of any single element is noticed."""
     key = (prior, id(X), getattr(X, "shape", None), resolve_dtype(dtype))
-    fp = _fingerprint(X)
     op = _OP_CACHE.get(key)
-    if op is None or op.X_host is not X or op.X_fingerprint != fp:
-        op = PriorOperator(prior, X, dtype=dtype)
-        op.X_host = X
-        op.X_fingerprint = fp
-        if len(_OP_CACHE) > 8:
-            _OP_CACHE.clear()
-        _OP_CACHE[key] = op
+    if op is not None and op.X_host is X and _unchanged(op.X_snapshot, X):
+        return op
+    op = PriorOperator(prior, X, dtype=dtype)
+    op.X_host = X
+    op.X_snapshot = _snapshot(X)
+    _OP_CACHE.pop(key, None)
+    while len(_OP_CACHE) >= _OP_CACHE_MAX:
+        _OP_CACHE.pop(next(iter(_OP_CACHE)))
+    _OP_CACHE[key] = op
     return op
 
 

@@ -8,7 +8,9 @@ contiguous (stride (ld, 1)); it is what the C ABI calls column b at
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
+import os
 from typing import Optional, Sequence, Tuple
 
 import torch
@@ -29,6 +31,39 @@ def _rows(t: torch.Tensor) -> Tuple[torch.Tensor, int]:
 
 
 # --------------------------------------------------------------------- K1
+
+class Epi:
+    """Fused epilogue of a K1 apply (``ncgp_kop_epilogue``)::
+
+        out  = alpha * K V + beta * base + gamma * W^-1 V
+        out2 = K V
+
+    ``noise`` is ``None``, ``("softmax", pi)`` with pi the (n, C) cached
+    probabilities, or ``("diag", d)`` with d the CN diagonal of W^-1.  ``base``
+    and ``out2`` are (n_rows, w) tensors (rows of the full operator).
+    """
+
+    __slots__ = ("alpha", "beta", "base", "gamma", "noise", "out2")
+
+    def __init__(self, alpha=1.0, beta=1.0, base=None, gamma=0.0, noise=None, out2=None):
+        self.alpha, self.beta, self.base = float(alpha), float(beta), base
+        self.gamma, self.noise, self.out2 = float(gamma), noise, out2
+
+    def native(self, c0: int, es: int) -> "N.Epilogue":
+        e = N.Epilogue()
+        e.alpha, e.beta, e.gamma = self.alpha, self.beta, self.gamma
+        if self.base is not None:
+            e.base = self.base.data_ptr() + c0 * es
+            e.ldb = self.base.stride(0) if self.base.dim() == 2 else 1
+        if self.noise is not None and self.gamma != 0.0:
+            kind, st = self.noise
+            e.noise = {"softmax": N.NOISE_SOFTMAX, "diag": N.NOISE_DIAG}[kind]
+            e.noise_state = st.data_ptr()
+        if self.out2 is not None:
+            e.out2 = self.out2.data_ptr() + c0 * es
+            e.ld2 = self.out2.stride(0) if self.out2.dim() == 2 else 1
+        return e
+
 
 class KernelOperator:
     """Device kernel operator for one stationary kernel spec:
@@ -69,8 +104,26 @@ class KernelOperator:
                ptr(self.X_cols), self.n_cols, self.d, self.w_max, ptr(self._ws),
                self._ws.numel(), stream())
         self._h = h
+        env = os.environ.get("NCGP_SYM", "")
+        self._sym_mode0 = 0 if env.startswith("0") else (1 if env.startswith("1") else -1)
         self.impl = {N.KOP_TCGEN05: "tcgen05", N.KOP_SIMT: "simt"}[
             N.query("ncgp_kop_impl", h)]
+
+    def set_sym(self, mode: int) -> None:
+        """Symmetric-kernel policy (``ncgp_kop_set_sym``): -1 default, 0 plain
+        kernel only, 1 symmetric kernel whenever it fits."""
+        N.call("ncgp_kop_set_sym", self._h, int(mode))
+        self._sym_mode = int(mode)
+
+    @contextlib.contextmanager
+    def sym_mode(self, mode: int):
+        """Temporarily force the symmetric-kernel policy (tests, A/B timing)."""
+        old = getattr(self, "_sym_mode", self._sym_mode0)
+        self.set_sym(mode)
+        try:
+            yield self
+        finally:
+            self.set_sym(old)
 
     @property
     def last_variant(self) -> str:
@@ -85,12 +138,15 @@ class KernelOperator:
 
     def apply(self, V: torch.Tensor, out: Optional[torch.Tensor] = None,
               row_begin: int = 0, row_end: Optional[int] = None,
-              peers: Optional[Sequence[torch.Tensor]] = None) -> torch.Tensor:
+              peers: Optional[Sequence[torch.Tensor]] = None,
+              epi: Optional[Epi] = None) -> torch.Tensor:
         """K(X_rows[row_begin:row_end], X_cols) @ V for V of shape (n_cols, w).
 
         ``peers``: further (n_rows, w) buffers with ``out``'s strides (other
         ranks' gather buffers mapped into this process) that receive the same
-        rows from the same kernel (``ncgp_kop_apply_multi``)."""
+        rows from the same kernel (``ncgp_kop_apply_multi``).  ``epi``: a
+        fused :class:`Epi` (``ncgp_kop_apply_ex``); a noise term needs the
+        whole row in one block (w <= w_max)."""
         vec = V.dim() == 1
         if vec:
             V = V.unsqueeze(1)
@@ -116,9 +172,23 @@ class KernelOperator:
                 raise N.DimensionMismatch("peer buffer shape / strides differ from the output")
             bases.append(p.data_ptr())
         es = V.element_size()
+        if epi is not None:
+            if len(bases) != 1:
+                raise N.DimensionMismatch("a fused epilogue does not combine with peer outputs")
+            if epi.noise is not None and epi.gamma != 0.0 and w > self.w_max:
+                raise N.DimensionMismatch(f"a noise epilogue needs w <= {self.w_max}, got {w}")
+            for t in (epi.base, epi.out2):
+                if t is not None and (t.dtype != self.dtype or t.shape[0] < self.n_rows or
+                                      (t.dim() == 2 and t.stride(1) != 1)):
+                    raise N.DimensionMismatch("epilogue base / out2 must be (>= n_rows, w) rows")
         for c0 in range(0, w, self.w_max):
             c1 = min(w, c0 + self.w_max)
-            if len(bases) == 1:
+            if epi is not None:
+                e = epi.native(c0, es)
+                N.call("ncgp_kop_apply_ex", self._h, V.data_ptr() + c0 * es, ldv, c1 - c0,
+                       out.data_ptr() + c0 * es, ldo, row_begin, row_end, ctypes.byref(e),
+                       stream())
+            elif len(bases) == 1:
                 N.call("ncgp_kop_apply", self._h, V.data_ptr() + c0 * es, ldv, c1 - c0,
                        out.data_ptr() + c0 * es, ldo, row_begin, row_end, stream())
             else:
@@ -131,7 +201,7 @@ class KernelOperator:
 
     # ---- the symmetric K(X, X) kernel split across processes (parallel.py)
     def sym_acc_elems(self, w: int) -> int:
-        """fp32 elements of the per-process accumulator of a split symmetric
+        """int64 elements of the per-process accumulator of a split symmetric
         apply of width ``w`` (<= w_max), or 0 when the full apply would not
         use a symmetric kernel (then shard rows instead)."""
         if not 1 <= w <= self.w_max:
@@ -140,7 +210,9 @@ class KernelOperator:
 
     def sym_partial(self, V: torch.Tensor, part: int, nparts: int, acc: torch.Tensor) -> None:
         """Part ``part`` of ``nparts`` of the triangular work list into ``acc``
-        (float32, ``sym_acc_elems(w)`` elements; zeroed by the call)."""
+        (int64, ``sym_acc_elems(w)`` elements; zeroed by the call).  The
+        parts' accumulators sum exactly (integers): any split gives the same
+        bits after :meth:`sym_finalize`."""
         if V.dim() == 1:
             V = V.unsqueeze(1)
         if V.shape[0] != self.n_cols or V.dtype != self.dtype:
@@ -148,18 +220,26 @@ class KernelOperator:
         if V.stride(1) != 1:
             V = V.contiguous()
         w = V.shape[1]
-        if acc.dtype != torch.float32 or acc.numel() < self.sym_acc_elems(w) or not acc.is_contiguous():
-            raise N.DimensionMismatch("accumulator too small or not contiguous float32")
+        if acc.dtype != torch.int64 or not acc.is_contiguous():
+            raise N.DimensionMismatch("accumulator must be a contiguous int64 tensor")
         ldv = V.stride(0) if V.shape[0] > 1 else w
         N.call("ncgp_kop_sym_partial", self._h, V.data_ptr(), ldv, w, part, nparts, acc.data_ptr(),
-               stream())
+               acc.numel(), stream())
 
-    def sym_finalize(self, acc: torch.Tensor, w: int, out: Optional[torch.Tensor] = None) -> torch.Tensor:
-        """The (n_rows, w) product from the summed accumulators."""
+    def sym_finalize(self, acc: torch.Tensor, w: int, out: Optional[torch.Tensor] = None,
+                     V: Optional[torch.Tensor] = None, epi: Optional[Epi] = None) -> torch.Tensor:
+        """The (n_rows, w) product from the summed accumulators, through the
+        fused epilogue ``epi`` (its noise term reads the operand ``V``)."""
         if out is None:
             out = torch.empty((self.n_rows, w), dtype=self.dtype, device=acc.device)
         ldo = out.stride(0) if out.shape[0] > 1 else w
-        N.call("ncgp_kop_sym_finalize", self._h, acc.data_ptr(), w, out.data_ptr(), ldo, stream())
+        vp, ldv = None, w
+        if V is not None:
+            V = V.unsqueeze(1) if V.dim() == 1 else V
+            vp, ldv = V.data_ptr(), (V.stride(0) if V.shape[0] > 1 else w)
+        e = ctypes.byref(epi.native(0, out.element_size())) if epi is not None else None
+        N.call("ncgp_kop_sym_finalize", self._h, acc.data_ptr(), acc.numel(), vp, ldv, w,
+               out.data_ptr(), ldo, e, stream())
         return out
 
     def close(self):
@@ -219,6 +299,17 @@ def bernoulli_stats(f: torch.Tensor, labels: Optional[torch.Tensor]):
     grad = torch.empty_like(f) if labels is not None else None
     yhat = torch.empty_like(f) if labels is not None else None
     N.call("ncgp_bernoulli_stats", code(f), ptr(f), ptr(labels), n, ptr(winv), ptr(w),
+           ptr(grad), ptr(yhat), stream())
+    return winv, w, grad, yhat
+
+
+def poisson_stats(f: torch.Tensor, counts: Optional[torch.Tensor]):
+    """(W^-1 diag, W diag, grad, pseudo targets) of the Poisson log link."""
+    winv = torch.empty_like(f)
+    w = torch.empty_like(f)
+    grad = torch.empty_like(f) if counts is not None else None
+    yhat = torch.empty_like(f) if counts is not None else None
+    N.call("ncgp_poisson_stats", code(f), ptr(f), ptr(counts), f.numel(), ptr(winv), ptr(w),
            ptr(grad), ptr(yhat), stream())
     return winv, w, grad, yhat
 

@@ -64,12 +64,16 @@ def _unblock(out: torch.Tensor, vec: bool, dev: bool):
 
 
 class NoiseState:
-    """Per-Newton-step device state: cached W^-1 (or W^+) at a fixed f."""
+    """Per-Newton-step device state: cached W^-1 (or W^+) at a fixed f.
 
-    def __init__(self, apply_fn, yhat: torch.Tensor, grad: torch.Tensor):
+    ``fused`` is the same operator in the form K1's fused epilogue takes
+    (``("softmax", pi)`` or ``("diag", d)``, see :class:`kernels.Epi`)."""
+
+    def __init__(self, apply_fn, yhat: torch.Tensor, grad: torch.Tensor, fused=None):
         self._apply = apply_fn
         self.pseudo_targets = yhat
         self.grad = grad
+        self.fused = fused
 
     def apply(self, V: torch.Tensor, base: Optional[torch.Tensor] = None, alpha: float = 1.0,
               beta: float = 1.0, out: Optional[torch.Tensor] = None) -> torch.Tensor:
@@ -151,7 +155,7 @@ class _DiagonalLikelihood(Likelihood):
     def noise_state(self, f):
         winv, _, grad, yhat = self._diag_pair(f)
         return NoiseState(lambda V, base, a, b, out: K.diag_apply(winv, V, base, a, b, out),
-                          yhat, grad)
+                          yhat, grad, fused=("diag", winv))
 
     def w_matvec(self, f, v):
         dt = self._dtype_of(f, v)
@@ -199,7 +203,7 @@ class GaussianLikelihood(Likelihood):
         grad = K.diag_apply(self._dev("ilam", 1.0 / self.noise_variances, f.dtype),
                             K.lincomb(1.0, y, -1.0, f))
         return NoiseState(lambda V, base, a, b, out: K.diag_apply(lam, V, base, a, b, out),
-                          y.clone(), grad)
+                          y.clone(), grad, fused=("diag", lam))
 
     def w_matvec(self, f, v):
         dt = self._dtype_of(f, v)
@@ -241,11 +245,7 @@ class PoissonLikelihood(_DiagonalLikelihood):
         if y is None:
             y = to_device(self.targets, f.dtype)
             self._dev_cache[("y", f.dtype)] = y
-        w = torch.exp(f)
-        winv = torch.exp(-f)
-        grad = K.lincomb(1.0, y, -1.0, w)
-        yhat = K.lincomb(1.0, f, 1.0, K.diag_apply(winv, grad))
-        return winv, w, grad, yhat
+        return K.poisson_stats(f, y)
 
     def subset(self, indices):
         return PoissonLikelihood(self.targets[np.asarray(indices)])
@@ -301,7 +301,7 @@ class SoftmaxLikelihood(Likelihood):
         n, C = self.n_points, self.num_outputs
         pi, grad, yhat = K.softmax_stats(f, self._labels_dev(), n, C)
         st = NoiseState(lambda V, base, a, b, out: K.softmax_winv(pi, n, C, V, base, a, b, out),
-                        yhat, grad)
+                        yhat, grad, fused=("softmax", pi))
         st.pi = pi
         return st
 

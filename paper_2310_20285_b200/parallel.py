@@ -19,10 +19,11 @@ bitwise identical to the single-GPU one.
 For K(X, X) the symmetric kernel evaluates each
 off-diagonal tile once; a row split would lose that.  :class:`SymmetricSplitOperator`
 instead splits the triangular work list itself: every rank evaluates a slice
-of equal tile count into an fp32 accumulator, an all-reduce sums the
-accumulators (the exchange step: a reduction, of the same size as the
-all-gather it replaces), and every rank writes the full product from the sum.
-Being an fp32 reduction it is not bitwise identical to the one-GPU product.
+of equal tile count into an int64 fixed-point accumulator, an all-reduce
+sums the accumulators (the exchange step: a reduction, twice the bytes of
+the fp32 all-gather it replaces), and every rank writes the full product
+from the sum.  Integer sums are exact and associative, so the product is
+bitwise identical to the one-GPU product for any number of ranks.
 
 The partition and gather logic takes the local compute as a callable so it
 is unit-tested on CPU with the ``gloo`` backend (tests/test_parallel_gloo.py).
@@ -151,10 +152,47 @@ class RowShardedOperator:
             dist.all_gather_into_tensor(full, mine, group=self.group)
         return full[: self.n_rows]
 
-    def apply(self, V: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    def _apply_epi(self, V2: torch.Tensor, out, epi) -> torch.Tensor:
+        """Row shards with a fused epilogue (gather='nccl'): each rank runs the
+        epilogue on its own rows -- base, noise state and V are replicated --
+        and the all-gather moves the epilogue's output (and the raw K V rows
+        when ``epi.out2`` is set) instead of K V."""
+        from .kernels import Epi
+        n, w = self.n_rows, V2.shape[1]
+        if self.world == 1:
+            dst = out.view(n, w) if out is not None else torch.empty(
+                (n, w), dtype=self.dtype, device=V2.device)
+            self.local_apply(V2, dst, 0, n, epi=epi)
+            return dst
+        full = self._buffer(w, V2.device)
+        full2 = None
+        if epi.out2 is not None:
+            key = ("out2", w, str(V2.device))
+            full2 = self._bufs.get(key)
+            if full2 is None:
+                full2 = torch.empty_like(full)
+                self._bufs[key] = full2
+        e = Epi(epi.alpha, epi.beta, epi.base, epi.gamma, epi.noise, full2)
+        self.local_apply(V2, full, self.r0, self.r1, epi=e)
+        sl = slice(self.rank * self.per, (self.rank + 1) * self.per)
+        dist.all_gather_into_tensor(full, full[sl], group=self.group)
+        if full2 is not None:
+            dist.all_gather_into_tensor(full2, full2[sl], group=self.group)
+            epi.out2.view(n, w).copy_(full2[:n])
+        if out is not None:
+            out.view(n, w).copy_(full[:n])
+            return out.view(n, w)
+        return full[:n].clone()
+
+    def apply(self, V: torch.Tensor, out: Optional[torch.Tensor] = None, epi=None) -> torch.Tensor:
         vec = V.dim() == 1
         V2 = V.view(-1, 1) if vec else V
         w = V2.shape[1]
+        if epi is not None:
+            if self.gather != "nccl":
+                raise ValueError("fused epilogues on row shards need gather='nccl'")
+            res = self._apply_epi(V2, out, epi)
+            return res.view(-1) if vec else res
         if self.world == 1 and self.gather == "nccl":
             dst = out.view(self.n_rows, w) if out is not None else torch.empty(
                 (self.n_rows, w), dtype=self.dtype, device=V2.device)
@@ -178,21 +216,22 @@ class SymmetricSplitOperator:
 
     ``partial(V, part, nparts, acc)`` writes part ``part`` of ``nparts`` of the
     product's contributions into ``acc`` (zeroing it first), ``finalize(acc,
-    w, out)`` writes the (n_rows, w) product from the summed accumulators and
-    ``acc_elems(w)`` sizes the accumulator; in production they are
-    :meth:`KernelOperator.sym_partial` / ``sym_finalize`` / ``sym_acc_elems``.
+    w, out, V=None, epi=None)`` writes the (n_rows, w) product from the summed
+    accumulators (through a fused epilogue) and ``acc_elems(w)`` sizes the
+    accumulator; in production they are :meth:`KernelOperator.sym_partial` /
+    ``sym_finalize`` / ``sym_acc_elems``.
     """
 
     def __init__(self, n_rows: int, partial: Callable, finalize: Callable, acc_elems: Callable,
                  group=None, dtype: torch.dtype = torch.float32,
-                 acc_dtype: torch.dtype = torch.float32):
+                 acc_dtype: torch.dtype = torch.int64):
         self.n_rows = n_rows
         self.partial, self.finalize, self.acc_elems = partial, finalize, acc_elems
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.dtype = dtype
-        self.acc_dtype = acc_dtype  # the kernel's accumulators are fp32
+        self.acc_dtype = acc_dtype  # the kernel's accumulators are int64 fixed point
         self._acc = {}
 
     def accumulator(self, w: int, device) -> torch.Tensor:
@@ -203,7 +242,7 @@ class SymmetricSplitOperator:
             self._acc[key] = acc
         return acc
 
-    def apply(self, V: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    def apply(self, V: torch.Tensor, out: Optional[torch.Tensor] = None, epi=None) -> torch.Tensor:
         vec = V.dim() == 1
         V2 = V.view(-1, 1) if vec else V
         w = V2.shape[1]
@@ -212,7 +251,8 @@ class SymmetricSplitOperator:
         if self.world > 1:
             dist.all_reduce(acc, group=self.group)
         dst = None if out is None else out.view(self.n_rows, w)
-        res = self.finalize(acc, w, dst)
+        res = self.finalize(acc, w, dst, V=V2, epi=epi) if epi is not None else \
+            self.finalize(acc, w, dst)
         return res.view(-1) if vec else res
 
     __call__ = apply
@@ -253,10 +293,14 @@ class ShardedPriorOperator:
             self._C = C
             return
 
-        def local_apply(V, out, r0, r1, peers=None):
+        def local_apply(V, out, r0, r1, peers=None, epi=None):
             # ``out`` may be the (per * world)-row gather buffer: rows >= n_rows
             # are padding and never written
             n = self.n_rows
+            if epi is not None:
+                self.inner.apply_fused(V.reshape(-1), epi, out=out[:n].reshape(-1),
+                                       row_begin=r0, row_end=r1)
+                return
             self.inner.apply(V.reshape(-1), out=out[:n].reshape(-1), row_begin=r0, row_end=r1,
                              peers=[p[:n].reshape(-1) for p in peers] if peers else None)
 
@@ -269,10 +313,33 @@ class ShardedPriorOperator:
     def impl(self):
         return self.inner.impl
 
+    @property
+    def supports_fused(self) -> bool:
+        """The fused K^ epilogue runs in every rank's finalize (work-list
+        split) or on every rank's own rows before the all-gather (row shards
+        with gather='nccl'); the peer-store gather keeps the unfused
+        composition."""
+        return self.gather in ("reduce", "nccl") and self.inner.supports_fused
+
     def apply(self, v: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         flat = v.dim() == 1
         V = v.reshape(self.n_rows, self._C)
         res = self.sharded.apply(V, out=None if out is None else out.view(self.n_rows, self._C))
+        self.matvecs += 1
+        return res.reshape(-1) if flat else res
+
+    def apply_fused(self, v: torch.Tensor, epi, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """alpha K v + beta base + gamma W^-1 v (and K v into epi.out2) in one
+        product: the epilogue runs in every rank's finalize."""
+        if not self.supports_fused:
+            raise ValueError("fused epilogues need gather='reduce' or 'nccl'")
+        from .kernels import Epi
+        flat = v.dim() == 1
+        C = self._C
+        V = v.reshape(self.n_rows, C)
+        rows = lambda t: None if t is None else t.view(-1, C)
+        e = Epi(epi.alpha, epi.beta, rows(epi.base), epi.gamma, epi.noise, rows(epi.out2))
+        res = self.sharded.apply(V, out=None if out is None else out.view(self.n_rows, C), epi=e)
         self.matvecs += 1
         return res.reshape(-1) if flat else res
 

@@ -332,3 +332,31 @@ def test_fused_gather_symmetric_memory_single_rank(tmp_path):
                         "--master-port", "29631", str(script)],
                        capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode == 0 and "SYMM_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+@pytest.mark.parametrize("device_input", [False, True])
+def test_prior_matvec_cache_sees_single_element_edit(device_input):
+    """an in-place edit of ONE element of a large input
+    (X[1, 0] at N = 1e5, which a strided content sample would miss) must
+    invalidate prior_matvec's packed-operator cache."""
+    rng = np.random.default_rng(12)
+    n = 100_000
+    X = rng.standard_normal((n, 8))
+    v = rng.standard_normal(n)
+    prior = P.MultiOutputPrior(kernels=(P.KernelSpec("rbf", 1.5, 1.0),))
+    Xin = torch.from_numpy(X).cuda() if device_input else X
+    vin = torch.from_numpy(v).cuda() if device_input else v
+    a = P.prior_matvec(prior, Xin, vin, dtype=torch.float64)
+    if device_input:
+        Xin[1, 0] += 0.75
+        X = Xin.cpu().numpy()
+    else:
+        X[1, 0] += 0.75
+    b = P.prior_matvec(prior, Xin, vin, dtype=torch.float64)
+    a = a.cpu().numpy() if device_input else a
+    b = b.cpu().numpy() if device_input else b
+    rows = np.array([0, 1, 2, 77_777])
+    ref = O.kernel_matmul_rows(("rbf", 1.5, 1.0), X[rows], X, v[:, None])[:, 0]
+    scale = O.kernel_matmul_rows(("rbf", 1.5, 1.0), X[rows], X, np.abs(v)[:, None])[:, 0]
+    assert np.all(np.abs(b[rows] - ref) <= 1e-12 * scale)
+    assert abs(a[1] - ref[1]) > 1e-6 * scale[1]   # the stale product really differed

@@ -72,13 +72,24 @@ def test_bernoulli_kernels(dt, tol):
     assert rel(lik.grad_log_lik(f).cpu().numpy(), g["be_grad"]) < tol
     w = lik.w_inv_matvec(f, dev(g["be_v"], dt)).cpu().numpy()
     assert np.isfinite(w).all()
-    # entry 2 (f=40) is in the reference's own cancellation regime: skip it in fp64
-    mask = np.ones(len(w), bool)
-    mask[2] = False
-    assert rel(w[mask], g["be_winv_v"][mask]) < tol * 10
-    assert rel(lik.w_matvec(f, dev(g["be_v"], dt)).cpu().numpy(), g["be_w_v"]) < tol
     yh = P.pseudo_targets(lik, f).cpu().numpy()
-    assert rel(yh[mask], g["be_yhat"][mask]) < tol * 10
+    assert rel(lik.w_matvec(f, dev(g["be_v"], dt)).cpu().numpy(), g["be_w_v"]) < tol
+    if dt == F64:
+        # the reference clamp verbatim (likelihoods.py:210-212): every entry,
+        # the saturated f = +-500 and f = 40 included, to 1e-12
+        assert rel(w, g["be_winv_v"]) < tol
+        assert rel(yh, g["be_yhat"]) < tol
+        np.testing.assert_allclose(w, g["be_winv_v"], rtol=1e-13)
+        return
+    # fp32: 1 - 1e-12 rounds to 1, so the floor is applied to s * sigma(-f)
+    # (SURVEY.md 8(a) a12).  At f = 40 that gives W^-1 = 1e12 exactly, where the
+    # fp64 reference gets 1 / ((1 - 1e-12) (1 - (1 - 1e-12))) = 1.0000221e12 from
+    # the cancellation in 1 - (1 - 1e-12): a 2.2e-5 relative difference on that
+    # one entry, larger than the fp32 bound the other entries meet.
+    sat = np.abs(g["be_f"]) >= 40
+    assert np.allclose(w[sat], g["be_winv_v"][sat], rtol=3e-5)
+    assert rel(w[~sat], g["be_winv_v"][~sat]) < tol
+    assert rel(yh[~sat], g["be_yhat"][~sat]) < tol
 
 
 def _solver_setup(dt):
@@ -209,6 +220,69 @@ def test_fit_cfg2_small_recycling(dt):
         assert [s.inner_iterations for s in trace.steps] == list(g["steps_iters"])
 
 
+def _spread():
+    import json
+    import os
+    from conftest import GOLDEN
+    return json.load(open(os.path.join(GOLDEN, "fit_cfg2_spread.json")))
+
+
+@pytest.mark.parametrize("dt", [F64, F32])
+def test_fit_cfg2_full_size(dt):
+    """BASELINE cfg2 at its full size (N = 5000, C = 3, 1000 test points, RBF
+    l = 1 s2 = 2, residual policy, 10 x 50, recycling) against the reference's
+    own fit (tests/golden/fit_cfg2_full.npz, outer.py:149-257).
+
+    Asserted: latent mean within 1e-3, >= 99.9 % identical
+    labels.  The marginal variance is reported beside the reference's own
+    spread: the same reference fit with its K products perturbed by 1e-14
+    moves the variance by ~1e-2 (tests/golden/fit_cfg2_spread.json), so a
+    1e-3 variance bound cannot hold for any implementation whose rounding
+    differs; it is asserted at 3x that spread (fp64) and 10x (fp32)."""
+    import json
+    import os
+    g = golden("fit_cfg2_full")
+    sp = _spread()
+    prior = P.MultiOutputPrior(kernels=(P.KernelSpec("rbf", 1.0, 2.0),) * 3)
+    ds = P.Dataset(g["X"], g["y"], "class-index", 3)
+    lik = P.SoftmaxLikelihood(ds.targets, 3)
+    belief, trace = P.fit(prior, ds, lik,
+                          P.OuterConfig(max_newton_steps=10, delta=0.01, inner_schedule=50,
+                                        recycle=True),
+                          P.InnerConfig(max_iters=1), policy_kind="residual", dtype=dt)
+    mean = P.posterior_mean(belief, g["X_test"])
+    var = P.posterior_marginal_var(belief, g["X_test"])
+    probs = P.probit_predict(mean, var)
+    report = {
+        "dtype": str(dt), "steps_iters": [s.inner_iterations for s in trace.steps],
+        "ref_steps_iters": [int(i) for i in g["steps_iters"]],
+        "ref_spread_steps_iters": sp["steps_iters"],
+        "total_matvecs": trace.total_kernel_matvecs, "ref_total_matvecs": int(g["total_matvecs"]),
+        "weights_rel": rel(belief.weights, g["weights"]), "ref_spread_weights_rel": sp["weights_rel"],
+        "mean_rel": rel(mean, g["mean"]), "ref_spread_mean_rel": sp["mean_rel"],
+        "var_rel": rel(var, g["var"]), "ref_spread_var_rel": sp["var_rel"],
+        "label_agreement": float(np.mean(probs.argmax(1) == g["probs"].argmax(1))),
+        "test_accuracy": float(np.mean(probs.argmax(1) == g["y_test"])),
+        "ref_test_accuracy": float(np.mean(g["probs"].argmax(1) == g["y_test"])),
+        "wallclock_s": trace.wallclock_s, "ref_wallclock_s_cpu": float(g["wallclock_s"]),
+    }
+    out = os.environ.get("NCGP_REPORT_DIR")
+    if out:
+        os.makedirs(out, exist_ok=True)
+        with open(os.path.join(out, f"cfg2_full_{'f64' if dt == F64 else 'f32'}.json"), "w") as fh:
+            json.dump(report, fh, indent=1)
+    print(report)
+    assert report["mean_rel"] < 1e-3, report
+    assert report["label_agreement"] >= 0.999, report
+    assert report["var_rel"] < (3.0 if dt == F64 else 10.0) * sp["var_rel"], report
+    if dt == F64:
+        # the reference's own 1e-14 spread moves 6 + 6 iterations ([.., 49, 50] -> [.., 43, 50])
+        assert abs(sum(report["steps_iters"]) - sum(report["ref_steps_iters"])) <= 15, report
+    # (fp32: the explicit residual r = rhs - K^ v cannot fall below the fp32
+    # rounding of K^ v, ~1e-6 |rhs|, so the 1e-5 relative tolerance exit
+    # (solver.py:252) rarely fires and every step runs its 50-iteration budget)
+
+
 def test_fit_cfg4_small_compressed():
     g = golden("fit_cfg4s")
     prior = P.MultiOutputPrior(kernels=(P.KernelSpec("matern32", 3.0, 1.0),) * 10)
@@ -325,11 +399,14 @@ def test_recurrence_residual_mode_matches_explicit():
                                     P.make_policy("residual", 180), buf,
                                     P.InnerConfig(max_iters=12, residual=mode))
     e, r = runs["explicit"], runs["recurrence"]
-    assert r.iterations_run == e.iterations_run
+    assert r.iterations_run == e.iterations_run == int(g["r_iters"])
     assert r.kernel_matvecs == r.iterations_run
     assert e.kernel_matvecs == int(g["r_matvecs"])
     assert rel(r.weights.cpu().numpy(), e.weights.cpu().numpy()) < 1e-9
     assert rel(r.root.columns, e.root.columns) < 1e-9
+    # against the reference's own iterates (golden solver.npz)
+    assert rel(r.weights.cpu().numpy(), g["r_weights"]) < 1e-8
+    assert rel(r.root.columns, g["r_Q"]) < 1e-8
     # from a recycled belief: K^ Q0 comes from the virtual solver run, no products
     n2 = lik.noise_state(dev(g["f2"]))
     outs = {}
@@ -342,8 +419,10 @@ def test_recurrence_residual_mode_matches_explicit():
                                     P.InnerConfig(max_iters=6, residual=mode),
                                     initial_root=root)
     assert outs["recurrence"].kernel_matvecs == outs["recurrence"].iterations_run
+    assert outs["recurrence"].iterations_run == int(g["r2_iters"])
     assert rel(outs["recurrence"].weights.cpu().numpy(),
                outs["explicit"].weights.cpu().numpy()) < 1e-8
+    assert rel(outs["recurrence"].weights.cpu().numpy(), g["r2_weights"]) < 1e-7
 
 
 def test_fit_recurrence_mode_cfg2_small():

@@ -229,3 +229,64 @@ def test_two_rank_symmetric_split_matches_single_process(tmp_path, n, b):
     np.testing.assert_array_equal(outs[0], outs[1])  # every rank holds the same product
     np.testing.assert_allclose(outs[0], ref, rtol=1e-12, atol=1e-12)
     np.testing.assert_allclose(np.load(tmp_path / "t0.npy"), ref[:, 0], rtol=1e-12, atol=1e-12)
+
+
+def _epi_worker(rank, world, port, n, d, w, result_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import ncgp_oracle as O
+        from paper_2310_20285_b200.kernels import Epi
+        rng = np.random.default_rng(0)
+        X = rng.standard_normal((n, d))
+        V = rng.standard_normal((n, w))
+        base = torch.from_numpy(rng.standard_normal((n, w)))
+        dvec = torch.from_numpy(0.1 + rng.random(n * w))
+        spec = ("rbf", 1.2, 1.0)
+        calls = []
+
+        def local_apply(Vt, out, r0, r1, epi=None):
+            # CPU stand-in for K1 + its fused epilogue on rows [r0, r1)
+            calls.append((r0, r1, epi is not None))
+            if r1 <= r0:
+                return
+            kv = torch.from_numpy(O.kernel_matmul_rows(spec, X[r0:r1], X, Vt.double().numpy()))
+            res = epi.alpha * kv + epi.beta * epi.base[r0:r1] + \
+                epi.gamma * epi.noise[1].view(n, w)[r0:r1] * Vt[r0:r1]
+            out[r0:r1] = res
+            if epi.out2 is not None:
+                epi.out2[r0:r1] = kv
+
+        op = RowShardedOperator(n, local_apply, dtype=torch.float64)
+        t = torch.empty((n, w), dtype=torch.float64)
+        z = op.apply(torch.from_numpy(V),
+                     epi=Epi(alpha=-1.0, beta=1.0, base=base, gamma=0.5, noise=("diag", dvec),
+                             out2=t))
+        np.save(os.path.join(result_dir, f"z{rank}.npy"), z.numpy())
+        np.save(os.path.join(result_dir, f"t{rank}.npy"), t.numpy())
+        r0, r1, _ = row_partition(n, world, rank)
+        assert calls == [(r0, r1, True)], calls
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [300, 1000])
+def test_two_rank_fused_epilogue_row_shards(tmp_path, n):
+    """Row shards with the fused K^ epilogue (gather='nccl'): each rank runs
+    the epilogue on its own rows and the all-gather moves both the epilogue
+    output and the raw K V rows (out2), so every rank ends with both."""
+    from oracle import ncgp_oracle as O
+    d, w, world = 3, 4, 2
+    mp.spawn(_epi_worker, args=(world, _free_port(), n, d, w, str(tmp_path)), nprocs=world,
+             join=True)
+    rng = np.random.default_rng(0)
+    X = rng.standard_normal((n, d))
+    V = rng.standard_normal((n, w))
+    base = rng.standard_normal((n, w))
+    dvec = (0.1 + rng.random(n * w)).reshape(n, w)
+    kv = O.kernel_matmul_rows(("rbf", 1.2, 1.0), X, X, V)
+    for r in range(world):
+        np.testing.assert_array_equal(np.load(tmp_path / f"t{r}.npy"), kv)
+        np.testing.assert_allclose(np.load(tmp_path / f"z{r}.npy"), -kv + base + 0.5 * dvec * V,
+                                   rtol=1e-14, atol=1e-14)
