@@ -1,16 +1,21 @@
 #!/usr/bin/env python
-"""Benchmark: fused kernel-operator product K(X, X) S on B200 (BASELINE cfg3).
+"""Benchmark: fused kernel-operator product K(X, X) S on B200 (BASELINE cfg3)
+and the IterNCGP fit time (cfg4, and cfg5 = N 1M, C 10).
 
-BASELINE.json metric: "fused K^.S GFLOP/s (%roofline) ...".  One step is one
-kernel-operator product over the cfg3 workload (N = 1e6 points, D = 8,
-S of width 32, RBF l = 1.5; ``--workload cfg3-matern`` for the Matern
-variant) with inputs resident in HBM.  Algorithmic FLOPs per (i, j) pair are
-F = 2D + 2w, i.e. 80 at cfg3.
+BASELINE.json metric: "fused K^.S GFLOP/s (%roofline) and IterNCGP fit time,
+N=1M C=10".  One step is one kernel-operator product over the cfg3 workload
+(N = 1e6 points, D = 8, S of width 32, RBF l = 1.5; ``--workload
+cfg3-matern`` for the Matern variant) with inputs resident in HBM.
+Algorithmic FLOPs per (i, j) pair are F = 2D + 2w,
+i.e. 80 at cfg3.  The same JSON line carries, under ``fit``, the end-to-end
+fit time of cfg4 and cfg5 (``FitTrace.wallclock_s``, outer.py:103-126,
+253-255), its K-product count and the reference CPU time extrapolated from
+the reference tile body timed on sample rows.
 
-Multi-GPU (torchrun): contiguous row blocks of X (multiples of 128 rows) per
-rank, X and S replicated, and each step ends with the all-gather of the
-output row blocks (the exchange the solver needs before the next product).
-Total work is fixed as N grows -> "strong" scaling.
+Multi-GPU (torchrun): the symmetric kernel's work list split across ranks
+with an int64 all-reduce (``--gather reduce``, the default when available),
+or contiguous row blocks with the output all-gathered.  Total work is fixed
+as N grows -> "strong" scaling.
 
 ``--impl reference`` times the reference algorithm's CPU implementation (the
 numpy restatement in oracle/, bit-identical to the reference, run with all
@@ -51,6 +56,38 @@ def workload(name):
     fam = "matern32" if name.endswith("matern") else "rbf"
     c = configs.cfg3(family=fam)
     return c
+
+
+def product_config(c):
+    """The workload-defining config, identical in both arms (``same_config``)."""
+    X, S, spec = c["X"], c["S"], c["kernel"]
+    n, d = X.shape
+    w = S.shape[1]
+    return {"workload": c["name"], "n": int(n), "d": int(d), "w": int(w), "kernel": list(spec),
+            "flops_per_pair": 2 * d + 2 * w, "exp_per_pair": 1 if spec[0] == "rbf" else 2,
+            "l2": "flushed (256 MiB write) before every timed GPU step; fresh random rows per "
+                  "CPU step"}
+
+
+def executed_per_pair(variant, d, w, n):
+    """Executed tensor flops and evaluated-pair fraction of a K1 variant
+    (DESIGN.md 3.1/3.1b): GEMM1 2 ka, GEMM2 2 (2 WP + WP) per evaluated
+    pair, plus the symmetric kernels' transposed product on off-diagonal
+    tiles (pair kernel: N = 2 WP per CTA pair, half of it discarded)."""
+    ka = -(-(3 * d + 4) // 16) * 16
+    wp = 16 if w <= 16 else 32
+    nb = -(-n // 128)
+    base = 2 * ka + 6 * wp
+    if variant == 2:        # single-CTA symmetric kernel: row tile r covers [r, nb)
+        ev = (nb + 1) / (2.0 * nb)
+        tfrac = (nb - 1) / (nb + 1.0)
+        return base + 6 * wp * tfrac, ev
+    if variant == 1:        # pair kernel: row-tile pair a covers [2a, nb)
+        tiles = sum(nb - 2 * a for a in range((nb + 1) // 2))
+        trans = sum(max(0, nb - 2 * a - 2) for a in range((nb + 1) // 2))
+        ev = 2.0 * tiles / (nb * nb)
+        return base + 12 * wp * trans / max(tiles, 1), ev
+    return float(base), 1.0
 
 
 class ClockSampler(threading.Thread):
@@ -148,12 +185,11 @@ def run_reference(args, rank, world):
         "value": round(value, 4), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(1e3 * statistics.mean(times), 3),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": c["name"], "n": n, "d": d, "w": w,
-                                        "kernel": list(spec), "flops_per_pair": F},
+        "data": "synthetic", "config": product_config(c),
         "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", "cores": cores,
                          "kind": "port",
                          "sample": f"{rows_per_step} random rows x all {n} columns per step "
-                                   f"(reference tile body gp.py:240-249, numpy fp64, "
+                                   f"(reference tile body gp.py:162-171, numpy fp64, "
                                    f"{cores} worker processes)"},
         "e2e": {"value": round(value, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -187,13 +223,14 @@ def run_ours(args, rank, world, local_rank):
     # symmetric memory and K1 stores every row into all ranks' buffers
     # (parallel.RowShardedOperator implements both).
     # reduce: the symmetric kernel's triangular work list is split across the
-    # ranks and an NCCL all-reduce sums the fp32 accumulators
-    # (parallel.SymmetricSplitOperator); auto takes it when available.
+    # ranks and an NCCL all-reduce sums the int64 fixed-point accumulators
+    # (parallel.SymmetricSplitOperator; exact, so 1 and N GPUs give the same
+    # bits); auto takes it when available.
     gather = args.gather
     if gather == "auto":
         gather = "reduce" if world > 1 and op.sym_acc_elems(w) > 0 else "nccl"
     reduce_ = world > 1 and gather == "reduce"
-    acc = torch.empty(max(1, op.sym_acc_elems(w)), dtype=torch.float32, device=dev) if reduce_ else None
+    acc = torch.empty(max(1, op.sym_acc_elems(w)), dtype=torch.int64, device=dev) if reduce_ else None
     fused = world > 1 and gather == "fused"
     peer_rows = None
     if fused:
@@ -305,6 +342,26 @@ def run_ours(args, rank, world, local_rank):
                          device=dev)
     if world > 1:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_np = None
+    if world == 1:
+        # the reference's own call shape: numpy fp64 X and v in, numpy fp64
+        # out (gp.py:144-172), pageable host memory both ways
+        Snp = np.ascontiguousarray(S).reshape(-1)
+        call_np = lambda: P.prior_matvec(prior, X, Snp, dtype=torch.float32)  # noqa: E731
+        call_np()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        k_np = max(1, min(3, args.steps))
+        for _ in range(k_np):
+            r_np = call_np()
+        torch.cuda.synchronize()
+        s_np = (time.perf_counter() - t0) / k_np
+        e2e_np = {"value": round(F * pairs / s_np / 1e9, 3), "unit": "GFLOP/s",
+                  "ms_per_call": round(1e3 * s_np, 2),
+                  "h2d_bytes_per_step": int(Snp.nbytes), "d2h_bytes_per_step": int(r_np.nbytes),
+                  "note": "gp.prior_matvec(prior, X, v) with numpy fp64 X and v (pageable), numpy "
+                          "fp64 result: the reference's signature; the cached operator is "
+                          "validated against a full copy of X every call"}
     e2e = {"value": round(F * pairs / float(e2e_s[0]) / 1e9, 3), "unit": "GFLOP/s",
            "h2d_bytes_per_step": int(Sh.numel() * 4),
            "d2h_bytes_per_step": int(res.numel() * res.element_size()),
@@ -317,49 +374,12 @@ def run_ours(args, rank, world, local_rank):
     if reduce_:
         e2e["note"] = ("X resident in the cached operator; S (pinned fp32) uploaded and the product "
                        f"downloaded every step on each of the {world} ranks (symmetric kernel's work "
-                       "list split across ranks, fp32 accumulators summed by an NCCL all-reduce)")
+                       "list split across ranks, int64 accumulators summed by an NCCL all-reduce)")
 
     # ---- roofline of the dominant kernel (the fused kernel-matmul)
-    pk = peaks()
-    sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    mufu_rate = sms * P_MUFU_PER_SM_CLK * pk["sm_max_mhz"] * 1e6   # ex2 / s
-    tensor_tflops = pk["bf16"] / 2.0                                 # tf32-class dense
-    local_pairs = float(n) * n / world if reduce_ else float(r1 - r0) * n
-    t_kernel = kern_total / args.steps / 1e3
-    achieved = F * local_pairs / t_kernel / 1e12
-    peak_tflops = min(tensor_tflops, F * mufu_rate / E / 1e12)
-    # DRAM traffic of the same kernel variant on the same workload, from the
-    # committed ncu --set full capture (profiles/*_summary.json)
-    traffic, traffic_src = None, None
-    captures = {("cfg3", 2): "r01i_summary.json", ("cfg3", 0): "r01e_summary.json"}
-    prof = captures.get((c["name"], op.last_variant_code))
-    if prof and world == 1 and os.path.exists(os.path.join(ROOT, "profiles", prof)):
-        with open(os.path.join(ROOT, "profiles", prof)) as fh:
-            traffic = json.load(fh).get("traffic_bytes_per_launch")
-        traffic_src = f"profiles/{prof} (ncu --set full, dram read+write)"
-    roofline = {"bound": "tensor", "limiter": "MUFU ex2" if peak_tflops < tensor_tflops
-                else "tensor pipe", "achieved": round(achieved, 3), "peak": round(peak_tflops, 3),
-                "unit": "TFLOP/s", "frac": round(achieved / peak_tflops, 4), "traffic": traffic,
-                "traffic_source": traffic_src,
-                "peak_basis": f"min({pk['source']} bf16 {pk['bf16']}/2 TF/s, "
-                              f"{sms} SM x {P_MUFU_PER_SM_CLK} ex2/clk x "
-                              f"{pk['sm_max_mhz']} MHz x F/E={F}/{E})",
-                "kernel_ms": round(1e3 * t_kernel, 3), "impl": op.impl,
-                "variant": {0: "plain", 1: "symmetric (CTA pairs)",
-                            2: "symmetric (single CTA)"}.get(op.last_variant_code, "none")}
-    if op.last_variant_code in (1, 2):
-        # each off-diagonal 128 x 128 tile is evaluated once and serves both
-        # K V and K^T V; `achieved` / `frac` count the algorithmic n^2 pairs
-        nb = -(-n // 128)
-        if op.last_variant_code == 2:  # single-CTA kernel: row tile r covers [r, nb)
-            ev = (nb + 1) / (2.0 * nb)
-        else:                          # pair kernel: row-tile pair a covers [2a, nb)
-            ev = sum(2 * (nb - 2 * a) for a in range((nb + 1) // 2)) / float(nb * nb)
-        roofline["evaluated_pair_fraction"] = round(ev, 4)
-        roofline["frac_executed"] = round(achieved * ev / peak_tflops, 4)
-        roofline["note"] = ("symmetric K(X,X) kernel: evaluated_pair_fraction of the n^2 kernel "
-                            "values are computed; frac_executed is the executed exp rate "
-                            "against the MUFU peak")
+    roofline = product_roofline(op, n, d, w, F, E, world, local_pairs=(
+        float(n) * n / world if reduce_ else float(r1 - r0) * n), t_kernel=kern_total / args.steps / 1e3,
+        dev=dev, workload_name=c["name"])
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -370,29 +390,110 @@ def run_ours(args, rank, world, local_rank):
                "sample": f"{len(rows)} random rows x all {n} columns (reference tile body, "
                          f"numpy fp64, 1 core), {cpu_s:.1f} s"}
 
+    line = None
     if rank == 0:
         line = {"metric": "fused K^.S GFLOP/s (cfg3 K(X,X)S)", "value": round(value, 3),
                 "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": round(total_ms / args.steps, 3), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-                "data": "synthetic",
-                "config": {"workload": c["name"], "n": n, "d": d, "w": w, "kernel": list(spec),
-                           "flops_per_pair": F, "exp_per_pair": E,
-                           "l2": "flushed (256 MiB write) before every timed step",
-                           "parallelism": (f"symmetric work list split x{world}" if reduce_
-                                           else f"row-sharded x{world}"),
-                           "gather": gather if world > 1 else None},
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "data": "synthetic", "config": product_config(c),
+                "parallelism": (f"symmetric work list split x{world}" if reduce_
+                                else f"row-sharded x{world}"),
+                "gather": gather if world > 1 else None,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_numpy_f64": e2e_np,
                 "gpu_launches": int(launches), "clocks": clocks}
+    del op, Xd, Sd, out_full, flush
+    torch.cuda.empty_cache()
+    # the metric's second half: IterNCGP fit time (cfg4, and cfg5 = N 1M C 10)
+    if not args.no_fit:
+        fits = {}
+        for name in args.fits.split(","):
+            if name:
+                fits[name] = measure_fit(name, args, rank, world, local_rank, warmup_fits=1,
+                                         timed_fits=1, cpu_extrapolate=not args.no_cpu_baseline)
+        if line is not None:
+            line["fit"] = fits
+            line["gpu_launches"] = int(line["gpu_launches"]) + sum(
+                int(f["gpu_launches"]) for f in fits.values())
+    if line is not None:
         print(json.dumps(line), flush=True)
     return 0
 
 
-def run_fit(args, rank, world, local_rank):
+def product_roofline(op, n, d, w, F, E, world, local_pairs, t_kernel, dev, workload_name):
+    """Roofline of one K1 launch, two ways.
+
+    - ``frac`` (BASELINE.md section 4 / SURVEY.md 8(d)): ALGORITHMIC flops F
+      per pair over all local pairs, against t* = max(F / P_tensor, E /
+      P_mufu) per pair.  For the symmetric kernels this can exceed 1 (they
+      evaluate half of the kernel values), so it is not a bound there.
+    - ``executed``: the work the kernel actually issues -- tensor flops of
+      the 3-term fp16 GEMMs (kind::f16, against the measured dense bf16
+      peak) and ex2 (+ sqrt) per evaluated pair (against 16 per clock per
+      SM) -- the utilisation of each pipe; ``limiter`` is the busier one.
+    """
+    import torch
+    pk = peaks()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    mufu_rate = sms * P_MUFU_PER_SM_CLK * pk["sm_max_mhz"] * 1e6   # ex2 / s
+    tensor_tflops = pk["bf16"] / 2.0                                 # tf32-class dense
+    achieved = F * local_pairs / t_kernel / 1e12
+    peak_tflops = min(tensor_tflops, F * mufu_rate / E / 1e12)
+    variant = op.last_variant_code
+    fx, ev = executed_per_pair(variant, d, w, n)
+    pairs_eval = local_pairs * ev
+    ten = fx * pairs_eval / t_kernel / 1e12
+    mufu = E * pairs_eval / t_kernel
+    executed = {"tensor": {"achieved": round(ten, 2), "peak": pk["bf16"], "unit": "TFLOP/s",
+                           "frac": round(ten / pk["bf16"], 4),
+                           "flops_per_evaluated_pair": round(fx, 2),
+                           "basis": "kind::f16 MMAs (GEMM1 3-term split along K, GEMM2 "
+                                    "P_hi [Vhi|Vlo] + P_lo Vhi, transposed product) against "
+                                    f"the {pk['source']} dense bf16 peak"},
+                "mufu": {"achieved": round(mufu / 1e12, 4), "peak": round(mufu_rate / 1e12, 4),
+                         "unit": "Tex2/s", "frac": round(mufu / mufu_rate, 4),
+                         "per_evaluated_pair": E},
+                "evaluated_pair_fraction": round(ev, 4)}
+    lim = "tensor pipe" if executed["tensor"]["frac"] >= executed["mufu"]["frac"] else "MUFU ex2"
+    # DRAM traffic of the same kernel variant on the same workload: copied
+    # from the committed ncu --set full capture (a number taken under a
+    # profiler cannot be measured inside this run)
+    traffic, traffic_src = None, None
+    captures = {("cfg3", 2): "r02_summary.json"}
+    prof = captures.get((workload_name, variant))
+    if prof and world == 1 and os.path.exists(os.path.join(ROOT, "profiles", prof)):
+        with open(os.path.join(ROOT, "profiles", prof)) as fh:
+            traffic = json.load(fh).get("traffic_bytes_per_launch")
+        traffic_src = f"copied from profiles/{prof} (ncu --set full of this kernel on this " \
+                      "workload: dram__bytes_read.sum + dram__bytes_write.sum)"
+    return {"bound": "tensor", "limiter": lim, "achieved": round(achieved, 3),
+            "peak": round(peak_tflops, 3), "unit": "TFLOP/s",
+            "frac": round(achieved / peak_tflops, 4), "traffic": traffic,
+            "traffic_source": traffic_src, "executed": executed,
+            "frac_executed": round(max(executed["tensor"]["frac"], executed["mufu"]["frac"]), 4),
+            "peak_basis": f"algorithmic: min({pk['source']} bf16 {pk['bf16']}/2 TF/s, "
+                          f"{sms} SM x {P_MUFU_PER_SM_CLK} ex2/clk x {pk['sm_max_mhz']} MHz x "
+                          f"F/E={F}/{E}); bound 'tensor' = compute-bound (tensor pipe / MUFU), "
+                          f"not HBM",
+            "kernel_ms": round(1e3 * t_kernel, 3), "impl": op.impl,
+            "variant": {0: "plain", 1: "symmetric (CTA pairs)",
+                        2: "symmetric (single CTA)"}.get(variant, "none")}
+
+
+CPU_FIT_ROWS = {"cfg4": 64, "cfg5": 8}   # reference tile-body sample rows per K product
+
+
+def measure_fit(name, args, rank, world, local_rank, warmup_fits=1, timed_fits=1,
+                cpu_extrapolate=True):
     """End-to-end IterNCGP fit on a BASELINE config (synthetic, seeded):
-    FitTrace.wallclock_s, the reference's fit-time definition (outer.py:434-457,
-    metric hooks excluded), max over ranks.  Warm-up fits use a 1-step
-    schedule on the same data (operator packing, allocator, library load)."""
+    FitTrace.wallclock_s, the reference's fit-time definition (outer.py:103-126,
+    253-255: solver clock, metric hooks excluded), max over ranks.  Warm-up
+    fits use a 1-step schedule on the same data (operator packing, allocator,
+    library load).  The posterior mean / marginal variance at the test
+    points are timed separately.  The reference CPU time is
+    extrapolated as BASELINE.md section 3 prescribes: the reference tile body
+    (gp.py:162-171) timed on sample rows x all N columns at the config's
+    shape, scaled to one K product, times the K-product count of this fit."""
     import torch
     import torch.distributed as dist
     import paper_2310_20285_b200 as P
@@ -400,16 +501,16 @@ def run_fit(args, rank, world, local_rank):
     from paper_2310_20285_b200.parallel import ShardedPriorOperator
 
     torch.cuda.set_device(local_rank)
-    name = args.workload[len("fit-"):]
     c = configs.CONFIGS[name]()
     dt = torch.float32
     C = c["C"]
     prior = P.MultiOutputPrior(kernels=(P.KernelSpec(*c["kernel"]),) * C)
     ds = P.Dataset(c["X"], c["y"], "class-index", C)
     lik = P.SoftmaxLikelihood(ds.targets, C)
-    op = ShardedPriorOperator(prior, c["X"], dtype=dt, gather=args.gather) if world > 1 else None
+    op = ShardedPriorOperator(prior, c["X"], dtype=dt, gather=args.gather) if world > 1 else \
+        P.PriorOperator(prior, c["X"], dtype=dt)
     inner = P.InnerConfig(max_iters=1, residual=args.residual)
-    for _ in range(max(0, args.warmup)):
+    for _ in range(max(0, warmup_fits)):
         P.fit(prior, ds, lik, P.OuterConfig(max_newton_steps=1, inner_schedule=2), inner,
               policy_kind=c["policy"], dtype=dt, operator=op)
     oc = P.OuterConfig(max_newton_steps=c["steps"], delta=c["delta"], inner_schedule=c["inner"],
@@ -418,7 +519,7 @@ def run_fit(args, rank, world, local_rank):
     sampler.start()
     launches0 = _native_launches()
     times, trace, belief = [], None, None
-    for _ in range(max(1, args.steps)):
+    for _ in range(max(1, timed_fits)):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -432,9 +533,10 @@ def run_fit(args, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     secs = float(t[0]) / len(times)
-    # posterior at the full test set, timed separately: mean,
-    # then marginal variance (C * rank right-hand-side columns per test block)
-    post = None
+    inner_kind = getattr(getattr(op, "inner", op), "groups", [[None]])[0][0]
+    variant = inner_kind.last_variant if inner_kind is not None else None
+    del op
+    rec = None
     if rank == 0:
         Xt = c["X_test"]
         torch.cuda.synchronize()
@@ -444,28 +546,49 @@ def run_fit(args, rank, world, local_rank):
         var = P.posterior_marginal_var(belief, Xt)
         t2 = time.perf_counter()
         probs = P.probit_predict(mean, var)
-        acc = float(np.mean(probs.argmax(1) == c["y_test"]))
-        post = {"n_test": int(Xt.shape[0]), "root_rank": int(belief.root.rank),
-                "mean_s": round(t1 - t0, 3), "marginal_var_s": round(t2 - t1, 3),
-                "test_accuracy": round(acc, 4)}
+        rec = {"metric": f"IterNCGP fit time ({name})", "value": round(secs, 3), "unit": "s",
+               "higher_is_better": False, "wallclock_s": round(secs, 3),
+               "kernel_matvecs": trace.total_kernel_matvecs,
+               "inner_iters": [s.inner_iterations for s in trace.steps],
+               "termination": trace.termination,
+               "config": {"workload": f"fit-{name}", "n": int(c["X"].shape[0]), "C": C,
+                          "d": int(c["X"].shape[1]), "kernel": list(c["kernel"]),
+                          "schedule": [c["steps"], c["inner"]], "rank": c["rank"],
+                          "policy": c["policy"], "recycle": c["recycle"],
+                          "residual": args.residual},
+               "k_product_variant": variant,
+               "posterior": {"n_test": int(Xt.shape[0]), "root_rank": int(belief.root.rank),
+                             "mean_s": round(t1 - t0, 3), "marginal_var_s": round(t2 - t1, 3),
+                             "test_accuracy": round(float(np.mean(probs.argmax(1) == c["y_test"])), 4)},
+               "gpu_launches": int(launches), "clocks": clocks}
+        if cpu_extrapolate:
+            rows_n = CPU_FIT_ROWS.get(name, 16)
+            rng = np.random.default_rng(7)
+            rows = np.sort(rng.choice(c["X"].shape[0], size=rows_n, replace=False))
+            V = rng.standard_normal((c["X"].shape[0], C))
+            t_rows = cpu_reference_sample(c["kernel"], c["X"], V, rows, 1)
+            per_product = t_rows * c["X"].shape[0] / rows_n
+            rec["cpu_baseline"] = {
+                "value": round(per_product * trace.total_kernel_matvecs, 1), "unit": "s",
+                "cores": 1, "kind": "port",
+                "k_product_s": round(per_product, 2),
+                "sample": f"reference tile body (gp.py:162-171, numpy fp64) on {rows_n} random rows "
+                          f"x all {c['X'].shape[0]} columns, w={C}: {t_rows:.2f} s, scaled to one K "
+                          f"product and multiplied by this fit's {trace.total_kernel_matvecs} K "
+                          f"products (BASELINE.md 3); the vector work of the solver is not counted"}
+    return rec
+
+
+def run_fit(args, rank, world, local_rank):
+    """``--workload fit-cfgN``: one JSON line with the fit time alone."""
+    name = args.workload[len("fit-"):]
+    rec = measure_fit(name, args, rank, world, local_rank, warmup_fits=args.warmup,
+                      timed_fits=args.steps, cpu_extrapolate=not args.no_cpu_baseline)
     if rank == 0:
-        line = {
-            "metric": f"IterNCGP fit time ({name})", "value": round(secs, 3), "unit": "s",
-            "n_gpus": world, "steps": len(times), "warmup": args.warmup,
-            "ms_per_step": round(1e3 * secs, 1), "higher_is_better": False,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": args.workload, "n": int(c["X"].shape[0]), "C": C,
-                       "kernel": list(c["kernel"]), "schedule": [c["steps"], c["inner"]],
-                       "rank": c["rank"], "residual": args.residual,
-                       "parallelism": (f"symmetric work list split x{world}"
-                                       if op is not None and op.gather == "reduce"
-                                       else f"row-sharded x{world}"),
-                       "gather": op.gather if op is not None else None},
-            "kernel_matvecs": trace.total_kernel_matvecs,
-            "inner_iters": [s.inner_iterations for s in trace.steps],
-            "posterior": post,
-            "gpu_launches": launches, "clocks": clocks,
-        }
+        line = dict(rec)
+        line.update({"n_gpus": world, "steps": max(1, args.steps), "warmup": args.warmup,
+                     "ms_per_step": round(1e3 * rec["value"], 1), "scaling": "strong",
+                     "vs_baseline": None, "dtype": "f32", "data": "synthetic"})
         print(json.dumps(line), flush=True)
     return 0
 
@@ -495,6 +618,10 @@ def main():
                          "symmetric-memory buffer; auto = reduce when available, else nccl")
     ap.add_argument("--cpu-rows", type=int, default=24)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fits", default="cfg4,cfg5",
+                    help="product workloads: fit configs timed after the product (the metric's "
+                         "second half, 'IterNCGP fit time N=1M C=10' = cfg5)")
+    ap.add_argument("--no-fit", action="store_true", help="skip the fit records")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -5,8 +5,8 @@
  * replaces is its operator plug-in boundary:
  *
  *   RegressionSystem(apply_kernel, apply_noise, rhs)      solver.py:42-57
- *   apply_kernel = prior_matvec(prior, X, ., tile)          outer.py:511-512, gp.py:222-250
- *   apply_noise  = likelihood.w_inv_matvec(f, .)           outer.py:517, likelihoods.py:258-262
+ *   apply_kernel = prior_matvec(prior, X, ., tile)          outer.py:180-181, gp.py:144-172
+ *   apply_noise  = likelihood.w_inv_matvec(f, .)           outer.py:186, likelihoods.py:258-262
  *
  * Every entry point below names the reference function it replaces.
  *
@@ -25,7 +25,7 @@
  *    floating-point array of the call.  Reductions accumulate in fp64 with
  *    a fixed order, so results are deterministic run to run.
  *  - Vectors over (point, output) pairs use the reference's CN layout
- *    (gp.py:1-8): entry n*C + c, i.e. an N x C row-major matrix.
+ *    (gp.py:4-8): entry n*C + c, i.e. an N x C row-major matrix.
  *  - Column blocks (solver buffers S, T, Q) are stored column-contiguous:
  *    column b starts at ptr + b * ld.
  *  - Operators are bound to the device current at creation; an operator
@@ -64,9 +64,9 @@ int ncgp_device_info(int* sm_count, int* cc_major, int* cc_minor);
 int64_t ncgp_launch_count(void);
 
 /* ---------------------------------------------------------------------
- * K1 fused kernel-matmul (replaces prior_matvec gp.py:222-250 with the
- * tile body gp.py:240-249, _sqdist gp.py:179-191, kernel_from_sqdist
- * gp.py:156-176; newton_update outer.py:465-468; and, with X_rows =
+ * K1 fused kernel-matmul (replaces prior_matvec gp.py:144-172 with the
+ * tile body gp.py:162-171, _sqdist gp.py:101-113, kernel_from_sqdist
+ * gp.py:78-98; newton_update outer.py:134-137; and, with X_rows =
  * X_test, the dense cross_covariance products of posterior.py:52-84).
  *
  *   out[i, c] = sum_j k(Xr[i], Xc[j]) * V[j, c]      0 <= i < n_rows, c < w
@@ -183,12 +183,31 @@ int ncgp_kop_sym_finalize(ncgp_kop* op, const int64_t* acc, int64_t acc_elems,
  * in the last bits.  The initial mode comes from NCGP_SYM (read at creation). */
 int ncgp_kop_set_sym(ncgp_kop* op, int mode);
 
+/* K2 fused cross-kernel posterior variance (replaces posterior_marginal_var,
+ * posterior.py:67-84, and its dense cross_covariance, gp.py:175-196):
+ *
+ *   var[t, c] = max(s2[c] - sum_{r<R} (sum_j k(Xr[t], Xc[j]) W[j, c*R + r])^2, 0)
+ *
+ * for the operator's rows t (test points) and C outputs sharing its kernel
+ * spec.  W is (n_cols, C*R) with row stride ldw: the class-major root
+ * [Q_0 | ... | Q_{C-1}], Q_c[j, r] = Q[j*C + c, r].  Each kernel tile is
+ * evaluated once per 128 root columns (not per 32), its product with the
+ * root accumulates in TMEM over <= 8192 training points, and the fp32
+ * partials are summed in fp64 in a fixed order and squared per row -- A is
+ * never materialised.  s2: device fp64 [C]; var: (n_rows, C) row stride
+ * ldvar, in the operator's dtype.  Needs a tcgen05 operator created with
+ * w_max > 32 (else NCGP_UNSUPPORTED; callers then use the product path). */
+int ncgp_kop_posterior_var(ncgp_kop* op, const void* W, int64_t ldw, int C,
+                           int R, const double* s2, void* var, int64_t ldvar,
+                           void* stream);
+
 /* Actual implementation chosen (NCGP_KOP_TCGEN05 or NCGP_KOP_SIMT). */
 int ncgp_kop_impl(const ncgp_kop* op);
 /* Kernel variant of the last apply (telemetry, no reference counterpart):
  * 0 = plain tiled product, 1 = symmetric K(X, X) kernel on CTA pairs, 2 =
  * symmetric K(X, X) kernel on single CTAs (each off-diagonal tile evaluated
- * once, serving both K V and K^T V), -1 = none yet. */
+ * once, serving both K V and K^T V), 3 = wide-RHS kernel (32 < w <= 128,
+ * K2), -1 = none yet. */
 int ncgp_kop_last_variant(const ncgp_kop* op);
 int ncgp_kop_destroy(ncgp_kop* op);
 
@@ -197,7 +216,7 @@ int ncgp_kop_destroy(ncgp_kop* op);
  * ------------------------------------------------------------------- */
 
 /* Softmax per-point statistics (likelihoods.py:235-238 probabilities,
- * :285-288 softmax_rows, :247-250 grad_log_lik, outer.py:460-462
+ * :285-288 softmax_rows, :247-250 grad_log_lik, outer.py:129-131
  * pseudo_targets).  f, grad, yhat: CN (n*C); pi: (n, C).  grad / yhat may
  * be NULL. */
 int ncgp_softmax_stats(int dtype, const void* f, const int64_t* labels,
@@ -218,7 +237,7 @@ int ncgp_softmax_w(int dtype, const void* pi, int64_t n, int C,
                    const void* V, int64_t ldv, int k, void* out, int64_t ldo,
                    void* stream);
 
-/* Bernoulli-logit statistics (likelihoods.py:202-212, outer.py:460-462):
+/* Bernoulli-logit statistics (likelihoods.py:202-212, outer.py:129-131):
  * winv = 1/(s(1-s)) with the reference's clamp, w = s(1-s),
  * grad = y - s, yhat = f + winv * grad.  Any output may be NULL. */
 int ncgp_bernoulli_stats(int dtype, const void* f, const int64_t* labels,
@@ -241,7 +260,7 @@ int ncgp_diag_apply(int dtype, const void* dvec, int64_t n, const void* V,
 
 /* ---------------------------------------------------------------------
  * K6 vector / tall-skinny kernels for the inner solver (solver.py:203-331,
- * linalg.py:389-400).  Reductions write fp64 results to DEVICE memory.
+ * linalg.py:51-62).  Reductions write fp64 results to DEVICE memory.
  * ------------------------------------------------------------------- */
 
 size_t ncgp_reduce_workspace_bytes(int64_t n, int k);
@@ -252,7 +271,7 @@ int ncgp_dots(int dtype, int64_t n, int npairs, const void* const* xs,
               const void* const* ys, double* out, void* workspace,
               size_t workspace_bytes, void* stream);
 
-/* out[r] = sum_i Q[r*ldq + i] * z[i]  for r < k   (Q' z, linalg.py:400). */
+/* out[r] = sum_i Q[r*ldq + i] * z[i]  for r < k   (Q' z, linalg.py:62). */
 int ncgp_gemv_t(int dtype, const void* Q, int64_t ldq, int k, const void* z,
                 int64_t n, double* out, void* workspace,
                 size_t workspace_bytes, void* stream);

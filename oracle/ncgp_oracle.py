@@ -46,7 +46,7 @@ def as_spec(spec) -> Spec:
 # --------------------------------------------------------------------------
 
 def sqdist(A: np.ndarray, B: np.ndarray) -> np.ndarray:
-    """Pairwise squared distances, one feature at a time (gp.py:179-191).
+    """Pairwise squared distances, one feature at a time (gp.py:101-113).
 
     The accumulation order over features is the reference's, so every entry
     is independent of the block shape.
@@ -60,10 +60,10 @@ def sqdist(A: np.ndarray, B: np.ndarray) -> np.ndarray:
 
 
 def kernel_values(spec, d2: np.ndarray) -> np.ndarray:
-    """Stationary kernel from squared distances (gp.py:156-176).
+    """Stationary kernel from squared distances (gp.py:78-98).
 
     RBF: s2 * exp(-d2 / (2 l^2)); Matern-3/2: s2 * (1 + a) e^-a with
-    a = sqrt(3 d2) / l.  d2 is clamped at 0 first (gp.py:162).
+    a = sqrt(3 d2) / l.  d2 is clamped at 0 first (gp.py:84).
     """
     fam, ell, s2 = as_spec(spec)
     d2 = np.maximum(d2, 0.0)
@@ -86,7 +86,7 @@ def kernel_values(spec, d2: np.ndarray) -> np.ndarray:
 
 
 def kernel_pair(spec, x, y) -> float:
-    """Single-pair kernel evaluation (gp.py:144-153)."""
+    """Single-pair kernel evaluation (gp.py:66-75)."""
     x = np.atleast_1d(np.asarray(x, dtype=np.float64))
     y = np.atleast_1d(np.asarray(y, dtype=np.float64))
     return float(kernel_values(spec, np.array([float(((x - y) ** 2).sum())]))[0])
@@ -94,10 +94,10 @@ def kernel_pair(spec, x, y) -> float:
 
 def prior_matvec(specs: Sequence, X: np.ndarray, v: np.ndarray,
                  tile: int = 256) -> np.ndarray:
-    """Tiled block-diagonal prior product K v, CN layout (gp.py:222-250).
+    """Tiled block-diagonal prior product K v, CN layout (gp.py:144-172).
 
-    One Gram tile per *unique* spec per row tile (gp.py:243-248); each output
-    row is reduced with numpy's pairwise sum over the full row (gp.py:249),
+    One Gram tile per *unique* spec per row tile (gp.py:165-170); each output
+    row is reduced with numpy's pairwise sum over the full row (gp.py:171),
     which makes the result bit-identical for every tile size.
     """
     specs = [as_spec(s) for s in specs]
@@ -123,7 +123,7 @@ def kernel_matmul_rows(spec, X_rows: np.ndarray, X_cols: np.ndarray,
                        V: np.ndarray, tile: int = 64) -> np.ndarray:
     """K(X_rows, X_cols) @ V for one shared spec, V of shape (n_cols, w).
 
-    This is exactly the reference tile body (gp.py:240-249) applied with all
+    This is exactly the reference tile body (gp.py:162-171) applied with all
     ``w`` right-hand columns sharing one spec -- the form SURVEY.md 8(a) a1
     uses for cfg3 (``v = S.ravel()`` with 32 identical-spec outputs).  Used
     as the row-sampled oracle at N >= 1e5.
@@ -143,7 +143,7 @@ def kernel_matmul_rows(spec, X_rows: np.ndarray, X_cols: np.ndarray,
 
 def cross_covariance(specs: Sequence, X_train: np.ndarray,
                      X_test: np.ndarray) -> np.ndarray:
-    """Dense (Nt*C) x (N*C) cross-covariance, CN both ways (gp.py:253-274)."""
+    """Dense (Nt*C) x (N*C) cross-covariance, CN both ways (gp.py:175-196)."""
     specs = [as_spec(s) for s in specs]
     X_train = np.asarray(X_train, dtype=np.float64)
     X_test = np.asarray(X_test, dtype=np.float64)
@@ -159,7 +159,7 @@ def cross_covariance(specs: Sequence, X_train: np.ndarray,
 
 
 def cn_to_nc(v: np.ndarray, n: int, C: int) -> np.ndarray:
-    """CN -> NC permutation (gp.py:109-120)."""
+    """CN -> NC permutation (gp.py:31-42)."""
     return np.asarray(v).reshape(n, C).T.ravel().copy()
 
 
@@ -285,14 +285,14 @@ def pseudo_targets(lik: OracleLikelihood, f: np.ndarray) -> np.ndarray:
 # --------------------------------------------------------------------------
 
 def lowrank_apply(Q: np.ndarray, w: np.ndarray) -> np.ndarray:
-    """Q (Q' w) (linalg.py:389-400)."""
+    """Q (Q' w) (linalg.py:51-62)."""
     if Q.shape[1] == 0:
         return np.zeros_like(np.asarray(w, dtype=np.float64))
     return Q @ (Q.T @ w)
 
 
 def eigh_desc(M: np.ndarray, keep: int):
-    """Symmetrise, eigh, sort descending, keep ``keep`` (linalg.py:403-424)."""
+    """Symmetrise, eigh, sort descending, keep ``keep`` (linalg.py:65-86)."""
     n = M.shape[0]
     if n == 0 or keep == 0:
         return np.zeros((n, 0)), np.zeros(0)
@@ -441,7 +441,7 @@ def virtual_solver_run(buffers: Buffers, apply_Winv: Callable,
 # --------------------------------------------------------------------------
 
 def relative_change_stop(g_new, g_old, delta) -> bool:
-    """outer_stop (outer.py:471-477)."""
+    """outer_stop (outer.py:140-146)."""
     nn = float(np.linalg.norm(g_new))
     diff = float(np.linalg.norm(g_new - g_old))
     if nn == 0.0:
@@ -455,7 +455,7 @@ def fit(specs: Sequence, X: np.ndarray, lik: OracleLikelihood,
         abs_tol: float = 1e-5, rel_tol: float = 1e-5,
         policy: str = "residual", means: Optional[Sequence[float]] = None,
         apply_K: Optional[Callable] = None) -> dict:
-    """Algorithm 1 (outer.py:480-588), without hooks or clocks.
+    """Algorithm 1 (outer.py:149-257), without hooks or clocks.
 
     ``apply_K`` overrides the prior product (default: :func:`prior_matvec`).
     Returns weights, root Q, f, per-step records and totals.

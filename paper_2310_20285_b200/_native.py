@@ -14,7 +14,9 @@ import threading
 from .exceptions import DimensionMismatch, InvalidInput, NcgpError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libncgp_b200.so")
+# NCGP_LIB: an alternative build of the same library (timing A/B of build-time
+# variants, tools/sym_ab.py); entry points it lacks stay unbound
+LIB_PATH = os.environ.get("NCGP_LIB") or os.path.join(HERE, "libncgp_b200.so")
 
 F32, F64 = 0, 1
 RBF, MATERN32 = 0, 1
@@ -68,6 +70,7 @@ _SIGS = {
     "ncgp_kop_impl": (_i32, [_vp]),
     "ncgp_kop_set_sym": (_i32, [_vp, _i32]),
     "ncgp_kop_last_variant": (_i32, [_vp]),
+    "ncgp_kop_posterior_var": (_i32, [_vp, _vp, _i64, _i32, _i32, _vp, _vp, _i64, _vp]),
     "ncgp_kop_sym_acc_elems": (_i64, [_vp, _i32]),
     "ncgp_kop_sym_partial": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _i64, _vp]),
     "ncgp_kop_sym_finalize": (_i32, [_vp, _vp, _i64, _vp, _i64, _i32, _vp, _i64,
@@ -112,6 +115,8 @@ def load() -> ctypes.CDLL:
                 f"paper_2310_20285_b200/csrc` or __graft_entry__.build()")
         lib = ctypes.CDLL(LIB_PATH)
         for name, (res, args) in _SIGS.items():
+            if os.environ.get("NCGP_LIB") and not hasattr(lib, name):
+                continue
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

@@ -1,5 +1,5 @@
 // K6: deterministic reductions and tall-skinny products for the inner
-// solver (solver.py:203-331) and the low-rank root (linalg.py:389-400).
+// solver (solver.py:203-331) and the low-rank root (linalg.py:51-62).
 //
 // Every long reduction is two-pass with a fixed block partition and fp64
 // partials summed in index order, so results are bit-reproducible for a

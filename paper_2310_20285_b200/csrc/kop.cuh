@@ -45,7 +45,8 @@ struct ncgp_kop {
   int knob_rings[3] = {0, 0, 0};  // NCGP_RINGS "na,sx,sv" (plain kernel)
   std::vector<int64_t> sym_cum;  // host: tiles before each work item (partition of the list)
   int sym_cg = 2;         // symmetric kernel flavour the work list was built for (1 or 2)
-  int last_variant = -1;  // 0 plain, 1 symmetric pair kernel, 2 symmetric single-CTA kernel
+  int last_variant = -1;  // 0 plain, 1 symmetric pair kernel, 2 symmetric single-CTA kernel,
+                          // 3 wide-RHS kernel (K2)
 };
 
 // Epilogue of an apply (ncgp_kop_epilogue, include/ncgp_b200.h), with every
@@ -155,6 +156,9 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
              int64_t r0, int64_t r1, cudaStream_t st, const EpiDev& epi,
              const SymPart* part = nullptr);
 int64_t tc_sym_acc_elems(const ncgp_kop* op, int w);
+// K2: posterior marginal variance through the wide kernel's square-reduce
+int tc_posterior_var(ncgp_kop* op, const void* W, int64_t ldw, int C, int R, const double* s2,
+                     void* var, int64_t ldvar, cudaStream_t st);
 int tc_sym_finalize(ncgp_kop* op, const unsigned long long* acc, int w, const OutSet& out,
                     int64_t ldo, cudaStream_t st, const EpiDev& epi);
 

@@ -268,6 +268,17 @@ int ncgp_kop_sym_finalize(ncgp_kop* op, const int64_t* acc, int64_t acc_elems, c
                                ncgp::as_stream(stream), ed);
 }
 
+int ncgp_kop_posterior_var(ncgp_kop* op, const void* W, int64_t ldw, int C, int R,
+                           const double* s2, void* var, int64_t ldvar, void* stream) {
+  NCGP_CHECK_ARG(op != nullptr && W != nullptr && s2 != nullptr && var != nullptr,
+                 NCGP_INVALID_INPUT, "null argument");
+  NCGP_CHECK_ARG(op->impl == NCGP_KOP_TCGEN05 && op->w_max > 32, NCGP_UNSUPPORTED,
+                 "the posterior kernel needs a tcgen05 operator created with w_max > 32");
+  if (op->n_rows == 0) return NCGP_OK;
+  NCGP_CHECK_ARG(op->n_cols > 0, NCGP_UNSUPPORTED, "empty training set");
+  return ncgp::tc_posterior_var(op, W, ldw, C, R, s2, var, ldvar, ncgp::as_stream(stream));
+}
+
 int ncgp_kop_last_variant(const ncgp_kop* op) { return op ? op->last_variant : -1; }
 
 int ncgp_kop_destroy(ncgp_kop* op) {

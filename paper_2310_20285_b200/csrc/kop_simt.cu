@@ -5,9 +5,9 @@
 //   out[i, c] = sum_j k(Xr[i], Xc[j]) V[j, c]
 //
 // fp64 arithmetic replays the reference's operation order per entry:
-// _sqdist accumulates (x_i - x_j)^2 feature by feature (gp.py:186-191) and
+// _sqdist accumulates (x_i - x_j)^2 feature by feature (gp.py:108-113) and
 // kernel_from_sqdist applies clamp / divide / exp / scale in the same order
-// (gp.py:162-176); explicit _rn intrinsics stop the compiler from fusing
+// (gp.py:84-98); explicit _rn intrinsics stop the compiler from fusing
 // those into FMAs.  Only the long j-sum differs from numpy's pairwise sum
 // (it is a fixed-order split sum here), i.e. results agree to ~1e-15.
 #include <math.h>

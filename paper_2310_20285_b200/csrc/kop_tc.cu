@@ -1,5 +1,5 @@
 // K1 on tcgen05/TMEM: fused kernel-matmul  out = K(Xr, Xc) V  with K never
-// materialised (replaces the tile body of prior_matvec, gp.py:240-249).
+// materialised (replaces the tile body of prior_matvec, gp.py:162-171).
 //
 // One CTA pair (cluster of 2, cta_group::2 MMAs with M = 256) per two SMs;
 // each CTA owns a 128-row tile and both sweep the same column tiles.
@@ -89,8 +89,18 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifndef NCGP_SYM1_PT
+// K1-sym1: GEMM2 reads P from TMEM (TS MMA, no shared-memory A reads) and the
+// three split terms accumulate into one set of WP columns, which frees TMEM
+// for a third S buffer (build-time A/B: 0 = the round-1 layout, P only in
+// shared memory, [hi Vhi + lo Vhi | hi Vlo] accumulators, two S buffers at WP = 32)
+#define NCGP_SYM1_PT 1
+#endif
 #ifndef NCGP_SYM1_NS16
 #define NCGP_SYM1_NS16 3  // K1-sym1 S buffers at WP = 16 (build-time A/B: 2 or 3)
+#endif
+#ifndef NCGP_FX_CVT
+#define NCGP_FX_CVT 1  // fixed-point conversion: 0 cvt.rni.s64.f32 (XU), 1 two-limb FMA (build-time A/B)
 #endif
 #ifndef NCGP_WAIT_MODE
 #define NCGP_WAIT_MODE 0  // 0: try_wait + suspend hint, 1: try_wait (default limit), 2: test_wait spin
@@ -374,7 +384,7 @@ struct TcParams {
   // partial x (kernel's scaled domain) adds round(x * fx), fx = 2^F
   unsigned long long* acc;
   int64_t acc_rows;
-  float fx;
+  float fx, fxi;
   int sym_dbg;           // symmetric kernel variant bits (correct results): 64 = flip whether
                          // T(g) is held back behind GEMM1(g + NS); 128 (single-CTA kernel) =
                          // GEMM2 reads P from TMEM (TS), as measured slower.  Debug
@@ -511,8 +521,25 @@ __device__ __forceinline__ void transform_chunk(const uint32_t (&r)[32], float L
 // commutative, so the sums do not depend on the order in which CTAs flush,
 // on the number of CTAs, or on how the work list is split across processes:
 // the product is bitwise reproducible (hard part 5) and 1-GPU
-// and N-GPU results are identical.  F = 33 - ceil(log2 n) keeps |sum| < 2^62
-// (|P V| < 2^28 per pair after the fp16 prescaling).
+// and N-GPU results are identical.  |P V| < 2^28 per pair after the fp16
+// prescaling, so a flush (<= 2048 columns) is below 2^39 and the sum below
+// n 2^28: F = min(3, 33 - ceil(log2 n)) keeps every flush below 2^42 (the
+// conversion's range) and the sum below 2^62, at a resolution of 2^-31 of
+// the largest entry scale.
+// fp32 -> int64 round-to-nearest for |v| < 2^43 on the FMA / ALU pipes: two
+// 21-bit limbs, each rounded with the 1.5 * 2^23 magic constant
+// (cvt.rni.s64.f32 executes on the XU pipe at the MUFU's 16 per clock and
+// would compete with the epilogue's ex2; tools/cvt_probe.cu).  s is the
+// unscaled partial, fx = 2^F, fxi = 2^(21 - F).
+__device__ __forceinline__ long long fx_round(float s, float fx, float fxi) {
+  const float M = 12582912.0f;
+  const float th = fmaf(s, fx * 0x1p-21f, M);   // rint(s 2^F / 2^21) + M
+  const float hf = th - M;
+  const float rs = fmaf(hf, -fxi, s);           // s - h 2^(21 - F), exact
+  const float tl = fmaf(rs, fx, M);             // rint(rs 2^F) + M, |rs 2^F| <= 2^20
+  const long long h = (long long)(__float_as_int(th) - 0x4B400000);
+  return (h << 21) + (long long)(__float_as_int(tl) - 0x4B400000);
+}
 // One call adds 8 columns (group h) of the warp's 32 rows (one per lane)
 // through a 2 KB staging block (row r at 64 r, 16-byte chunk k at
 // k ^ ((r >> 1) & 3): conflict-free stores); NBLK blocks per warp rotate.
@@ -533,8 +560,13 @@ __device__ __forceinline__ void fx_flush8(const TcParams& p, uint32_t stg_warp, 
   const uint32_t swz = (uint32_t)((lane >> 1) & 3);
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
+#if NCGP_FX_CVT == 0
     const long long q0 = __float2ll_rn(v[2 * k] * p.fx);
     const long long q1 = __float2ll_rn(v[2 * k + 1] * p.fx);
+#else
+    const long long q0 = fx_round(v[2 * k], p.fx, p.fxi);
+    const long long q1 = fx_round(v[2 * k + 1], p.fx, p.fxi);
+#endif
     st_shared_v4(rowa + 16u * ((uint32_t)k ^ swz), (uint32_t)q0, (uint32_t)((unsigned long long)q0 >> 32),
                  (uint32_t)q1, (uint32_t)((unsigned long long)q1 >> 32));
   }
@@ -550,6 +582,13 @@ template <int FAM, int WP, bool DBG, bool SYM, bool ATM = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     kop_tc_kernel(const TcParams p) {
   static_assert(!ATM || (SYM && WP == 16), "row tile in TMEM: symmetric kernel, WP = 16");
+  // WP = 128: the wide-RHS kernel (K2, posterior variance and products with
+  // 32 < w <= 128).  Its O (2 x 128 TMEM columns) is single-buffered next to
+  // two S buffers; every item (row-tile pair x <= 64 column tiles)
+  // accumulates in fp32 TMEM and leaves an fp32 partial row block in HBM,
+  // summed in fp64 by the reduce pass.
+  constexpr bool WIDE = WP == 128;
+  static_assert(!WIDE || !SYM, "the wide kernel is the plain kernel");
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -558,7 +597,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   // S/P buffers in TMEM.  The symmetric kernel double-buffers its O and D_T
   // accumulators (2 x 2 WP columns each): with WP = 32 that leaves room for
   // two S/P buffers only, with WP = 16 for three.
-  constexpr int NS = (SYM && (WP == 32 || ATM)) ? 2 : NS_MAX;
+  constexpr int NS = (WIDE || (SYM && (WP == 32 || ATM))) ? 2 : NS_MAX;
 
   // ---- shared-memory carve-up (identical offsets in both CTAs)
   const uint32_t vslot = p.v2_bytes + p.v3_bytes;       // this CTA's V half
@@ -579,7 +618,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   // only sees every other phase, alias a phase two behind as complete.
   auto pbuf = [&](uint32_t g) -> uint32_t { return p.npb == 2 ? (g & 1u) : 0u; };
   double* sAcc = reinterpret_cast<double*>(sStage + (SYM ? BM * WP : 0));  // [WP][128]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sAcc + (SYM ? 0 : WP * BM));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sAcc + ((SYM || WIDE) ? 0 : WP * BM));
   uint64_t* xb_land = bars;               // [6]   local copy completion
   uint64_t* v_land = xb_land + 6;         // [9]   local copy completion
   uint64_t* a_land = v_land + 9;          // [2]   local copy completion
@@ -660,7 +699,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   auto tO = [&](int b) -> uint32_t { return tmem + (uint32_t)(NS * BN + b * 2 * WP); };
   auto tDT = [&](uint32_t b) -> uint32_t { return tmem + (uint32_t)(NS * BN + 4 * WP) + b * 2u * WP; };
   const uint32_t tA = tmem + (uint32_t)(NS * BN + 8 * WP);  // ATM: row tile, ka / 2 columns
-  constexpr uint32_t NO = 2u;  // O buffers
+  constexpr uint32_t NO = WIDE ? 1u : 2u;  // O buffers
   const int64_t half_off = (int64_t)rank * p.rec_bytes;   // this CTA's half of a record
 
   // setmaxnreg sits at the top of each warpgroup's branch so that ptxas sees
@@ -863,10 +902,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         uint64_t dv = dV0;
         uint32_t s2 = 0, r = 0, rph = 0, q = 0, gt = 0;
         while (cur.valid) {
-          const bool fresh = cur.first_in_chunk(), last = cur.last_in_chunk();
+          // (wide kernel: one O accumulation per item)
+          const bool fresh = WIDE ? cur.first_in_item() : cur.first_in_chunk();
+          const bool last = WIDE ? cur.last_in_item() : cur.last_in_chunk();
           if (lane == 0) trace_ev<DBG>(p, gt, 11);
           mbar_wait(&rdy[r], rph);  // P(g), V(g) (and XB(g + NS)) present
-          const uint32_t ob = q & 1u;
+          const uint32_t ob = NO == 2u ? (q & 1u) : 0u;
           if (fresh) mbar_wait(&o_empty[ob], ((q / NO) & 1u) ^ 1u);
           tc_fence_after();
           if (lane == 0) trace_ev<DBG>(p, gt, 0);
@@ -1160,6 +1201,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         ti.next(p, items);
       }
       if (lane == 0) bulk_wait_all();
+    } else if constexpr (WIDE) {
+      // wide kernel: each item's O (fp32, accumulated in TMEM over <= 64
+      // column tiles) -> the fp32 partial [split][local row][WP] in HBM
+      TileIter ti;
+      ti.start(p, items);
+      uint32_t q = 0;
+      float* const part = reinterpret_cast<float*>(p.partial);
+      while (ti.valid) {
+        if (ti.last_in_item()) {
+          mbar_wait(&o_full[0], q & 1u);
+          tc_fence_after();
+          const int64_t i = (2 * (int64_t)ti.cur.pp + rank) * BM + row;  // local row
+          const int64_t sp = ti.it % p.splits;
+          float4* dst = reinterpret_cast<float4*>(part + (sp * p.nloc + i) * WP);
+#pragma unroll 1
+          for (int h = 0; h < WP / 8; ++h) {
+            uint32_t x[8], y[8];
+            tmem_ld8(tO(0) + lane_off + 8 * h, x);       // P_hi Vhi + P_lo Vhi
+            tmem_ld8(tO(0) + lane_off + WP + 8 * h, y);  // P_hi Vlo
+            tmem_wait_ld();
+            if (i < p.nloc) {
+              dst[2 * h] = make_float4(__uint_as_float(x[0]) + __uint_as_float(y[0]),
+                                       __uint_as_float(x[1]) + __uint_as_float(y[1]),
+                                       __uint_as_float(x[2]) + __uint_as_float(y[2]),
+                                       __uint_as_float(x[3]) + __uint_as_float(y[3]));
+              dst[2 * h + 1] = make_float4(__uint_as_float(x[4]) + __uint_as_float(y[4]),
+                                           __uint_as_float(x[5]) + __uint_as_float(y[5]),
+                                           __uint_as_float(x[6]) + __uint_as_float(y[6]),
+                                           __uint_as_float(x[7]) + __uint_as_float(y[7]));
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(leader_addr(&o_empty[0]));
+          ++q;
+        }
+        ti.next(p, items);
+      }
     } else {
     double* acc = sAcc + row;  // acc[c * BM], conflict-free across the warp
 #pragma unroll
@@ -1308,7 +1387,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
   const int lane = threadIdx.x & 31;
   // S buffers next to double-buffered O and D_T (2 x 2 WP columns each):
   // two at WP = 32, three at WP = 16
-  constexpr int NS1 = WP == 16 ? NCGP_SYM1_NS16 : 2;
+  constexpr bool PT = NCGP_SYM1_PT != 0;
+  constexpr int NS1 = PT ? 3 : (WP == 16 ? NCGP_SYM1_NS16 : 2);
+  constexpr uint32_t AW = PT ? WP : 2 * WP;  // TMEM columns of one O / D_T accumulator
   const uint32_t xb_bytes = 2u * p.xbh_bytes;  // 128 XB rows
   const uint32_t vb_bytes = 2u * p.v2_bytes;   // [Vhi | Vlo]: 2 WP rows
   uint8_t* sA = smem;
@@ -1377,8 +1458,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
   }
   const uint32_t tmem = *tmem_slot;
   auto tS = [&](uint32_t b) -> uint32_t { return tmem + b * (uint32_t)BN; };
-  auto tO = [&](uint32_t b) -> uint32_t { return tmem + (uint32_t)(NS1 * BN) + b * 2u * WP; };
-  auto tDT = [&](uint32_t b) -> uint32_t { return tmem + (uint32_t)(NS1 * BN + 4 * WP) + b * 2u * WP; };
+  auto tO = [&](uint32_t b) -> uint32_t { return tmem + (uint32_t)(NS1 * BN) + b * AW; };
+  auto tDT = [&](uint32_t b) -> uint32_t { return tmem + (uint32_t)(NS1 * BN) + 2u * AW + b * AW; };
+  const bool p_tmem = PT || (p.sym_dbg & 128) != 0;  // P also in TMEM (over S) for GEMM2
 
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
@@ -1445,7 +1527,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
         mbar_wait(&xb_full[xr.idx], xr.phase);
         if (g >= (uint32_t)NS1) {  // S buffer free once the epilogue loaded S(g - NS1)
           // (P in TMEM, sym_dbg 128: once GEMM2(g - NS1) has read it)
-          mbar_wait(p.sym_dbg & 128 ? &g2done[sf.idx] : &s_free[sf.idx], sf.phase);
+          mbar_wait(p_tmem ? &g2done[sf.idx] : &s_free[sf.idx], sf.phase);
           sf.adv();
         }
         tc_fence_after();
@@ -1492,7 +1574,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
         const uint64_t pl = ph + ((PBUF / 2) >> 4);
         const uint32_t dO = tO(ob);
         if (elect_one()) {
-          if (p.sym_dbg & 128) {  // A = P from TMEM (the epilogue's copy over S(g))
+          if (PT) {  // A = P from TMEM; P_hi Vhi, P_hi Vlo, P_lo Vhi into the same WP columns
+            const uint32_t a0 = tS(sb);
+            const uint64_t vlo = (uint64_t)(p.v2_bytes >> 4);
+#pragma unroll
+            for (int m = 0; m < BN / 16; ++m) {
+              const uint32_t ahi = a0 + 32u * (m >> 1) + 8u * (m & 1);
+              const uint64_t b = dv + (uint64_t)(16 * m);
+              mma1_ts(dO, ahi, b, id2h, (fresh && m == 0) ? 0u : 1u);
+              mma1_ts(dO, ahi, b + vlo, id2h, 1u);
+              mma1_ts(dO, ahi + 16u, b, id2h, 1u);
+            }
+          } else if (p.sym_dbg & 128) {  // A = P from TMEM (the epilogue's copy over S(g))
             const uint32_t a0 = tS(sb);
 #pragma unroll
             for (int m = 0; m < BN / 16; ++m) {
@@ -1560,11 +1653,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
           if (tp && !(DBG && (p.sym_dbg & 4))) {
             const uint64_t pa = dP0 + (uint64_t)pbuf(g) * (PBUF >> 4);
             const uint32_t dt = tDT(dtq & 1u);
+            const uint64_t vlo = (uint64_t)(p.v2_bytes >> 4);
 #pragma unroll 1
             for (int m = 0; m < BN / 16; ++m) {
               const uint64_t ah = pa + (uint64_t)m * (4096 >> 4), al = ah + ((PBUF / 2) >> 4);
-              mma1_ss(dt, ah, dVI + (uint64_t)(16 * m), idT, m > 0 ? 1u : 0u);
-              mma1_ss(dt, al, dVI + (uint64_t)(16 * m), idTh, 1u);
+              const uint64_t b = dVI + (uint64_t)(16 * m);
+              if (PT) {  // P_hi^T Vhi, P_hi^T Vlo, P_lo^T Vhi into the same WP columns
+                mma1_ss(dt, ah, b, idTh, m > 0 ? 1u : 0u);
+                mma1_ss(dt, ah, b + vlo, idTh, 1u);
+                mma1_ss(dt, al, b, idTh, 1u);
+              } else {
+                mma1_ss(dt, ah, b, idT, m > 0 ? 1u : 0u);
+                mma1_ss(dt, al, b, idTh, 1u);
+              }
             }
           }
           if (tp) tc_commit1(&dt_full[dtq & 1u]);
@@ -1605,7 +1706,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
         if (tr) trace_ev<DBG>(p, g, 4 + 2 * e);
         const uint32_t base = tS(sb) + lane_off + col0;
         const uint32_t rowb0 = smem_u32(sP) + pbuf(g) * PBUF + rowb_base;
-        const bool p_tmem = (p.sym_dbg & 128) != 0;
         uint32_t ra[32], hi[16], lo[16];
 #pragma unroll
         for (int c = 0; c < BN / 64; ++c) {
@@ -1667,12 +1767,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
 #pragma unroll
       for (int h = 0; h < WP / 8; ++h) {
         uint32_t x[8], y[8];
-        tmem_ld8(tacc + lane_off + 8 * h, x);       // [0, WP): hi Vhi + lo Vhi
-        tmem_ld8(tacc + lane_off + WP + 8 * h, y);  // [WP, 2 WP): hi Vlo
+        tmem_ld8(tacc + lane_off + 8 * h, x);       // PT: all three terms; else hi Vhi + lo Vhi
+        if (!PT) tmem_ld8(tacc + lane_off + WP + 8 * h, y);  // [WP, 2 WP): hi Vlo
         tmem_wait_ld();
         float v[8];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) v[c] = __uint_as_float(x[c]) + __uint_as_float(y[c]);
+        for (int c = 0; c < 8; ++c) v[c] = PT ? __uint_as_float(x[c]) : __uint_as_float(x[c]) + __uint_as_float(y[c]);
         fx_flush8<NBLK>(p, stg_warp, nst, lane, h, v, row0, skip);
       }
       tc_fence_before();
@@ -1913,6 +2013,71 @@ __global__ void reduce_partial_kernel(const double* __restrict__ partial, int sp
     if (k < out.n) out.p[k][(e / w) * ldo + (e % w)] = (T)s;
 }
 
+// wide kernel: fixed-order fp64 sum of the fp32 partials [split][row][128],
+// scaled back by 2^-(s + e_c), to every destination (coalesced over columns)
+template <typename T>
+__global__ void wide_reduce_kernel(const float* __restrict__ part, int splits, int64_t nloc,
+                                   int w, int s_exp, const int* __restrict__ col_exp,
+                                   const ncgp::OutPtrs<T> out, int64_t ldo) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nloc * w) return;
+  const int64_t i = e / w;
+  const int c = (int)(e % w);
+  double acc = 0.0;
+  for (int sp = 0; sp < splits; ++sp) acc += (double)part[((int64_t)sp * nloc + i) * 128 + c];
+  const T v = (T)ldexp(acc, -(s_exp + __ldg(&col_exp[c])));
+#pragma unroll
+  for (int k = 0; k < NCGP_MAX_OUTS; ++k)
+    if (k < out.n) out.p[k][i * ldo + c] = v;
+}
+
+// K2 square-reduce (posterior.py:67-84): the pass's columns g0 + c (c < w) of
+// A = K(X*, X) [Q_0 | ... | Q_{C-1}] (class-major, R columns per class) are
+// summed over splits in fp64 (fixed order), squared, and added to
+// sq[row][class] in column order by one thread per row -- A never reaches HBM
+// as a whole and the sums are deterministic.  One block of 128 threads per row.
+__global__ void wide_sqsum_kernel(const float* __restrict__ part, int splits, int64_t nloc,
+                                  int w, int s_exp, const int* __restrict__ col_exp, int g0,
+                                  int R, int C, double* __restrict__ sq) {
+  __shared__ double a2[128];
+  const int64_t i = blockIdx.x;
+  const int c = threadIdx.x;
+  double a = 0.0;
+  if (c < w) {
+    for (int sp = 0; sp < splits; ++sp) a += (double)part[((int64_t)sp * nloc + i) * 128 + c];
+    a = ldexp(a, -(s_exp + __ldg(&col_exp[c])));
+  }
+  a2[c] = a * a;
+  __syncthreads();
+  if (c == 0) {
+    int cls = g0 / R;
+    double run = 0.0;
+    for (int k = 0; k < w; ++k) {
+      const int ck = (g0 + k) / R;
+      if (ck != cls) {
+        sq[i * C + cls] += run;
+        run = 0.0;
+        cls = ck;
+      }
+      run += a2[k];
+    }
+    if (cls < C) sq[i * C + cls] += run;
+  }
+}
+
+// var[t, c] = max(s2[c] - sq[t, c], 0)  (posterior.py:80-84)
+template <typename T>
+__global__ void var_finalize_kernel(const double* __restrict__ sq, int64_t n, int C,
+                                    const double* __restrict__ s2, T* __restrict__ var,
+                                    int64_t ldv) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * C) return;
+  const int64_t i = e / C;
+  const int c = (int)(e % C);
+  const double v = s2[c] - sq[e];
+  var[i * ldv + c] = (T)(v > 0.0 ? v : 0.0);
+}
+
 // split columns: the fixed-order fp64 sum of the partial rows, one thread per
 // row, through the apply's epilogue
 template <typename T>
@@ -1973,10 +2138,15 @@ bool sym_enabled(const ncgp_kop* op, int family, int wp, int64_t col_tiles, int 
 int g_debug_mode = 0;          // debug hook (ncgp_debug_set_mode)
 
 int ka_of(int d) { return ((3 * d + 4) + 15) / 16 * 16; }
-int wp_of(int w) { return w <= 16 ? 16 : 32; }
+// padded RHS width of a launch: 16 / 32 (the plain and symmetric kernels) or
+// 128 (the wide kernel, 32 < w <= 128)
+int wp_of(int w) { return w <= 16 ? 16 : (w <= 32 ? 32 : 128); }
+constexpr int WIDE_WP = 128;
+constexpr int WIDE_ITEM = 64;        // column tiles per wide item (fp32 TMEM accumulation span)
+constexpr int64_t WIDE_ROWS = 8192;  // rows per wide launch (bounds the fp32 partials)
 
 struct Layout {
-  size_t mu, guard, colexp, bits, xa, col, partial, symacc, symtab, total;
+  size_t mu, guard, colexp, bits, xa, col, partial, symacc, symtab, varacc, total;
   uint32_t a_bytes, xbh_bytes, rec_bytes;
   int64_t tile_stride, row_tiles, col_tiles;
 };
@@ -2104,24 +2274,41 @@ Layout layout_of(int64_t n_rows, int64_t n_cols, int d, int w_max, int sms) {
   };
   L.mu = take(64 * sizeof(double));
   L.guard = take(16);
-  L.colexp = take(64 * sizeof(int));
-  L.bits = take(64 * sizeof(unsigned));
+  L.colexp = take(WIDE_WP * sizeof(int));
+  L.bits = take(WIDE_WP * sizeof(unsigned));
   L.xa = take((size_t)L.row_tiles * L.a_bytes);
   // square operators get one zero record past the last column tile: the
   // symmetric kernel reads the padding row tile's V block from it
   L.col = take((size_t)(L.col_tiles + (n_rows == n_cols ? 1 : 0)) * L.tile_stride);
-  // fp64 partial rows [splits][rows][w] when a pair's columns are split
+  // fp64 partial rows [splits][rows][w] when a pair's columns are split; the
+  // wide kernel's fp32 partials [splits][WIDE_ROWS][128] share the region
   const int sp = splits_for(L.row_tiles / 2, L.col_tiles, std::max(1, sms / 2));
-  L.partial = take((size_t)(sp > 1 ? sp : 0) * (size_t)(L.row_tiles * BM) * w_max *
-                   sizeof(double) + 256);
+  size_t part = (size_t)(sp > 1 ? sp : 0) * (size_t)(L.row_tiles * BM) * std::min(w_max, 32) *
+                sizeof(double);
+  if (wpm == WIDE_WP) {
+    const int64_t spw = (L.col_tiles + WIDE_ITEM - 1) / WIDE_ITEM;
+    const size_t wide = (size_t)spw * std::min<int64_t>(WIDE_ROWS, L.row_tiles * BM) * WIDE_WP *
+                        sizeof(float);
+    part = std::max(part, wide);
+    // posterior variance: fp64 sum of squares per (row, output) (ncgp_kop_posterior_var)
+    L.varacc = take((size_t)L.row_tiles * BM * 64 * sizeof(double));
+  }
+  L.partial = take(part + 256);
   // symmetric kernel (square operators): int64 accumulator and item table
   const bool sq = n_rows == n_cols;
-  L.symacc = take(sq ? (size_t)L.row_tiles * BM * wp_of(w_max) * sizeof(unsigned long long) : 0);
+  L.symacc = take(sq ? (size_t)L.row_tiles * BM * std::min(wpm, 32) * sizeof(unsigned long long) : 0);
   L.symtab = take(sq ? (size_t)std::max(sym_item_count(L.row_tiles / 2, L.col_tiles),
                                          sym1_item_count(L.col_tiles)) * 16
                      : 0);
   L.total = off;
   return L;
+}
+
+// the wide kernel (WP = 128): no fp64 accumulator rows in shared memory
+size_t smem_wide(uint32_t a_bytes, int sx, int sv) {
+  const size_t v2 = (size_t)WIDE_WP * BN * 2, v3 = v2 / 2;
+  return (size_t)a_bytes + (size_t)sx * (a_bytes / 2) + (size_t)sv * (v2 + v3) +
+         (6 + 9 + 2 + NS_MAX + 5 * NR + 8 + 12) * sizeof(uint64_t) + 16 + 1024;
 }
 
 size_t smem_bytes(uint32_t a_bytes, int wp, int na, int sx, int sv, int sym_npb = 0) {
@@ -2140,6 +2327,7 @@ bool atm_allowed(const ncgp_kop* op) { return op->knob_atm; }
 int sym_variant(const ncgp_kop* op, int w) {
   if (op->sym_items <= 0 || g_debug_mode != 0) return 0;
   const int wp = wp_of(w);
+  if (wp > 32) return 0;
   if (!sym_enabled(op, op->family, wp, op->col_tiles, op->sym_cg)) return 0;
   const uint32_t a_bytes = (uint32_t)(BM * op->ka * 2);
   if (op->sym_cg == 1) return smem1_bytes(a_bytes, wp, 2, 2, 1) <= SMEM_MAX ? 2 : 0;
@@ -2155,6 +2343,34 @@ int sym_variant(const ncgp_kop* op, int w) {
 }  // namespace
 
 namespace ncgp {
+
+struct VarPass {
+  int g0, R, C;
+  double* sq;  // [n_rows][C] fp64 sums of squares
+};
+int tc_wide(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet* out, int64_t ldo,
+            int64_t r0, int64_t r1, cudaStream_t st, const VarPass* var);
+int tc_posterior_var(ncgp_kop* op, const void* W, int64_t ldw, int C, int R, const double* s2,
+                     void* var, int64_t ldvar, cudaStream_t st) {
+  NCGP_CHECK_ARG(C >= 1 && C <= 64 && R >= 1, NCGP_DIMENSION_MISMATCH, "C = %d, R = %d", C, R);
+  NCGP_CHECK_ARG(ldw >= (int64_t)C * R && ldvar >= C, NCGP_DIMENSION_MISMATCH, "leading dimension");
+  const Layout L = layout_of(op->n_rows, op->n_cols, op->d, op->w_max, op->sms);
+  double* sq = reinterpret_cast<double*>(op->ws + L.varacc);
+  NCGP_CUDA(cudaMemsetAsync(sq, 0, (size_t)op->n_rows * C * sizeof(double), st));
+  const int total = C * R;
+  for (int g0 = 0; g0 < total; g0 += WIDE_WP) {
+    const int w = std::min(WIDE_WP, total - g0);
+    const VarPass vp{g0, R, C, sq};
+    const int rc = tc_wide(op, static_cast<const float*>(W) + g0, ldw, w, nullptr, 0, 0,
+                           op->n_rows, st, &vp);
+    if (rc != NCGP_OK) return rc;
+  }
+  const int64_t tot = op->n_rows * C;
+  var_finalize_kernel<float><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+      sq, op->n_rows, C, s2, static_cast<float*>(var), ldvar);
+  NCGP_LAUNCHED();
+  return NCGP_OK;
+}
 
 int64_t tc_sym_acc_elems(const ncgp_kop* op, int w) {
   return sym_variant(op, w) ? op->row_tiles * BM * wp_of(w) : 0;
@@ -2174,8 +2390,102 @@ int tc_sym_finalize(ncgp_kop* op, const unsigned long long* acc, int w, const Ou
 
 bool tc_supported(int dtype, int d, int w_max) {
   if (dtype != NCGP_F32) return false;
-  if (d < 1 || d > 64 || w_max < 1 || w_max > 32) return false;
-  return smem_bytes((uint32_t)(BM * ka_of(d) * 2), wp_of(w_max), 1, 3, 6) <= (size_t)SMEM_BUDGET;
+  if (d < 1 || d > 64 || w_max < 1 || w_max > WIDE_WP) return false;
+  const uint32_t a = (uint32_t)(BM * ka_of(d) * 2);
+  if (smem_bytes(a, wp_of(std::min(w_max, 32)), 1, 3, 6) > (size_t)SMEM_BUDGET) return false;
+  // wide RHS (w_max > 32): the WP = 128 kernel with (XB 2, V 3) rings, D <= ~50
+  return w_max <= 32 || smem_wide(a, 2, 3) <= SMEM_MAX;
+}
+
+// The wide kernel over rows [r0, r1) in blocks of WIDE_ROWS: products with
+// 32 < w <= 128 (out != nullptr) or, with `var`, one 128-column pass of K2's
+// square-reduce (posterior variance).
+int tc_wide(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet* out, int64_t ldo,
+            int64_t r0, int64_t r1, cudaStream_t st, const VarPass* var) {
+  NCGP_CHECK_ARG(op->w_max > 32, NCGP_UNSUPPORTED,
+                 "w = %d needs an operator created with w_max > 32 (the wide kernel)", w);
+  NCGP_CHECK_ARG(w >= 1 && w <= WIDE_WP, NCGP_DIMENSION_MISMATCH, "wide width %d", w);
+  NCGP_CHECK_ARG(r0 % (2 * BM) == 0, NCGP_DIMENSION_MISMATCH,
+                 "row_begin must be a multiple of %d for the tcgen05 operator", 2 * BM);
+  const Layout L = layout_of(op->n_rows, op->n_cols, op->d, op->w_max, op->sms);
+  int* col_exp = reinterpret_cast<int*>(op->ws + L.colexp);
+  unsigned int* bits = reinterpret_cast<unsigned int*>(op->ws + L.bits);
+  const float* Vf = static_cast<const float*>(V);
+  const int wp = WIDE_WP;
+  NCGP_CUDA(cudaMemsetAsync(bits, 0, WIDE_WP * sizeof(unsigned), st));
+  {
+    dim3 grid((unsigned)std::min<int64_t>(1024, (op->n_cols + 7) / 8), (unsigned)((w + 31) / 32));
+    col_absmax_kernel<float><<<grid, 256, 0, st>>>(Vf, ldv, op->n_cols, w, bits);
+    NCGP_LAUNCHED();
+    col_exp_kernel<<<1, WIDE_WP, 0, st>>>(bits, w, wp, col_exp);
+    NCGP_LAUNCHED();
+  }
+  const uint32_t v2 = (uint32_t)(wp * BN * 2);
+  {
+    const int64_t tot = op->col_tiles * (BN / 8) * wp;
+    pack_v_kernel<float><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+        Vf, ldv, op->n_cols, w, wp, col_exp, op->col_pack, L.tile_stride, L.rec_bytes,
+        L.xbh_bytes, v2, op->col_tiles);
+    NCGP_LAUNCHED();
+  }
+  TcParams p{};
+  p.xa_pack = op->xa_pack;
+  p.col_pack = op->col_pack;
+  p.tile_stride = L.tile_stride;
+  p.rec_bytes = L.rec_bytes;
+  p.a_bytes = L.a_bytes;
+  p.xbh_bytes = L.xbh_bytes;
+  p.v2_bytes = v2;
+  p.v3_bytes = v2 / 2;
+  p.ka = op->ka;
+  p.w = w;
+  p.col_tiles = op->col_tiles;
+  // items of <= WIDE_ITEM column tiles: each accumulates in fp32 TMEM over
+  // at most 8192 columns; the splits are summed in fp64 in a fixed order
+  p.splits = (int)((op->col_tiles + WIDE_ITEM - 1) / WIDE_ITEM);
+  p.tiles_per_split = (p.col_tiles + p.splits - 1) / p.splits;
+  p.splits = (int)((p.col_tiles + p.tiles_per_split - 1) / p.tiles_per_split);
+  const int s_exp = (int)lround(log2(op->k_scale));
+  p.s_exp = s_exp;
+  p.L = (float)(log2(op->s2) + s_exp);
+  p.col_exp = col_exp;
+  p.out_f64 = 0;
+  p.n_out = 0;
+  p.ldo = ldo;
+  p.partial = op->partial;
+  p.na = 1;
+  p.sx = smem_wide(p.a_bytes, 3, 3) <= SMEM_MAX ? 3 : 2;
+  p.sv = 3;
+  p.epi.alpha = 1.0;
+  const size_t smem = smem_wide(p.a_bytes, p.sx, p.sv);
+  NCGP_CHECK_ARG(smem <= SMEM_MAX, NCGP_UNSUPPORTED, "wide kernel: shared memory for d=%d", op->d);
+  const int clusters = std::max(1, op->sms / 2);
+  auto kern = op->family == NCGP_RBF ? kop_tc_kernel<NCGP_RBF, WIDE_WP, false, false>
+                                     : kop_tc_kernel<NCGP_MATERN32, WIDE_WP, false, false>;
+  NCGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  op->last_variant = 3;
+  const float* part = reinterpret_cast<const float*>(op->partial);
+  for (int64_t rb = r0; rb < r1; rb += WIDE_ROWS) {
+    const int64_t re = std::min(r1, rb + WIDE_ROWS);
+    p.rt0 = rb / BM;
+    p.nloc = re - rb;
+    p.pairs = (p.nloc + 2 * BM - 1) / (2 * BM);
+    p.n_items = (int)(p.pairs * p.splits);
+    const unsigned grid = 2u * (unsigned)std::min<int64_t>(p.n_items, clusters);
+    kern<<<grid, NTHREADS, smem, st>>>(p);
+    NCGP_LAUNCHED();
+    if (var != nullptr) {
+      wide_sqsum_kernel<<<(unsigned)p.nloc, 128, 0, st>>>(part, p.splits, p.nloc, w, s_exp, col_exp,
+                                                          var->g0, var->R, var->C,
+                                                          var->sq + rb * var->C);
+    } else {
+      const int64_t tot = p.nloc * w;
+      wide_reduce_kernel<float><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+          part, p.splits, p.nloc, w, s_exp, col_exp, ncgp::out_ptrs<float>(*out, rb, ldo), ldo);
+    }
+    NCGP_LAUNCHED();
+  }
+  return NCGP_OK;
 }
 
 size_t tc_workspace_bytes(int64_t n_rows, int64_t n_cols, int d, int w_max) {
@@ -2195,8 +2505,9 @@ int tc_prepare(ncgp_kop* op, cudaStream_t st) {
   op->partial = reinterpret_cast<double*>(op->ws + L.partial);
   op->sym_items = 0;
   op->sym_acc = reinterpret_cast<unsigned long long*>(op->ws + L.symacc);
-  // fixed-point fraction bits of the symmetric accumulator: |sum| < n 2^28 2^F < 2^62
-  op->sym_fx = 33 - (int)ceil(log2((double)std::max<int64_t>(op->n_cols, 2)));
+  // fixed-point fraction bits of the symmetric accumulator (fx_round):
+  // flushes below 2^42, |sum| < n 2^28 2^F < 2^62
+  op->sym_fx = std::min(3, 33 - (int)ceil(log2((double)std::max<int64_t>(op->n_cols, 2))));
   op->sym_tab = reinterpret_cast<int4*>(op->ws + L.symtab);
   std::vector<int4> tab;
   if (op->n_rows == op->n_cols)
@@ -2273,6 +2584,11 @@ int tc_prepare(ncgp_kop* op, cudaStream_t st) {
 
 int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out, int64_t ldo,
              int64_t r0, int64_t r1, cudaStream_t st, const EpiDev& epi, const SymPart* part) {
+  if (wp_of(w) == WIDE_WP) {
+    NCGP_CHECK_ARG(part == nullptr, NCGP_UNSUPPORTED, "no symmetric kernel for w = %d", w);
+    NCGP_CHECK_ARG(!epi.active, NCGP_UNSUPPORTED, "fused epilogues need w <= 32 (got %d)", w);
+    return tc_wide(op, V, ldv, w, &out, ldo, r0, r1, st, nullptr);
+  }
   if (part != nullptr) {
     NCGP_CHECK_ARG(sym_variant(op, w) != 0, NCGP_UNSUPPORTED,
                    "no symmetric kernel for this operator and width");
@@ -2288,12 +2604,12 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
   int* col_exp = reinterpret_cast<int*>(op->ws + L.colexp);
   unsigned int* bits = reinterpret_cast<unsigned int*>(op->ws + L.bits);
   const float* Vf = static_cast<const float*>(V);
-  NCGP_CUDA(cudaMemsetAsync(bits, 0, 64 * sizeof(unsigned), st));
+  NCGP_CUDA(cudaMemsetAsync(bits, 0, WIDE_WP * sizeof(unsigned), st));
   {
     dim3 grid((unsigned)std::min<int64_t>(1024, (op->n_cols + 7) / 8), (unsigned)((w + 31) / 32));
     col_absmax_kernel<float><<<grid, 256, 0, st>>>(Vf, ldv, op->n_cols, w, bits);
     NCGP_LAUNCHED();
-    col_exp_kernel<<<1, 64, 0, st>>>(bits, w, wp, col_exp);
+    col_exp_kernel<<<1, WIDE_WP, 0, st>>>(bits, w, wp, col_exp);
     NCGP_LAUNCHED();
   }
   const uint32_t v2 = (uint32_t)(wp * BN * 2);
@@ -2342,6 +2658,7 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
   p.acc = nullptr;
   p.acc_rows = op->row_tiles * BM;
   p.fx = ldexpf(1.f, op->sym_fx);
+  p.fxi = ldexpf(1.f, 21 - op->sym_fx);
   p.epi = epi;
   // symmetric kernel: K(X, X) with the whole row range in one launch
   const bool dbg = (g_trace != nullptr) || (g_debug_mode != 0);

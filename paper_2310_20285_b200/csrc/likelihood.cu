@@ -19,7 +19,7 @@ template <>
 __device__ __forceinline__ float dev_exp<float>(float x) { return expf(x); }
 
 // softmax_rows (likelihoods.py:285-288) + grad_log_lik (:247-250) +
-// pseudo_targets (outer.py:460-462) for one point.
+// pseudo_targets (outer.py:129-131) for one point.
 template <typename T, int CMAX>
 __global__ void softmax_stats_kernel(const T* __restrict__ f, const int64_t* __restrict__ y,
                                      int64_t n, int C, T* __restrict__ pi_out,
@@ -52,7 +52,7 @@ __global__ void softmax_stats_kernel(const T* __restrict__ f, const int64_t* __r
       gm += g[c];
     }
   if (!yhat_out) return;
-  // W^+ g = P diag(1/max(pi, floor)) P g  (likelihoods.py:298-301)
+  // W^+ g = P diag(1/max(pi, floor)) P g  (likelihoods.py:302-305)
   gm /= T(C);
   T um = 0;
 #pragma unroll
@@ -121,7 +121,7 @@ __global__ void softmax_stats_tiled_kernel(const T* __restrict__ f, const int64_
         for (int c = 0; c < CMAX; ++c)
           if (c < C) tile[t * C + c] = g[c];
       } else {
-        // W^+ g = P diag(1/max(pi, floor)) P g  (likelihoods.py:298-301)
+        // W^+ g = P diag(1/max(pi, floor)) P g  (likelihoods.py:302-305)
         const T gmean = gm / T(C);
         T u[CMAX];
         T um = 0;
@@ -207,7 +207,7 @@ __device__ __forceinline__ T expit(T x) {
   return e / (T(1) + e);
 }
 
-// likelihoods.py:202-212 and pseudo_targets outer.py:460-462
+// likelihoods.py:202-212 and pseudo_targets outer.py:129-131
 template <typename T>
 __global__ void bernoulli_stats_kernel(const T* __restrict__ f, const int64_t* __restrict__ y,
                                        int64_t n, T* __restrict__ winv, T* __restrict__ w,

@@ -1,12 +1,12 @@
 """Multi-output GP priors on the device (mirror of ncgp/gp.py).
 
 Public names and semantics follow the reference: ``KernelSpec``
-(gp.py:123-141), ``MultiOutputPrior`` (gp.py:194-219), CN layout
-(gp.py:1-8, entry n*C + c), ``reorder`` (gp.py:109-120), ``kernel_eval``
-(gp.py:144-153), ``prior_matvec`` (gp.py:222-250) and ``cross_covariance``
-(gp.py:253-274).  The products run on the B200 through
+(gp.py:45-63), ``MultiOutputPrior`` (gp.py:116-141), CN layout
+(gp.py:4-8, entry n*C + c), ``reorder`` (gp.py:31-42), ``kernel_eval``
+(gp.py:66-75), ``prior_matvec`` (gp.py:144-172) and ``cross_covariance``
+(gp.py:175-196).  The products run on the B200 through
 :class:`PriorOperator`, which groups outputs by unique kernel spec (the
-reference's per-tile dedup, gp.py:243-248) and issues one fused
+reference's per-tile dedup, gp.py:165-170) and issues one fused
 kernel-matmul per group with all of that group's outputs as right-hand
 columns.  The ``tile`` argument is accepted for signature compatibility;
 the device operator's reduction order does not depend on it.
@@ -34,7 +34,7 @@ class Ordering(enum.Enum):
 
 
 def reorder(v, src: Ordering, dst: Ordering, n_points: int, n_outputs: int):
-    """CN <-> NC permutation of a length N*C vector (gp.py:109-120)."""
+    """CN <-> NC permutation of a length N*C vector (gp.py:31-42)."""
     dev = is_device(v)
     a = v if dev else np.asarray(v)
     if a.shape[0] != n_points * n_outputs:
@@ -49,7 +49,7 @@ def reorder(v, src: Ordering, dst: Ordering, n_points: int, n_outputs: int):
 
 @dataclass(frozen=True)
 class KernelSpec:
-    """Stationary kernel (gp.py:123-141).
+    """Stationary kernel (gp.py:45-63).
 
     rbf:      s2 * exp(-d^2 / (2 l^2))
     matern32: s2 * (1 + sqrt(3) d / l) * exp(-sqrt(3) d / l)
@@ -70,7 +70,7 @@ class KernelSpec:
 
 @dataclass(frozen=True)
 class MultiOutputPrior:
-    """Independent constant-mean GPs, one kernel per output (gp.py:194-219)."""
+    """Independent constant-mean GPs, one kernel per output (gp.py:116-141)."""
 
     kernels: Tuple[KernelSpec, ...]
     mean: Tuple[float, ...] = ()
@@ -267,7 +267,7 @@ def _cached_operator(prior, X, dtype) -> PriorOperator:
 
 
 def prior_matvec(prior: MultiOutputPrior, X, v, tile: int = 256, dtype=None):
-    """K v for a CN vector (gp.py:222-250), computed by the fused device
+    """K v for a CN vector (gp.py:144-172), computed by the fused device
     kernel-matmul.  Returns the same kind of array it is given (numpy in,
     numpy out; CUDA tensor in, CUDA tensor out)."""
     if tile < 1:
@@ -287,7 +287,7 @@ def prior_matvec(prior: MultiOutputPrior, X, v, tile: int = 256, dtype=None):
 
 
 def kernel_eval(spec: KernelSpec, x, x2) -> float:
-    """Kernel on one pair of input vectors (gp.py:144-153), on the device."""
+    """Kernel on one pair of input vectors (gp.py:66-75), on the device."""
     x = np.atleast_1d(np.asarray(x, dtype=np.float64))
     x2 = np.atleast_1d(np.asarray(x2, dtype=np.float64))
     if not (np.isfinite(x).all() and np.isfinite(x2).all()):
@@ -302,7 +302,7 @@ def kernel_eval(spec: KernelSpec, x, x2) -> float:
 
 
 def cross_covariance(prior: MultiOutputPrior, X_train, X_test, dtype=None) -> np.ndarray:
-    """Dense (N_test*C) x (N_train*C) cross-covariance (gp.py:253-274).
+    """Dense (N_test*C) x (N_train*C) cross-covariance (gp.py:175-196).
 
     Materialised by applying the device operator to identity column blocks;
     intended, like the reference, for small problems only.
@@ -330,7 +330,7 @@ def cross_covariance(prior: MultiOutputPrior, X_train, X_test, dtype=None) -> np
 
 @dataclass(frozen=True)
 class Dataset:
-    """Inputs, targets and a target-domain tag (gp.py:277-319)."""
+    """Inputs, targets and a target-domain tag (gp.py:199-241)."""
 
     inputs: np.ndarray
     targets: np.ndarray

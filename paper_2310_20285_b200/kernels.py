@@ -69,8 +69,8 @@ class KernelOperator:
     """Device kernel operator for one stationary kernel spec:
     ``apply(V) = K(X_rows, X_cols) @ V`` without materialising K.
 
-    Replaces the tile loop of prior_matvec (gp.py:222-250) and the dense
-    cross_covariance products (gp.py:253-274, posterior.py:52-84).
+    Replaces the tile loop of prior_matvec (gp.py:144-172) and the dense
+    cross_covariance products (gp.py:175-196, posterior.py:52-84).
     """
 
     def __init__(self, family: str, lengthscale: float, outputscale: float,
@@ -91,7 +91,9 @@ class KernelOperator:
         self.dtype = self.X_rows.dtype
         self.n_rows, self.d = self.X_rows.shape
         self.n_cols = self.X_cols.shape[0]
-        self.w_max = int(max(1, min(w_max, 32)))
+        # up to 32 RHS columns per K1 launch; 32 < w_max <= 128 selects the
+        # wide-RHS kernel (K2) for wide products and the posterior variance
+        self.w_max = int(max(1, min(w_max, 128)))
         impl_code = {"auto": N.KOP_AUTO, "tcgen05": N.KOP_TCGEN05, "simt": N.KOP_SIMT}[impl]
         dt = code(self.dtype)
         nbytes = N.query("ncgp_kop_workspace_bytes", impl_code, dt, self.n_rows, self.n_cols,
@@ -127,8 +129,9 @@ class KernelOperator:
 
     @property
     def last_variant(self) -> str:
-        """Kernel variant of the last apply: "plain", "symmetric" or "none"."""
-        return {0: "plain", 1: "symmetric", 2: "symmetric"}.get(self.last_variant_code, "none")
+        """Kernel variant of the last apply: "plain", "symmetric", "wide" or "none"."""
+        return {0: "plain", 1: "symmetric", 2: "symmetric", 3: "wide"}.get(self.last_variant_code,
+                                                                           "none")
 
     @property
     def last_variant_code(self) -> int:
@@ -198,6 +201,26 @@ class KernelOperator:
         return out[:, 0] if vec else out
 
     __call__ = apply
+
+    def posterior_var(self, W: torch.Tensor, C: int, R: int, s2: torch.Tensor,
+                      out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """K2 (``ncgp_kop_posterior_var``): var[t, c] = max(s2[c] -
+        sum_r (K(X_rows, X_cols) W[:, c R + r])[t]^2, 0) for the class-major
+        root W (n_cols, C R), without materialising K W.  Raises
+        :class:`_native.Unsupported` unless this is a tcgen05 operator
+        created with w_max > 32 (callers fall back to the product path)."""
+        if W.shape[0] != self.n_cols or W.dim() != 2 or W.shape[1] != C * R:
+            raise N.DimensionMismatch(f"root block {tuple(W.shape)} != ({self.n_cols}, {C * R})")
+        if W.dtype != self.dtype or W.stride(1) != 1:
+            W = W.to(self.dtype).contiguous()
+        s2 = s2.to(device=W.device, dtype=torch.float64).contiguous()
+        if out is None:
+            out = torch.empty((self.n_rows, C), dtype=self.dtype, device=W.device)
+        ldw = W.stride(0) if W.shape[0] > 1 else W.shape[1]
+        ldo = out.stride(0) if out.shape[0] > 1 else C
+        N.call("ncgp_kop_posterior_var", self._h, W.data_ptr(), ldw, C, R, s2.data_ptr(),
+               out.data_ptr(), ldo, stream())
+        return out
 
     # ---- the symmetric K(X, X) kernel split across processes (parallel.py)
     def sym_acc_elems(self, w: int) -> int:

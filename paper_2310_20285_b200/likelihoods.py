@@ -10,7 +10,7 @@ For the Newton loop, :meth:`Likelihood.noise_state` evaluates the per-point
 statistics ONCE per Newton step (the reference recomputes pi inside every
 ``w_inv_matvec`` call, likelihoods.py:259) and returns a :class:`NoiseState`
 whose ``apply`` is the cached W^-1 operator and whose ``pseudo_targets`` is
-f + W^-1 grad (outer.py:460-462).
+f + W^-1 grad (outer.py:129-131).
 """
 
 from __future__ import annotations
@@ -314,7 +314,7 @@ class SoftmaxLikelihood(Likelihood):
 
     def _count(self, counter, k):
         size = self.n_points * self.num_outputs
-        counter.add(2 * size + 5 * size * k)   # likelihoods.py:302-309
+        counter.add(2 * size + 5 * size * k)   # likelihoods.py:306-313
 
     def w_inv_dense_blocks(self, f):
         C = self.num_outputs

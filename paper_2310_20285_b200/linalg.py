@@ -5,7 +5,7 @@ column of Q contiguous), which is the layout the gemv / Gram / rotation
 kernels read at full HBM bandwidth.  ``.columns`` returns the reference's
 (dim, rank) host array lazily.
 
-``sym_eigh_truncated`` (linalg.py:403-424) is K7: a <= ~600 x 600 fp64
+``sym_eigh_truncated`` (linalg.py:65-86) is K7: a <= ~600 x 600 fp64
 eigensolve run on the host with LAPACK, as SURVEY.md 7 hard part 8 allows
 (it is latency-bound and must be computed identically on every rank).
 """
@@ -23,7 +23,7 @@ from .exceptions import DimensionMismatch, InvalidInput
 
 
 class LowRankRoot:
-    """Root Q of the PSD operator Q Q' (linalg.py:357-378)."""
+    """Root Q of the PSD operator Q Q' (linalg.py:19-40)."""
 
     def __init__(self, columns=None, *, block: torch.Tensor = None,
                  kblock: torch.Tensor = None):
@@ -88,7 +88,7 @@ class EigenPairs:
 
 
 def apply_lowrank(root: LowRankRoot, w, dtype=None):
-    """Q (Q' w) without densifying (linalg.py:389-400); device gemv pair."""
+    """Q (Q' w) without densifying (linalg.py:51-62); device gemv pair."""
     dev = is_device(w)
     dt = resolve_dtype(w.dtype if dev else dtype)
     t = to_device(w, dt)
@@ -110,7 +110,7 @@ def apply_lowrank(root: LowRankRoot, w, dtype=None):
 
 def sym_eigh_truncated(M, rank_bound: int) -> EigenPairs:
     """Symmetrise, eigendecompose, keep the ``rank_bound`` largest pairs
-    (linalg.py:403-424).  Host LAPACK, fp64."""
+    (linalg.py:65-86).  Host LAPACK, fp64."""
     M = to_host(M) if is_device(M) else np.asarray(M, dtype=np.float64)
     if M.ndim != 2 or M.shape[0] != M.shape[1]:
         raise DimensionMismatch(f"expected a square matrix, got shape {M.shape}")

@@ -4,7 +4,7 @@ The belief (v, Q) stays on the device.  ``posterior_mean`` (posterior.py:52-64)
 and ``posterior_marginal_var`` (posterior.py:67-84) apply the fused
 cross-kernel operator K(X*, X) to v and to the class-gathered root
 [Q_0 | ... | Q_{C-1}] instead of densifying the (N*·C) x (N·C) block matrix
-the reference builds per chunk (gp.py:253-274), so they run at cfg4/cfg5
+the reference builds per chunk (gp.py:175-196), so they run at cfg4/cfg5
 scale where the reference cannot.  ``probit_predict`` (posterior.py:104-121)
 is O(N*·C) host arithmetic, as SURVEY.md 8(a) a9 allows.
 """
@@ -69,16 +69,29 @@ class PosteriorBelief:
         return cls(prior, train_inputs, np.zeros(dim), LowRankRoot.zero(dim))
 
 
-def _cross_ops(belief: PosteriorBelief, X_test, dt):
+def _cross_ops(belief: PosteriorBelief, X_test, dt, w_max=32):
     """One K(X*, X) operator per unique spec with its output indices."""
     Xr = to_device(X_test, dt)
     Xc = to_device(belief.train_inputs, dt)
     if Xr.dim() != 2 or Xr.shape[1] != Xc.shape[1]:
         raise DimensionMismatch(f"incompatible input shapes {tuple(Xr.shape)} vs "
                                 f"{tuple(Xc.shape)}")
-    return [(K.KernelOperator(spec.family, spec.lengthscale, spec.outputscale, Xr, Xc,
-                              w_max=64), cols)
+    return [(_wide_or_plain(spec, Xr, Xc, w_max), cols)
             for spec, cols in belief.prior.spec_groups()]
+
+
+def _wide_or_plain(spec, Xr, Xc, w_max):
+    """The cross operator; w_max > 32 asks for the wide-RHS kernel (K2),
+    which exists for the fp32 tcgen05 path at D <= ~50 -- otherwise the
+    32-column operator (the product path loops RHS blocks)."""
+    try:
+        return K.KernelOperator(spec.family, spec.lengthscale, spec.outputscale, Xr, Xc,
+                                w_max=w_max)
+    except (K.N.Unsupported, K.N.InvalidInput):
+        if w_max <= 32:
+            raise
+        return K.KernelOperator(spec.family, spec.lengthscale, spec.outputscale, Xr, Xc,
+                                w_max=32)
 
 
 def posterior_mean(belief: PosteriorBelief, X_test, chunk: int = 512, dtype=None):
@@ -115,6 +128,23 @@ def posterior_marginal_var(belief: PosteriorBelief, X_test, chunk: int = 512, dt
     dev = W.device
     var = torch.empty((nt, C), dtype=dt, device=dev)
     s2d = s2.to(dev)
+    # K2: the fused cross-kernel posterior (ncgp_kop_posterior_var): each
+    # kernel tile once per 128 root columns, square-reduce in the kernel's
+    # fp64 reduction pass, A never stored
+    if dt == torch.float32 and C * R > 32:
+        done = True
+        for op, cols in _cross_ops(belief, X_test, dt, w_max=128):
+            if op.impl != "tcgen05" or op.w_max <= 32:
+                done = False
+                break
+            if len(cols) == C:
+                op.posterior_var(W, C, R, s2d, out=var)
+            else:
+                idx = torch.tensor(cols, device=dev)
+                Wg = W.view(n, C, R).index_select(1, idx).reshape(n, len(cols) * R).contiguous()
+                var[:, cols] = op.posterior_var(Wg, len(cols), R, s2d[idx])
+        if done:
+            return to_host(var)
     # bound the (rows x C*R) intermediate to ~256 MiB
     rows = max(128, min(nt, int(2 ** 28 // max(1, C * R * W.element_size()))) // 128 * 128)
     for t0 in range(0, nt, rows):
