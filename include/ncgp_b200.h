@@ -192,7 +192,7 @@ int ncgp_kop_set_sym(ncgp_kop* op, int mode);
  * spec.  W is (n_cols, C*R) with row stride ldw: the class-major root
  * [Q_0 | ... | Q_{C-1}], Q_c[j, r] = Q[j*C + c, r].  Each kernel tile is
  * evaluated once per 128 root columns (not per 32), its product with the
- * root accumulates in TMEM over <= 8192 training points, and the fp32
+ * root accumulates in TMEM over <= 2048 training points, and the fp32
  * partials are summed in fp64 in a fixed order and squared per row -- A is
  * never materialised.  s2: device fp64 [C]; var: (n_rows, C) row stride
  * ldvar, in the operator's dtype.  Needs a tcgen05 operator created with

@@ -583,10 +583,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     kop_tc_kernel(const TcParams p) {
   static_assert(!ATM || (SYM && WP == 16), "row tile in TMEM: symmetric kernel, WP = 16");
   // WP = 128: the wide-RHS kernel (K2, posterior variance and products with
-  // 32 < w <= 128).  Its O (2 x 128 TMEM columns) is single-buffered next to
-  // two S buffers; every item (row-tile pair x <= 64 column tiles)
-  // accumulates in fp32 TMEM and leaves an fp32 partial row block in HBM,
-  // summed in fp64 by the reduce pass.
+  // 32 < w <= 128).  The three split terms P_hi Vhi + P_hi Vlo + P_lo Vhi
+  // accumulate into one set of 128 TMEM columns (N = 128 MMAs on the
+  // CTA-split B blocks [Vhi half | Vlo half]), so O is double-buffered next
+  // to two S buffers; every item (row-tile pair x <= 16 column tiles, K1's
+  // fp32 accumulation span) leaves an fp32 partial row block in HBM, summed
+  // in fp64 by the reduce pass.
   constexpr bool WIDE = WP == 128;
   static_assert(!WIDE || !SYM, "the wide kernel is the plain kernel");
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -600,7 +602,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   constexpr int NS = (WIDE || (SYM && (WP == 32 || ATM))) ? 2 : NS_MAX;
 
   // ---- shared-memory carve-up (identical offsets in both CTAs)
-  const uint32_t vslot = p.v2_bytes + p.v3_bytes;       // this CTA's V half
+  // this CTA's V half: [B2 | B3] (wide kernel: [B3 | B4], the CTA-split Vhi and Vlo)
+  const uint32_t vslot = WIDE ? 2u * p.v3_bytes : p.v2_bytes + p.v3_bytes;
   uint8_t* sA = smem;                                   // na x a_bytes (own row tile)
   uint8_t* sXB = sA + (size_t)p.na * p.a_bytes;         // sx x xbh_bytes
   uint8_t* sV = sXB + (size_t)p.sx * p.xbh_bytes;       // sv x vslot
@@ -696,10 +699,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   // symmetric kernel: S/P [0, 256), O double buffer [256, 256 + 4 WP),
   // D_T double buffer [256 + 4 WP, 256 + 8 WP)
   auto tS = [&](int b) -> uint32_t { return tmem + (uint32_t)(b * BN); };
-  auto tO = [&](int b) -> uint32_t { return tmem + (uint32_t)(NS * BN + b * 2 * WP); };
+  constexpr uint32_t AW = WIDE ? WP : 2 * WP;  // TMEM columns of one O accumulator
+  auto tO = [&](int b) -> uint32_t { return tmem + (uint32_t)(NS * BN) + (uint32_t)b * AW; };
   auto tDT = [&](uint32_t b) -> uint32_t { return tmem + (uint32_t)(NS * BN + 4 * WP) + b * 2u * WP; };
   const uint32_t tA = tmem + (uint32_t)(NS * BN + 8 * WP);  // ATM: row tile, ka / 2 columns
-  constexpr uint32_t NO = WIDE ? 1u : 2u;  // O buffers
+  constexpr uint32_t NO = 2u;  // O buffers
   const int64_t half_off = (int64_t)rank * p.rec_bytes;   // this CTA's half of a record
 
   // setmaxnreg sits at the top of each warpgroup's branch so that ptxas sees
@@ -928,7 +932,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
               tc_commit2(&g2done[r]);           // V slot g free (both CTAs)
               tc_commit2(&pt_free[gt & 1u]);    // with T(g): P(g)'s buffer free
             } else {
-              if (!(DBG && (p.debug_mode == 2 || p.debug_mode == 6))) {
+              if (WIDE) {  // P_hi Vhi, P_hi Vlo, P_lo Vhi into the same 128 columns
+                const uint64_t b4 = (uint64_t)(p.v3_bytes >> 4);
+#pragma unroll
+                for (int m = 0; m < BN / 16; ++m) {
+                  const uint32_t ahi = a0 + 32u * (m >> 1) + 8u * (m & 1);
+                  const uint64_t b = dv + (uint64_t)(16 * m);
+                  mma_ts(dO, ahi, b, id2h, (fresh && m == 0) ? 0u : 1u);
+                  mma_ts(dO, ahi, b + b4, id2h, 1u);
+                  mma_ts(dO, ahi + 16u, b, id2h, 1u);
+                }
+              } else if (!(DBG && (p.debug_mode == 2 || p.debug_mode == 6))) {
 #pragma unroll
                 for (int m = 0; m < BN / 16; ++m) {
                   const uint32_t ahi = a0 + 32u * (m >> 1) + 8u * (m & 1);
@@ -1210,31 +1224,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       float* const part = reinterpret_cast<float*>(p.partial);
       while (ti.valid) {
         if (ti.last_in_item()) {
-          mbar_wait(&o_full[0], q & 1u);
+          const uint32_t ob = q & 1u;
+          mbar_wait(&o_full[ob], (q >> 1) & 1u);
           tc_fence_after();
           const int64_t i = (2 * (int64_t)ti.cur.pp + rank) * BM + row;  // local row
           const int64_t sp = ti.it % p.splits;
           float4* dst = reinterpret_cast<float4*>(part + (sp * p.nloc + i) * WP);
 #pragma unroll 1
           for (int h = 0; h < WP / 8; ++h) {
-            uint32_t x[8], y[8];
-            tmem_ld8(tO(0) + lane_off + 8 * h, x);       // P_hi Vhi + P_lo Vhi
-            tmem_ld8(tO(0) + lane_off + WP + 8 * h, y);  // P_hi Vlo
+            uint32_t x[8];
+            tmem_ld8(tO((int)ob) + lane_off + 8 * h, x);  // all three split terms
             tmem_wait_ld();
             if (i < p.nloc) {
-              dst[2 * h] = make_float4(__uint_as_float(x[0]) + __uint_as_float(y[0]),
-                                       __uint_as_float(x[1]) + __uint_as_float(y[1]),
-                                       __uint_as_float(x[2]) + __uint_as_float(y[2]),
-                                       __uint_as_float(x[3]) + __uint_as_float(y[3]));
-              dst[2 * h + 1] = make_float4(__uint_as_float(x[4]) + __uint_as_float(y[4]),
-                                           __uint_as_float(x[5]) + __uint_as_float(y[5]),
-                                           __uint_as_float(x[6]) + __uint_as_float(y[6]),
-                                           __uint_as_float(x[7]) + __uint_as_float(y[7]));
+              dst[2 * h] = make_float4(__uint_as_float(x[0]), __uint_as_float(x[1]),
+                                       __uint_as_float(x[2]), __uint_as_float(x[3]));
+              dst[2 * h + 1] = make_float4(__uint_as_float(x[4]), __uint_as_float(x[5]),
+                                           __uint_as_float(x[6]), __uint_as_float(x[7]));
             }
           }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(leader_addr(&o_empty[0]));
+          if (lane == 0) mbar_arrive_cluster(leader_addr(&o_empty[ob]));
           ++q;
         }
         ti.next(p, items);
@@ -1963,7 +1973,7 @@ template <typename T>
 __global__ void pack_v_kernel(const T* __restrict__ V, int64_t ldv, int64_t n, int w, int wp,
                               const int* __restrict__ col_exp, uint8_t* __restrict__ col_pack,
                               int64_t tile_stride, int64_t half, uint32_t xbh_bytes,
-                              uint32_t v2_bytes, int64_t col_tiles) {
+                              uint32_t v2_bytes, int64_t col_tiles, int wide = 0) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t chunks = col_tiles * (BN / 8);
   if (e >= chunks * wp) return;
@@ -1990,12 +2000,19 @@ __global__ void pack_v_kernel(const T* __restrict__ V, int64_t ldv, int64_t n, i
   a.z = hi[4] | ((uint32_t)hi[5] << 16); a.w = hi[6] | ((uint32_t)hi[7] << 16);
   b.x = lo[0] | ((uint32_t)lo[1] << 16); b.y = lo[2] | ((uint32_t)lo[3] << 16);
   b.z = lo[4] | ((uint32_t)lo[5] << 16); b.w = lo[6] | ((uint32_t)lo[7] << 16);
+  const int gh = wp / 16;  // c-groups per CTA in B3 / B4
+  const int cta = g / gh;
+  if (wide) {
+    // wide kernel: B3 (Vhi) then B4 (Vlo), each split between the CTAs
+    uint8_t* r = rec + (cta ? half : 0) + (int64_t)(g - cta * gh) * 2048 + in_blk;
+    *reinterpret_cast<uint4*>(r) = a;
+    *reinterpret_cast<uint4*>(r + v2_bytes / 2) = b;
+    return;
+  }
   // B2: CTA0 <- Vhi, CTA1 <- Vlo, c-group g at g * 2048
   *reinterpret_cast<uint4*>(rec + (int64_t)g * 2048 + in_blk) = a;
   *reinterpret_cast<uint4*>(rec + half + (int64_t)g * 2048 + in_blk) = b;
   // B3: Vhi c-groups split between the CTAs
-  const int gh = wp / 16;  // c-groups per CTA in B3
-  const int cta = g / gh;
   *reinterpret_cast<uint4*>(rec + (cta ? half : 0) + v2_bytes + (int64_t)(g - cta * gh) * 2048 +
                             in_blk) = a;
 }
@@ -2142,8 +2159,11 @@ int ka_of(int d) { return ((3 * d + 4) + 15) / 16 * 16; }
 // 128 (the wide kernel, 32 < w <= 128)
 int wp_of(int w) { return w <= 16 ? 16 : (w <= 32 ? 32 : 128); }
 constexpr int WIDE_WP = 128;
-constexpr int WIDE_ITEM = 64;        // column tiles per wide item (fp32 TMEM accumulation span)
-constexpr int64_t WIDE_ROWS = 8192;  // rows per wide launch (bounds the fp32 partials)
+#ifndef NCGP_WIDE_ITEM
+#define NCGP_WIDE_ITEM 16
+#endif
+constexpr int WIDE_ITEM = NCGP_WIDE_ITEM;  // column tiles per wide item (fp32 TMEM accumulation span)
+constexpr int64_t WIDE_ROWS = 4096;  // rows per wide launch (bounds the fp32 partials)
 
 struct Layout {
   size_t mu, guard, colexp, bits, xa, col, partial, symacc, symtab, varacc, total;
@@ -2306,8 +2326,8 @@ Layout layout_of(int64_t n_rows, int64_t n_cols, int d, int w_max, int sms) {
 
 // the wide kernel (WP = 128): no fp64 accumulator rows in shared memory
 size_t smem_wide(uint32_t a_bytes, int sx, int sv) {
-  const size_t v2 = (size_t)WIDE_WP * BN * 2, v3 = v2 / 2;
-  return (size_t)a_bytes + (size_t)sx * (a_bytes / 2) + (size_t)sv * (v2 + v3) +
+  const size_t v2 = (size_t)WIDE_WP * BN * 2;  // a CTA's [B3 | B4] V slot
+  return (size_t)a_bytes + (size_t)sx * (a_bytes / 2) + (size_t)sv * v2 +
          (6 + 9 + 2 + NS_MAX + 5 * NR + 8 + 12) * sizeof(uint64_t) + 16 + 1024;
 }
 
@@ -2394,7 +2414,7 @@ bool tc_supported(int dtype, int d, int w_max) {
   const uint32_t a = (uint32_t)(BM * ka_of(d) * 2);
   if (smem_bytes(a, wp_of(std::min(w_max, 32)), 1, 3, 6) > (size_t)SMEM_BUDGET) return false;
   // wide RHS (w_max > 32): the WP = 128 kernel with (XB 2, V 3) rings, D <= ~50
-  return w_max <= 32 || smem_wide(a, 2, 3) <= SMEM_MAX;
+  return w_max <= 32 || smem_wide(a, 3, 3) <= SMEM_MAX;
 }
 
 // The wide kernel over rows [r0, r1) in blocks of WIDE_ROWS: products with
@@ -2425,7 +2445,7 @@ int tc_wide(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet* out, 
     const int64_t tot = op->col_tiles * (BN / 8) * wp;
     pack_v_kernel<float><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
         Vf, ldv, op->n_cols, w, wp, col_exp, op->col_pack, L.tile_stride, L.rec_bytes,
-        L.xbh_bytes, v2, op->col_tiles);
+        L.xbh_bytes, v2, op->col_tiles, 1);
     NCGP_LAUNCHED();
   }
   TcParams p{};
@@ -2441,7 +2461,8 @@ int tc_wide(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet* out, 
   p.w = w;
   p.col_tiles = op->col_tiles;
   // items of <= WIDE_ITEM column tiles: each accumulates in fp32 TMEM over
-  // at most 8192 columns; the splits are summed in fp64 in a fixed order
+  // at most 2048 columns (K1's chunk); the splits are summed in fp64 in a
+  // fixed order
   p.splits = (int)((op->col_tiles + WIDE_ITEM - 1) / WIDE_ITEM);
   p.tiles_per_split = (p.col_tiles + p.splits - 1) / p.splits;
   p.splits = (int)((p.col_tiles + p.tiles_per_split - 1) / p.tiles_per_split);
@@ -2454,8 +2475,8 @@ int tc_wide(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet* out, 
   p.ldo = ldo;
   p.partial = op->partial;
   p.na = 1;
-  p.sx = smem_wide(p.a_bytes, 3, 3) <= SMEM_MAX ? 3 : 2;
-  p.sv = 3;
+  p.sx = 3;
+  p.sv = smem_wide(p.a_bytes, 3, 4) <= SMEM_MAX ? 4 : 3;
   p.epi.alpha = 1.0;
   const size_t smem = smem_wide(p.a_bytes, p.sx, p.sv);
   NCGP_CHECK_ARG(smem <= SMEM_MAX, NCGP_UNSUPPORTED, "wide kernel: shared memory for d=%d", op->d);

@@ -372,3 +372,49 @@ class Dataset:
     @property
     def n_features(self) -> int:
         return self.inputs.shape[1]
+
+
+def _fmt_value(x) -> str:
+    """repr of a float (round-trip exact) or an integer (gp.py:244-247)."""
+    if isinstance(x, (int, np.integer)):
+        return str(int(x))
+    return repr(float(x))
+
+
+def write_dataset_csv(path, dataset: Dataset) -> None:
+    """CSV with header x_0..x_{D-1}, y; integer targets except for 'real'
+    data (gp.py:250-260)."""
+    import csv
+    import io
+    buf = io.StringIO()
+    w = csv.writer(buf, lineterminator="\n")
+    w.writerow([f"x_{d}" for d in range(dataset.n_features)] + ["y"])
+    ints = dataset.domain != "real"
+    for row, y in zip(dataset.inputs, dataset.targets):
+        w.writerow([_fmt_value(x) for x in row] + [str(int(y)) if ints else _fmt_value(y)])
+    with open(path, "w", newline="") as fh:
+        fh.write(buf.getvalue())
+
+
+def read_dataset_csv(path, domain: str, num_classes: int = 0) -> Dataset:
+    """Read a dataset CSV written by :func:`write_dataset_csv` (gp.py:263-278)."""
+    import csv
+    with open(path, newline="") as fh:
+        rows = list(csv.reader(fh))
+    header, body = (rows[0] if rows else []), [r for r in rows[1:] if r]
+    if not header or header[-1] != "y":
+        raise InvalidInput(f"{path}: expected header ending in 'y'")
+    if any(not h.startswith("x_") for h in header[:-1]):
+        raise InvalidInput(f"{path}: expected feature columns named x_0..x_{{D-1}}")
+    if not body:
+        raise InvalidInput(f"{path}: dataset has no rows")
+    data = np.array([[float(x) for x in r] for r in body])
+    return Dataset(inputs=data[:, :-1], targets=data[:, -1], domain=domain,
+                   num_classes=num_classes)
+
+
+def write_sidecar_json(path, payload: dict) -> None:
+    import json
+    with open(path, "w") as fh:
+        json.dump(payload, fh, indent=2, sort_keys=True)
+        fh.write("\n")

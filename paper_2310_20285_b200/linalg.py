@@ -19,7 +19,7 @@ import torch
 
 from . import kernels as K
 from .device import is_device, resolve_dtype, to_device, to_host
-from .exceptions import DimensionMismatch, InvalidInput
+from .exceptions import CgBreakdown, DimensionMismatch, InvalidInput, NotPositiveDefinite
 
 
 class LowRankRoot:
@@ -59,18 +59,28 @@ class LowRankRoot:
         return kb if kb.dtype == dt else kb.to(dt)
 
     def block(self, dtype=None) -> torch.Tensor:
-        """(rank, dim) device column block in ``dtype``."""
+        """(rank, dim) device column block in ``dtype``.  Each precision is
+        derived from the most precise copy held (the host fp64 columns or
+        the device block the root was built with), never from a rounded one."""
         dt = resolve_dtype(dtype)
         b = self._block
-        if b is not None:
-            return b if b.dtype == dt else b.to(dt)
+        if b is not None and b.dtype == dt:
+            return b
+        cache = self.__dict__.setdefault("_blocks", {})
+        if dt in cache:
+            return cache[dt]
         src = self._host
-        if is_device(src):
-            b = src.t().to(dt).contiguous()
+        if src is not None and not is_device(src):
+            out = to_device(np.ascontiguousarray(src.T), dt)
+        elif src is not None:
+            out = src.t().to(dt).contiguous()
         else:
-            b = to_device(np.ascontiguousarray(src.T), dt)
-        self._block = b
-        return b
+            out = b.to(dt)
+        if b is None:
+            self._block = out
+        else:
+            cache[dt] = out
+        return out
 
     @property
     def columns(self) -> np.ndarray:
@@ -124,3 +134,67 @@ def sym_eigh_truncated(M, rank_bound: int) -> EigenPairs:
     vals, vecs = np.linalg.eigh(0.5 * (M + M.T))
     order = np.argsort(vals)[::-1][:rank_bound]
     return EigenPairs(np.ascontiguousarray(vecs[:, order]), vals[order])
+
+
+def _spd_factor(A: torch.Tensor) -> torch.Tensor:
+    L, info = torch.linalg.cholesky_ex(A)
+    code = int(info.item())
+    if code > 0:
+        raise NotPositiveDefinite(code)
+    return L
+
+
+def dense_spd_solve(A, b):
+    """Solve A x = b for SPD A by Cholesky (linalg.py:89-96), on the device
+    through cuSOLVER (torch.linalg); NotPositiveDefinite carries the order of
+    the first non-positive leading minor.  numpy in, numpy out."""
+    dev = is_device(A)
+    At = to_device(A, A.dtype if dev else torch.float64)
+    bt = to_device(b, At.dtype)
+    if At.dim() != 2 or At.shape[0] != At.shape[1]:
+        raise DimensionMismatch(f"expected a square matrix, got shape {tuple(At.shape)}")
+    if bt.shape[0] != At.shape[0]:
+        raise DimensionMismatch(
+            f"right-hand side length {bt.shape[0]} != system size {At.shape[0]}")
+    L = _spd_factor(At)
+    x = torch.cholesky_solve(bt.reshape(bt.shape[0], -1), L).reshape(bt.shape)
+    return x if dev else to_host(x)
+
+
+def cholesky_inverse_root(A):
+    """Upper-triangular Q with Q Q' = inv(A): the inverse transpose of the
+    lower Cholesky factor (linalg.py:119-132), on the device."""
+    dev = is_device(A)
+    At = to_device(A, A.dtype if dev else torch.float64)
+    L = _spd_factor(At)
+    eye = torch.eye(At.shape[0], dtype=At.dtype, device=At.device)
+    Q = torch.linalg.solve_triangular(L, eye, upper=False).t().contiguous()
+    return Q if dev else to_host(Q)
+
+
+def cg_reference(apply_A, b, iters: int):
+    """Textbook conjugate gradients from zero (linalg.py:135-162), device
+    vectors with fp64 dot products (K6 ``dots``); ``apply_A`` takes and
+    returns device vectors.  Non-positive curvature raises CgBreakdown."""
+    dev = is_device(b)
+    bt = to_device(b, b.dtype if dev else torch.float64)
+    x = torch.zeros_like(bt)
+    r = bt.clone()
+    rs = float(K.dots([(r, r)]).item())
+    if rs == 0.0:
+        return x if dev else to_host(x)
+    p = r.clone()
+    for k in range(iters):
+        Ap = apply_A(p)
+        curv = float(K.dots([(p, Ap)]).item())
+        if curv <= 0.0:
+            raise CgBreakdown(k, curv)
+        alpha = rs / curv
+        x = K.lincomb(1.0, x, alpha, p)
+        r = K.lincomb(1.0, r, -alpha, Ap)
+        rs_new = float(K.dots([(r, r)]).item())
+        if rs_new == 0.0:
+            break
+        p = K.lincomb(1.0, r, rs_new / rs, p)
+        rs = rs_new
+    return x if dev else to_host(x)

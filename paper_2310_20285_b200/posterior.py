@@ -160,6 +160,42 @@ def posterior_marginal_var(belief: PosteriorBelief, X_test, chunk: int = 512, dt
     return to_host(var)
 
 
+def posterior_covariance(belief: PosteriorBelief, X_test, dtype=None) -> np.ndarray:
+    """Full predictive covariance over (point, output) pairs, CN layout,
+    K(X*, X*) - A A' with A = K(X*, X) Q (posterior.py:87-101); dense in
+    the test dimension, limited to 1000 test points like the reference.
+    Both products run on K1 (identity blocks for K(X*, X*), the root block
+    for A); the (N* C)^2 assembly is a device GEMM."""
+    Xt = np.asarray(X_test, dtype=np.float64)
+    if Xt.shape[0] > 1000:
+        raise InvalidInput("full covariance limited to 1000 test points")
+    dt = resolve_dtype(dtype if dtype is not None else belief.dtype)
+    C = belief.prior.num_outputs
+    nt, n = Xt.shape[0], belief.train_inputs.shape[0]
+    Xr = to_device(Xt, dt)
+    Xc = to_device(belief.train_inputs, dt)
+    out = torch.zeros((nt * C, nt * C), dtype=dt, device=Xr.device)
+    o4 = out.view(nt, C, nt, C)
+    eye = torch.eye(nt, dtype=dt, device=Xr.device)
+    R = belief.root.rank
+    Qb = belief.root.block(dt) if R else None
+    for spec, cols in belief.prior.spec_groups():
+        op_tt = K.KernelOperator(spec.family, spec.lengthscale, spec.outputscale, Xr, w_max=32)
+        with op_tt.sym_mode(0):
+            Ktt = op_tt.apply(eye)
+        for c in cols:
+            o4[:, c, :, c] = Ktt
+    if R:
+        A = torch.empty((nt, C, R), dtype=dt, device=Xr.device)
+        W = Qb.view(R, n, C).permute(1, 2, 0)                # W[j, c, r] = Q[j C + c, r]
+        for op, cols in _cross_ops(belief, Xt, dt):
+            for c in cols:
+                A[:, c, :] = op.apply(W[:, c, :].contiguous())
+        A2 = A.reshape(nt * C, R)
+        out -= A2 @ A2.t()
+    return to_host(out)
+
+
 def probit_predict(mean, var) -> np.ndarray:
     """Moderated softmax / logistic probabilities (posterior.py:104-121)."""
     mean = np.atleast_2d(np.asarray(mean, dtype=np.float64))
@@ -177,7 +213,5 @@ def probit_predict(mean, var) -> np.ndarray:
     return e / e.sum(axis=1, keepdims=True)
 
 
-def metric_accuracy(probabilities, targets) -> float:
-    """Fraction whose arg-max class is the target (posterior.py:237-244)."""
-    probs = np.asarray(probabilities, dtype=np.float64)
-    return float(np.mean(np.argmax(probs, axis=1) == np.asarray(targets, dtype=np.int64)))
+from .metrics import (PredictiveSummary, mc_predict, metric_accuracy, metric_ece,  # noqa: E402
+                      metric_nll, poisson_predictive_density)
