@@ -97,14 +97,67 @@ def labels_to_device(y) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(np.asarray(y), dtype=np.int64)).to(dev)
 
 
+_range_log = None  # active RangeTimer (profile_ranges), else None
+
+
+class RangeTimer:
+    """CUDA-event timings of the named ranges (nvtx_range) entered while it
+    is active: exclusive device-stream time per name (a nested range's time
+    is not also charged to its parent).  For fit breakdowns
+    (tools/fit_breakdown.py)."""
+
+    def __init__(self):
+        self.records = []  # (name, start, end, [(child start, child end)])
+        self.stack = []
+
+    def push(self, name):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.stack.append((name, e, []))
+
+    def pop(self):
+        name, e0, kids = self.stack.pop()
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record()
+        self.records.append((name, e0, e1, kids))
+        if self.stack:
+            self.stack[-1][2].append((e0, e1))
+
+    def totals(self) -> dict:
+        """Seconds per range name, exclusive of nested ranges, and calls."""
+        torch.cuda.synchronize()
+        out = {}
+        for name, e0, e1, kids in self.records:
+            t = e0.elapsed_time(e1) - sum(a.elapsed_time(b) for a, b in kids)
+            s, c = out.get(name, (0.0, 0))
+            out[name] = (s + t / 1e3, c + 1)
+        return out
+
+
+@contextlib.contextmanager
+def profile_ranges():
+    """Collect CUDA-event timings of every nvtx_range entered in the block."""
+    global _range_log
+    old, _range_log = _range_log, RangeTimer()
+    try:
+        yield _range_log
+    finally:
+        _range_log = old
+
+
 @contextlib.contextmanager
 def nvtx_range(name: str):
-    """NVTX range for ncu / Nsight filtering (no-op cost when no tool listens)."""
+    """NVTX range for ncu / Nsight filtering (no-op cost when no tool listens);
+    timed with CUDA events inside profile_ranges()."""
     if torch.cuda.is_available():
         torch.cuda.nvtx.range_push(name)
+        if _range_log is not None:
+            _range_log.push(name)
         try:
             yield
         finally:
+            if _range_log is not None:
+                _range_log.pop()
             torch.cuda.nvtx.range_pop()
     else:
         yield
