@@ -96,11 +96,15 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // shared memory, [hi Vhi + lo Vhi | hi Vlo] accumulators, two S buffers at WP = 32)
 #define NCGP_SYM1_PT 1
 #endif
+// (2: as 1, but the transposed product keeps the two-instruction form --
+// P_hi^T [Vhi | Vlo] (N = 2 WP) + P_lo^T Vhi -- so P^T is read from shared
+// memory once per k-step instead of twice, into a single-buffered D_T of
+// 2 WP columns)
 #ifndef NCGP_SYM1_NS16
 #define NCGP_SYM1_NS16 3  // K1-sym1 S buffers at WP = 16 (build-time A/B: 2 or 3)
 #endif
 #ifndef NCGP_FX_CVT
-#define NCGP_FX_CVT 1  // fixed-point conversion: 0 cvt.rni.s64.f32 (XU), 1 two-limb FMA (build-time A/B)
+#define NCGP_FX_CVT 0  // fixed-point conversion: 0 cvt.rni.s64.f32 (XU), 1 two-limb FMA (build-time A/B)
 #endif
 #ifndef NCGP_WAIT_MODE
 #define NCGP_WAIT_MODE 0  // 0: try_wait + suspend hint, 1: try_wait (default limit), 2: test_wait spin
@@ -1398,8 +1402,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
   // S buffers next to double-buffered O and D_T (2 x 2 WP columns each):
   // two at WP = 32, three at WP = 16
   constexpr bool PT = NCGP_SYM1_PT != 0;
+  constexpr bool TM = NCGP_SYM1_PT == 1;     // D_T merged into WP columns (double-buffered)
   constexpr int NS1 = PT ? 3 : (WP == 16 ? NCGP_SYM1_NS16 : 2);
-  constexpr uint32_t AW = PT ? WP : 2 * WP;  // TMEM columns of one O / D_T accumulator
+  constexpr uint32_t AW = PT ? WP : 2 * WP;  // TMEM columns of one O accumulator
+  constexpr uint32_t DW = TM ? WP : 2 * WP;  // TMEM columns of one D_T accumulator
+  constexpr uint32_t NDT = (PT && !TM) ? 1u : 2u;  // D_T buffers
   const uint32_t xb_bytes = 2u * p.xbh_bytes;  // 128 XB rows
   const uint32_t vb_bytes = 2u * p.v2_bytes;   // [Vhi | Vlo]: 2 WP rows
   uint8_t* sA = smem;
@@ -1469,7 +1476,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
   const uint32_t tmem = *tmem_slot;
   auto tS = [&](uint32_t b) -> uint32_t { return tmem + b * (uint32_t)BN; };
   auto tO = [&](uint32_t b) -> uint32_t { return tmem + (uint32_t)(NS1 * BN) + b * AW; };
-  auto tDT = [&](uint32_t b) -> uint32_t { return tmem + (uint32_t)(NS1 * BN) + 2u * AW + b * AW; };
+  auto tDT = [&](uint32_t b) -> uint32_t { return tmem + (uint32_t)(NS1 * BN) + 2u * AW + b * DW; };
   const bool p_tmem = PT || (p.sym_dbg & 128) != 0;  // P also in TMEM (over S) for GEMM2
 
   if (warp < 4) {
@@ -1653,7 +1660,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
         mbar_wait(&rdy[rr.idx], rr.phase);
         if (lane == 0) trace_ev<DBG>(p, g, 12);
         const bool tp = ti.transposed();
-        if (tp) mbar_wait(&dt_empty[dtq & 1u], ((dtq >> 1) & 1u) ^ 1u);
+        if (tp) mbar_wait(&dt_empty[dtq % NDT], ((dtq / NDT) & 1u) ^ 1u);
         if (hold)  // T(g) behind GEMM1(g + NS1) in the in-order tensor pipe
           while (*g1_cnt < g + (uint32_t)NS1 + 1u) {
           }
@@ -1662,13 +1669,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
         if (elect_one()) {
           if (tp && !(DBG && (p.sym_dbg & 4))) {
             const uint64_t pa = dP0 + (uint64_t)pbuf(g) * (PBUF >> 4);
-            const uint32_t dt = tDT(dtq & 1u);
+            const uint32_t dt = tDT(dtq % NDT);
             const uint64_t vlo = (uint64_t)(p.v2_bytes >> 4);
 #pragma unroll 1
             for (int m = 0; m < BN / 16; ++m) {
               const uint64_t ah = pa + (uint64_t)m * (4096 >> 4), al = ah + ((PBUF / 2) >> 4);
               const uint64_t b = dVI + (uint64_t)(16 * m);
-              if (PT) {  // P_hi^T Vhi, P_hi^T Vlo, P_lo^T Vhi into the same WP columns
+              if (TM) {  // P_hi^T Vhi, P_hi^T Vlo, P_lo^T Vhi into the same WP columns
                 mma1_ss(dt, ah, b, idTh, m > 0 ? 1u : 0u);
                 mma1_ss(dt, ah, b + vlo, idTh, 1u);
                 mma1_ss(dt, al, b, idTh, 1u);
@@ -1678,7 +1685,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
               }
             }
           }
-          if (tp) tc_commit1(&dt_full[dtq & 1u]);
+          if (tp) tc_commit1(&dt_full[dtq % NDT]);
           tc_commit1(&pt_free[g & 1u]);
           if (ti.last_in_item()) tc_commit1(vi_empty);
         }
@@ -1773,16 +1780,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
     constexpr uint32_t NBLK = WP == 32 ? 2u : 1u;  // staging blocks per warp (BM x WP x 4 bytes)
     const uint32_t stg_warp = smem_u32(sStage) + (uint32_t)wq * NBLK * 2048u;
     uint32_t nst = 0;
-    auto drain = [&](uint32_t tacc, int64_t row0, bool skip) {
+    auto drain = [&](uint32_t tacc, int64_t row0, bool skip, bool two) {
 #pragma unroll
       for (int h = 0; h < WP / 8; ++h) {
         uint32_t x[8], y[8];
-        tmem_ld8(tacc + lane_off + 8 * h, x);       // PT: all three terms; else hi Vhi + lo Vhi
-        if (!PT) tmem_ld8(tacc + lane_off + WP + 8 * h, y);  // [WP, 2 WP): hi Vlo
+        tmem_ld8(tacc + lane_off + 8 * h, x);       // merged: all three terms; else hi Vhi + lo Vhi
+        if (two) tmem_ld8(tacc + lane_off + WP + 8 * h, y);  // [WP, 2 WP): hi Vlo
         tmem_wait_ld();
         float v[8];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) v[c] = PT ? __uint_as_float(x[c]) : __uint_as_float(x[c]) + __uint_as_float(y[c]);
+        for (int c = 0; c < 8; ++c) v[c] = two ? __uint_as_float(x[c]) + __uint_as_float(y[c]) : __uint_as_float(x[c]);
         fx_flush8<NBLK>(p, stg_warp, nst, lane, h, v, row0, skip);
       }
       tc_fence_before();
@@ -1792,17 +1799,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
     uint32_t q = 0, dtq = 0;
     while (ti.valid) {
       if (ti.transposed()) {
-        mbar_wait(&dt_full[dtq & 1u], (dtq >> 1) & 1u);
+        mbar_wait(&dt_full[dtq % NDT], (dtq / NDT) & 1u);
         tc_fence_after();
-        if (!(DBG && (p.sym_dbg & 8))) drain(tDT(dtq & 1u), (int64_t)ti.ct * BM + 32 * wq, DBG && (p.sym_dbg & 1));
+        if (!(DBG && (p.sym_dbg & 8))) drain(tDT(dtq % NDT), (int64_t)ti.ct * BM + 32 * wq, DBG && (p.sym_dbg & 1), !TM);
         else tc_fence_before();
-        if (lane == 0) mbar_arrive(&dt_empty[dtq & 1u]);
+        if (lane == 0) mbar_arrive(&dt_empty[dtq % NDT]);
         ++dtq;
       }
       if (ti.last_in_chunk()) {
         mbar_wait(&o_full[q & 1u], (q >> 1) & 1u);
         tc_fence_after();
-        drain(tO(q & 1u), (int64_t)ti.r * BM + 32 * wq, DBG && (p.sym_dbg & 2));
+        drain(tO(q & 1u), (int64_t)ti.r * BM + 32 * wq, DBG && (p.sym_dbg & 2), !PT);
         if (lane == 0) mbar_arrive(&o_empty[q & 1u]);
         ++q;
       }
