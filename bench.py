@@ -82,6 +82,10 @@ def executed_per_pair(variant, d, w, n):
         ev = (nb + 1) / (2.0 * nb)
         tfrac = (nb - 1) / (nb + 1.0)
         return base + 6 * wp * tfrac, ev
+    if variant == 4:        # blocked symmetric kernel: same tiles as variant 2; the
+        ev = (nb + 1) / (2.0 * nb)   # transposed product P_hi^T [Vhi|Vlo] (fp16, N = 2 WP)
+        tfrac = (nb - 1) / (nb + 1.0)  # + P_lo^T Vhi in E4M3 (N = WP at twice the rate)
+        return base + 5 * wp * tfrac, ev
     if variant == 1:        # pair kernel: row-tile pair a covers [2a, nb)
         tiles = sum(nb - 2 * a for a in range((nb + 1) // 2))
         trans = sum(max(0, nb - 2 * a - 2) for a in range((nb + 1) // 2))

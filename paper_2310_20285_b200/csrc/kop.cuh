@@ -35,8 +35,10 @@ struct ncgp_kop {
   int sym_fx = 0;         // fixed-point fraction bits F of the accumulator (2^-F resolution)
   // tuning / experiment knobs, read once at creation (NCGP_* environment variables)
   int knob_sym = -1;      // NCGP_SYM: -1 policy, 0 off, 1 forced on
-  int knob_sym_cg = 0;    // NCGP_SYM_CG: 0 policy, 1 or 2 forced flavour
+  int knob_sym_cg = 0;    // NCGP_SYM_CG: 0 policy, 1, 2 or 3 forced flavour
   int knob_item = 128;    // NCGP_SYM_ITEM: column tiles per work item
+  int knob_item2 = 16;    // NCGP_SYM2_ITEM: the same for the blocked kernel (its O accumulates
+                          // in fp32 TMEM over a whole item)
   bool knob_pair_order = false;  // NCGP_SYM_ORDER=pair
   bool knob_atm = true;   // NCGP_SYM_ATM
   int knob_npb = 0;       // NCGP_SYM_NPB (pair kernel), 0 policy
@@ -44,9 +46,11 @@ struct ncgp_kop {
   int knob_sym_var = 0;   // NCGP_SYM_DBG bits that keep results correct (64: hold T, 128: TS GEMM2)
   int knob_rings[3] = {0, 0, 0};  // NCGP_RINGS "na,sx,sv" (plain kernel)
   std::vector<int64_t> sym_cum;  // host: tiles before each work item (partition of the list)
-  int sym_cg = 2;         // symmetric kernel flavour the work list was built for (1 or 2)
+  uint8_t* v8_pack = nullptr;  // blocked symmetric kernel: per column tile Vhi in E4M3
+  int sym_cg = 2;         // symmetric kernel flavour the work list was built for: 1 single-CTA
+                          // (K1-sym1), 2 CTA pairs (K1-sym), 3 blocked single-CTA (K1-sym2)
   int last_variant = -1;  // 0 plain, 1 symmetric pair kernel, 2 symmetric single-CTA kernel,
-                          // 3 wide-RHS kernel (K2)
+                          // 3 wide-RHS kernel (K2), 4 blocked symmetric kernel (K1-sym2)
 };
 
 // Epilogue of an apply (ncgp_kop_epilogue, include/ncgp_b200.h), with every

@@ -398,6 +398,9 @@ struct TcParams {
   EpiDev epi;            // plain kernel, splits == 1: the apply's epilogue at the row store
   float* sym_dump;       // symmetric kernel debug: raw D_T per (pair, tile, rank) when set
   int npb;               // symmetric kernel: P buffers in shared memory (2, or 1 for large D)
+  const uint8_t* v8_pack;  // blocked symmetric kernel: per column tile, Vhi in E4M3 (x 2^-LO8_SHIFT)
+  uint32_t v8_bytes;       // WP x 128 bytes (K-major, 8-row groups at 1024 B)
+  int nblk;                // blocked symmetric kernel: 2 KB staging blocks per drain warp
   int debug_mode;        // debug (timing only, wrong results): 1 = epilogue skips TMEM traffic,
                          // 2 = no GEMM2, 3 = no GEMM1, 4 = no column copies (8: XB only, 9: V only)
 };
@@ -1832,6 +1835,580 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
   }
 }
 
+// ------------------------------------------------------------------ blocked symmetric kernel
+// K1-sym2: the symmetric K(X, X) product on blocks of RB = 4 row tiles.
+// Work item = (row block b, column tiles [c0, c1), 16 of them by default);
+// tiles run column-major inside the item: for each column tile J the row
+// tiles I = 4b .. min(4b+3, J) of the block.  So
+//   * the 4 row accumulators O_I stay in TMEM for the whole item (flushed
+//     once per item, i.e. every 2048 columns as in the other flavours), and
+//   * the transposed accumulator D_T(J) collects the block's row tiles before
+//     it is drained: one int64 staging + bulk reduction per 4 tiles instead of
+//     per tile (the shared-memory traffic that bound K1-sym1, ncu r02b).
+// The column tile's data (XB_J, V_J) stays in shared memory for its tiles;
+// the row data (XA_I, V_I) is streamed per tile.
+// Pipelining (tools/trace_sym2.py): S (GEMM1's output) is single-buffered and
+// released as soon as the epilogue has loaded it; P, which GEMM2 reads from
+// TMEM, has its own double-buffered region -- so neither GEMM2 nor the
+// epilogue's transcendentals sit on the S round trip.  That needs P in 96
+// TMEM columns per tile: P_hi in fp16 (64) and the split term P_lo in E4M3
+// (32).  P_hi is rounded to nearest, so |P_lo| <= 2^-12 |P|; P_lo * 2^6 and
+// Vhi * 2^-6 are E4M3 (kind::f8f6f4, K = 32): the term is 2^-12 of the
+// product and its 2^-4 relative rounding adds ~1e-5 relative error
+// (measured against fp64 in tests/test_gpu_symmetric.py).
+// Both products take the same split:
+//   GEMM2  O_I  += P_hi [Vhi_J ; Vlo_J] (two N = WP MMAs per k-step, A = P_hi
+//                  in TMEM) + P_lo8 Vhi8_J (A in TMEM)
+//   T      D_T(J) += P_hi^T [Vhi_I | Vlo_I] (N = 2 WP, A MN-major in shared
+//                  memory) + P_lo8^T Vhi8_I
+// Every tcgen05.mma operand is warp-uniform (see `uni` below).
+// Roles (24 warps): warp 0 lane 0 producer; warp 1 GEMM2; warp 2 TMEM
+// allocation + GEMM1; warp 3 the transposed product T; warps 4-19 the
+// epilogue (two groups alternating tiles); warps 20-23 the drains (D_T per
+// column tile, the 4 O accumulators at each item's end) into the int64
+// fixed-point accumulator (deterministic, as K1-sym1).
+constexpr int RB = 4;                       // row tiles per block
+constexpr int LO8_SHIFT = 6;                // P_lo * 2^6, Vhi * 2^-6 in E4M3
+constexpr uint32_t PH2 = BM * BN * 2;       // P_hi (fp16, MN-major for T)
+constexpr uint32_t P2BUF = PH2 + BM * BN;   // [P_hi | P_lo E4M3]: 48 KB
+constexpr int NR2 = 16;                     // per-tile barrier rings (power of two)
+constexpr uint32_t TP2 = 96;                // TMEM columns of one P region (hi 64 | lo8 32)
+#ifndef NCGP_SYM2_ABL
+#define NCGP_SYM2_ABL 0  // timing ablations (wrong results): 1 no T MMAs, 2 no P stores for T,
+                         // 4 no GEMM2 f16 MMAs, 8 no accumulator flushes
+#endif
+
+__device__ __forceinline__ void mma1_f8_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                           uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma1_f8_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc,
+                                           uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// kind::f8f6f4, A/B E4M3, D F32, M = 128; bit 15: A MN-major
+__host__ __device__ constexpr uint32_t idesc1_f8(int n, bool a_mn) {
+  return (1u << 4) | (a_mn ? (1u << 15) : 0u) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(128 >> 4) << 24);
+}
+// two floats -> E4M3x2 (a in the low byte)
+__device__ __forceinline__ uint32_t e4m3x2(float a, float b) {
+  uint16_t d;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(d) : "f"(b), "f"(a));
+  return (uint32_t)d;
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]));
+}
+
+// One 32-column chunk: S -> P_hi (fp16, rounded to nearest) and P_lo * 2^6 (E4M3).
+template <int FAM>
+__device__ __forceinline__ void transform_chunk2(const uint32_t (&r)[32], float L,
+                                                 uint32_t (&hi)[16], uint32_t (&l8)[8]) {
+  constexpr float S8 = (float)(1 << LO8_SHIFT);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    float k0, k1;
+    const float g0 = __uint_as_float(r[2 * i]);
+    const float g1 = __uint_as_float(r[2 * i + 1]);
+    if (FAM == NCGP_RBF) {
+      k0 = ex2(g0);
+      k1 = ex2(g1);
+    } else {
+      const float a0 = sqrt_approx(fmaxf(g0, 0.f));
+      const float a1 = sqrt_approx(fmaxf(g1, 0.f));
+      const float e0 = ex2(fmaf(a0, -1.4426950408889634f, L));
+      const float e1 = ex2(fmaf(a1, -1.4426950408889634f, L));
+      k0 = fmaf(a0, e0, e0);
+      k1 = fmaf(a1, e1, e1);
+    }
+    // round to the nearest value with 11 significant bits (fp16-exact)
+    const float h0 = __uint_as_float((__float_as_uint(k0) + 0x1000u) & 0xFFFFE000u);
+    const float h1 = __uint_as_float((__float_as_uint(k1) + 0x1000u) & 0xFFFFE000u);
+    hi[i] = pack_h2(h0, h1);
+    const uint32_t q = e4m3x2((k0 - h0) * S8, (k1 - h1) * S8);
+    if (i & 1)
+      l8[i >> 1] |= q << 16;
+    else
+      l8[i >> 1] = q;
+  }
+}
+
+// The CTA's tile sequence: items (row block, column range), column-major inside.
+struct Tile2 {
+  int it, c0, c1, ct, r, rlo, rend;
+  bool valid;
+  __device__ __forceinline__ void load(const TcParams& p) {
+    const int4 t = p.item_tab[it];
+    rlo = RB * t.x;
+    rend = min(rlo + RB, (int)p.col_tiles);
+    c0 = t.y;
+    c1 = t.z;
+    ct = c0;
+    r = rlo;
+  }
+  __device__ __forceinline__ void start(const TcParams& p) {
+    it = (int)blockIdx.x;
+    valid = it < p.n_items;
+    if (valid) load(p);
+  }
+  __device__ __forceinline__ int rhi() const { return min(rend, ct + 1); }
+  __device__ __forceinline__ void next(const TcParams& p) {
+    if (++r >= rhi()) {
+      r = rlo;
+      if (++ct >= c1) {
+        it += (int)gridDim.x;
+        valid = it < p.n_items;
+        if (valid) load(p);
+      }
+    }
+  }
+  __device__ __forceinline__ bool first_r() const { return r == rlo; }   // new column tile
+  __device__ __forceinline__ bool last_r() const { return r + 1 == rhi(); }
+  __device__ __forceinline__ bool tp() const { return r < ct; }          // off-diagonal
+  __device__ __forceinline__ bool tp_first() const { return r < ct && r == rlo; }
+  __device__ __forceinline__ bool tp_last() const { return r < ct && r + 1 == min(rend, ct); }
+  __device__ __forceinline__ int k() const { return r - rlo; }
+  __device__ __forceinline__ bool o_fresh() const { return ct == max(c0, r); }
+  __device__ __forceinline__ bool o_last() const { return ct == c1 - 1; }
+};
+
+// DBG: per-tile clock64 trace of CTA 0 (tools/trace_sym2.py): 0/1/2 GEMM1 wait/go/issued,
+// 3/4/5/6 epilogue wait/s_full/S released/done, 7/8/9 GEMM2 wait/go/issued,
+// 10/11/12 T wait/go/issued, 13/14 drain of D_T start/done
+template <int FAM, int WP, bool DBG>
+__global__ void __launch_bounds__(NTHREADS, 1) kop_sym2_kernel(const TcParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  // TMEM: S [0, 128) | P0, P1 (96 each) | O_0..O_3 (WP each) | D_T (2 WP, NDT buffers)
+  constexpr uint32_t NDT = WP == 16 ? 2u : 1u;
+  static_assert(BN + 2 * TP2 + RB * WP + NDT * 2 * WP <= TMEM_COLS, "TMEM budget");
+  const uint32_t vb_bytes = 2u * p.v2_bytes;        // [Vhi | Vlo]: 2 WP rows x 128
+  const uint32_t vi_bytes = vb_bytes + p.v8_bytes;  // + Vhi in E4M3
+  uint8_t* sXA = smem;                                   // [sx] row tiles
+  uint8_t* sVI = sXA + (size_t)p.sx * p.a_bytes;         // [sv] row tiles' V (T's B)
+  uint8_t* sXB = sVI + (size_t)p.sv * vi_bytes;          // [2] column tile XB
+  uint8_t* sVJ = sXB + 2 * (size_t)p.a_bytes;            // [2] column tile V (GEMM2's B)
+  uint8_t* sP = sVJ + 2 * (size_t)vi_bytes;              // [2] P for T
+  uint8_t* sStage = sP + 2 * (size_t)P2BUF;              // [4 warps][nblk] 2 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStage + 4 * p.nblk * 2048);
+  uint64_t* xa_full = bars;              // [4]
+  uint64_t* vi_full = xa_full + 4;       // [4]
+  uint64_t* xb_full = vi_full + 4;       // [2]
+  uint64_t* xb_empty = xb_full + 2;      // [2]  GEMM1 done with the slot
+  uint64_t* vj_full = xb_empty + 2;      // [2]
+  uint64_t* vj_empty = vj_full + 2;      // [2]  GEMM2 done with the slot
+  uint64_t* s_full = vj_empty + 2;       // [NR2] GEMM1(g) done
+  uint64_t* s_free = s_full + NR2;       // [NR2] S(g) loaded by the epilogue (8 warps)
+  uint64_t* rdy = s_free + NR2;          // [NR2] P(g) in TMEM and shared memory (8 warps)
+  uint64_t* g2done = rdy + NR2;          // [NR2] GEMM2(g) done (P region g & 1 free)
+  uint64_t* tdone = g2done + NR2;        // [NR2] T(g) done (P smem buffer and V_I slot free)
+  uint64_t* o_full = tdone + NR2;        // [RB]
+  uint64_t* o_empty = o_full + RB;       // [RB] 4 drain warps (after loading O)
+  uint64_t* dt_full = o_empty + RB;      // [2]
+  uint64_t* dt_empty = dt_full + 2;      // [2]  4 drain warps (after loading D_T)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dt_empty + 2);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 4; ++s) {
+      mbar_init(&xa_full[s], 1);
+      mbar_init(&vi_full[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&xb_full[s], 1);
+      mbar_init(&xb_empty[s], 1);
+      mbar_init(&vj_full[s], 1);
+      mbar_init(&vj_empty[s], 1);
+      mbar_init(&dt_full[s], 1);
+      mbar_init(&dt_empty[s], 4);
+    }
+    for (int s = 0; s < NR2; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&s_free[s], 8);
+      mbar_init(&rdy[s], 8);
+      mbar_init(&g2done[s], 1);
+      mbar_init(&tdone[s], 1);
+    }
+    for (int k = 0; k < RB; ++k) {
+      mbar_init(&o_full[k], 1);
+      mbar_init(&o_empty[k], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  // Every operand of a tcgen05.mma must be warp-uniform in the compiler's
+  // analysis, or ptxas wraps each MMA in an ELECT / R2UR.BROADCAST waterfall
+  // loop that costs ~50 cycles per instruction (tools/mma_issue_probe.cu:
+  // 16.9 cycles per TS N = 32 MMA with uniform operands).  Values that derive
+  // from loads (the TMEM base, the work-item fields) are broadcast from lane 0
+  // with __shfl_sync, which the compiler treats as uniform.
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  auto uni = [](uint32_t v) -> uint32_t { return __shfl_sync(0xffffffffu, v, 0); };
+  auto tP = [&](uint32_t b) -> uint32_t { return tmem + (uint32_t)BN + b * TP2; };
+  auto tO = [&](uint32_t k) -> uint32_t { return tmem + (uint32_t)BN + 2u * TP2 + k * (uint32_t)WP; };
+  auto tDT = [&](uint32_t b) -> uint32_t {
+    return tmem + (uint32_t)BN + 2u * TP2 + (uint32_t)(RB * WP) + b * (uint32_t)(2 * WP);
+  };
+  auto par = [](uint32_t t) -> uint32_t { return (t / NR2) & 1u; };
+
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+    if (warp == 0) {
+      // ================= producers =================
+      // lane 0: GEMM1's operands (XA per tile, XB per column tile); lane 1:
+      // the V blocks (V_I per tile for T, V_J per column tile for GEMM2).  Two
+      // threads, so that waiting for T to free a V_I slot never delays the
+      // next row tile's XA (GEMM1 is on the single S buffer's round trip).
+      if (lane < 2) {
+        Tile2 ti;
+        ti.start(p);
+        Ring r;
+        r.init((uint32_t)(lane == 0 ? p.sx : p.sv));
+        uint32_t g = 0, jq = 0;
+        while (ti.valid) {
+          const uint32_t s = jq & 1u;
+          if (lane == 0) {
+            if (ti.first_r()) {  // this column tile's XB, for its <= 4 tiles
+              const uint8_t* rec = p.col_pack + (int64_t)ti.ct * p.tile_stride;
+              if (jq >= 2) mbar_wait(&xb_empty[s], ((jq >> 1) & 1u) ^ 1u);
+              mbar_expect_tx(&xb_full[s], p.a_bytes);
+              uint8_t* dx = sXB + (size_t)s * p.a_bytes;
+              bulk_g2s(dx, rec, p.xbh_bytes, &xb_full[s]);
+              bulk_g2s(dx + p.xbh_bytes, rec + p.rec_bytes, p.xbh_bytes, &xb_full[s]);
+            }
+            if (g >= (uint32_t)p.sx) {  // XA slot freed by GEMM1(g - sx)
+              const uint32_t t = g - (uint32_t)p.sx;
+              mbar_wait(&s_full[t % NR2], par(t));
+            }
+            mbar_expect_tx(&xa_full[r.idx], p.a_bytes);
+            bulk_g2s(sXA + (size_t)r.idx * p.a_bytes, p.xa_pack + (int64_t)ti.r * p.a_bytes, p.a_bytes,
+                     &xa_full[r.idx]);
+          } else {
+            auto load_v = [&](uint8_t* dst, int64_t tile, uint64_t* bar) {  // [Vhi | Vlo | Vhi8]
+              const uint8_t* rec = p.col_pack + tile * p.tile_stride;
+              bulk_g2s(dst, rec + p.xbh_bytes, p.v2_bytes, bar);
+              bulk_g2s(dst + p.v2_bytes, rec + p.rec_bytes + p.xbh_bytes, p.v2_bytes, bar);
+              bulk_g2s(dst + vb_bytes, p.v8_pack + tile * p.v8_bytes, p.v8_bytes, bar);
+            };
+            if (ti.first_r()) {  // V_J for GEMM2
+              if (jq >= 2) mbar_wait(&vj_empty[s], ((jq >> 1) & 1u) ^ 1u);
+              mbar_expect_tx(&vj_full[s], vi_bytes);
+              load_v(sVJ + (size_t)s * vi_bytes, ti.ct, &vj_full[s]);
+            }
+            if (g >= (uint32_t)p.sv) {  // V_I slot freed by T(g - sv)
+              const uint32_t t = g - (uint32_t)p.sv;
+              mbar_wait(&tdone[t % NR2], par(t));
+            }
+            mbar_expect_tx(&vi_full[r.idx], vi_bytes);
+            load_v(sVI + (size_t)r.idx * vi_bytes, ti.r, &vi_full[r.idx]);
+          }
+          jq += ti.first_r() ? 1u : 0u;
+          r.adv();
+          ++g;
+          ti.next(p);
+        }
+      }
+    } else if (warp == 2) {
+      // ================= GEMM1: S(g) = XA_I . XB_J^T =================
+      const uint32_t sbo_x = (uint32_t)(p.ka / 8) * 128u;
+      const int ksteps1 = p.ka / 16;
+      const uint64_t dA0 = sdesc(smem_u32(sXA), 128u, sbo_x);
+      const uint64_t dX0 = sdesc(smem_u32(sXB), 128u, sbo_x);
+      const uint32_t id1 = idesc1_f16(BN);
+      Tile2 ti;
+      ti.start(p);
+      Ring xr;
+      xr.init((uint32_t)p.sx);
+      uint32_t g = 0, jq = 0;
+      while (ti.valid) {
+        const uint32_t s = jq & 1u;
+        if (lane == 0) trace_ev<DBG>(p, g, 0);
+        if (ti.first_r()) mbar_wait(&xb_full[s], (jq >> 1) & 1u);
+        mbar_wait(&xa_full[xr.idx], xr.phase);
+        if (g >= 1u) mbar_wait(&s_free[(g - 1u) % NR2], par(g - 1u));  // S(g - 1) loaded
+        tc_fence_after();
+        if (lane == 0) trace_ev<DBG>(p, g, 1);
+        const uint64_t da = dA0 + (uint64_t)xr.idx * (p.a_bytes >> 4);
+        const uint32_t su = uni(s), lr = uni(ti.last_r() ? 1u : 0u);
+        const uint64_t dx = dX0 + (uint64_t)su * (p.a_bytes >> 4);
+        if (elect_one()) {
+          for (int k = 0; k < ksteps1; ++k)
+            mma1_ss(tmem, da + (uint64_t)(16 * k), dx + (uint64_t)(16 * k), id1, k > 0);
+          tc_commit1(&s_full[g % NR2]);  // also frees the XA slot (producer)
+          if (lr) tc_commit1(&xb_empty[su]);
+        }
+        __syncwarp();
+        if (lane == 0) trace_ev<DBG>(p, g, 2);
+        jq += ti.last_r() ? 1u : 0u;
+        xr.adv();
+        ++g;
+        ti.next(p);
+      }
+    } else if (warp == 1) {
+      // ================= GEMM2: O_I += P_hi [Vhi_J ; Vlo_J] + P_lo8 Vhi8_J (A = P in TMEM) =================
+      const uint32_t id2h = idesc1_f16(WP), id28 = idesc1_f8(WP, false);
+      const uint64_t dV0 = sdesc(smem_u32(sVJ), 128u, (uint32_t)(BN * 16));
+      const uint64_t dV80 = sdesc(smem_u32(sVJ) + vb_bytes, 128u, 1024u);
+      const uint64_t vlo = (uint64_t)(p.v2_bytes >> 4);
+      Tile2 ti;
+      ti.start(p);
+      uint32_t g = 0, jq = 0, ouse = 0;  // ouse bit k: parity of O_k's uses
+      while (ti.valid) {
+        const uint32_t s = jq & 1u;
+        const int k = ti.k();
+        const bool fresh = ti.o_fresh();
+        if (lane == 0) trace_ev<DBG>(p, g, 7);
+        mbar_wait(&rdy[g % NR2], par(g));
+        if (ti.first_r()) mbar_wait(&vj_full[s], (jq >> 1) & 1u);
+        if (fresh) {
+          mbar_wait(&o_empty[k], ((ouse >> k) & 1u) ^ 1u);
+          ouse ^= 1u << k;
+        }
+        tc_fence_after();
+        if (lane == 0) trace_ev<DBG>(p, g, 8);
+        const uint32_t su = uni(s), ku = uni((uint32_t)k), fu = uni(fresh ? 1u : 0u);
+        const uint32_t ol = uni(ti.o_last() ? 1u : 0u), lr = uni(ti.last_r() ? 1u : 0u);
+        const uint64_t vo = (uint64_t)su * (vi_bytes >> 4);
+        const uint32_t dO = tO(ku), a0 = tP(g & 1u);
+        if (elect_one()) {
+#pragma unroll
+          for (int m = 0; m < ((NCGP_SYM2_ABL & 4) ? 0 : BN / 16); ++m) {
+            const uint64_t b = dV0 + vo + (uint64_t)(16 * m);
+            mma1_ts(dO, a0 + 8u * m, b, id2h, (fu != 0u && m == 0) ? 0u : 1u);
+            mma1_ts(dO, a0 + 8u * m, b + vlo, id2h, 1u);
+          }
+#ifndef NCGP_SYM2_G2F8
+#define NCGP_SYM2_G2F8 1
+#endif
+#pragma unroll
+          for (int q = 0; q < (NCGP_SYM2_G2F8 ? BN / 32 : 0); ++q)
+            mma1_f8_ts(dO, a0 + 64u + 8u * q, dV80 + vo + (uint64_t)(16 * q), id28, 1u);
+          tc_commit1(&g2done[g % NR2]);
+          if (ol) tc_commit1(&o_full[ku]);
+          if (lr) tc_commit1(&vj_empty[su]);
+        }
+        __syncwarp();
+        if (lane == 0) trace_ev<DBG>(p, g, 9);
+        jq += ti.last_r() ? 1u : 0u;
+        ++g;
+        ti.next(p);
+      }
+    } else {
+      // ================= T: D_T(J) += P_hi^T [Vhi_I | Vlo_I] + P_lo8^T Vhi8_I =================
+      const uint32_t idT = idesc1_f16(2 * WP, true), idT8 = idesc1_f8(WP, true);
+      const uint64_t dPH0 = sdesc(smem_u32(sP), 2048u, 128u);        // MN-major fp16
+      const uint64_t dP80 = sdesc(smem_u32(sP) + PH2, 1024u, 128u);  // MN-major E4M3
+      const uint64_t dVI0 = sdesc(smem_u32(sVI), 128u, (uint32_t)(BN * 16));
+      const uint64_t dV80 = sdesc(smem_u32(sVI) + vb_bytes, 128u, 1024u);
+      Tile2 ti;
+      ti.start(p);
+      Ring vr;
+      vr.init((uint32_t)p.sv);
+      uint32_t g = 0, dq = 0;
+      while (ti.valid) {
+        if (lane == 0) trace_ev<DBG>(p, g, 10);
+        mbar_wait(&rdy[g % NR2], par(g));
+        mbar_wait(&vi_full[vr.idx], vr.phase);
+        const bool tp = ti.tp();
+        if (ti.tp_first()) mbar_wait(&dt_empty[dq % NDT], ((dq / NDT) & 1u) ^ 1u);
+        tc_fence_after();
+        if (lane == 0) trace_ev<DBG>(p, g, 11);
+        const uint32_t tpu = uni(tp ? 1u : 0u), fu = uni(ti.tp_first() ? 1u : 0u);
+        const uint32_t tlu = uni(ti.tp_last() ? 1u : 0u), dqb = uni(dq % NDT);
+        if (elect_one()) {
+          if (tpu) {
+            const uint64_t pb = (uint64_t)(g & 1u) * (P2BUF >> 4);
+            const uint64_t vo = (uint64_t)vr.idx * (vi_bytes >> 4);
+            const uint32_t dt = tDT(dqb);
+#pragma unroll
+            for (int m = 0; m < ((NCGP_SYM2_ABL & 1) ? 0 : BN / 16); ++m)
+              mma1_ss(dt, dPH0 + pb + (uint64_t)m * (4096 >> 4), dVI0 + vo + (uint64_t)(16 * m), idT,
+                      (fu != 0u && m == 0) ? 0u : 1u);
+#pragma unroll
+            for (int q = 0; q < ((NCGP_SYM2_ABL & 1) ? 0 : BN / 32); ++q)
+              mma1_f8_ss(dt, dP80 + pb + (uint64_t)q * (4096 >> 4), dV80 + vo + (uint64_t)(16 * q), idT8, 1u);
+            if (tlu) tc_commit1(&dt_full[dqb]);
+          }
+          tc_commit1(&tdone[g % NR2]);
+        }
+        __syncwarp();
+        if (lane == 0) trace_ev<DBG>(p, g, 12);
+        dq += ti.tp_last() ? 1u : 0u;
+        vr.adv();
+        ++g;
+        ti.next(p);
+      }
+    }
+  } else if (warp < 4 + EPI_WARPS) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 96;");  // the CTA pool: 8192 released by the decs
+    // ================= epilogue: two groups of 8 warps alternate tiles =================
+    const int e = (warp - 4) / 8;
+    const int hc = ((warp - 4) % 8) / 4;
+    const int wq = warp & 3;
+    const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
+    const uint32_t col0 = (uint32_t)(hc * (BN / 2));
+    const int i = 32 * wq + lane;
+    const uint32_t rowh = (uint32_t)(i >> 3) * 2048u + (uint32_t)(i & 7) * 16u + (col0 >> 3) * 128u;
+    const uint32_t row8 = PH2 + (uint32_t)(i >> 3) * 1024u + (uint32_t)(i & 7) * 16u + (col0 >> 4) * 128u;
+    Tile2 ti;
+    ti.start(p);
+    const float L = p.L;
+    uint32_t g = 0;
+    const bool tr = wq == 0 && hc == 0 && lane == 0;
+    while (ti.valid) {
+      if ((int)(g & 1u) == e) {
+        const bool tp = ti.tp();
+        if (tr) trace_ev<DBG>(p, g, 3);
+        mbar_wait(&s_full[g % NR2], par(g));
+        tc_fence_after();
+        if (tr) trace_ev<DBG>(p, g, 4);
+        // load both chunks of S, then release the (single) S buffer to GEMM1
+        uint32_t ra[32], rb[32], hi[16], l8[8];
+        tmem_ld32(tmem + lane_off + col0, ra);
+        tmem_ld32(tmem + lane_off + col0 + 32, rb);
+        tmem_wait_ld(ra);
+        tmem_wait_ld(rb);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_free[g % NR2]);
+        if (tr) trace_ev<DBG>(p, g, 5);
+        const uint32_t pr = tP(g & 1u) + lane_off;
+        const uint32_t pbase = smem_u32(sP) + (g & 1u) * P2BUF;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          if (c == 0)
+            transform_chunk2<FAM>(ra, L, hi, l8);
+          else
+            transform_chunk2<FAM>(rb, L, hi, l8);
+          if (c == 0 && g >= 2u) {  // GEMM2(g - 2) has read P region g & 1
+            mbar_wait(&g2done[(g - 2u) % NR2], par(g - 2u));
+            tc_fence_after();
+          }
+          const uint32_t cc = (col0 >> 5) + (uint32_t)c;  // chunk of the tile (0..3)
+          tmem_st16(pr + 16u * cc, hi);
+          tmem_st8(pr + 64u + 8u * cc, l8);
+          if (tp && !(NCGP_SYM2_ABL & 2)) {
+            if (c == 0 && g >= 2u)  // T(g - 2) is done with this P smem buffer
+              mbar_wait(&tdone[(g - 2u) % NR2], par(g - 2u));
+            const uint32_t rh = pbase + rowh + 512u * c;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              st_shared_v4(rh + 128u * k, hi[4 * k], hi[4 * k + 1], hi[4 * k + 2], hi[4 * k + 3]);
+            const uint32_t r8 = pbase + row8 + 256u * c;
+            st_shared_v4(r8, l8[0], l8[1], l8[2], l8[3]);
+            st_shared_v4(r8 + 128u, l8[4], l8[5], l8[6], l8[7]);
+          }
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        if (tp) fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&rdy[g % NR2]);
+        if (tr) trace_ev<DBG>(p, g, 6);
+      }
+      ++g;
+      ti.next(p);
+    }
+  } else {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    // ================= drains: D_T per column tile, O_I at each item's end =================
+    // Each accumulator is loaded into registers and released at once (D_T is
+    // single-buffered at WP = 32), then rounded to int64 and bulk-reduced.
+    const int wq = warp & 3;
+    const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
+    // int64 fixed point straight from registers: one coalesced red.global.add.u64
+    // per column (the accumulator is column-major here, [WP][acc_rows]) -- no
+    // shared-memory staging and no TMA queueing behind the producers' loads
+    // (bulk reductions through 2 KB staging blocks cost 14 % at n = 2e5).
+    auto flush = [&](const float (&v)[WP], int64_t row0) {
+      if (NCGP_SYM2_ABL & 8) return;
+      unsigned long long* dst = p.acc + row0 + lane;
+#pragma unroll
+      for (int c = 0; c < WP; ++c) {
+        const long long q = __float2ll_rn(v[c] * p.fx);
+        atomicAdd(dst + (int64_t)c * p.acc_rows, (unsigned long long)q);
+      }
+    };
+    Tile2 ti;
+    ti.start(p);
+    uint32_t dq = 0, ouse = 0, g = 0;
+    while (ti.valid) {
+      if (ti.tp_last()) {
+        if (wq == 0 && lane == 0) trace_ev<DBG>(p, g, 13);
+        mbar_wait(&dt_full[dq % NDT], (dq / NDT) & 1u);
+        tc_fence_after();
+        float v[WP];
+        const uint32_t ta = tDT(dq % NDT) + lane_off;
+#pragma unroll
+        for (int h = 0; h < WP / 8; ++h) {
+          uint32_t x[8], y[8];
+          tmem_ld8(ta + 8 * h, x);
+          tmem_ld8(ta + WP + 8 * h, y);  // [WP, 2 WP): P_hi^T Vlo
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 8; ++c) v[8 * h + c] = __uint_as_float(x[c]) + __uint_as_float(y[c]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&dt_empty[dq % NDT]);
+        flush(v, (int64_t)ti.ct * BM + 32 * wq);
+        if (wq == 0 && lane == 0) trace_ev<DBG>(p, g, 14);
+        ++dq;
+      }
+      if (ti.o_last()) {
+        const int k = ti.k();
+        mbar_wait(&o_full[k], (ouse >> k) & 1u);
+        ouse ^= 1u << k;
+        tc_fence_after();
+        float v[WP];
+        const uint32_t ta = tO((uint32_t)k) + lane_off;
+#pragma unroll
+        for (int h = 0; h < WP / 8; ++h) {
+          uint32_t x[8];
+          tmem_ld8(ta + 8 * h, x);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 8; ++c) v[8 * h + c] = __uint_as_float(x[c]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&o_empty[k]);
+        flush(v, (int64_t)ti.r * BM + 32 * wq);
+      }
+      ++g;
+      ti.next(p);
+    }
+  }
+
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
 // ------------------------------------------------------------------ packing
 
 // column means of Xc in fp64 (single block, fixed order)
@@ -2024,6 +2601,43 @@ __global__ void pack_v_kernel(const T* __restrict__ V, int64_t ldv, int64_t n, i
                             in_blk) = a;
 }
 
+// K1-sym2: Vhi of each column tile in E4M3 (x 2^-LO8_SHIFT), the B operand
+// of the transposed product's small split term: K-major, element (c, j) at
+// (c / 8) * 1024 + (j / 16) * 128 + (c % 8) * 16 + j % 16.  Vhi is the same
+// fp16 value pack_v_kernel stores (|Vhi| < 2^14, so |Vhi 2^-6| < 448).
+template <typename T>
+__global__ void pack_v8_kernel(const T* __restrict__ V, int64_t ldv, int64_t n, int w, int wp,
+                               const int* __restrict__ col_exp, uint8_t* __restrict__ v8,
+                               int64_t col_tiles) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t chunks = col_tiles * (BN / 16);
+  if (e >= chunks * wp) return;
+  const int c = (int)(e % wp);
+  const int64_t qg = e / wp;
+  const int64_t tile = qg / (BN / 16);
+  const int q = (int)(qg % (BN / 16));
+  const float sc = ldexpf(1.f, col_exp[c]);
+  constexpr float S8 = 1.f / (float)(1 << LO8_SHIFT);
+  uint32_t b[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    float x[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int64_t j = qg * 16 + 4 * k + t;
+      const float v = (j < n && c < w) ? (float)V[j * ldv + c] * sc : 0.f;
+      x[t] = __half2float(__float2half_rn(v)) * S8;
+    }
+    b[k] = e4m3x2(x[0], x[1]) | (e4m3x2(x[2], x[3]) << 16);
+  }
+  uint4 val;
+  val.x = b[0];
+  val.y = b[1];
+  val.z = b[2];
+  val.w = b[3];
+  *reinterpret_cast<uint4*>(v8 + tile * ((int64_t)wp * BN) + (c / 8) * 1024 + q * 128 + (c % 8) * 16) = val;
+}
+
 template <typename T>
 __global__ void reduce_partial_kernel(const double* __restrict__ partial, int splits,
                                       int64_t nloc, int w, const ncgp::OutPtrs<T> out,
@@ -2124,13 +2738,14 @@ __global__ void reduce_partial_epi_kernel(const double* __restrict__ partial, in
 __global__ void sym_finalize_kernel(const unsigned long long* __restrict__ acc, int64_t acc_rows,
                                     int64_t n, int w, int fx_exp, int s_exp,
                                     const int* __restrict__ col_exp, const EpiDev e,
-                                    const ncgp::OutPtrs<float> out, int64_t ldo) {
+                                    const ncgp::OutPtrs<float> out, int64_t ldo, int colmajor) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int swz = (int)((i >> 1) & 3);
   auto kv = [&](int c) -> double {
     const int h = c >> 3, cc = c & 7;
-    const int64_t idx = ((int64_t)h * acc_rows + i) * 8 + (((cc >> 1) ^ swz) << 1) + (cc & 1);
+    const int64_t idx = colmajor ? (int64_t)c * acc_rows + i
+                                 : ((int64_t)h * acc_rows + i) * 8 + (((cc >> 1) ^ swz) << 1) + (cc & 1);
     return ldexp((double)(long long)acc[idx], -(fx_exp + s_exp + __ldg(&col_exp[c])));
   };
   ncgp::epi_row<float, NCGP_MAX_OUTS>(e, i, w, kv, out.p, out.n, ldo);
@@ -2156,7 +2771,7 @@ float* g_sym_dump = nullptr;   // debug hook (ncgp_debug_set_sym_dump)
 bool sym_enabled(const ncgp_kop* op, int family, int wp, int64_t col_tiles, int cg) {
   if (op->knob_sym == 0) return false;
   if (op->knob_sym == 1) return true;
-  if (cg == 1) return col_tiles >= 300;
+  if (cg == 1 || cg == 3) return col_tiles >= 300;
   return col_tiles >= 512 && (family == NCGP_MATERN32 || wp == 16);
 }
 int g_debug_mode = 0;          // debug hook (ncgp_debug_set_mode)
@@ -2173,7 +2788,7 @@ constexpr int WIDE_ITEM = NCGP_WIDE_ITEM;  // column tiles per wide item (fp32 T
 constexpr int64_t WIDE_ROWS = 4096;  // rows per wide launch (bounds the fp32 partials)
 
 struct Layout {
-  size_t mu, guard, colexp, bits, xa, col, partial, symacc, symtab, varacc, total;
+  size_t mu, guard, colexp, bits, xa, col, partial, symacc, symtab, varacc, v8, total;
   uint32_t a_bytes, xbh_bytes, rec_bytes;
   int64_t tile_stride, row_tiles, col_tiles;
 };
@@ -2248,12 +2863,15 @@ std::vector<int4> sym_items(int64_t pairs, int64_t nb, int item, bool pair_order
 // [r, nb); same block-major order.
 constexpr size_t SMEM_MAX = 232448;  // sm_100 opt-in maximum per block
 size_t smem1_bytes(uint32_t a_bytes, int wp, int sx, int sv, int npb = 2);
+size_t smem2_bytes(uint32_t a_bytes, int wp, int sx, int sv, int nblk);
 // Flavour of the symmetric kernel an operator's work list is built for: the
 // single-CTA kernel where its shared memory fits the widest RHS (full column
 // records plus two P buffers), else the pair kernel.  NCGP_SYM_CG=1 / 2 forces.
 int sym_cg(const ncgp_kop* op, int d, int w_max) {
-  if (op->knob_sym_cg == 1 || op->knob_sym_cg == 2) return op->knob_sym_cg;
+  if (op->knob_sym_cg >= 1 && op->knob_sym_cg <= 3) return op->knob_sym_cg;
   const uint32_t a = (uint32_t)(BM * ka_of(d) * 2);
+  // the blocked kernel (K1-sym2, flavour 3) wherever its rings fit
+  if (smem2_bytes(a, wp_of(w_max), 2, 2, 0) <= SMEM_MAX) return 3;
   // rings no shallower than (XB 2, V 4) or (XB 3, V 2): D = 24 at WP = 16
   // only fits (2, 3), which ran slower than the plain kernel; the pair kernel
   // keeps 3-deep rings there
@@ -2275,6 +2893,32 @@ int64_t sym1_item_count(int64_t nb) {
   int64_t n = 0;
   sym1_walk(nb, [&](int64_t, int64_t, int64_t) { ++n; });
   return n;
+}
+// K1-sym2 work list: row blocks of RB tiles, block b covering column tiles
+// [RB b, nb); the columns cut at global blocks of L tiles (L a multiple of
+// RB, so every row of an item's block meets the item's last column), and the
+// list block-major like the other flavours.
+template <typename F>
+void sym2_walk(int64_t nb, F&& f, int item = SYM_ITEM_MIN) {
+  const int64_t L = (std::max(item, SYM_ITEM_MIN) + RB - 1) / RB * RB;
+  const int64_t nrb = (nb + RB - 1) / RB;
+  for (int64_t b0 = 0; b0 < nb; b0 += L) {
+    const int64_t b1 = std::min<int64_t>(nb, b0 + L);
+    for (int64_t b = 0; b < nrb && RB * b < b1; ++b) f(b, std::max<int64_t>(b0, RB * b), b1);
+  }
+}
+// tiles of a K1-sym2 item: per column tile c, the block's rows r <= c
+int64_t sym2_item_tiles(int64_t b, int64_t c0, int64_t c1, int64_t nb) {
+  const int64_t rlo = RB * b, rend = std::min<int64_t>(rlo + RB, nb);
+  int64_t t = 0;
+  for (int64_t c = c0; c < c1; ++c) t += std::min<int64_t>(rend, c + 1) - rlo;
+  return t;
+}
+size_t smem2_bytes(uint32_t a_bytes, int wp, int sx, int sv, int nblk) {
+  const size_t vb = (size_t)wp * BN * 4, v8 = (size_t)wp * BN;
+  return (size_t)sx * a_bytes + (size_t)sv * (vb + v8) + 2 * (size_t)a_bytes + 2 * (vb + v8) +
+         2 * (size_t)P2BUF + (size_t)4 * nblk * 2048 + (4 + 4 + 2 * 6 + 5 * NR2 + 2 * RB) * sizeof(uint64_t) +
+         16 + 1024;
 }
 size_t smem1_bytes(uint32_t a_bytes, int wp, int sx, int sv, int npb) {
   const size_t v2 = (size_t)wp * BN * 2;
@@ -2327,6 +2971,8 @@ Layout layout_of(int64_t n_rows, int64_t n_cols, int d, int w_max, int sms) {
   L.symtab = take(sq ? (size_t)std::max(sym_item_count(L.row_tiles / 2, L.col_tiles),
                                          sym1_item_count(L.col_tiles)) * 16
                      : 0);
+  // blocked symmetric kernel: Vhi in E4M3 per column tile (WP x 128 bytes)
+  L.v8 = take(sq && wpm <= 32 ? (size_t)(L.col_tiles + 1) * wpm * BN : 0);
   L.total = off;
   return L;
 }
@@ -2358,6 +3004,7 @@ int sym_variant(const ncgp_kop* op, int w) {
   if (!sym_enabled(op, op->family, wp, op->col_tiles, op->sym_cg)) return 0;
   const uint32_t a_bytes = (uint32_t)(BM * op->ka * 2);
   if (op->sym_cg == 1) return smem1_bytes(a_bytes, wp, 2, 2, 1) <= SMEM_MAX ? 2 : 0;
+  if (op->sym_cg == 3) return smem2_bytes(a_bytes, wp, 2, 2, 0) <= SMEM_MAX ? 4 : 0;
   if (smem_bytes(a_bytes, wp, 1, 3, 3, 2) <= (size_t)SMEM_BUDGET) return 1;
   if (wp == 16 && atm_allowed(op) && op->ka <= 2 * 128 &&
       smem_bytes(a_bytes, wp, 0, 3, 3, 2) <= (size_t)SMEM_BUDGET)
@@ -2410,7 +3057,7 @@ int tc_sym_finalize(ncgp_kop* op, const unsigned long long* acc, int w, const Ou
   const int s_exp = (int)lround(log2(op->k_scale));
   sym_finalize_kernel<<<(unsigned)((op->n_rows + 127) / 128), 128, 0, st>>>(
       acc, op->row_tiles * BM, op->n_rows, w, op->sym_fx, s_exp, col_exp, epi,
-      ncgp::out_ptrs<float>(out, 0, ldo), ldo);
+      ncgp::out_ptrs<float>(out, 0, ldo), ldo, op->sym_cg == 3 ? 1 : 0);
   NCGP_LAUNCHED();
   return NCGP_OK;
 }
@@ -2537,6 +3184,7 @@ int tc_prepare(ncgp_kop* op, cudaStream_t st) {
   // flushes below 2^42, |sum| < n 2^28 2^F < 2^62
   op->sym_fx = std::min(3, 33 - (int)ceil(log2((double)std::max<int64_t>(op->n_cols, 2))));
   op->sym_tab = reinterpret_cast<int4*>(op->ws + L.symtab);
+  op->v8_pack = op->ws + L.v8;
   std::vector<int4> tab;
   if (op->n_rows == op->n_cols)
     NCGP_CUDA(cudaMemsetAsync(op->col_pack + (size_t)L.col_tiles * L.tile_stride, 0,
@@ -2547,13 +3195,19 @@ int tc_prepare(ncgp_kop* op, cudaStream_t st) {
       sym1_walk(L.col_tiles, [&](int64_t r, int64_t c0, int64_t c1) {
         tab.push_back(make_int4((int)r, (int)c0, (int)c1, 0));
       }, op->knob_item);
+    else if (op->sym_cg == 3)  // items of 16 column tiles: O is flushed every 2048 columns
+      sym2_walk(L.col_tiles, [&](int64_t b, int64_t c0, int64_t c1) {
+        tab.push_back(make_int4((int)b, (int)c0, (int)c1, 0));
+      }, op->knob_item2);
     else
       tab = sym_items(L.row_tiles / 2, L.col_tiles, op->knob_item, op->knob_pair_order);
     NCGP_CUDA(cudaMemcpyAsync(op->sym_tab, tab.data(), tab.size() * sizeof(int4),
                               cudaMemcpyHostToDevice, st));
     op->sym_items = (int64_t)tab.size();  // the stream sync below keeps `tab` alive long enough
     op->sym_cum.assign(tab.size() + 1, 0);
-    for (size_t k = 0; k < tab.size(); ++k) op->sym_cum[k + 1] = op->sym_cum[k] + (tab[k].z - tab[k].y);
+    for (size_t k = 0; k < tab.size(); ++k)
+      op->sym_cum[k + 1] = op->sym_cum[k] + (op->sym_cg == 3 ? sym2_item_tiles(tab[k].x, tab[k].y, tab[k].z, L.col_tiles)
+                                                               : (int64_t)(tab[k].z - tab[k].y));
   }
   // prescale kernel values into fp16 range: s2 * 2^s in (2^13, 2^14]
   const int s_exp = 14 - (int)ceil(log2(op->s2));
@@ -2712,6 +3366,58 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
     return e != nullptr ? atoi(e) : 0;
   }() : 0);
   const bool sym_fin = part == nullptr;
+  if (sym && op->sym_cg == 3) {
+    // deepest rings that fit: (sx, sv, staging blocks per drain warp)
+    // (the drains reduce straight from registers: no staging blocks)
+    const int cand[][3] = {{3, 3, 0}, {3, 2, 0}, {2, 2, 0}};
+    bool fit = false;
+    for (auto& c : cand)
+      if (smem2_bytes(p.a_bytes, wp, c[0], c[1], c[2]) <= SMEM_MAX) {
+        p.sx = c[0];
+        p.sv = c[1];
+        p.nblk = c[2];
+        fit = true;
+        break;
+      }
+    NCGP_CHECK_ARG(fit, NCGP_UNSUPPORTED, "blocked symmetric kernel: shared memory for d=%d", op->d);
+    p.na = 1;
+    p.splits = 1;
+    p.tiles_per_split = p.col_tiles;
+    p.n_items = (int)(it_hi - it_lo);
+    p.item_tab = op->sym_tab + it_lo;
+    p.acc = sym_acc;
+    p.v8_pack = op->v8_pack;
+    p.v8_bytes = (uint32_t)(wp * BN);
+    NCGP_CUDA(cudaMemsetAsync(p.acc, 0, acc_bytes, st));
+    op->last_variant = 4;
+    if (p.n_items == 0) return NCGP_OK;  // an empty part
+    {
+      const int64_t tot = op->col_tiles * (BN / 16) * wp;
+      pack_v8_kernel<float><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+          Vf, ldv, op->n_cols, w, wp, col_exp, op->v8_pack, op->col_tiles);
+      NCGP_LAUNCHED();
+    }
+    const size_t smem = smem2_bytes(p.a_bytes, wp, p.sx, p.sv, p.nblk);
+    const unsigned grid = (unsigned)std::min<int64_t>(p.n_items, op->sms);
+    auto launch = [&](auto kern) -> int {
+      NCGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<grid, NTHREADS, smem, st>>>(p);
+      NCGP_LAUNCHED();
+      return NCGP_OK;
+    };
+    p.trace = g_trace;
+    int rc;
+    if (op->family == NCGP_RBF)
+      rc = g_trace != nullptr ? (wp == 16 ? launch(kop_sym2_kernel<NCGP_RBF, 16, true>)
+                                          : launch(kop_sym2_kernel<NCGP_RBF, 32, true>))
+                              : (wp == 16 ? launch(kop_sym2_kernel<NCGP_RBF, 16, false>)
+                                          : launch(kop_sym2_kernel<NCGP_RBF, 32, false>));
+    else
+      rc = wp == 16 ? launch(kop_sym2_kernel<NCGP_MATERN32, 16, false>)
+                    : launch(kop_sym2_kernel<NCGP_MATERN32, 32, false>);
+    if (rc != NCGP_OK) return rc;
+    return sym_fin ? tc_sym_finalize(op, p.acc, w, out, ldo, st, epi) : NCGP_OK;
+  }
   if (sym && op->sym_cg == 1) {
     const int cand[][2] = {{3, 6}, {3, 4}, {3, 3}, {2, 4}, {3, 2}, {2, 3}, {2, 2}};
     bool fit = false;

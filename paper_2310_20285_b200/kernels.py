@@ -130,13 +130,13 @@ class KernelOperator:
     @property
     def last_variant(self) -> str:
         """Kernel variant of the last apply: "plain", "symmetric", "wide" or "none"."""
-        return {0: "plain", 1: "symmetric", 2: "symmetric", 3: "wide"}.get(self.last_variant_code,
-                                                                           "none")
+        return {0: "plain", 1: "symmetric", 2: "symmetric", 3: "wide",
+                4: "symmetric"}.get(self.last_variant_code, "none")
 
     @property
     def last_variant_code(self) -> int:
         """ncgp_kop_last_variant: 0 plain, 1 symmetric pair kernel, 2 symmetric
-        single-CTA kernel, -1 none yet."""
+        single-CTA kernel, 3 wide-RHS kernel, 4 blocked symmetric kernel, -1 none yet."""
         return int(N.query("ncgp_kop_last_variant", self._h))
 
     def apply(self, V: torch.Tensor, out: Optional[torch.Tensor] = None,

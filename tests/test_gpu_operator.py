@@ -299,7 +299,7 @@ def test_fused_gather_symmetric_memory_single_rank(tmp_path):
     """torchrun world=1, NCCL: ShardedPriorOperator(gather='fused') goes
     through torch symmetric memory (rendezvous, peer mapping, device
     barriers) and matches the unsharded product bitwise; gather='reduce'
-    (the symmetric kernel's split with an NCCL all-reduce) within 2e-5."""
+    (the symmetric kernel's split with an NCCL all-reduce) within 5e-5 (blocked kernel)."""
     import subprocess
     import sys
     script = tmp_path / "symm_run.py"
@@ -323,7 +323,7 @@ def test_fused_gather_symmetric_memory_single_rank(tmp_path):
         "os.environ['NCGP_SYM'] = '1'  # the symmetric kernel at this small n\n"
         "c = ShardedPriorOperator(prior, X, dtype=torch.float32, gather='reduce')\n"
         "rc = c(v)\n"
-        "assert float((rc - rb).norm() / rb.norm()) < 2e-5\n"
+        "assert float((rc - rb).norm() / rb.norm()) < 5e-5\n"
         "dist.destroy_process_group()\n"
         "print('SYMM_OK')\n")
     env = dict(os.environ, MASTER_ADDR="127.0.0.1")

@@ -3,7 +3,9 @@ against the CPU oracle and the plain kernel.
 
 Tolerances (north_star): fp32 operator products within 1e-4 relative of
 |K||V| per entry; checked here at 1e-5 of the entry scale (measured 1-4e-6)
-and against the plain kernel at 2e-5 in norm.
+and against the plain kernel at 2e-5 in norm -- 5e-5 for both with the
+blocked kernel (K1-sym2), whose P_lo . Vhi split term runs in E4M3 (measured
+0.7-2.3e-5 in norm, 1.8e-5 of the entry scale at worst).
 
 Determinism (hard part 5; the reference pins tile-size
 invariance at test_gp.py:106-110): the symmetric kernels accumulate in int64
@@ -55,6 +57,26 @@ def _case(n, d, w, spec, seed, cg=None, **env):
     return X, V, op, torch.from_numpy(V).float().cuda()
 
 
+# ncgp_kop_last_variant of each flavour (NCGP_SYM_CG): 1 single-CTA K1-sym1,
+# 2 CTA pairs, 3 the blocked K1-sym2
+CODE = {1: 2, 2: 1, 3: 4}
+
+
+def _code(x):
+    return x if isinstance(x, int) else x.last_variant_code
+
+
+def ntol(x):
+    """Norm tolerance against the plain kernel for the flavour that ran
+    (an operator after its symmetric apply, or its variant code)."""
+    return 5e-5 if _code(x) == 4 else 2e-5
+
+
+def etol(x):
+    """Entry-scale tolerance (|error| / (K |V|)) for the flavour that ran."""
+    return 5e-5 if _code(x) == 4 else 1e-5
+
+
 def _plain(op, V):
     with op.sym_mode(0):
         out = op.apply(V)
@@ -70,15 +92,15 @@ def _plain(op, V):
     (2561, 8, 7, ("rbf", 1.5, 1.0)),
     (4096, 8, 32, ("rbf", 1.2, 0.7)),
 ])
-@pytest.mark.parametrize("cg", [1, 2])
+@pytest.mark.parametrize("cg", [1, 2, 3])
 def test_symmetric_kernel_matches_oracle(n, d, w, spec, cg):
     X, V, op, Vd = _case(n, d, w, spec, n + d, cg)
     with op.sym_mode(1):
         got = op.apply(Vd).double().cpu().numpy()
-    assert op.last_variant_code == (2 if cg == 1 else 1)
+    assert op.last_variant_code == CODE[cg]
     ref = O.kernel_matmul_rows(spec, X, X, V)
     bound = O.kernel_matmul_rows(spec, X, X, np.abs(V))
-    assert np.all(np.abs(got - ref) <= 1e-5 * bound), float(np.max(np.abs(got - ref) / bound))
+    assert np.all(np.abs(got - ref) <= etol(op) * bound), float(np.max(np.abs(got - ref) / bound))
 
 
 @pytest.mark.parametrize("item", [16, 48, 128])
@@ -88,12 +110,12 @@ def test_symmetric_kernel_item_transitions(item):
     flush boundaries."""
     X, V, op, Vd = _case(20000, 8, 16, ("matern32", 1.5, 1.0), 7)
     plain = _plain(op, Vd).double()
-    for cg in (1, 2):
-        with _Env(NCGP_SYM=1, NCGP_SYM_ITEM=item, NCGP_SYM_CG=cg):
+    for cg in (1, 2, 3):
+        with _Env(NCGP_SYM=1, NCGP_SYM_ITEM=item, NCGP_SYM2_ITEM=item, NCGP_SYM_CG=cg):
             op2 = KernelOperator("matern32", 1.5, 1.0, op.X_rows, w_max=32)  # table built at creation
         got = op2.apply(Vd).double()
-        assert op2.last_variant_code == (2 if cg == 1 else 1)
-        assert float((got - plain).norm() / plain.norm()) < 2e-5
+        assert op2.last_variant_code == CODE[cg]
+        assert float((got - plain).norm() / plain.norm()) < ntol(op2)
 
 
 def test_symmetric_kernel_only_on_full_square_launches():
@@ -125,11 +147,12 @@ def test_symmetric_default_policy(n, w, fam, variant):
     X, V, op, Vd = _case(n, 8, w, (fam, 1.5, 1.0), 11)
     got = op.apply(Vd)
     assert op.last_variant == variant
+    code = op.last_variant_code
     if variant == "plain":
         assert torch.equal(got, _plain(op, Vd))
         return
     plain = _plain(op, Vd)
-    assert float((got.double() - plain.double()).norm() / plain.double().norm()) < 2e-5
+    assert float((got.double() - plain.double()).norm() / plain.double().norm()) < ntol(code)
     # fp64 CUDA-core reference on the first and last row blocks (ragged tail)
     op64 = KernelOperator(fam, 1.5, 1.0, op.X_rows.double(), w_max=32, impl="simt")
     Vd64, Va64 = Vd.double(), Vd.double().abs()
@@ -139,12 +162,13 @@ def test_symmetric_default_policy(n, w, fam, variant):
         op64.apply(Vd64, out=ref, row_begin=r0, row_end=r1)
         op64.apply(Va64, out=sc, row_begin=r0, row_end=r1)
         err = (got[r0:r1].double() - ref[r0:r1]).abs() / sc[r0:r1]
-        assert float(err.max()) < 1e-5
+        assert float(err.max()) < etol(code)
 
 
 @pytest.mark.parametrize("n,d,w,fam,cg", [
-    (200_000, 8, 32, "rbf", None),        # cfg3 path (single-CTA kernel, WP = 32)
-    (100_000, 20, 10, "matern32", None),  # cfg4 path
+    (200_000, 8, 32, "rbf", None),        # cfg3 path (blocked kernel, WP = 32)
+    (100_000, 20, 10, "matern32", None),  # cfg4 path (blocked kernel, WP = 16)
+    (70_001, 8, 32, "rbf", 1),            # K1-sym1
     (70_001, 50, 10, "rbf", None),        # cfg5 path (pair kernel, row tile in TMEM)
     (70_001, 8, 32, "matern32", 2),       # pair kernel, WP = 32
 ])
@@ -188,11 +212,13 @@ def test_symmetric_kernel_single_p_buffer(n, d, w, fam, env):
     got = op.apply(Vd).double()
     assert op.last_variant_code == 1
     plain = _plain(op, Vd).double()
-    assert float((got - plain).norm() / plain.norm()) < 2e-5
+    assert float((got - plain).norm() / plain.norm()) < ntol(1)
 
 
 @pytest.mark.parametrize("n,d,w,fam,cg,parts", [
     (45000, 8, 32, "rbf", 1, (1, 2, 3, 8)),
+    (45000, 8, 32, "rbf", 3, (1, 2, 3, 8)),
+    (50001, 20, 10, "matern32", 3, (2, 7)),
     (70001, 8, 10, "matern32", 2, (1, 2, 5)),
     (70001, 50, 10, "matern32", None, (2, 8)),   # pair kernel, row tile in TMEM
 ])
@@ -204,8 +230,9 @@ def test_symmetric_split_across_parts(n, d, w, fam, cg, parts):
     X, V, op, Vd = _case(n, d, w, (fam, 2.0, 1.0), 17, cg)
     full = op.apply(Vd)
     assert op.last_variant == "symmetric"
+    code = op.last_variant_code
     plain = _plain(op, Vd).double()
-    assert float((full.double() - plain).norm() / plain.norm()) < 2e-5
+    assert float((full.double() - plain).norm() / plain.norm()) < ntol(code)
     m = op.sym_acc_elems(w)
     assert m >= n * w
     for P in parts:
@@ -252,7 +279,7 @@ def test_sharded_prior_operator_reduce_single_rank():
     one = P.PriorOperator(prior, X, dtype=torch.float32)
     a, b = red(v), rows(v)
     assert torch.equal(a, one(v))
-    assert float((a.double() - b.double()).norm() / b.double().norm()) < 2e-5
+    assert float((a.double() - b.double()).norm() / b.double().norm()) < 5e-5  # blocked kernel
 
 
 @pytest.mark.parametrize("n,d,w,fam", [
@@ -268,11 +295,12 @@ def test_symmetric_default_shapes_sweep(n, d, w, fam):
     X, V, op, Vd = _case(n, d, w, (fam, 1.7, 1.3), n + w)
     got = op.apply(Vd).double()
     assert op.last_variant == "symmetric"
+    code = op.last_variant_code
     with op.sym_mode(0):
         plain = op.apply(Vd).double()
         scale = op.apply(Vd.abs()).double()  # K |V|: the entry scale
-    assert float((got - plain).norm() / plain.norm()) < 2e-5
-    assert float(((got - plain).abs() / scale).max()) < 1e-5
+    assert float((got - plain).norm() / plain.norm()) < ntol(code)
+    assert float(((got - plain).abs() / scale).max()) < etol(code)
 
 
 @pytest.mark.parametrize("n,d,w,fam,item", [
@@ -288,11 +316,12 @@ def test_symmetric_row_tile_in_tmem(n, d, w, fam, item):
     X, V, op, Vd = _case(n, d, w, (fam, 4.0, 1.0), n + d, cg=2, NCGP_SYM=1, NCGP_SYM_ITEM=item)
     got = op.apply(Vd).double()
     assert op.last_variant_code == 1
+    code = 1
     with op.sym_mode(0):
         plain = op.apply(Vd).double()
         scale = op.apply(Vd.abs()).double()
-    assert float((got - plain).norm() / plain.norm()) < 2e-5
-    assert float(((got - plain).abs() / scale).max()) < 1e-5
+    assert float((got - plain).norm() / plain.norm()) < ntol(code)
+    assert float(((got - plain).abs() / scale).max()) < etol(code)
 
 
 @pytest.mark.parametrize("spec", [("rbf", 1.5, 1.0), ("rbf", 1.5, 1e-12), ("matern32", 2.0, 3e-9)])
@@ -312,8 +341,9 @@ def test_symmetric_tiny_column_scale(spec):
     with op.sym_mode(1):
         got = op.apply(Vd).double()
     assert op.last_variant == "symmetric"
+    tol = ntol(op)
     assert bool(torch.isfinite(got).all())
     plain = _plain(op, Vd).double()
     for c in range(w):
         g, p_ = got[:, c], plain[:, c]
-        assert float((g - p_).norm() / p_.norm()) < 2e-5, c
+        assert float((g - p_).norm() / p_.norm()) < tol, c
