@@ -701,7 +701,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     p.trace[TRACE_TILES * TRACE_EV + 4 * blockIdx.x] = (long long)t;
   }
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  // warp-uniform (see kop_sym2_kernel): MMA operands derived from it stay in
+  // uniform registers instead of a per-MMA ELECT / R2UR waterfall loop
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
   // TMEM columns: S/P buffers [0, 384), O double buffer [384, 384 + 4 WP);
   // symmetric kernel: S/P [0, 256), O double buffer [256, 256 + 4 WP),
   // D_T double buffer [256 + 4 WP, 256 + 8 WP)
@@ -882,6 +884,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           const uint32_t ab = p.na == 2 ? ((item1 - 1u) & 1u) : 0u;
           const uint64_t da = dA0 + ab * astep;
           const uint32_t d = tmem + s1 * (uint32_t)BN;
+          const uint32_t liu = __shfl_sync(0xffffffffu, li ? 1u : 0u, 0);
           if (elect_one()) {
             if (ATM)  // A = this CTA's row tile in TMEM (8 columns per K step of 16)
               for (int k = 0; k < ksteps1; ++k)
@@ -890,7 +893,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
               for (int k = 0; k < ksteps1; ++k)
                 mma_ss(d, da + (uint64_t)(16 * k), dx + (uint64_t)(16 * k), id1, k > 0);
             tc_commit2(&s_full[c1]);  // also releases XB / V slots (see producers)
-            if (li) tc_commit2(&a_empty[ab]);
+            if (liu) tc_commit2(&a_empty[ab]);
           }
           __syncwarp();
           if (lane == 0) trace_ev<DBG>(p, g1n, 2);
@@ -924,7 +927,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           if (lane == 0) trace_ev<DBG>(p, gt, 0);
           // GEMM2: P_hi x [Vhi | Vlo] (N = 2 WP: CTA0 supplies Vhi, CTA1 Vlo), then
           // P_lo x Vhi (N = WP: each CTA supplies half of Vhi's rows).
-          const uint32_t a0 = tmem + s2 * (uint32_t)BN, dO = tO((int)ob);
+          const uint32_t a0 = tmem + s2 * (uint32_t)BN;
+          const uint32_t obu = __shfl_sync(0xffffffffu, ob, 0);
+          const uint32_t fu = __shfl_sync(0xffffffffu, fresh ? 1u : 0u, 0);
+          const uint32_t lu = __shfl_sync(0xffffffffu, last ? 1u : 0u, 0);
+          const uint32_t dO = tO((int)obu);
           if (elect_one()) {
             if (SYM) {
               // symmetric kernel: P(g) from shared-memory buffer g mod 2 (K-major
@@ -933,7 +940,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
               const uint64_t pl = ph + ((PBUF / 2) >> 4);
 #pragma unroll
               for (int m = 0; m < BN / 16; ++m) {
-                mma_ss(dO, ph + (uint64_t)(16 * m), dv + (uint64_t)(16 * m), id2, (fresh && m == 0) ? 0u : 1u);
+                mma_ss(dO, ph + (uint64_t)(16 * m), dv + (uint64_t)(16 * m), id2, (fu && m == 0) ? 0u : 1u);
                 mma_ss(dO, pl + (uint64_t)(16 * m), dv + v3off + (uint64_t)(16 * m), id2h, 1u);
               }
               tc_commit2(&g2done[r]);           // V slot g free (both CTAs)
@@ -945,7 +952,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 for (int m = 0; m < BN / 16; ++m) {
                   const uint32_t ahi = a0 + 32u * (m >> 1) + 8u * (m & 1);
                   const uint64_t b = dv + (uint64_t)(16 * m);
-                  mma_ts(dO, ahi, b, id2h, (fresh && m == 0) ? 0u : 1u);
+                  mma_ts(dO, ahi, b, id2h, (fu && m == 0) ? 0u : 1u);
                   mma_ts(dO, ahi, b + b4, id2h, 1u);
                   mma_ts(dO, ahi + 16u, b, id2h, 1u);
                 }
@@ -953,13 +960,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 #pragma unroll
                 for (int m = 0; m < BN / 16; ++m) {
                   const uint32_t ahi = a0 + 32u * (m >> 1) + 8u * (m & 1);
-                  mma_ts(dO, ahi, dv + (uint64_t)(16 * m), id2, (fresh && m == 0) ? 0u : 1u);
+                  mma_ts(dO, ahi, dv + (uint64_t)(16 * m), id2, (fu && m == 0) ? 0u : 1u);
                   mma_ts(dO, ahi + 16u, dv + v3off + (uint64_t)(16 * m), id2h, 1u);
                 }
               }
               tc_commit2_leader(&g2done[r]);  // frees S buffer g for GEMM1(g + NS)
             }
-            if (last) tc_commit2(&o_full[ob]);
+            if (lu) tc_commit2(&o_full[obu]);
           }
           __syncwarp();
           if (lane == 0) trace_ev<DBG>(p, gt, 1);
@@ -1007,22 +1014,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             }
           tc_fence_after();
           if (lane == 0) trace_ev<DBG>(p, gt, 13);
+          const uint32_t tpu = __shfl_sync(0xffffffffu, tp ? 1u : 0u, 0);
+          const uint32_t dtb = __shfl_sync(0xffffffffu, dtq & 1u, 0);
+          const uint32_t liu = __shfl_sync(0xffffffffu, cur.last_in_item() ? 1u : 0u, 0);
           if (elect_one()) {
-            if (tp && !(DBG && (p.sym_dbg & 4))) {
+            if (tpu && !(DBG && (p.sym_dbg & 4))) {
               const uint64_t pa = dP0 + (uint64_t)pbuf(gt) * (PBUF >> 4);
 #pragma unroll 1
               for (int m = 0; m < BN / 16; ++m) {
                 const uint64_t ah = pa + (uint64_t)m * (4096 >> 4), al = ah + ((PBUF / 2) >> 4);
                 const uint64_t bh = dVh + (uint64_t)(16 * m), bl = dVl + (uint64_t)(16 * m);
-                const uint32_t dt = tDT(dtq & 1u);
+                const uint32_t dt = tDT(dtb);
                 mma_ss(dt, ah, bh, idT, m > 0 ? 1u : 0u);
                 mma_ss(dt, ah, bl, idT, 1u);
                 mma_ss(dt, al, bh, idT, 1u);
               }
             }
-            if (tp) tc_commit2(&dt_full[dtq & 1u]);
+            if (tpu) tc_commit2(&dt_full[dtb]);
             tc_commit2(&pt_free[gt & 1u]);
-            if (cur.last_in_item()) tc_commit2(vi_empty);
+            if (liu) tc_commit2(vi_empty);
           }
           __syncwarp();
           if (lane == 0) trace_ev<DBG>(p, gt, 14);
@@ -1476,7 +1486,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     p.trace[TRACE_TILES * TRACE_EV + 4 * blockIdx.x] = (long long)t;
   }
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform MMA operands
   auto tS = [&](uint32_t b) -> uint32_t { return tmem + b * (uint32_t)BN; };
   auto tO = [&](uint32_t b) -> uint32_t { return tmem + (uint32_t)(NS1 * BN) + b * AW; };
   auto tDT = [&](uint32_t b) -> uint32_t { return tmem + (uint32_t)(NS1 * BN) + 2u * AW + b * DW; };
@@ -1554,11 +1564,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
         if (lane == 0) trace_ev<DBG>(p, g, 9);
         const uint64_t dx = dX0 + (uint64_t)xr.idx * (xb_bytes >> 4);
         const uint32_t d = tS(sb);
+        const uint32_t liu = __shfl_sync(0xffffffffu, li ? 1u : 0u, 0);
         if (elect_one()) {
           for (int k = 0; k < ksteps1; ++k)
             mma1_ss(d, dA + (uint64_t)(16 * k), dx + (uint64_t)(16 * k), id1, k > 0);
           tc_commit1(&s_full[c1]);  // also frees XB slot g (producer)
-          if (li) tc_commit1(a_empty);
+          if (liu) tc_commit1(a_empty);
         }
         __syncwarp();
         if (lane == 0) trace_ev<DBG>(p, g, 2);
@@ -1592,7 +1603,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
         const uint64_t dv = dV0 + (uint64_t)vr.idx * (vb_bytes >> 4);
         const uint64_t ph = sdesc(smem_u32(sP) + pbuf(g) * PBUF, 128u, 2048u);
         const uint64_t pl = ph + ((PBUF / 2) >> 4);
-        const uint32_t dO = tO(ob);
+        const uint32_t obu = __shfl_sync(0xffffffffu, ob, 0);
+        const bool fu = __shfl_sync(0xffffffffu, fresh ? 1u : 0u, 0) != 0u;
+        const bool lu = __shfl_sync(0xffffffffu, last ? 1u : 0u, 0) != 0u;
+        const uint32_t dO = tO(obu);
         if (elect_one()) {
           if (PT) {  // A = P from TMEM; P_hi Vhi, P_hi Vlo, P_lo Vhi into the same WP columns
             const uint32_t a0 = tS(sb);
@@ -1601,7 +1615,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
             for (int m = 0; m < BN / 16; ++m) {
               const uint32_t ahi = a0 + 32u * (m >> 1) + 8u * (m & 1);
               const uint64_t b = dv + (uint64_t)(16 * m);
-              mma1_ts(dO, ahi, b, id2h, (fresh && m == 0) ? 0u : 1u);
+              mma1_ts(dO, ahi, b, id2h, (fu && m == 0) ? 0u : 1u);
               mma1_ts(dO, ahi, b + vlo, id2h, 1u);
               mma1_ts(dO, ahi + 16u, b, id2h, 1u);
             }
@@ -1610,19 +1624,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
 #pragma unroll
             for (int m = 0; m < BN / 16; ++m) {
               const uint32_t ahi = a0 + 32u * (m >> 1) + 8u * (m & 1);
-              mma1_ts(dO, ahi, dv + (uint64_t)(16 * m), id2, (fresh && m == 0) ? 0u : 1u);
+              mma1_ts(dO, ahi, dv + (uint64_t)(16 * m), id2, (fu && m == 0) ? 0u : 1u);
               mma1_ts(dO, ahi + 16u, dv + (uint64_t)(16 * m), id2h, 1u);
             }
           } else {
 #pragma unroll
             for (int m = 0; m < BN / 16; ++m) {
-              mma1_ss(dO, ph + (uint64_t)(16 * m), dv + (uint64_t)(16 * m), id2, (fresh && m == 0) ? 0u : 1u);
+              mma1_ss(dO, ph + (uint64_t)(16 * m), dv + (uint64_t)(16 * m), id2, (fu && m == 0) ? 0u : 1u);
               mma1_ss(dO, pl + (uint64_t)(16 * m), dv + (uint64_t)(16 * m), id2h, 1u);
             }
           }
           tc_commit1(&g2done[rr.idx]);  // V slot g free
           tc_commit1(&pt_free[g & 1u]);
-          if (last) tc_commit1(&o_full[ob]);
+          if (lu) tc_commit1(&o_full[obu]);
         }
         __syncwarp();
         if (lane == 0) trace_ev<DBG>(p, g, 1);
@@ -1669,10 +1683,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
           }
         tc_fence_after();
         if (lane == 0) trace_ev<DBG>(p, g, 13);
+        const bool tpu = __shfl_sync(0xffffffffu, tp ? 1u : 0u, 0) != 0u;
+        const uint32_t dtb = __shfl_sync(0xffffffffu, dtq % NDT, 0);
+        const bool liu = __shfl_sync(0xffffffffu, ti.last_in_item() ? 1u : 0u, 0) != 0u;
         if (elect_one()) {
-          if (tp && !(DBG && (p.sym_dbg & 4))) {
+          if (tpu && !(DBG && (p.sym_dbg & 4))) {
             const uint64_t pa = dP0 + (uint64_t)pbuf(g) * (PBUF >> 4);
-            const uint32_t dt = tDT(dtq % NDT);
+            const uint32_t dt = tDT(dtb);
             const uint64_t vlo = (uint64_t)(p.v2_bytes >> 4);
 #pragma unroll 1
             for (int m = 0; m < BN / 16; ++m) {
@@ -1688,9 +1705,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
               }
             }
           }
-          if (tp) tc_commit1(&dt_full[dtq % NDT]);
+          if (tpu) tc_commit1(&dt_full[dtb]);
           tc_commit1(&pt_free[g & 1u]);
-          if (ti.last_in_item()) tc_commit1(vi_empty);
+          if (liu) tc_commit1(vi_empty);
         }
         __syncwarp();
         if (lane == 0) trace_ev<DBG>(p, g, 14);
@@ -2870,8 +2887,10 @@ size_t smem2_bytes(uint32_t a_bytes, int wp, int sx, int sv, int nblk);
 int sym_cg(const ncgp_kop* op, int d, int w_max) {
   if (op->knob_sym_cg >= 1 && op->knob_sym_cg <= 3) return op->knob_sym_cg;
   const uint32_t a = (uint32_t)(BM * ka_of(d) * 2);
-  // the blocked kernel (K1-sym2, flavour 3) wherever its rings fit
-  if (smem2_bytes(a, wp_of(w_max), 2, 2, 0) <= SMEM_MAX) return 3;
+  // the blocked kernel (K1-sym2, flavour 3) at WP = 32 wherever its rings fit
+  // (one B200: cfg3 283 ms against K1-sym1's 328; at WP = 16 K1-sym1 stays
+  // ahead, n = 2e5 RBF w = 10: 8.7 against 9.3 ms, tools/flavours.py)
+  if (wp_of(w_max) == 32 && smem2_bytes(a, 32, 2, 2, 0) <= SMEM_MAX) return 3;
   // rings no shallower than (XB 2, V 4) or (XB 3, V 2): D = 24 at WP = 16
   // only fits (2, 3), which ran slower than the plain kernel; the pair kernel
   // keeps 3-deep rings there
