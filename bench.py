@@ -463,7 +463,7 @@ def product_roofline(op, n, d, w, F, E, world, local_pairs, t_kernel, dev, workl
     # from the committed ncu --set full capture (a number taken under a
     # profiler cannot be measured inside this run)
     traffic, traffic_src = None, None
-    captures = {("cfg3", 2): "r02_summary.json"}
+    captures = {("cfg3", 2): "r02_summary.json", ("cfg3", 4): "r02c_summary.json"}
     prof = captures.get((workload_name, variant))
     if prof and world == 1 and os.path.exists(os.path.join(ROOT, "profiles", prof)):
         with open(os.path.join(ROOT, "profiles", prof)) as fh:
@@ -480,8 +480,8 @@ def product_roofline(op, n, d, w, F, E, world, local_pairs, t_kernel, dev, workl
                           f"F/E={F}/{E}); bound 'tensor' = compute-bound (tensor pipe / MUFU), "
                           f"not HBM",
             "kernel_ms": round(1e3 * t_kernel, 3), "impl": op.impl,
-            "variant": {0: "plain", 1: "symmetric (CTA pairs)",
-                        2: "symmetric (single CTA)"}.get(variant, "none")}
+            "variant": {0: "plain", 1: "symmetric (CTA pairs)", 2: "symmetric (single CTA)",
+                        4: "symmetric (blocked, single CTA)"}.get(variant, "none")}
 
 
 CPU_FIT_ROWS = {"cfg4": 64, "cfg5": 8}   # reference tile-body sample rows per K product

@@ -4,7 +4,7 @@
 # usage (on the GPU box): tools/profile_round.sh TAG [WORKLOAD] [KREGEX]   -> gpurun_out/TAG_*
 T=${1:?tag}
 W=${2:-cfg3}
-K=${3:-"kop_tc_kernel|kop_sym1_kernel"}
+K=${3:-"kop_tc_kernel|kop_sym1_kernel|kop_sym2_kernel"}
 O=gpurun_out
 mkdir -p $O
 timeout 1200 python bench.py --workload $W --steps 5 --warmup 3 > $O/${T}_bench.log 2>&1 || { tail $O/${T}_bench.log; exit 1; }
