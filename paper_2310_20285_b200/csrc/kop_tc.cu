@@ -1890,6 +1890,9 @@ constexpr uint32_t PH2 = BM * BN * 2;       // P_hi (fp16, MN-major for T)
 constexpr uint32_t P2BUF = PH2 + BM * BN;   // [P_hi | P_lo E4M3]: 48 KB
 constexpr int NR2 = 16;                     // per-tile barrier rings (power of two)
 constexpr uint32_t TP2 = 96;                // TMEM columns of one P region (hi 64 | lo8 32)
+#ifndef NCGP_SYM2_HOLD
+#define NCGP_SYM2_HOLD 0  // build-time A/B: T(g) issued only after GEMM1(g + HOLD)
+#endif
 #ifndef NCGP_SYM2_ABL
 #define NCGP_SYM2_ABL 0  // timing ablations (wrong results): 1 no T MMAs, 2 no P stores for T,
                          // 4 no GEMM2 f16 MMAs, 8 no accumulator flushes
@@ -2037,6 +2040,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym2_kernel(const TcParams p)
   uint64_t* dt_full = o_empty + RB;      // [2]
   uint64_t* dt_empty = dt_full + 2;      // [2]  4 drain warps (after loading D_T)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dt_empty + 2);
+  volatile uint32_t* g1_cnt = tmem_slot + 1;  // GEMM1 tiles issued (NCGP_SYM2_HOLD)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < 4; ++s) {
@@ -2062,6 +2066,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym2_kernel(const TcParams p)
       mbar_init(&o_full[k], 1);
       mbar_init(&o_empty[k], 4);
     }
+    *g1_cnt = 0u;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -2176,11 +2181,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym2_kernel(const TcParams p)
         }
         __syncwarp();
         if (lane == 0) trace_ev<DBG>(p, g, 2);
+        if (NCGP_SYM2_HOLD && lane == 0) *g1_cnt = g + 1u;
         jq += ti.last_r() ? 1u : 0u;
         xr.adv();
         ++g;
         ti.next(p);
       }
+      if (lane == 0) *g1_cnt = 0xFFFFFFFFu;
     } else if (warp == 1) {
       // ================= GEMM2: O_I += P_hi [Vhi_J ; Vlo_J] + P_lo8 Vhi8_J (A = P in TMEM) =================
       const uint32_t id2h = idesc1_f16(WP), id28 = idesc1_f8(WP, false);
@@ -2248,6 +2255,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym2_kernel(const TcParams p)
         mbar_wait(&vi_full[vr.idx], vr.phase);
         const bool tp = ti.tp();
         if (ti.tp_first()) mbar_wait(&dt_empty[dq % NDT], ((dq / NDT) & 1u) ^ 1u);
+        if (NCGP_SYM2_HOLD)  // T(g) behind GEMM1(g + HOLD) in the in-order tensor pipe
+          while (*g1_cnt < g + 1u + (uint32_t)NCGP_SYM2_HOLD && *g1_cnt != 0xFFFFFFFFu) {
+          }
         tc_fence_after();
         if (lane == 0) trace_ev<DBG>(p, g, 11);
         const uint32_t tpu = uni(tp ? 1u : 0u), fu = uni(ti.tp_first() ? 1u : 0u);
