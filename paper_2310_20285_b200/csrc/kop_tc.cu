@@ -1884,7 +1884,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
 // epilogue (two groups alternating tiles); warps 20-23 the drains (D_T per
 // column tile, the 4 O accumulators at each item's end) into the int64
 // fixed-point accumulator (deterministic, as K1-sym1).
-constexpr int RB = 4;                       // row tiles per block
+#ifndef NCGP_SYM2_RB
+#define NCGP_SYM2_RB 4  // row tiles per block (build-time A/B: 4 or 2)
+#endif
+#ifndef NCGP_SYM2_NS
+#define NCGP_SYM2_NS 1  // S buffers in TMEM (build-time A/B: 1 or 2)
+#endif
+#ifndef NCGP_SYM2_NP
+#define NCGP_SYM2_NP 2  // P regions in TMEM (build-time A/B: 2 or 1)
+#endif
+constexpr int RB = NCGP_SYM2_RB;            // row tiles per block
 constexpr int LO8_SHIFT = 6;                // P_lo * 2^6, Vhi * 2^-6 in E4M3
 constexpr uint32_t PH2 = BM * BN * 2;       // P_hi (fp16, MN-major for T)
 constexpr uint32_t P2BUF = PH2 + BM * BN;   // [P_hi | P_lo E4M3]: 48 KB
@@ -2012,9 +2021,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym2_kernel(const TcParams p)
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  // TMEM: S [0, 128) | P0, P1 (96 each) | O_0..O_3 (WP each) | D_T (2 WP, NDT buffers)
-  constexpr uint32_t NDT = WP == 16 ? 2u : 1u;
-  static_assert(BN + 2 * TP2 + RB * WP + NDT * 2 * WP <= TMEM_COLS, "TMEM budget");
+  // TMEM: S (NS x 128) | P (NP x 96) | O_0..O_{RB-1} (WP each) | D_T (2 WP, NDT buffers)
+  constexpr uint32_t NS = NCGP_SYM2_NS, NP = NCGP_SYM2_NP;
+  constexpr uint32_t TBASE = NS * BN + NP * TP2 + RB * WP;
+  constexpr uint32_t NDT = TBASE + 4 * WP <= TMEM_COLS ? 2u : 1u;
+  static_assert(TBASE + NDT * 2 * WP <= TMEM_COLS, "TMEM budget");
   const uint32_t vb_bytes = 2u * p.v2_bytes;        // [Vhi | Vlo]: 2 WP rows x 128
   const uint32_t vi_bytes = vb_bytes + p.v8_bytes;  // + Vhi in E4M3
   uint8_t* sXA = smem;                                   // [sx] row tiles
@@ -2086,11 +2097,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym2_kernel(const TcParams p)
   // with __shfl_sync, which the compiler treats as uniform.
   const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
   auto uni = [](uint32_t v) -> uint32_t { return __shfl_sync(0xffffffffu, v, 0); };
-  auto tP = [&](uint32_t b) -> uint32_t { return tmem + (uint32_t)BN + b * TP2; };
-  auto tO = [&](uint32_t k) -> uint32_t { return tmem + (uint32_t)BN + 2u * TP2 + k * (uint32_t)WP; };
-  auto tDT = [&](uint32_t b) -> uint32_t {
-    return tmem + (uint32_t)BN + 2u * TP2 + (uint32_t)(RB * WP) + b * (uint32_t)(2 * WP);
-  };
+  auto tS = [&](uint32_t b) -> uint32_t { return tmem + b * (uint32_t)BN; };
+  auto tP = [&](uint32_t b) -> uint32_t { return tmem + NS * (uint32_t)BN + b * TP2; };
+  auto tO = [&](uint32_t k) -> uint32_t { return tmem + NS * (uint32_t)BN + NP * TP2 + k * (uint32_t)WP; };
+  auto tDT = [&](uint32_t b) -> uint32_t { return tmem + TBASE + b * (uint32_t)(2 * WP); };
   auto par = [](uint32_t t) -> uint32_t { return (t / NR2) & 1u; };
 
   if (warp < 4) {
@@ -2167,7 +2177,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym2_kernel(const TcParams p)
         if (lane == 0) trace_ev<DBG>(p, g, 0);
         if (ti.first_r()) mbar_wait(&xb_full[s], (jq >> 1) & 1u);
         mbar_wait(&xa_full[xr.idx], xr.phase);
-        if (g >= 1u) mbar_wait(&s_free[(g - 1u) % NR2], par(g - 1u));  // S(g - 1) loaded
+        if (g >= NS) mbar_wait(&s_free[(g - NS) % NR2], par(g - NS));  // S(g - NS) loaded
         tc_fence_after();
         if (lane == 0) trace_ev<DBG>(p, g, 1);
         const uint64_t da = dA0 + (uint64_t)xr.idx * (p.a_bytes >> 4);
@@ -2175,7 +2185,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym2_kernel(const TcParams p)
         const uint64_t dx = dX0 + (uint64_t)su * (p.a_bytes >> 4);
         if (elect_one()) {
           for (int k = 0; k < ksteps1; ++k)
-            mma1_ss(tmem, da + (uint64_t)(16 * k), dx + (uint64_t)(16 * k), id1, k > 0);
+            mma1_ss(tS(g % NS), da + (uint64_t)(16 * k), dx + (uint64_t)(16 * k), id1, k > 0);
           tc_commit1(&s_full[g % NR2]);  // also frees the XA slot (producer)
           if (lr) tc_commit1(&xb_empty[su]);
         }
@@ -2213,7 +2223,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym2_kernel(const TcParams p)
         const uint32_t su = uni(s), ku = uni((uint32_t)k), fu = uni(fresh ? 1u : 0u);
         const uint32_t ol = uni(ti.o_last() ? 1u : 0u), lr = uni(ti.last_r() ? 1u : 0u);
         const uint64_t vo = (uint64_t)su * (vi_bytes >> 4);
-        const uint32_t dO = tO(ku), a0 = tP(g & 1u);
+        const uint32_t dO = tO(ku), a0 = tP(g % NP);
         if (elect_one()) {
 #pragma unroll
           for (int m = 0; m < ((NCGP_SYM2_ABL & 4) ? 0 : BN / 16); ++m) {
@@ -2311,15 +2321,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym2_kernel(const TcParams p)
         if (tr) trace_ev<DBG>(p, g, 4);
         // load both chunks of S, then release the (single) S buffer to GEMM1
         uint32_t ra[32], rb[32], hi[16], l8[8];
-        tmem_ld32(tmem + lane_off + col0, ra);
-        tmem_ld32(tmem + lane_off + col0 + 32, rb);
+        tmem_ld32(tS(g % NS) + lane_off + col0, ra);
+        tmem_ld32(tS(g % NS) + lane_off + col0 + 32, rb);
         tmem_wait_ld(ra);
         tmem_wait_ld(rb);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_free[g % NR2]);
         if (tr) trace_ev<DBG>(p, g, 5);
-        const uint32_t pr = tP(g & 1u) + lane_off;
+        const uint32_t pr = tP(g % NP) + lane_off;
         const uint32_t pbase = smem_u32(sP) + (g & 1u) * P2BUF;
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
@@ -2327,8 +2337,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym2_kernel(const TcParams p)
             transform_chunk2<FAM>(ra, L, hi, l8);
           else
             transform_chunk2<FAM>(rb, L, hi, l8);
-          if (c == 0 && g >= 2u) {  // GEMM2(g - 2) has read P region g & 1
-            mbar_wait(&g2done[(g - 2u) % NR2], par(g - 2u));
+          if (c == 0 && g >= NP) {  // GEMM2(g - NP) has read this P region
+            mbar_wait(&g2done[(g - NP) % NR2], par(g - NP));
             tc_fence_after();
           }
           const uint32_t cc = (col0 >> 5) + (uint32_t)c;  // chunk of the tile (0..3)
