@@ -2,7 +2,7 @@
 
 usage: python tools/trace_sym2.py [n] [w]
 Events (clock64, per tile step g; see kop_sym2_kernel):
-  0/1/2 GEMM1 wait/go/issued  3/4/5/6 epilogue wait/s_full/P buffer free/done
+  0/1/2 GEMM1 wait/go/issued  3/4/5/6 epilogue wait/s_full/S released/done
   7/8/9 GEMM2 wait/go/issued  10/11/12 T wait/go/issued  13/14 D_T drain start/done
 """
 import ctypes
@@ -53,11 +53,14 @@ rows = [("GEMM1 wait (S buffer / XA)", 1, 0), ("GEMM1 issue", 2, 1),
 for name, a, b in rows:
     print(f"{name:34s}", med((e[:, a] - e[:, b]).astype(float)))
 pt = e[:, 5] - e[:, 4]
-print(f"{'epi s_full -> P buffer free':34s}", med(np.where(e[:, 5] > 0, pt, np.nan).astype(float)))
+print(f"{'epi s_full -> S released':34s}", med(np.where(e[:, 5] > 0, pt, np.nan).astype(float)))
+print(f"{'epi S released -> done':34s}", med((e[:, 6] - e[:, 5]).astype(float)))
+print(f"{'epi done(g-1) -> epi wait(g+1)':34s}", "(group idle between its tiles)", med((t[lo + 1:hi + 1, 3] - t[lo:hi, 6]).astype(float)))
 print(f"{'GEMM1 issued -> epi s_full seen':34s}", med((e[:, 4] - e[:, 2]).astype(float)))
 print(f"{'epi done -> GEMM2 go':34s}", med((e[:, 8] - e[:, 6]).astype(float)))
 print(f"{'epi done -> T go':34s}", med((e[:, 11] - e[:, 6]).astype(float)))
-print(f"{'GEMM2 issued(g-2) -> GEMM1 go(g)':34s}", med((e[:, 1] - t[lo - 2:hi - 2, 9]).astype(float)))
+print(f"{'S released(g-1) -> GEMM1 go(g)':34s}", med((e[:, 1] - t[lo - 1:hi - 1, 5]).astype(float)))
+print(f"{'GEMM2 issued(g-2) -> epi S released(g)':34s}", med((e[:, 5] - t[lo - 2:hi - 2, 9]).astype(float)))
 dr = e[:, 14] - e[:, 13]
 print(f"{'D_T drain':34s}", med(np.where(e[:, 13] > 0, dr, np.nan).astype(float)))
 np.set_printoptions(linewidth=200)
