@@ -2907,10 +2907,12 @@ size_t smem2_bytes(uint32_t a_bytes, int wp, int sx, int sv, int nblk);
 int sym_cg(const ncgp_kop* op, int d, int w_max) {
   if (op->knob_sym_cg >= 1 && op->knob_sym_cg <= 3) return op->knob_sym_cg;
   const uint32_t a = (uint32_t)(BM * ka_of(d) * 2);
-  // the blocked kernel (K1-sym2, flavour 3) at WP = 32 wherever its rings fit
-  // (one B200: cfg3 283 ms against K1-sym1's 328; at WP = 16 K1-sym1 stays
-  // ahead, n = 2e5 RBF w = 10: 8.7 against 9.3 ms, tools/flavours.py)
-  if (wp_of(w_max) == 32 && smem2_bytes(a, 32, 2, 2, 0) <= SMEM_MAX) return 3;
+  // the blocked kernel (K1-sym2, flavour 3) for RBF at WP = 32 wherever its
+  // rings fit (one B200: cfg3 283 ms against K1-sym1's 328; K1-sym1 stays ahead
+  // at WP = 16 -- n = 2e5 RBF w = 10: 8.7 against 9.3 ms -- and for Matern-3/2,
+  // whose two MUFU ops per pair outweigh the shared-memory savings: cfg3-matern
+  // 372 against 389 ms; tools/flavours.py)
+  if (op->family == NCGP_RBF && wp_of(w_max) == 32 && smem2_bytes(a, 32, 2, 2, 0) <= SMEM_MAX) return 3;
   // rings no shallower than (XB 2, V 4) or (XB 3, V 2): D = 24 at WP = 16
   // only fits (2, 3), which ran slower than the plain kernel; the pair kernel
   // keeps 3-deep rings there
