@@ -100,6 +100,12 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // P_hi^T [Vhi | Vlo] (N = 2 WP) + P_lo^T Vhi -- so P^T is read from shared
 // memory once per k-step instead of twice, into a single-buffered D_T of
 // 2 WP columns)
+#ifndef NCGP_PAIR_PT
+// symmetric pair kernel: GEMM2 reads P from TMEM (written over S, as in the
+// plain kernel) instead of from shared memory; shared memory then only holds
+// P for the transposed product (build-time A/B)
+#define NCGP_PAIR_PT 0
+#endif
 #ifndef NCGP_SYM1_NS16
 #define NCGP_SYM1_NS16 3  // K1-sym1 S buffers at WP = 16 (build-time A/B: 2 or 3)
 #endif
@@ -676,7 +682,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       mbar_init(&a_empty[b], 1);
       mbar_init(&o_full[b], 1);
       mbar_init(&o_empty[b], 8);
-      mbar_init(&pt_free[b], SYM ? 2 : 1);  // SYM: GEMM2(g) and T(g) both read P(g)
+      mbar_init(&pt_free[b], (SYM && !NCGP_PAIR_PT) ? 2 : 1);  // SYM: GEMM2(g) and T(g) both read P(g)
       mbar_init(&dt_full[b], 1);
       mbar_init(&dt_empty[b], 8);
     }
@@ -862,9 +868,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             ++item1;
           }
           if (SYM) {  // XB(t) landed; S buffer free once the epilogue loaded S(t - NS)
+            // (NCGP_PAIR_PT: once GEMM2(t - NS) has read P over it)
             mbar_wait(&xb_full[c1], (g1n / (uint32_t)NR) & 1u);
             if (g1n >= (uint32_t)NS) {
-              mbar_wait(&s_free[gd], gdph);
+              mbar_wait(NCGP_PAIR_PT ? &g2done[gd] : &s_free[gd], gdph);
               if (++gd == (uint32_t)NR) {
                 gd = 0;
                 gdph ^= 1u;
@@ -933,7 +940,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           const uint32_t lu = __shfl_sync(0xffffffffu, last ? 1u : 0u, 0);
           const uint32_t dO = tO((int)obu);
           if (elect_one()) {
-            if (SYM) {
+            if (SYM && NCGP_PAIR_PT) {
+              // symmetric kernel, P in TMEM over S(g) (the plain kernel's TS MMAs);
+              // the shared-memory copy is the transposed product's only
+#pragma unroll
+              for (int m = 0; m < BN / 16; ++m) {
+                const uint32_t ahi = a0 + 32u * (m >> 1) + 8u * (m & 1);
+                mma_ts(dO, ahi, dv + (uint64_t)(16 * m), id2, (fu && m == 0) ? 0u : 1u);
+                mma_ts(dO, ahi + 16u, dv + v3off + (uint64_t)(16 * m), id2h, 1u);
+              }
+              tc_commit2(&g2done[r]);  // V slot g and S buffer g free (both CTAs)
+            } else if (SYM) {
               // symmetric kernel: P(g) from shared-memory buffer g mod 2 (K-major
               // canonical layout, the same bytes the transposed product reads)
               const uint64_t ph = sdesc(smem_u32(sP) + pbuf(gt) * PBUF, 128u, 2048u);
@@ -1091,12 +1108,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             for (int c = 0; c < BN / 64; ++c) {
               tmem_ld32(base + 32 * c, ra);
               tmem_wait_ld(ra);
-              if (c == BN / 64 - 1) {
+              if (!NCGP_PAIR_PT && c == BN / 64 - 1) {
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(leader_addr(&s_free[er.idx]));
               }
               transform_chunk<FAM>(ra, L, hi, lo);
+              if (NCGP_PAIR_PT) {  // P over S(g) for GEMM2's TS MMAs
+                if (FAM == NCGP_RBF) {
+                  tmem_st_hilo(base + 32 * c, hi, lo);
+                } else {
+                  tmem_st16(base + 32 * c, hi);
+                  tmem_st16(base + 32 * c + 16, lo);
+                }
+              }
               if (pt_wait) {
                 const uint32_t t = gt - (uint32_t)p.npb;
                 mbar_wait(&pt_free[t & 1u], (t >> 1) & 1u);
@@ -1113,6 +1138,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 }
               }
             }
+            if (NCGP_PAIR_PT) tmem_wait_st();
             fence_proxy_async_smem();
           } else {
 #pragma unroll
