@@ -5,6 +5,8 @@
 // a contiguous C-element segment and a warp covers 32*C contiguous elements.
 #include <math.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace {
@@ -270,12 +272,15 @@ __global__ void __launch_bounds__(PTS) softmax_stats_staged_kernel(
 
 // out = beta base + alpha W^+ V (likelihoods.py:291-310), staged.  The pi
 // tile is loaded once per block and turned into 1 / max(pi, floor) in place
-// (one division per entry), then the k column blocks of V are swept through
-// in turn (pi is not re-read per column block).
+// (one division per entry), then the block's kb column blocks of V
+// (grid.y slices the k columns so that wide W+ applies -- the virtual
+// solver run's S blocks, k ~ 800 -- still fill the GPU) are swept through in
+// turn (pi is not re-read per column block).
 template <typename T>
 __global__ void __launch_bounds__(PTS) softmax_winv_staged_kernel(
     const T* __restrict__ pi, int64_t n, int C, const T* __restrict__ V, int64_t ldv, int k,
-    const T* __restrict__ base, int64_t ldb, T alpha, T beta, T* __restrict__ out, int64_t ldo) {
+    const T* __restrict__ base, int64_t ldb, T alpha, T beta, T* __restrict__ out, int64_t ldo,
+    int kb) {
   extern __shared__ __align__(16) unsigned char smraw[];
   T* tp = reinterpret_cast<T*>(smraw);
   T* tv = tp + PTS * C;
@@ -284,9 +289,10 @@ __global__ void __launch_bounds__(PTS) softmax_winv_staged_kernel(
   const int np = n - p0 < PTS ? (int)(n - p0) : PTS;
   const int m = np * C;
   const int t = threadIdx.x;
+  const int b0 = blockIdx.y * kb, b1 = min(k, b0 + kb);
   sweep_in(tp, pi + p0 * C, m);
-  sweep_in(tv, V + p0 * C, m);
-  if (base) sweep_in(tb, base + p0 * C, m);
+  sweep_in(tv, V + b0 * ldv + p0 * C, m);
+  if (base) sweep_in(tb, base + b0 * ldb + p0 * C, m);
   async_wait_all();
   __syncthreads();
   if (t < np)
@@ -294,8 +300,8 @@ __global__ void __launch_bounds__(PTS) softmax_winv_staged_kernel(
       const T pc = tp[t * C + c] > T(kProbFloor) ? tp[t * C + c] : T(kProbFloor);
       tp[t * C + c] = T(1) / pc;
     }
-  for (int b = 0; b < k; ++b) {
-    if (b > 0) {
+  for (int b = b0; b < b1; ++b) {
+    if (b > b0) {
       sweep_in(tv, V + b * ldv + p0 * C, m);
       if (base) sweep_in(tb, base + b * ldb + p0 * C, m);
       async_wait_all();
@@ -553,8 +559,12 @@ int launch_winv(const T* pi, int64_t n, int C, const T* V, int64_t ldv, int k, c
   if (sm <= kStagedSmem) {
     auto kern = softmax_winv_staged_kernel<T>;
     NCGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStagedSmem));
-    kern<<<(unsigned)((n + PTS - 1) / PTS), PTS, sm, st>>>(pi, n, C, V, ldv, k, base, ldb, a, b, out,
-                                                          ldo);
+    // column blocks per CTA: enough CTAs (~2048) to fill the GPU, pi loaded once per CTA
+    const int64_t nbx = (n + PTS - 1) / PTS;
+    const int slices = (int)std::max<int64_t>(1, std::min<int64_t>(k, 2048 / std::max<int64_t>(1, nbx)));
+    const int kb = (k + slices - 1) / slices;
+    kern<<<dim3((unsigned)nbx, (unsigned)((k + kb - 1) / kb)), PTS, sm, st>>>(pi, n, C, V, ldv, k, base,
+                                                                            ldb, a, b, out, ldo, kb);
     NCGP_LAUNCHED();
     return NCGP_OK;
   }
