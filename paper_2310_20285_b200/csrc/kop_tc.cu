@@ -106,6 +106,14 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // P for the transposed product (build-time A/B)
 #define NCGP_PAIR_PT 0
 #endif
+#ifndef NCGP_PAIR_RED
+#define NCGP_PAIR_RED 0  // the pair kernel's flushes by RED (build-time A/B)
+#endif
+#ifndef NCGP_SYM1_RED
+// K1-sym1 flushes with coalesced red.global.add.u64 into a column-major
+// accumulator (as K1-sym2) instead of staging + TMA bulk reductions (build-time A/B)
+#define NCGP_SYM1_RED 1
+#endif
 #ifndef NCGP_SYM1_NS16
 #define NCGP_SYM1_NS16 3  // K1-sym1 S buffers at WP = 16 (build-time A/B: 2 or 3)
 #endif
@@ -586,6 +594,20 @@ __device__ __forceinline__ void fx_flush8(const TcParams& p, uint32_t stg_warp, 
   fence_proxy_async_smem();
   __syncwarp();
   if (lane == 0 && !skip) bulk_reduce_add_u64(p.acc + ((int64_t)h * p.acc_rows + row0) * 8, blk, 2048u);
+}
+
+// The same 8 columns of the warp's 32 rows straight from registers: one
+// coalesced red.global.add.u64 per column into the column-major [WP][rows]
+// accumulator -- no shared-memory staging, no TMA queueing behind the
+// producers' loads (K1-sym2 and, with NCGP_SYM1_RED / NCGP_PAIR_RED, the
+// other symmetric kernels; sym_finalize_kernel(colmajor = 1) reads it).
+__device__ __forceinline__ void fx_red8(const TcParams& p, int lane, int h, const float (&v)[8],
+                                        int64_t row0, bool skip) {
+  if (skip) return;
+  unsigned long long* dst = p.acc + row0 + lane;
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    atomicAdd(dst + (int64_t)(8 * h + c) * p.acc_rows, (unsigned long long)__float2ll_rn(v[c] * p.fx));
 }
 
 // ATM (symmetric kernel, WP = 16, large D): the row tile lives in TMEM (the
@@ -1229,7 +1251,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 #pragma unroll
               for (int c = 0; c < 8; ++c) dd[c] = v[c];
             }
-            fx_flush8<NBLK>(p, stg_warp, nst, lane, h, v, j0, DBG && (p.sym_dbg & 1));
+            if (NCGP_PAIR_RED)
+              fx_red8(p, lane, h, v, j0, DBG && (p.sym_dbg & 1));
+            else
+              fx_flush8<NBLK>(p, stg_warp, nst, lane, h, v, j0, DBG && (p.sym_dbg & 1));
           }
           tc_fence_before();
           if (lane == 0) mbar_arrive_cluster(leader_addr(&dt_empty[dtq & 1u]));
@@ -1249,7 +1274,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             float v[8];
 #pragma unroll
             for (int c = 0; c < 8; ++c) v[c] = __uint_as_float(x[c]) + __uint_as_float(y[c]);
-            fx_flush8<NBLK>(p, stg_warp, nst, lane, h, v, i0, DBG && (p.sym_dbg & 2));
+            if (NCGP_PAIR_RED)
+              fx_red8(p, lane, h, v, i0, DBG && (p.sym_dbg & 2));
+            else
+              fx_flush8<NBLK>(p, stg_warp, nst, lane, h, v, i0, DBG && (p.sym_dbg & 2));
           }
           tc_fence_before();
           if (lane == 0) mbar_arrive_cluster(leader_addr(&o_empty[q & 1u]));
@@ -1257,7 +1285,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         }
         ti.next(p, items);
       }
-      if (lane == 0) bulk_wait_all();
+      if (lane == 0 && !NCGP_PAIR_RED) bulk_wait_all();
     } else if constexpr (WIDE) {
       // wide kernel: each item's O (fp32, accumulated in TMEM over <= 64
       // column tiles) -> the fp32 partial [split][local row][WP] in HBM
@@ -1836,7 +1864,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
         float v[8];
 #pragma unroll
         for (int c = 0; c < 8; ++c) v[c] = two ? __uint_as_float(x[c]) + __uint_as_float(y[c]) : __uint_as_float(x[c]);
-        fx_flush8<NBLK>(p, stg_warp, nst, lane, h, v, row0, skip);
+        if (NCGP_SYM1_RED) {
+          fx_red8(p, lane, h, v, row0, skip);
+        } else {
+          fx_flush8<NBLK>(p, stg_warp, nst, lane, h, v, row0, skip);
+        }
       }
       tc_fence_before();
     };
@@ -1861,7 +1893,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
       }
       ti.next(p);
     }
-    if (lane == 0) bulk_wait_all();
+    if (lane == 0 && !NCGP_SYM1_RED) bulk_wait_all();
   }
 
   if (DBG && p.trace != nullptr && threadIdx.x == 0) {
@@ -1930,7 +1962,7 @@ constexpr uint32_t TP2 = 96;                // TMEM columns of one P region (hi 
 #endif
 #ifndef NCGP_SYM2_ABL
 #define NCGP_SYM2_ABL 0  // timing ablations (wrong results): 1 no T MMAs, 2 no P stores for T,
-                         // 4 no GEMM2 f16 MMAs, 8 no accumulator flushes
+                         // 4 no GEMM2 f16 MMAs, 8 no accumulator flushes, 16 no E4M3 conversion
 #endif
 
 __device__ __forceinline__ void mma1_f8_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
@@ -1992,7 +2024,8 @@ __device__ __forceinline__ void transform_chunk2(const uint32_t (&r)[32], float 
     const float h0 = __uint_as_float((__float_as_uint(k0) + 0x1000u) & 0xFFFFE000u);
     const float h1 = __uint_as_float((__float_as_uint(k1) + 0x1000u) & 0xFFFFE000u);
     hi[i] = pack_h2(h0, h1);
-    const uint32_t q = e4m3x2((k0 - h0) * S8, (k1 - h1) * S8);
+    const uint32_t q = (NCGP_SYM2_ABL & 16) ? __float_as_uint(k0 - h0) & 0xFFFFu
+                                            : e4m3x2((k0 - h0) * S8, (k1 - h1) * S8);
     if (i & 1)
       l8[i >> 1] |= q << 16;
     else
@@ -3124,7 +3157,8 @@ int tc_sym_finalize(ncgp_kop* op, const unsigned long long* acc, int w, const Ou
   const int s_exp = (int)lround(log2(op->k_scale));
   sym_finalize_kernel<<<(unsigned)((op->n_rows + 127) / 128), 128, 0, st>>>(
       acc, op->row_tiles * BM, op->n_rows, w, op->sym_fx, s_exp, col_exp, epi,
-      ncgp::out_ptrs<float>(out, 0, ldo), ldo, op->sym_cg == 3 ? 1 : 0);
+      ncgp::out_ptrs<float>(out, 0, ldo), ldo,
+      (op->sym_cg == 3 || (op->sym_cg == 1 && NCGP_SYM1_RED) || (op->sym_cg == 2 && NCGP_PAIR_RED)) ? 1 : 0);
   NCGP_LAUNCHED();
   return NCGP_OK;
 }
