@@ -1960,6 +1960,9 @@ constexpr uint32_t TP2 = 96;                // TMEM columns of one P region (hi 
 #ifndef NCGP_SYM2_HOLD
 #define NCGP_SYM2_HOLD 0  // build-time A/B: T(g) issued only after GEMM1(g + HOLD)
 #endif
+#ifndef NCGP_SYM2_HOLDG2
+#define NCGP_SYM2_HOLDG2 0  // build-time A/B: GEMM2(g) issued only after GEMM1(g + HOLDG2)
+#endif
 #ifndef NCGP_SYM2_ABL
 #define NCGP_SYM2_ABL 0  // timing ablations (wrong results): 1 no T MMAs, 2 no P stores for T,
                          // 4 no GEMM2 f16 MMAs, 8 no accumulator flushes, 16 no E4M3 conversion
@@ -2250,7 +2253,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym2_kernel(const TcParams p)
         }
         __syncwarp();
         if (lane == 0) trace_ev<DBG>(p, g, 2);
-        if (NCGP_SYM2_HOLD && lane == 0) *g1_cnt = g + 1u;
+        if ((NCGP_SYM2_HOLD || NCGP_SYM2_HOLDG2) && lane == 0) *g1_cnt = g + 1u;
         jq += ti.last_r() ? 1u : 0u;
         xr.adv();
         ++g;
@@ -2277,6 +2280,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym2_kernel(const TcParams p)
           mbar_wait(&o_empty[k], ((ouse >> k) & 1u) ^ 1u);
           ouse ^= 1u << k;
         }
+        if (NCGP_SYM2_HOLDG2)  // GEMM2(g) behind GEMM1(g + HOLDG2) in the in-order tensor pipe
+          while (*g1_cnt < g + 1u + (uint32_t)NCGP_SYM2_HOLDG2 && *g1_cnt != 0xFFFFFFFFu) {
+          }
         tc_fence_after();
         if (lane == 0) trace_ev<DBG>(p, g, 8);
         const uint32_t su = uni(s), ku = uni((uint32_t)k), fu = uni(fresh ? 1u : 0u);
