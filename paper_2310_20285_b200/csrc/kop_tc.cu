@@ -106,6 +106,12 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // P for the transposed product (build-time A/B)
 #define NCGP_PAIR_PT 0
 #endif
+#ifndef NCGP_PAIR_F8
+// symmetric pair kernel: the split term P_lo Vhi of both products in E4M3
+// (as K1-sym2): P buffers of 48 instead of 64 KB -- three of them where
+// shared memory allows -- and half the transposed product's P_lo MMAs
+#define NCGP_PAIR_F8 0
+#endif
 #ifndef NCGP_PAIR_RED
 #define NCGP_PAIR_RED 0  // the pair kernel's flushes by RED (build-time A/B)
 #endif
@@ -229,6 +235,16 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint3
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
       "r"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// the same, kind::f8f6f4 (E4M3 x E4M3); A MN-major via the idesc bit
+__device__ __forceinline__ void mma_f8_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
@@ -596,6 +612,102 @@ __device__ __forceinline__ void fx_flush8(const TcParams& p, uint32_t stg_warp, 
   if (lane == 0 && !skip) bulk_reduce_add_u64(p.acc + ((int64_t)h * p.acc_rows + row0) * 8, blk, 2048u);
 }
 
+// ---- shared by the blocked symmetric kernel (K1-sym2) and the pair kernel's
+// E4M3 split term (NCGP_PAIR_F8); see the K1-sym2 section below
+#ifndef NCGP_SYM2_RB
+#define NCGP_SYM2_RB 4  // row tiles per block (build-time A/B: 4 or 2)
+#endif
+#ifndef NCGP_SYM2_NS
+#define NCGP_SYM2_NS 1  // S buffers in TMEM (build-time A/B: 1 or 2)
+#endif
+#ifndef NCGP_SYM2_NP
+#define NCGP_SYM2_NP 2  // P regions in TMEM (build-time A/B: 2 or 1)
+#endif
+constexpr int RB = NCGP_SYM2_RB;            // row tiles per block
+constexpr int LO8_SHIFT = 6;                // P_lo * 2^6, Vhi * 2^-6 in E4M3
+constexpr uint32_t PH2 = BM * BN * 2;       // P_hi (fp16, MN-major for T)
+constexpr uint32_t P2BUF = PH2 + BM * BN;   // [P_hi | P_lo E4M3]: 48 KB
+constexpr int NR2 = 16;                     // per-tile barrier rings (power of two)
+constexpr uint32_t TP2 = 96;                // TMEM columns of one P region (hi 64 | lo8 32)
+#ifndef NCGP_SYM2_HOLD
+#define NCGP_SYM2_HOLD 0  // build-time A/B: T(g) issued only after GEMM1(g + HOLD)
+#endif
+#ifndef NCGP_SYM2_HOLDG2
+#define NCGP_SYM2_HOLDG2 0  // build-time A/B: GEMM2(g) issued only after GEMM1(g + HOLDG2)
+#endif
+#ifndef NCGP_SYM2_ABL
+#define NCGP_SYM2_ABL 0  // timing ablations (wrong results): 1 no T MMAs, 2 no P stores for T,
+                         // 4 no GEMM2 f16 MMAs, 8 no accumulator flushes, 16 no E4M3 conversion
+#endif
+
+__device__ __forceinline__ void mma1_f8_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                           uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma1_f8_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc,
+                                           uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// kind::f8f6f4, A/B E4M3, D F32, M = 128; bit 15: A MN-major
+__host__ __device__ constexpr uint32_t idesc1_f8(int n, bool a_mn) {
+  return (1u << 4) | (a_mn ? (1u << 15) : 0u) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(128 >> 4) << 24);
+}
+// two floats -> E4M3x2 (a in the low byte)
+__device__ __forceinline__ uint32_t e4m3x2(float a, float b) {
+  uint16_t d;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(d) : "f"(b), "f"(a));
+  return (uint32_t)d;
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]));
+}
+
+// One 32-column chunk: S -> P_hi (fp16, rounded to nearest) and P_lo * 2^6 (E4M3).
+template <int FAM>
+__device__ __forceinline__ void transform_chunk2(const uint32_t (&r)[32], float L,
+                                                 uint32_t (&hi)[16], uint32_t (&l8)[8]) {
+  constexpr float S8 = (float)(1 << LO8_SHIFT);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    float k0, k1;
+    const float g0 = __uint_as_float(r[2 * i]);
+    const float g1 = __uint_as_float(r[2 * i + 1]);
+    if (FAM == NCGP_RBF) {
+      k0 = ex2(g0);
+      k1 = ex2(g1);
+    } else {
+      const float a0 = sqrt_approx(fmaxf(g0, 0.f));
+      const float a1 = sqrt_approx(fmaxf(g1, 0.f));
+      const float e0 = ex2(fmaf(a0, -1.4426950408889634f, L));
+      const float e1 = ex2(fmaf(a1, -1.4426950408889634f, L));
+      k0 = fmaf(a0, e0, e0);
+      k1 = fmaf(a1, e1, e1);
+    }
+    // round to the nearest value with 11 significant bits (fp16-exact)
+    const float h0 = __uint_as_float((__float_as_uint(k0) + 0x1000u) & 0xFFFFE000u);
+    const float h1 = __uint_as_float((__float_as_uint(k1) + 0x1000u) & 0xFFFFE000u);
+    hi[i] = pack_h2(h0, h1);
+    const uint32_t q = (NCGP_SYM2_ABL & 16) ? __float_as_uint(k0 - h0) & 0xFFFFu
+                                            : e4m3x2((k0 - h0) * S8, (k1 - h1) * S8);
+    if (i & 1)
+      l8[i >> 1] |= q << 16;
+    else
+      l8[i >> 1] = q;
+  }
+}
+
 // The same 8 columns of the warp's 32 rows straight from registers: one
 // coalesced red.global.add.u64 per column into the column-major [WP][rows]
 // accumulator -- no shared-memory staging, no TMA queueing behind the
@@ -635,26 +747,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   // accumulators (2 x 2 WP columns each): with WP = 32 that leaves room for
   // two S/P buffers only, with WP = 16 for three.
   constexpr int NS = (WIDE || (SYM && (WP == 32 || ATM))) ? 2 : NS_MAX;
+  // NCGP_PAIR_F8: P_lo in E4M3 ([P_hi | P_lo8] buffers of 48 KB, up to three),
+  // Vhi in E4M3 next to each V slot (this CTA's half) and the own V block (full)
+  constexpr bool PF8 = SYM && NCGP_PAIR_F8;
+  constexpr uint32_t PB = PF8 ? P2BUF : PBUF;
 
   // ---- shared-memory carve-up (identical offsets in both CTAs)
   // this CTA's V half: [B2 | B3] (wide kernel: [B3 | B4], the CTA-split Vhi and Vlo)
-  const uint32_t vslot = WIDE ? 2u * p.v3_bytes : p.v2_bytes + p.v3_bytes;
+  const uint32_t vslot0 = WIDE ? 2u * p.v3_bytes : p.v2_bytes + p.v3_bytes;
+  const uint32_t v8h = PF8 ? p.v8_bytes / 2u : 0u;  // this CTA's half of the column tile's Vhi8
+  const uint32_t vslot = vslot0 + v8h;
   uint8_t* sA = smem;                                   // na x a_bytes (own row tile)
   uint8_t* sXB = sA + (size_t)p.na * p.a_bytes;         // sx x xbh_bytes
   uint8_t* sV = sXB + (size_t)p.sx * p.xbh_bytes;       // sv x vslot
   // symmetric kernel: this CTA's own V block [Vhi | Vlo] (the transposed
   // product's B) and two P buffers [P_hi | P_lo] (its MN-major A)
   uint8_t* sVI = sV + (size_t)p.sv * vslot;
-  uint8_t* sP = sVI + (SYM ? 2 * (size_t)p.v2_bytes : 0);
+  uint8_t* sP = sVI + (SYM ? 2 * (size_t)p.v2_bytes + (PF8 ? p.v8_bytes : 0u) : 0);
   // symmetric kernel: fp32 staging rows [128][WP] for the bulk reductions
-  float* sStage = reinterpret_cast<float*>(sP + (SYM ? (size_t)p.npb * PBUF : 0));
+  float* sStage = reinterpret_cast<float*>(sP + (SYM ? (size_t)p.npb * PB : 0));
   // symmetric kernel: P buffer of tile g (two alternate by tile parity; one
   // when shared memory is short).  GEMM2(g) and T(g) always commit to
   // pt_free[g & 1], whose phases then advance once per two tiles; the
   // epilogue of tile g waits for tile g - npb's phase, which with one buffer
   // is the other group's barrier.  A single barrier would let a group, which
   // only sees every other phase, alias a phase two behind as complete.
-  auto pbuf = [&](uint32_t g) -> uint32_t { return p.npb == 2 ? (g & 1u) : 0u; };
+  auto pbuf = [&](uint32_t g) -> uint32_t {
+    return PF8 ? g % (uint32_t)p.npb : (p.npb == 2 ? (g & 1u) : 0u);
+  };
+  // pt_free barrier of tile g and its phase: two alternating (a group sees
+  // every other phase), or with PF8 a ring of 6 (no waiter lags 6 tiles)
+  auto ptb = [&](uint32_t g) -> uint32_t { return PF8 ? g % 6u : (g & 1u); };
+  auto ptph = [&](uint32_t g) -> uint32_t { return PF8 ? (g / 6u) & 1u : (g >> 1) & 1u; };
   double* sAcc = reinterpret_cast<double*>(sStage + (SYM ? BM * WP : 0));  // [WP][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sAcc + ((SYM || WIDE) ? 0 : WP * BM));
   uint64_t* xb_land = bars;               // [6]   local copy completion
@@ -676,8 +800,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   uint64_t* vi_land = g2done + NR;        // [1]   SYM: local V block landed
   uint64_t* vi_full = vi_land + 1;        // [1]   SYM leader: both V blocks landed
   uint64_t* vi_empty = vi_full + 1;       // [1]   SYM both: V block free (multicast commit)
-  uint64_t* pt_free = vi_empty + 1;       // [2]   SYM both: P buffer free (multicast commit)
-  uint64_t* dt_full = pt_free + 2;        // [2]   SYM both: transposed product done
+  uint64_t* pt_free = vi_empty + 1;       // [2 / 6] SYM both: P buffer free (multicast commit)
+  uint64_t* dt_full = pt_free + (PF8 ? 6 : 2);  // [2] SYM both: transposed product done
   uint64_t* dt_empty = dt_full + 2;       // [2]   SYM leader: D_T drained (8 warp arrivals)
   uint64_t* s_free = dt_empty + 2;        // [NR]  SYM leader: S(g) loaded by the epilogue (16 warps)
   uint64_t* xb_full = s_free + NR;        // [NR]  SYM leader: XB(g) landed (2 halves)
@@ -705,6 +829,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       mbar_init(&o_full[b], 1);
       mbar_init(&o_empty[b], 8);
       mbar_init(&pt_free[b], (SYM && !NCGP_PAIR_PT) ? 2 : 1);  // SYM: GEMM2(g) and T(g) both read P(g)
+      if (PF8) {
+        mbar_init(&pt_free[2 + 2 * b], (SYM && !NCGP_PAIR_PT) ? 2 : 1);
+        mbar_init(&pt_free[3 + 2 * b], (SYM && !NCGP_PAIR_PT) ? 2 : 1);
+      }
       mbar_init(&dt_full[b], 1);
       mbar_init(&dt_empty[b], 8);
     }
@@ -796,8 +924,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                    &land[r.idx]);
         } else {
           mbar_expect_tx(&land[r.idx], vslot);
-          bulk_g2s(sV + (size_t)r.idx * vslot, p.col_pack + src + p.xbh_bytes, vslot,
+          bulk_g2s(sV + (size_t)r.idx * vslot, p.col_pack + src + p.xbh_bytes, vslot0,
                    &land[r.idx]);
+          if (PF8)  // this CTA's half (rows) of the column tile's Vhi8
+            bulk_g2s(sV + (size_t)r.idx * vslot + vslot0,
+                     p.v8_pack + (int64_t)ti.ct * p.v8_bytes + (int64_t)rank * v8h, v8h, &land[r.idx]);
         }
         r.adv();
         if (g >= lagt) sr.adv();
@@ -809,12 +940,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       for (int it = (int)(blockIdx.x >> 1); it < items; it += (int)(gridDim.x >> 1), ++nitem) {
         const Item cur = item_of(p, it);
         mbar_wait(vi_empty, (nitem & 1u) ^ 1u);
-        mbar_expect_tx(vi_land, 2 * p.v2_bytes);
+        mbar_expect_tx(vi_land, 2 * p.v2_bytes + (PF8 ? p.v8_bytes : 0u));
         // Vhi of column tile rt sits in the record's CTA0 half, Vlo in its CTA1 half
         const int64_t rt = p.rt0 + 2 * (int64_t)cur.pp + rank;
         const int64_t vb = rt * p.tile_stride + p.xbh_bytes;
         bulk_g2s(sVI, p.col_pack + vb, p.v2_bytes, vi_land);
         bulk_g2s(sVI + p.v2_bytes, p.col_pack + vb + p.rec_bytes, p.v2_bytes, vi_land);
+        if (PF8) bulk_g2s(sVI + 2 * p.v2_bytes, p.v8_pack + rt * p.v8_bytes, p.v8_bytes, vi_land);
       }
     } else if (SYM && role == 3) {
       uint32_t nitem = 0;
@@ -975,15 +1107,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             } else if (SYM) {
               // symmetric kernel: P(g) from shared-memory buffer g mod 2 (K-major
               // canonical layout, the same bytes the transposed product reads)
-              const uint64_t ph = sdesc(smem_u32(sP) + pbuf(gt) * PBUF, 128u, 2048u);
-              const uint64_t pl = ph + ((PBUF / 2) >> 4);
+              const uint64_t ph = sdesc(smem_u32(sP) + pbuf(gt) * PB, 128u, 2048u);
+              if (PF8) {  // P_hi [Vhi | Vlo] (f16) + P_lo8 Vhi8 (E4M3, K = 32, A K-major rows i)
+                const uint64_t p8 = sdesc(smem_u32(sP) + pbuf(gt) * PB + PH2, 128u, 1024u);
+                // this CTA's Vhi8 half behind the V slot: K-major, 8-row groups at 1024 B
+                const uint64_t b8 = sdesc(0u, 128u, 1024u) | (((dv & 0x3FFFull) + (vslot0 >> 4)) & 0x3FFFull);
+                constexpr uint32_t id28 = idesc1_f8(WP, false) + ((uint32_t)((256 - 128) >> 4) << 24);
 #pragma unroll
-              for (int m = 0; m < BN / 16; ++m) {
-                mma_ss(dO, ph + (uint64_t)(16 * m), dv + (uint64_t)(16 * m), id2, (fu && m == 0) ? 0u : 1u);
-                mma_ss(dO, pl + (uint64_t)(16 * m), dv + v3off + (uint64_t)(16 * m), id2h, 1u);
+                for (int m = 0; m < BN / 16; ++m)
+                  mma_ss(dO, ph + (uint64_t)(16 * m), dv + (uint64_t)(16 * m), id2, (fu && m == 0) ? 0u : 1u);
+#pragma unroll
+                for (int q2 = 0; q2 < BN / 32; ++q2)
+                  mma_f8_ss(dO, p8 + (uint64_t)(16 * q2), b8 + (uint64_t)(16 * q2), id28, 1u);
+              } else {
+                const uint64_t pl = ph + ((PBUF / 2) >> 4);
+#pragma unroll
+                for (int m = 0; m < BN / 16; ++m) {
+                  mma_ss(dO, ph + (uint64_t)(16 * m), dv + (uint64_t)(16 * m), id2, (fu && m == 0) ? 0u : 1u);
+                  mma_ss(dO, pl + (uint64_t)(16 * m), dv + v3off + (uint64_t)(16 * m), id2h, 1u);
+                }
               }
               tc_commit2(&g2done[r]);           // V slot g free (both CTAs)
-              tc_commit2(&pt_free[gt & 1u]);    // with T(g): P(g)'s buffer free
+              tc_commit2(&pt_free[ptb(gt)]);    // with T(g): P(g)'s buffer free
             } else {
               if (WIDE) {  // P_hi Vhi, P_hi Vlo, P_lo Vhi into the same 128 columns
                 const uint64_t b4 = (uint64_t)(p.v3_bytes >> 4);
@@ -1058,19 +1203,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           const uint32_t liu = __shfl_sync(0xffffffffu, cur.last_in_item() ? 1u : 0u, 0);
           if (elect_one()) {
             if (tpu && !(DBG && (p.sym_dbg & 4))) {
-              const uint64_t pa = dP0 + (uint64_t)pbuf(gt) * (PBUF >> 4);
-#pragma unroll 1
-              for (int m = 0; m < BN / 16; ++m) {
-                const uint64_t ah = pa + (uint64_t)m * (4096 >> 4), al = ah + ((PBUF / 2) >> 4);
-                const uint64_t bh = dVh + (uint64_t)(16 * m), bl = dVl + (uint64_t)(16 * m);
+              const uint64_t pa = dP0 + (uint64_t)pbuf(gt) * (PB >> 4);
+              if (PF8) {
+                // P_hi^T Vhi + P_hi^T Vlo (f16), then P_lo8^T Vhi8 (E4M3, K = 32, A MN-major,
+                // core matrix 8 K-rows x 16 MN-bytes) with B = this CTA's own Vhi8 block
                 const uint32_t dt = tDT(dtb);
-                mma_ss(dt, ah, bh, idT, m > 0 ? 1u : 0u);
-                mma_ss(dt, ah, bl, idT, 1u);
-                mma_ss(dt, al, bh, idT, 1u);
+                const uint64_t p8 = sdesc(smem_u32(sP) + pbuf(gt) * PB + PH2, 1024u, 128u);
+                const uint64_t b8 = sdesc(smem_u32(sVI) + 2u * p.v2_bytes, 128u, 1024u);
+                constexpr uint32_t idT8 = idesc1_f8(2 * WP, true) + ((uint32_t)((256 - 128) >> 4) << 24);
+#pragma unroll 1
+                for (int m = 0; m < BN / 16; ++m) {
+                  const uint64_t ah = pa + (uint64_t)m * (4096 >> 4);
+                  mma_ss(dt, ah, dVh + (uint64_t)(16 * m), idT, m > 0 ? 1u : 0u);
+                  mma_ss(dt, ah, dVl + (uint64_t)(16 * m), idT, 1u);
+                }
+#pragma unroll
+                for (int q2 = 0; q2 < BN / 32; ++q2)
+                  mma_f8_ss(dt, p8 + (uint64_t)q2 * (4096 >> 4), b8 + (uint64_t)(16 * q2), idT8, 1u);
+              } else {
+#pragma unroll 1
+                for (int m = 0; m < BN / 16; ++m) {
+                  const uint64_t ah = pa + (uint64_t)m * (4096 >> 4), al = ah + ((PBUF / 2) >> 4);
+                  const uint64_t bh = dVh + (uint64_t)(16 * m), bl = dVl + (uint64_t)(16 * m);
+                  const uint32_t dt = tDT(dtb);
+                  mma_ss(dt, ah, bh, idT, m > 0 ? 1u : 0u);
+                  mma_ss(dt, ah, bl, idT, 1u);
+                  mma_ss(dt, al, bh, idT, 1u);
+                }
               }
             }
             if (tpu) tc_commit2(&dt_full[dtb]);
-            tc_commit2(&pt_free[gt & 1u]);
+            tc_commit2(&pt_free[ptb(gt)]);
             if (liu) tc_commit2(vi_empty);
           }
           __syncwarp();
@@ -1124,8 +1287,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             // per 16 B): the K-major A of GEMM2 and the MN-major A of T.  S(g)
             // is released to GEMM1(g + NS) as soon as it is loaded.
             const int i = 32 * wq + lane;
-            const uint32_t rowb0 = smem_u32(sP) + pbuf(gt) * PBUF + (uint32_t)(i >> 3) * 2048u +
+            const uint32_t rowb0 = smem_u32(sP) + pbuf(gt) * PB + (uint32_t)(i >> 3) * 2048u +
                                    (uint32_t)(i & 7) * 16u + (col0 >> 3) * 128u;
+            // PF8: P_lo8 at + PH2, row i, 16 consecutive j per 16 B (as K1-sym2)
+            const uint32_t row8b = smem_u32(sP) + pbuf(gt) * PB + PH2 + (uint32_t)(i >> 3) * 1024u +
+                                   (uint32_t)(i & 7) * 16u + (col0 >> 4) * 128u;
+            uint32_t l8[8];
 #pragma unroll
             for (int c = 0; c < BN / 64; ++c) {
               tmem_ld32(base + 32 * c, ra);
@@ -1135,7 +1302,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(leader_addr(&s_free[er.idx]));
               }
-              transform_chunk<FAM>(ra, L, hi, lo);
+              if (PF8)
+                transform_chunk2<FAM>(ra, L, hi, l8);
+              else
+                transform_chunk<FAM>(ra, L, hi, lo);
               if (NCGP_PAIR_PT) {  // P over S(g) for GEMM2's TS MMAs
                 if (FAM == NCGP_RBF) {
                   tmem_st_hilo(base + 32 * c, hi, lo);
@@ -1146,17 +1316,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
               }
               if (pt_wait) {
                 const uint32_t t = gt - (uint32_t)p.npb;
-                mbar_wait(&pt_free[t & 1u], (t >> 1) & 1u);
+                mbar_wait(&pt_free[ptb(t)], ptph(t));
                 pt_wait = false;
                 if (tr) trace_ev<DBG>(p, gt, 8);
               }
               if (!(DBG && (p.sym_dbg & 16))) {
                 const uint32_t rowb = rowb0 + 512u * c;
 #pragma unroll
-                for (int g = 0; g < 4; ++g) {
+                for (int g = 0; g < 4; ++g)
                   st_shared_v4(rowb + 128u * g, hi[4 * g], hi[4 * g + 1], hi[4 * g + 2], hi[4 * g + 3]);
-                  st_shared_v4(rowb + PBUF / 2 + 128u * g, lo[4 * g], lo[4 * g + 1], lo[4 * g + 2],
-                               lo[4 * g + 3]);
+                if (PF8) {
+                  st_shared_v4(row8b + 256u * c, l8[0], l8[1], l8[2], l8[3]);
+                  st_shared_v4(row8b + 256u * c + 128u, l8[4], l8[5], l8[6], l8[7]);
+                } else {
+#pragma unroll
+                  for (int g = 0; g < 4; ++g)
+                    st_shared_v4(rowb + PBUF / 2 + 128u * g, lo[4 * g], lo[4 * g + 1], lo[4 * g + 2],
+                                 lo[4 * g + 3]);
                 }
               }
             }
@@ -1942,100 +2118,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
 // epilogue (two groups alternating tiles); warps 20-23 the drains (D_T per
 // column tile, the 4 O accumulators at each item's end) into the int64
 // fixed-point accumulator (deterministic, as K1-sym1).
-#ifndef NCGP_SYM2_RB
-#define NCGP_SYM2_RB 4  // row tiles per block (build-time A/B: 4 or 2)
-#endif
-#ifndef NCGP_SYM2_NS
-#define NCGP_SYM2_NS 1  // S buffers in TMEM (build-time A/B: 1 or 2)
-#endif
-#ifndef NCGP_SYM2_NP
-#define NCGP_SYM2_NP 2  // P regions in TMEM (build-time A/B: 2 or 1)
-#endif
-constexpr int RB = NCGP_SYM2_RB;            // row tiles per block
-constexpr int LO8_SHIFT = 6;                // P_lo * 2^6, Vhi * 2^-6 in E4M3
-constexpr uint32_t PH2 = BM * BN * 2;       // P_hi (fp16, MN-major for T)
-constexpr uint32_t P2BUF = PH2 + BM * BN;   // [P_hi | P_lo E4M3]: 48 KB
-constexpr int NR2 = 16;                     // per-tile barrier rings (power of two)
-constexpr uint32_t TP2 = 96;                // TMEM columns of one P region (hi 64 | lo8 32)
-#ifndef NCGP_SYM2_HOLD
-#define NCGP_SYM2_HOLD 0  // build-time A/B: T(g) issued only after GEMM1(g + HOLD)
-#endif
-#ifndef NCGP_SYM2_HOLDG2
-#define NCGP_SYM2_HOLDG2 0  // build-time A/B: GEMM2(g) issued only after GEMM1(g + HOLDG2)
-#endif
-#ifndef NCGP_SYM2_ABL
-#define NCGP_SYM2_ABL 0  // timing ablations (wrong results): 1 no T MMAs, 2 no P stores for T,
-                         // 4 no GEMM2 f16 MMAs, 8 no accumulator flushes, 16 no E4M3 conversion
-#endif
-
-__device__ __forceinline__ void mma1_f8_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
-                                           uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
-}
-__device__ __forceinline__ void mma1_f8_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc,
-                                           uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
-      "r"(a), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
-}
-// kind::f8f6f4, A/B E4M3, D F32, M = 128; bit 15: A MN-major
-__host__ __device__ constexpr uint32_t idesc1_f8(int n, bool a_mn) {
-  return (1u << 4) | (a_mn ? (1u << 15) : 0u) | ((uint32_t)(n >> 3) << 17) |
-         ((uint32_t)(128 >> 4) << 24);
-}
-// two floats -> E4M3x2 (a in the low byte)
-__device__ __forceinline__ uint32_t e4m3x2(float a, float b) {
-  uint16_t d;
-  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(d) : "f"(b), "f"(a));
-  return (uint32_t)d;
-}
-__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
-               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]));
-}
-
-// One 32-column chunk: S -> P_hi (fp16, rounded to nearest) and P_lo * 2^6 (E4M3).
-template <int FAM>
-__device__ __forceinline__ void transform_chunk2(const uint32_t (&r)[32], float L,
-                                                 uint32_t (&hi)[16], uint32_t (&l8)[8]) {
-  constexpr float S8 = (float)(1 << LO8_SHIFT);
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    float k0, k1;
-    const float g0 = __uint_as_float(r[2 * i]);
-    const float g1 = __uint_as_float(r[2 * i + 1]);
-    if (FAM == NCGP_RBF) {
-      k0 = ex2(g0);
-      k1 = ex2(g1);
-    } else {
-      const float a0 = sqrt_approx(fmaxf(g0, 0.f));
-      const float a1 = sqrt_approx(fmaxf(g1, 0.f));
-      const float e0 = ex2(fmaf(a0, -1.4426950408889634f, L));
-      const float e1 = ex2(fmaf(a1, -1.4426950408889634f, L));
-      k0 = fmaf(a0, e0, e0);
-      k1 = fmaf(a1, e1, e1);
-    }
-    // round to the nearest value with 11 significant bits (fp16-exact)
-    const float h0 = __uint_as_float((__float_as_uint(k0) + 0x1000u) & 0xFFFFE000u);
-    const float h1 = __uint_as_float((__float_as_uint(k1) + 0x1000u) & 0xFFFFE000u);
-    hi[i] = pack_h2(h0, h1);
-    const uint32_t q = (NCGP_SYM2_ABL & 16) ? __float_as_uint(k0 - h0) & 0xFFFFu
-                                            : e4m3x2((k0 - h0) * S8, (k1 - h1) * S8);
-    if (i & 1)
-      l8[i >> 1] |= q << 16;
-    else
-      l8[i >> 1] = q;
-  }
-}
-
 // The CTA's tile sequence: items (row block, column range), column-major inside.
 struct Tile2 {
   int it, c0, c1, ct, r, rlo, rend;
@@ -3092,9 +3174,14 @@ size_t smem_wide(uint32_t a_bytes, int sx, int sv) {
 
 size_t smem_bytes(uint32_t a_bytes, int wp, int na, int sx, int sv, int sym_npb = 0) {
   const size_t v2 = (size_t)wp * BN * 2, v3 = v2 / 2;
-  return (size_t)na * a_bytes + (size_t)sx * (a_bytes / 2) + (size_t)sv * (v2 + v3) +
-         (sym_npb ? 2 * v2 + sym_npb * (size_t)PBUF + (size_t)BM * wp * 4 : (size_t)wp * BM * 8) +
-         (6 + 9 + 2 + NS_MAX + 5 * NR + 8 + 12) * sizeof(uint64_t) + 16 + 1024;
+  // NCGP_PAIR_F8 (symmetric pair kernel): [P_hi | P_lo8] buffers, Vhi8 halves
+  // behind the V slots and a full Vhi8 block behind the own V block
+  const bool f8 = NCGP_PAIR_F8 && sym_npb > 0;
+  const size_t v8 = (size_t)wp * BN;
+  return (size_t)na * a_bytes + (size_t)sx * (a_bytes / 2) + (size_t)sv * (v2 + v3 + (f8 ? v8 / 2 : 0)) +
+         (sym_npb ? 2 * v2 + (f8 ? v8 : 0) + sym_npb * (size_t)(f8 ? P2BUF : PBUF) + (size_t)BM * wp * 4
+                  : (size_t)wp * BM * 8) +
+         (6 + 9 + 2 + NS_MAX + 5 * NR + 8 + 12 + (f8 ? 8 : 0)) * sizeof(uint64_t) + 16 + 1024;
 }
 
 // The pair kernel with its row tile in TMEM (large D, WP = 16).  NCGP_SYM_ATM=0
@@ -3574,7 +3661,9 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
     // two P buffers with the deepest rings that fit, else one P buffer
     // (large D: the row tile and XB ring outgrow the 227 KB)
     // (npb, na, sx, sv); na = 0: the row tile lives in TMEM (ATM, WP = 16)
-    const int cand[][4] = {{2, 1, 6, 6}, {2, 1, 3, 6}, {2, 1, 3, 5}, {2, 1, 3, 4}, {2, 1, 3, 3},
+    // (NCGP_PAIR_F8: three 48 KB P buffers first, where they fit)
+    const int cand[][4] = {{3, 1, 3, 3}, {3, 0, 3, 3}, {3, 1, 2, 3}, {3, 0, 2, 3},
+                           {2, 1, 6, 6}, {2, 1, 3, 6}, {2, 1, 3, 5}, {2, 1, 3, 4}, {2, 1, 3, 3},
                            {2, 0, 3, 6}, {2, 0, 3, 4}, {2, 0, 3, 3},
                            {1, 1, 3, 6}, {1, 1, 3, 4}, {1, 1, 3, 3}};
     const int force = op->knob_npb;  // NCGP_SYM_NPB experiments: force 1 or 2 P buffers
@@ -3582,7 +3671,8 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
     for (auto& c : cand)
       // one P buffer serialises the two epilogue groups on it: a 1.15x gain
       // for Matern-3/2 at D = 50 but a loss for RBF (tools/sym_exp.py)
-      if ((force == c[0] || (force == 0 && (c[0] == 2 || op->family == NCGP_MATERN32))) &&
+      if ((c[0] < 3 || NCGP_PAIR_F8) &&
+          (force == c[0] || (force == 0 && (c[0] >= 2 || op->family == NCGP_MATERN32))) &&
           (c[1] > 0 || (wp == 16 && atm_allowed(op))) &&
           smem_bytes(p.a_bytes, wp, c[1], c[2], c[3], c[0]) <= (size_t)SMEM_BUDGET) {
         p.npb = c[0];
@@ -3604,6 +3694,14 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
     NCGP_CUDA(cudaMemsetAsync(p.acc, 0, acc_bytes, st));
     op->last_variant = 1;
     if (p.n_items == 0) return NCGP_OK;
+    if (NCGP_PAIR_F8) {  // Vhi in E4M3 per column tile (the split term's B)
+      p.v8_pack = op->v8_pack;
+      p.v8_bytes = (uint32_t)(wp * BN);
+      const int64_t tot = op->col_tiles * (BN / 16) * wp;
+      pack_v8_kernel<float><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+          Vf, ldv, op->n_cols, w, wp, col_exp, op->v8_pack, op->col_tiles);
+      NCGP_LAUNCHED();
+    }
     const size_t smem = smem_bytes(p.a_bytes, wp, p.na, p.sx, p.sv, p.npb);
     const unsigned grid = 2u * (unsigned)std::min<int64_t>(p.n_items, clusters);
     auto launch = [&](auto kern) -> int {
@@ -3614,8 +3712,9 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
       return NCGP_OK;
     };
     int rc;
-    if (p.na == 0)  // row tile in TMEM
-      rc = op->family == NCGP_RBF ? launch(kop_tc_kernel<NCGP_RBF, 16, false, true, true>)
+    if (p.na == 0)  // row tile in TMEM (DBG trace: RBF only)
+      rc = op->family == NCGP_RBF ? (dbg ? launch(kop_tc_kernel<NCGP_RBF, 16, true, true, true>)
+                                         : launch(kop_tc_kernel<NCGP_RBF, 16, false, true, true>))
                                   : launch(kop_tc_kernel<NCGP_MATERN32, 16, false, true, true>);
     else if (dbg)  // per-tile trace of cluster 0 (tools/trace_sym.py)
       rc = op->family == NCGP_RBF

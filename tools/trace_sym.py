@@ -1,6 +1,6 @@
 """Per-tile timeline of cluster 0 of the symmetric K(X, X) kernel (debug hook).
 
-usage: NCGP_SYM=1 python tools/trace_sym.py [n] [family]
+usage: NCGP_SYM=1 [TRACE_D=8] [TRACE_W=32] python tools/trace_sym.py [n] [family]
 Item 0 is row-tile pair 0 over column tiles 0..127 (transposed from tile 2).
 Events (clock64 of CTA 0, row = tile step g):
   11 GEMM2 starts waiting rdy(g)    0 GEMM2 saw rdy(g)    1 GEMM2(g) issued
@@ -26,10 +26,11 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 200_000
 fam = sys.argv[2] if len(sys.argv) > 2 else "rbf"
 EV = 16
 rng = np.random.default_rng(0)
-X = torch.from_numpy(rng.standard_normal((n, 8))).float().cuda()
+D = int(os.environ.get("TRACE_D", "8"))
+X = torch.from_numpy(rng.standard_normal((n, D))).float().cuda()
 W = int(os.environ.get("TRACE_W", "32"))
 S = torch.from_numpy(rng.standard_normal((n, W))).float().cuda()
-op = KernelOperator(fam, 1.5, 1.0, X, w_max=32, impl="tcgen05")
+op = KernelOperator(fam, float(os.environ.get("TRACE_ELL", "1.5")), 1.0, X, w_max=W, impl="tcgen05")
 op.apply(S)
 buf = torch.zeros(256 * EV + 4 * 4096, dtype=torch.int64, device="cuda")
 lib = _native.load()
