@@ -120,6 +120,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // accumulator (as K1-sym2) instead of staging + TMA bulk reductions (build-time A/B)
 #define NCGP_SYM1_RED 1
 #endif
+#ifndef NCGP_SYM1_PT16
+#define NCGP_SYM1_PT16 2  // the same at WP = 16
+#endif
 #ifndef NCGP_SYM1_NS16
 #define NCGP_SYM1_NS16 3  // K1-sym1 S buffers at WP = 16 (build-time A/B: 2 or 3)
 #endif
@@ -1644,12 +1647,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
   const int lane = threadIdx.x & 31;
   // S buffers next to double-buffered O and D_T (2 x 2 WP columns each):
   // two at WP = 32, three at WP = 16
-  constexpr bool PT = NCGP_SYM1_PT != 0;
-  constexpr bool TM = NCGP_SYM1_PT == 1;     // D_T merged into WP columns (double-buffered)
+  // P-in-TMEM mode: 1 (merged D_T) at WP = 32, 2 (two-instruction T into a
+  // 2 WP-column D_T, double-buffered) at WP = 16, where TMEM has the room
+  // (RBF w = 10, n = 2e5: 8.8 -> 8.0 ms; cfg4 shape 3.41 -> 3.36 ms)
+  constexpr int PTM = WP == 16 ? NCGP_SYM1_PT16 : NCGP_SYM1_PT;
+  constexpr bool PT = PTM != 0;
+  constexpr bool TM = PTM == 1;     // D_T merged into WP columns (double-buffered)
   constexpr int NS1 = PT ? 3 : (WP == 16 ? NCGP_SYM1_NS16 : 2);
   constexpr uint32_t AW = PT ? WP : 2 * WP;  // TMEM columns of one O accumulator
   constexpr uint32_t DW = TM ? WP : 2 * WP;  // TMEM columns of one D_T accumulator
-  constexpr uint32_t NDT = (PT && !TM) ? 1u : 2u;  // D_T buffers
+  constexpr uint32_t NDT = (PT && !TM && WP == 32) ? 1u : 2u;  // D_T buffers (PT = 2: two fit at WP = 16)
   const uint32_t xb_bytes = 2u * p.xbh_bytes;  // 128 XB rows
   const uint32_t vb_bytes = 2u * p.v2_bytes;   // [Vhi | Vlo]: 2 WP rows
   uint8_t* sA = smem;
