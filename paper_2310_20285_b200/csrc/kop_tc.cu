@@ -120,6 +120,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // accumulator (as K1-sym2) instead of staging + TMA bulk reductions (build-time A/B)
 #define NCGP_SYM1_RED 1
 #endif
+#ifndef NCGP_SYM1_PT2NS
+#define NCGP_SYM1_PT2NS 0  // build-time A/B: PT = 2 at WP = 32 with two S buffers and two D_T buffers
+#endif
 #ifndef NCGP_SYM1_PT16
 #define NCGP_SYM1_PT16 2  // the same at WP = 16
 #endif
@@ -1653,10 +1656,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym1_kernel(const TcParams p)
   constexpr int PTM = WP == 16 ? NCGP_SYM1_PT16 : NCGP_SYM1_PT;
   constexpr bool PT = PTM != 0;
   constexpr bool TM = PTM == 1;     // D_T merged into WP columns (double-buffered)
-  constexpr int NS1 = PT ? 3 : (WP == 16 ? NCGP_SYM1_NS16 : 2);
+  constexpr int NS1 = (PTM == 2 && WP == 32 && NCGP_SYM1_PT2NS) ? 2 : (PT ? 3 : (WP == 16 ? NCGP_SYM1_NS16 : 2));
   constexpr uint32_t AW = PT ? WP : 2 * WP;  // TMEM columns of one O accumulator
   constexpr uint32_t DW = TM ? WP : 2 * WP;  // TMEM columns of one D_T accumulator
-  constexpr uint32_t NDT = (PT && !TM && WP == 32) ? 1u : 2u;  // D_T buffers (PT = 2: two fit at WP = 16)
+  constexpr uint32_t NDT = (PT && !TM && WP == 32 && !NCGP_SYM1_PT2NS) ? 1u : 2u;  // D_T buffers (PT = 2: two fit at WP = 16)
   const uint32_t xb_bytes = 2u * p.xbh_bytes;  // 128 XB rows
   const uint32_t vb_bytes = 2u * p.v2_bytes;   // [Vhi | Vlo]: 2 WP rows
   uint8_t* sA = smem;
