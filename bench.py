@@ -463,7 +463,7 @@ def product_roofline(op, n, d, w, F, E, world, local_pairs, t_kernel, dev, workl
     # from the committed ncu --set full capture (a number taken under a
     # profiler cannot be measured inside this run)
     traffic, traffic_src = None, None
-    captures = {("cfg3", 2): "r02_summary.json", ("cfg3", 4): "r02c_summary.json"}
+    captures = {("cfg3", 2): "r02_summary.json", ("cfg3", 4): "r02f_summary.json"}
     prof = captures.get((workload_name, variant))
     if prof and world == 1 and os.path.exists(os.path.join(ROOT, "profiles", prof)):
         with open(os.path.join(ROOT, "profiles", prof)) as fh:
