@@ -3816,6 +3816,34 @@ int tc_apply(ncgp_kop* op, const void* V, int64_t ldv, int w, const OutSet& out,
 
 }  // namespace ncgp
 
+// Debug / test hook (host only, no GPU): the symmetric kernels' work list for
+// nb column tiles -- flavour 1 (K1-sym1: row tile, c0, c1), 2 (CTA pairs:
+// row-tile pair, c0, c1) or 3 (K1-sym2: row block of 4, c0, c1) -- as int32
+// triples into out (capacity cap triples); returns the item count (or -1).
+// tests/test_sym_worklist.py checks that the tiles they cover are exactly the
+// on-or-above-diagonal tiles, each once.
+extern "C" int64_t ncgp_debug_sym_items(int flavour, int64_t nb, int item, int32_t* out, int64_t cap) {
+  if (nb < 1 || item < 1) return -1;
+  int64_t k = 0;
+  auto put = [&](int64_t a, int64_t c0, int64_t c1) {
+    if (out != nullptr && k < cap) {
+      out[3 * k] = (int32_t)a;
+      out[3 * k + 1] = (int32_t)c0;
+      out[3 * k + 2] = (int32_t)c1;
+    }
+    ++k;
+  };
+  if (flavour == 1)
+    sym1_walk(nb, put, item);
+  else if (flavour == 2)
+    sym_walk((nb + 1) / 2, nb, put, item);
+  else if (flavour == 3)
+    sym2_walk(nb, put, item);
+  else
+    return -1;
+  return k;
+}
+
 extern "C" int ncgp_debug_set_sym_dump(void* dev_buf) {
   g_sym_dump = static_cast<float*>(dev_buf);
   return 0;
