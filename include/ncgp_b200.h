@@ -174,6 +174,15 @@ int ncgp_kop_sym_partial(ncgp_kop* op, const void* V, int64_t ldv, int w, int pa
 int ncgp_kop_sym_finalize(ncgp_kop* op, const int64_t* acc, int64_t acc_elems,
                           const void* V, int64_t ldv, int w, void* out, int64_t ldo,
                           const ncgp_kop_epilogue* epi, void* stream);
+/* The same for rows [row_begin, row_end) only: the finalize of a process that
+ * keeps a row shard of the solver state.  out, V and the
+ * epilogue's base / out2 / noise_state stay indexed by the operator's global
+ * rows, as in ncgp_kop_apply_ex; only rows of the range are read or written,
+ * so a caller holding just its shard passes (shard pointer - row_begin * ld). */
+int ncgp_kop_sym_finalize_rows(ncgp_kop* op, const int64_t* acc, int64_t acc_elems,
+                               const void* V, int64_t ldv, int w, void* out, int64_t ldo,
+                               const ncgp_kop_epilogue* epi, int64_t row_begin,
+                               int64_t row_end, void* stream);
 
 /* Symmetric-kernel policy of an operator (no reference counterpart): -1 the
  * default size policy, 0 always the plain tiled kernel, 1 a symmetric kernel

@@ -75,6 +75,8 @@ _SIGS = {
     "ncgp_kop_sym_partial": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _i64, _vp]),
     "ncgp_kop_sym_finalize": (_i32, [_vp, _vp, _i64, _vp, _i64, _i32, _vp, _i64,
                                      ctypes.POINTER(Epilogue), _vp]),
+    "ncgp_kop_sym_finalize_rows": (_i32, [_vp, _vp, _i64, _vp, _i64, _i32, _vp, _i64,
+                                          ctypes.POINTER(Epilogue), _i64, _i64, _vp]),
     "ncgp_kop_destroy": (_i32, [_vp]),
     "ncgp_softmax_stats": (_i32, [_i32, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp]),
     "ncgp_softmax_winv": (_i32, [_i32, _vp, _i64, _i32, _vp, _i64, _i32, _vp, _i64, _f64, _f64,

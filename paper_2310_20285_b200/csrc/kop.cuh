@@ -164,6 +164,7 @@ int64_t tc_sym_acc_elems(const ncgp_kop* op, int w);
 int tc_posterior_var(ncgp_kop* op, const void* W, int64_t ldw, int C, int R, const double* s2,
                      void* var, int64_t ldvar, cudaStream_t st);
 int tc_sym_finalize(ncgp_kop* op, const unsigned long long* acc, int w, const OutSet& out,
-                    int64_t ldo, cudaStream_t st, const EpiDev& epi);
+                    int64_t ldo, cudaStream_t st, const EpiDev& epi, int64_t row_begin = 0,
+                    int64_t row_end = -1);
 
 }  // namespace ncgp

@@ -245,12 +245,16 @@ int ncgp_kop_sym_partial(ncgp_kop* op, const void* V, int64_t ldv, int w, int pa
   return ncgp::tc_apply(op, V, ldv, w, none, w, 0, op->n_rows, ncgp::as_stream(stream), ed, &sp);
 }
 
-int ncgp_kop_sym_finalize(ncgp_kop* op, const int64_t* acc, int64_t acc_elems, const void* V,
-                          int64_t ldv, int w, void* out, int64_t ldo,
-                          const ncgp_kop_epilogue* epi, void* stream) {
+int ncgp_kop_sym_finalize_rows(ncgp_kop* op, const int64_t* acc, int64_t acc_elems, const void* V,
+                               int64_t ldv, int w, void* out, int64_t ldo,
+                               const ncgp_kop_epilogue* epi, int64_t row_begin, int64_t row_end,
+                               void* stream) {
   NCGP_CHECK_ARG(op != nullptr && acc != nullptr && out != nullptr, NCGP_INVALID_INPUT,
                  "null argument");
   NCGP_CHECK_ARG(ldo >= w, NCGP_DIMENSION_MISMATCH, "leading dimension < width");
+  NCGP_CHECK_ARG(row_begin >= 0 && row_begin <= row_end && row_end <= op->n_rows,
+                 NCGP_DIMENSION_MISMATCH, "row range [%lld, %lld) outside [0, %lld]",
+                 (long long)row_begin, (long long)row_end, (long long)op->n_rows);
   const int64_t need = ncgp_kop_sym_acc_elems(op, w);
   NCGP_CHECK_ARG(need > 0, NCGP_UNSUPPORTED, "no symmetric kernel for this operator and width %d", w);
   NCGP_CHECK_ARG(acc_elems >= need, NCGP_DIMENSION_MISMATCH, "accumulator has %lld elements, need %lld",
@@ -266,7 +270,15 @@ int ncgp_kop_sym_finalize(ncgp_kop* op, const int64_t* acc, int64_t acc_elems, c
   o.n = 1;
   const EpiDev ed = ncgp::make_epi(epi, V, ldv, w, op->dtype, 0);
   return ncgp::tc_sym_finalize(op, reinterpret_cast<const unsigned long long*>(acc), w, o, ldo,
-                               ncgp::as_stream(stream), ed);
+                               ncgp::as_stream(stream), ed, row_begin, row_end);
+}
+
+int ncgp_kop_sym_finalize(ncgp_kop* op, const int64_t* acc, int64_t acc_elems, const void* V,
+                          int64_t ldv, int w, void* out, int64_t ldo,
+                          const ncgp_kop_epilogue* epi, void* stream) {
+  NCGP_CHECK_ARG(op != nullptr, NCGP_INVALID_INPUT, "null argument");
+  return ncgp_kop_sym_finalize_rows(op, acc, acc_elems, V, ldv, w, out, ldo, epi, 0, op->n_rows,
+                                    stream);
 }
 
 int ncgp_kop_posterior_var(ncgp_kop* op, const void* W, int64_t ldw, int C, int R,

@@ -641,6 +641,10 @@ constexpr uint32_t TP2 = 96;                // TMEM columns of one P region (hi 
 #ifndef NCGP_SYM2_HOLDG2
 #define NCGP_SYM2_HOLDG2 0  // build-time A/B: GEMM2(g) issued only after GEMM1(g + HOLDG2)
 #endif
+#ifndef NCGP_SYM2_LATE
+#define NCGP_SYM2_LATE 0  // epilogue: both chunks transformed before the P-buffer waits and stores
+                          // (build-time A/B; measured slower: cfg3 293.1 vs 280.9 ms, n = 2e5 10.48 vs 9.75 ms)
+#endif
 #ifndef NCGP_SYM2_ABL
 #define NCGP_SYM2_ABL 0  // timing ablations (wrong results): 1 no T MMAs, 2 no P stores for T,
                          // 4 no GEMM2 f16 MMAs, 8 no accumulator flushes, 16 no E4M3 conversion
@@ -2488,6 +2492,42 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym2_kernel(const TcParams p)
         if (tr) trace_ev<DBG>(p, g, 5);
         const uint32_t pr = tP(g % NP) + lane_off;
         const uint32_t pbase = smem_u32(sP) + (g & 1u) * P2BUF;
+#if NCGP_SYM2_LATE
+        // Transform both chunks into registers first, and only then wait for
+        // this group's P region (GEMM2(g - NP)) and P buffer (T(g - 2)): those
+        // were issued when this group finished its previous tile, so waiting
+        // before the first store would idle the group for most of their run.
+        uint32_t hi1[16], l81[8];
+        transform_chunk2<FAM>(ra, L, hi, l8);
+        transform_chunk2<FAM>(rb, L, hi1, l81);
+        if (g >= NP) {  // GEMM2(g - NP) has read this P region
+          mbar_wait(&g2done[(g - NP) % NR2], par(g - NP));
+          tc_fence_after();
+        }
+        {
+          const uint32_t cc = col0 >> 5;  // first chunk of the tile (0 or 2)
+          tmem_st16(pr + 16u * cc, hi);
+          tmem_st8(pr + 64u + 8u * cc, l8);
+          tmem_st16(pr + 16u * (cc + 1u), hi1);
+          tmem_st8(pr + 64u + 8u * (cc + 1u), l81);
+        }
+        if (tp && !(NCGP_SYM2_ABL & 2)) {
+          if (g >= 2u)  // T(g - 2) is done with this P smem buffer
+            mbar_wait(&tdone[(g - 2u) % NR2], par(g - 2u));
+          const uint32_t rh = pbase + rowh;
+          const uint32_t r8 = pbase + row8;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            st_shared_v4(rh + 128u * k, hi[4 * k], hi[4 * k + 1], hi[4 * k + 2], hi[4 * k + 3]);
+          st_shared_v4(r8, l8[0], l8[1], l8[2], l8[3]);
+          st_shared_v4(r8 + 128u, l8[4], l8[5], l8[6], l8[7]);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            st_shared_v4(rh + 512u + 128u * k, hi1[4 * k], hi1[4 * k + 1], hi1[4 * k + 2], hi1[4 * k + 3]);
+          st_shared_v4(r8 + 256u, l81[0], l81[1], l81[2], l81[3]);
+          st_shared_v4(r8 + 256u + 128u, l81[4], l81[5], l81[6], l81[7]);
+        }
+#else
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           if (c == 0)
@@ -2513,6 +2553,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym2_kernel(const TcParams p)
             st_shared_v4(r8 + 128u, l8[4], l8[5], l8[6], l8[7]);
           }
         }
+#endif
         tmem_wait_st();
         tc_fence_before();
         if (tp) fence_proxy_async_smem();
@@ -2930,10 +2971,12 @@ __global__ void reduce_partial_epi_kernel(const double* __restrict__ partial, in
 // fx_flush8) scaled back by 2^-(F + s + e_c) in fp64, through the epilogue,
 // to every destination; one thread per row
 __global__ void sym_finalize_kernel(const unsigned long long* __restrict__ acc, int64_t acc_rows,
-                                    int64_t n, int w, int fx_exp, int s_exp,
+                                    int64_t row_begin, int64_t n, int w, int fx_exp, int s_exp,
                                     const int* __restrict__ col_exp, const EpiDev e,
                                     const ncgp::OutPtrs<float> out, int64_t ldo, int colmajor) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // rows [row_begin, n): every pointer (out, base, out2, V, noise state) is
+  // indexed by the operator's global rows
+  const int64_t i = row_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int swz = (int)((i >> 1) & 3);
   auto kv = [&](int c) -> double {
@@ -3254,12 +3297,15 @@ int64_t tc_sym_acc_elems(const ncgp_kop* op, int w) {
 }
 
 int tc_sym_finalize(ncgp_kop* op, const unsigned long long* acc, int w, const OutSet& out,
-                    int64_t ldo, cudaStream_t st, const EpiDev& epi) {
+                    int64_t ldo, cudaStream_t st, const EpiDev& epi, int64_t row_begin,
+                    int64_t row_end) {
+  if (row_end < 0) row_end = op->n_rows;
+  if (row_end <= row_begin) return NCGP_OK;
   const Layout L = layout_of(op->n_rows, op->n_cols, op->d, op->w_max, op->sms);
   const int* col_exp = reinterpret_cast<const int*>(op->ws + L.colexp);
   const int s_exp = (int)lround(log2(op->k_scale));
-  sym_finalize_kernel<<<(unsigned)((op->n_rows + 127) / 128), 128, 0, st>>>(
-      acc, op->row_tiles * BM, op->n_rows, w, op->sym_fx, s_exp, col_exp, epi,
+  sym_finalize_kernel<<<(unsigned)((row_end - row_begin + 127) / 128), 128, 0, st>>>(
+      acc, op->row_tiles * BM, row_begin, row_end, w, op->sym_fx, s_exp, col_exp, epi,
       ncgp::out_ptrs<float>(out, 0, ldo), ldo,
       (op->sym_cg == 3 || (op->sym_cg == 1 && NCGP_SYM1_RED) || (op->sym_cg == 2 && NCGP_PAIR_RED)) ? 1 : 0);
   NCGP_LAUNCHED();

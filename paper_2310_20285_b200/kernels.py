@@ -11,6 +11,7 @@ from __future__ import annotations
 import contextlib
 import ctypes
 import os
+import threading
 from typing import Optional, Sequence, Tuple
 
 import torch
@@ -19,6 +20,34 @@ from . import _native
 from .device import code, ptr, require_cuda, stream, workspace
 
 N = _native
+
+# Cross-process sum of the fp64 partial reductions (dots, Q' z, Gram) when the
+# solver state is row-sharded (parallel.sharded_state): a callable that sums a
+# device tensor in place over the ranks, or None.  Thread-local, so that
+# in-process ranks (parallel.ThreadComm) can each install their own.
+_reduce_state = threading.local()
+
+
+def set_reducer(fn, shard=None) -> None:
+    """``shard``: (first global CN entry of this rank's shard, global dim), for
+    the code that needs global indices (the unit-vector policy)."""
+    _reduce_state.fn = fn
+    _reduce_state.shard = shard
+
+
+def get_shard():
+    return getattr(_reduce_state, "shard", None)
+
+
+def get_reducer():
+    return getattr(_reduce_state, "fn", None)
+
+
+def _allreduce(t: torch.Tensor) -> torch.Tensor:
+    fn = getattr(_reduce_state, "fn", None)
+    if fn is not None:
+        fn(t)
+    return t
 
 
 def _rows(t: torch.Tensor) -> Tuple[torch.Tensor, int]:
@@ -40,28 +69,37 @@ class Epi:
 
     ``noise`` is ``None``, ``("softmax", pi)`` with pi the (n, C) cached
     probabilities, or ``("diag", d)`` with d the CN diagonal of W^-1.  ``base``
-    and ``out2`` are (n_rows, w) tensors (rows of the full operator).
+    and ``out2`` are (n_rows, w) tensors (rows of the full operator).  With
+    ``row0`` > 0 they (and the noise state) are a row shard whose first row is
+    the operator's global row ``row0``: the C ABI indexes them by global rows
+    and only touches the rows of the apply's range, so the shard is passed as
+    (its pointer - row0 rows).
     """
 
-    __slots__ = ("alpha", "beta", "base", "gamma", "noise", "out2")
+    __slots__ = ("alpha", "beta", "base", "gamma", "noise", "out2", "row0")
 
-    def __init__(self, alpha=1.0, beta=1.0, base=None, gamma=0.0, noise=None, out2=None):
+    def __init__(self, alpha=1.0, beta=1.0, base=None, gamma=0.0, noise=None, out2=None,
+                 row0: int = 0):
         self.alpha, self.beta, self.base = float(alpha), float(beta), base
         self.gamma, self.noise, self.out2 = float(gamma), noise, out2
+        self.row0 = int(row0)
 
-    def native(self, c0: int, es: int) -> "N.Epilogue":
+    def native(self, c0: int, es: int, w: int = 0) -> "N.Epilogue":
+        """``w``: width of the apply (the noise state's row length; needed
+        only with ``row0``)."""
         e = N.Epilogue()
         e.alpha, e.beta, e.gamma = self.alpha, self.beta, self.gamma
+        r0 = self.row0
         if self.base is not None:
-            e.base = self.base.data_ptr() + c0 * es
             e.ldb = self.base.stride(0) if self.base.dim() == 2 else 1
+            e.base = self.base.data_ptr() + (c0 - r0 * e.ldb) * es
         if self.noise is not None and self.gamma != 0.0:
             kind, st = self.noise
             e.noise = {"softmax": N.NOISE_SOFTMAX, "diag": N.NOISE_DIAG}[kind]
-            e.noise_state = st.data_ptr()
+            e.noise_state = st.data_ptr() - r0 * w * st.element_size()
         if self.out2 is not None:
-            e.out2 = self.out2.data_ptr() + c0 * es
             e.ld2 = self.out2.stride(0) if self.out2.dim() == 2 else 1
+            e.out2 = self.out2.data_ptr() + (c0 - r0 * e.ld2) * es
         return e
 
 
@@ -142,8 +180,12 @@ class KernelOperator:
     def apply(self, V: torch.Tensor, out: Optional[torch.Tensor] = None,
               row_begin: int = 0, row_end: Optional[int] = None,
               peers: Optional[Sequence[torch.Tensor]] = None,
-              epi: Optional[Epi] = None) -> torch.Tensor:
+              epi: Optional[Epi] = None, out_row0: int = 0) -> torch.Tensor:
         """K(X_rows[row_begin:row_end], X_cols) @ V for V of shape (n_cols, w).
+
+        ``out_row0``: ``out`` is a row shard whose first row is global row
+        ``out_row0`` (it must cover [row_begin, row_end)); by default ``out``
+        has all n_rows rows.
 
         ``peers``: further (n_rows, w) buffers with ``out``'s strides (other
         ranks' gather buffers mapped into this process) that receive the same
@@ -162,12 +204,15 @@ class KernelOperator:
         w = V.shape[1]
         row_end = self.n_rows if row_end is None else row_end
         if out is None:
-            out = torch.empty((self.n_rows, w), dtype=self.dtype, device=V.device)
+            out = torch.empty((row_end - out_row0 if out_row0 else self.n_rows, w),
+                              dtype=self.dtype, device=V.device)
         elif out.dim() == 1:
             out = out.view(-1, 1)
+        if out_row0 and not (out_row0 <= row_begin and row_end <= out_row0 + out.shape[0]):
+            raise N.DimensionMismatch("output shard does not cover the row range")
         ldv = V.stride(0) if V.shape[0] > 1 else w
         ldo = out.stride(0) if out.shape[0] > 1 else w
-        bases = [out.data_ptr()]
+        bases = [out.data_ptr() - out_row0 * ldo * V.element_size()]
         for p in peers or ():
             p = p.view(-1, 1) if p.dim() == 1 else p
             if tuple(p.shape) != tuple(out.shape) or p.stride() != out.stride() or \
@@ -181,19 +226,20 @@ class KernelOperator:
             if epi.noise is not None and epi.gamma != 0.0 and w > self.w_max:
                 raise N.DimensionMismatch(f"a noise epilogue needs w <= {self.w_max}, got {w}")
             for t in (epi.base, epi.out2):
-                if t is not None and (t.dtype != self.dtype or t.shape[0] < self.n_rows or
+                if t is not None and (t.dtype != self.dtype or
+                                      epi.row0 + t.shape[0] < min(row_end, self.n_rows) or
                                       (t.dim() == 2 and t.stride(1) != 1)):
                     raise N.DimensionMismatch("epilogue base / out2 must be (>= n_rows, w) rows")
         for c0 in range(0, w, self.w_max):
             c1 = min(w, c0 + self.w_max)
             if epi is not None:
-                e = epi.native(c0, es)
+                e = epi.native(c0, es, c1 - c0)
                 N.call("ncgp_kop_apply_ex", self._h, V.data_ptr() + c0 * es, ldv, c1 - c0,
-                       out.data_ptr() + c0 * es, ldo, row_begin, row_end, ctypes.byref(e),
+                       bases[0] + c0 * es, ldo, row_begin, row_end, ctypes.byref(e),
                        stream())
             elif len(bases) == 1:
                 N.call("ncgp_kop_apply", self._h, V.data_ptr() + c0 * es, ldv, c1 - c0,
-                       out.data_ptr() + c0 * es, ldo, row_begin, row_end, stream())
+                       bases[0] + c0 * es, ldo, row_begin, row_end, stream())
             else:
                 arr = (ctypes.c_void_p * len(bases))(*[b + c0 * es for b in bases])
                 N.call("ncgp_kop_apply_multi", self._h, V.data_ptr() + c0 * es, ldv, c1 - c0,
@@ -250,9 +296,31 @@ class KernelOperator:
                acc.numel(), stream())
 
     def sym_finalize(self, acc: torch.Tensor, w: int, out: Optional[torch.Tensor] = None,
-                     V: Optional[torch.Tensor] = None, epi: Optional[Epi] = None) -> torch.Tensor:
+                     V: Optional[torch.Tensor] = None, epi: Optional[Epi] = None,
+                     row_begin: int = 0, row_end: Optional[int] = None) -> torch.Tensor:
         """The (n_rows, w) product from the summed accumulators, through the
-        fused epilogue ``epi`` (its noise term reads the operand ``V``)."""
+        fused epilogue ``epi`` (its noise term reads the operand ``V``).  With
+        a row range, only those rows are finalised and ``out`` (and ``epi``'s
+        tensors, ``epi.row0 == row_begin``) are the (row_end - row_begin)-row
+        shard (``ncgp_kop_sym_finalize_rows``)."""
+        row_end = self.n_rows if row_end is None else row_end
+        if row_begin or row_end != self.n_rows:
+            if out is None:
+                out = torch.empty((row_end - row_begin, w), dtype=self.dtype, device=acc.device)
+            if out.shape[0] < row_end - row_begin:
+                raise N.DimensionMismatch("output shard is shorter than the row range")
+            if epi is not None and epi.row0 != row_begin:
+                raise N.DimensionMismatch("epilogue shard must start at row_begin")
+            ldo = out.stride(0) if out.shape[0] > 1 else w
+            vp, ldv = None, w
+            if V is not None:  # the full operand (the noise term reads rows of the range)
+                V = V.unsqueeze(1) if V.dim() == 1 else V
+                vp, ldv = V.data_ptr(), (V.stride(0) if V.shape[0] > 1 else w)
+            e = ctypes.byref(epi.native(0, out.element_size(), w)) if epi is not None else None
+            N.call("ncgp_kop_sym_finalize_rows", self._h, acc.data_ptr(), acc.numel(), vp, ldv, w,
+                   out.data_ptr() - row_begin * ldo * out.element_size(), ldo, e, row_begin,
+                   row_end, stream())
+            return out
         if out is None:
             out = torch.empty((self.n_rows, w), dtype=self.dtype, device=acc.device)
         ldo = out.stride(0) if out.shape[0] > 1 else w
@@ -370,7 +438,7 @@ def dots(pairs: Sequence[Tuple[torch.Tensor, torch.Tensor]],
     ys = N.ptr_array([ptr(y) for _, y in pairs])
     N.call("ncgp_dots", code(x0), n, len(pairs), xs, ys, ptr(out), ptr(ws), ws.numel(),
            stream())
-    return out
+    return _allreduce(out)
 
 
 def gemv_t(Q: torch.Tensor, z: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
@@ -384,7 +452,7 @@ def gemv_t(Q: torch.Tensor, z: torch.Tensor, out: Optional[torch.Tensor] = None)
     ws = _reduce_ws(n, k)
     N.call("ncgp_gemv_t", code(z), ptr(Qr), ldq, k, ptr(z), n, ptr(out), ptr(ws), ws.numel(),
            stream())
-    return out
+    return _allreduce(out)
 
 
 def gemv_n(Q: torch.Tensor, y: torch.Tensor, s: Optional[torch.Tensor], alpha: float,
@@ -423,6 +491,11 @@ def gram(S: torch.Tensor, Y: torch.Tensor, out: Optional[torch.Tensor] = None) -
     ws = workspace().get("gram", nbytes)
     N.call("ncgp_gram", code(Sr), ptr(Sr), lds, ka, ptr(Yr), ldy, kb, n, ptr(out),
            out.stride(0), ptr(ws), ws.numel(), stream())
+    if get_reducer() is not None:  # ``out`` may be a strided block of the Gram matrix
+        tmp = out.contiguous()
+        _allreduce(tmp)
+        if tmp.data_ptr() != out.data_ptr():
+            out.copy_(tmp)
     return out
 
 

@@ -33,6 +33,8 @@ from __future__ import annotations
 
 from typing import Callable, Optional, Tuple
 
+import numpy as np
+
 import torch
 import torch.distributed as dist
 
@@ -344,3 +346,306 @@ class ShardedPriorOperator:
         return res.reshape(-1) if flat else res
 
     __call__ = apply
+
+
+# --------------------------------------------------------------------------
+# Row-sharded solver state
+#
+# Every CN vector of the fit (v, r, s, z, d, f, y^, pi) and every column block
+# (S, T, Q) is split by the same contiguous, 256-aligned partition of the N
+# points.  Elementwise kernels, the W^-1 / W^+ applications, Q y and the
+# rotation are then purely local, and the collectives are exactly the
+# reference algorithm's global reductions:
+#   * all-gather of the next K product's operand (N*C values; 40 MB at cfg5);
+#   * all-reduce of the fp64 partials of the fused dots, of Q' z (<= R values)
+#     and of the Gram blocks S'(T + W^+ S) (B x B, once per Newton step);
+#   * for the symmetric kernels' work-list split, the all-reduce of the int64
+#     accumulators (as SymmetricSplitOperator), finalised for the rank's rows.
+# The small eigenproblem is solved redundantly on every rank from the same
+# (all-reduced) Gram matrix, so U and Lambda agree without a broadcast.
+# Per-rank memory and vector work scale as 1 / world.
+
+class TorchDistComm:
+    """Collectives of a ``torch.distributed`` group (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+
+    def all_reduce_(self, t: torch.Tensor) -> torch.Tensor:
+        if self.world > 1:
+            dist.all_reduce(t, group=self.group)
+        return t
+
+    def all_gather_(self, full: torch.Tensor, mine: torch.Tensor) -> torch.Tensor:
+        """In place: ``mine`` is this rank's equal-sized slice of ``full``."""
+        if self.world > 1:
+            dist.all_gather_into_tensor(full, mine, group=self.group)
+        return full
+
+
+class ThreadComm:
+    """The same collectives between ``world`` Python threads of one process
+    sharing one device: N ranks' host logic and kernels exercised on a single
+    GPU (tests, per-rank timing).  Ranks meet at a host barrier; no kernel
+    waits on another rank's kernel.  Results are summed in rank order, so
+    every rank gets the same bits."""
+
+    class _Shared:
+        def __init__(self, world):
+            import threading
+            self.world = world
+            self.slots = [None] * world
+            self.barrier = threading.Barrier(world)
+
+    @classmethod
+    def create(cls, world: int):
+        shared = cls._Shared(world)
+        return [cls(shared, r) for r in range(world)]
+
+    def __init__(self, shared, rank):
+        self._s, self.rank, self.world = shared, rank, shared.world
+
+    def _exchange(self, t):
+        if t.is_cuda:
+            torch.cuda.current_stream(t.device).synchronize()
+        self._s.slots[self.rank] = t
+        self._s.barrier.wait()
+        peers = list(self._s.slots)
+        return peers
+
+    def _done(self, t):
+        if t.is_cuda:
+            torch.cuda.current_stream(t.device).synchronize()
+        self._s.barrier.wait()
+
+    def all_reduce_(self, t: torch.Tensor) -> torch.Tensor:
+        if self.world == 1:
+            return t
+        peers = self._exchange(t)
+        total = peers[0].clone()
+        for p in peers[1:]:
+            total += p
+        self._done(total)   # every rank has read every slot
+        t.copy_(total)
+        return t
+
+    def all_gather_(self, full: torch.Tensor, mine: torch.Tensor) -> torch.Tensor:
+        if self.world == 1:
+            return full
+        peers = self._exchange(mine)
+        per = mine.numel()
+        parts = [p.reshape(-1).clone() for p in peers]
+        self._done(parts[0])
+        flat = full.view(-1)
+        for r, p in enumerate(parts):
+            flat[r * per:(r + 1) * per].copy_(p)
+        return full
+
+
+class sharded_state:
+    """Context: the solver's global reductions (kernels.dots / gemv_t / gram,
+    the posterior's partial products) are summed over ``comm``'s ranks, and
+    the unit-vector policy indexes the global vector."""
+
+    def __init__(self, comm, offset: int, global_dim: int):
+        self.comm, self.offset, self.global_dim = comm, offset, global_dim
+
+    def __enter__(self):
+        from . import kernels as K
+        self._old = (K.get_reducer(), K.get_shard())
+        K.set_reducer(self.comm.all_reduce_, (self.offset, self.global_dim))
+        return self
+
+    def __exit__(self, *exc):
+        from . import kernels as K
+        K.set_reducer(*self._old)
+        return False
+
+
+class ShardedStateOperator:
+    """K product on a row shard of the solver state: takes this rank's rows of
+    the CN operand, returns this rank's rows of K v (or of the fused K^
+    epilogue, whose base / noise state / raw-product tensors are shards too).
+
+    The operand is all-gathered (the path's one exchange per product); then
+    either the rank's row block of the plain kernel (``gather="rows"``: no
+    further communication -- north_star's partition), or its slice of the
+    symmetric kernel's work list, an all-reduce of the int64 accumulators
+    and a finalize of its own rows (``gather="reduce"``, the default where a
+    symmetric kernel exists: half the kernel evaluations).
+    """
+
+    def __init__(self, prior, X, comm, dtype=None, gather: str = "auto"):
+        from .gp import PriorOperator
+        if gather not in ("auto", "reduce", "rows"):
+            raise ValueError(f"gather must be auto, reduce or rows, got {gather!r}")
+        self.comm = comm
+        self.inner = PriorOperator(prior, X, dtype=dtype)
+        self.C, self.n_rows, self.dtype = self.inner.C, self.inner.n_rows, self.inner.dtype
+        self.r0, self.r1, self.per = row_partition(self.n_rows, comm.world, comm.rank)
+        if self.r1 <= self.r0:
+            raise ValueError(f"rank {comm.rank} of {comm.world} holds no rows of {self.n_rows}")
+        g0 = self.inner.groups[0]
+        sym_ok = (len(self.inner.groups) == 1 and len(g0[1]) == self.C
+                  and g0[0].sym_acc_elems(self.C) > 0)
+        if gather == "auto":
+            gather = "reduce" if sym_ok else "rows"
+        if gather == "reduce" and not sym_ok:
+            raise ValueError("gather='reduce' needs a symmetric kernel for this prior / width")
+        self.gather = gather
+        self.matvecs = 0
+        self._full = None
+        self._acc = None
+
+    @property
+    def n_local(self) -> int:
+        return self.r1 - self.r0
+
+    @property
+    def impl(self):
+        return self.inner.impl
+
+    @property
+    def supports_fused(self) -> bool:
+        return self.inner.supports_fused
+
+    def shard(self, full: torch.Tensor) -> torch.Tensor:
+        """This rank's rows of a replicated CN vector / (n, C) matrix."""
+        C = self.C
+        return full.reshape(self.n_rows, C)[self.r0:self.r1].reshape(
+            -1 if full.dim() == 1 else (self.n_local, C)).contiguous()
+
+    def gather_vector(self, v_loc: torch.Tensor) -> torch.Tensor:
+        """All ranks' shards of a CN vector as the full (n, C) operand (a view
+        of an internal buffer, valid until the next call)."""
+        C, per = self.C, self.per
+        if self._full is None or self._full.device != v_loc.device:
+            self._full = torch.zeros((per * self.comm.world, C), dtype=self.dtype,
+                                     device=v_loc.device)
+        mine = self._full[self.comm.rank * per:(self.comm.rank + 1) * per]
+        mine[:self.n_local].copy_(v_loc.view(self.n_local, C))
+        self.comm.all_gather_(self._full, mine)
+        return self._full[:self.n_rows]
+
+    def _product(self, v_loc, out, epi):
+        from .kernels import Epi
+        C, r0, r1 = self.C, self.r0, self.r1
+        flat = v_loc.dim() == 1
+        if v_loc.numel() != self.n_local * C:
+            raise ValueError(f"operand shard has {v_loc.numel()} entries, expected "
+                             f"{self.n_local} * {C}")
+        V = self.gather_vector(v_loc)
+        if out is None:
+            out = torch.empty((self.n_local, C), dtype=self.dtype, device=V.device)
+        O = out.view(self.n_local, C)
+        e = None
+        if epi is not None:
+            rows = lambda t: None if t is None else t.view(self.n_local, C)
+            e = Epi(epi.alpha, epi.beta, rows(epi.base), epi.gamma, epi.noise, rows(epi.out2),
+                    row0=r0)
+        if self.gather == "reduce":
+            kop = self.inner.groups[0][0]
+            if self._acc is None:
+                self._acc = torch.empty(int(kop.sym_acc_elems(C)), dtype=torch.int64,
+                                        device=V.device)
+            kop.sym_partial(V, self.comm.rank, self.comm.world, self._acc)
+            self.comm.all_reduce_(self._acc)
+            kop.sym_finalize(self._acc, C, O, V=V, epi=e, row_begin=r0, row_end=r1)
+        else:
+            for kop, cols in self.inner.groups:
+                if len(cols) == C:
+                    kop.apply(V, out=O, row_begin=r0, row_end=r1, epi=e, out_row0=r0)
+                else:  # mixed specs: one pass per spec group on its outputs
+                    idx = torch.tensor(cols, device=V.device)
+                    sub = kop.apply(V.index_select(1, idx).contiguous(), row_begin=r0,
+                                    row_end=r1, out_row0=r0)
+                    O[:, cols] = sub[:self.n_local]
+        self.matvecs += 1
+        return out.reshape(-1) if flat else out
+
+    def apply(self, v_loc: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        return self._product(v_loc, out, None)
+
+    def apply_fused(self, v_loc: torch.Tensor, epi, out: Optional[torch.Tensor] = None):
+        if not self.supports_fused:
+            raise ValueError("fused epilogues need one kernel spec for all outputs")
+        return self._product(v_loc, out, epi)
+
+    __call__ = apply
+
+
+def fit_sharded(prior, dataset, likelihood, outer_config, inner_config, policy_kind="residual",
+                comm=None, dtype=None, gather: str = "auto", on_step=None, on_inner=None):
+    """:func:`outer.fit` with the solver state row-sharded over ``comm``'s
+    ranks (default: the ``torch.distributed`` world).  Every rank passes the
+    full dataset and likelihood (replicated inputs, as in SURVEY.md 8(e));
+    it returns this rank's shard of the belief -- ``belief.train_inputs`` are
+    its rows of X, ``belief.weights`` / ``belief.root`` its rows of v and Q --
+    and the trace (identical on every rank).  Use :func:`sharded_posterior`
+    to predict from the sharded belief, or :func:`gather_belief`."""
+    from .gp import Dataset
+    from .outer import fit
+    comm = comm if comm is not None else TorchDistComm()
+    op = ShardedStateOperator(prior, dataset.inputs, comm, dtype=dtype, gather=gather)
+    r0, r1, C = op.r0, op.r1, op.C
+    idx = np.arange(r0, r1)
+    local = Dataset(inputs=dataset.inputs[r0:r1], targets=dataset.targets[r0:r1],
+                    domain=dataset.domain, num_classes=dataset.num_classes)
+    lik = likelihood.subset(idx)
+    with sharded_state(comm, r0 * C, dataset.n_points * C):
+        belief, trace = fit(prior, local, lik, outer_config, inner_config, policy_kind,
+                            on_step=on_step, on_inner=on_inner, dtype=dtype, operator=op)
+    trace.shard = (r0, r1)
+    return belief, trace
+
+
+def sharded_posterior(belief, X_test, comm=None, dtype=None):
+    """(mean, marginal variance) at ``X_test`` from a row-sharded belief: every
+    rank multiplies its columns of K(X*, X) with its rows of v and Q, the
+    partial products are all-reduced, and the squares are taken after the
+    sum.  Identical on every rank."""
+    from .posterior import posterior_marginal_var, posterior_mean
+    comm = comm if comm is not None else TorchDistComm()
+    with sharded_state(comm, 0, 0):
+        mean = posterior_mean(belief, X_test, dtype=dtype)
+        var = posterior_marginal_var(belief, X_test, dtype=dtype)
+    return mean, var
+
+
+def gather_belief(belief, comm=None):
+    """The full belief on every rank from its row shards (weights N*C and the
+    root R x N*C: 10 GB at cfg5's rank 256 in fp32 -- prefer
+    :func:`sharded_posterior` at scale)."""
+    from .device import to_device
+    from .linalg import LowRankRoot
+    from .posterior import PosteriorBelief
+    comm = comm if comm is not None else TorchDistComm()
+    C = belief.prior.num_outputs
+    X_loc = np.asarray(belief.train_inputs)
+    dt = belief.dtype
+    w = belief.weights_device(dt)
+    counts = torch.zeros(comm.world, dtype=torch.int64, device=w.device)
+    counts[comm.rank] = X_loc.shape[0]
+    comm.all_reduce_(counts)
+    counts = [int(c) for c in counts.tolist()]
+    per = max(counts)
+    dev = w.device
+
+    def gather(block, width):  # (k, n_loc * width) row block -> (k, n * width)
+        k = block.shape[0]
+        full = torch.zeros((comm.world, k, per * width), dtype=block.dtype, device=dev)
+        full[comm.rank, :, :block.shape[1]].copy_(block)
+        comm.all_gather_(full, full[comm.rank])
+        return torch.cat([full[r, :, :counts[r] * width] for r in range(comm.world)], dim=1)
+
+    weights = gather(w.view(1, -1), C)[0]
+    Xd = to_device(X_loc, torch.float64)
+    X = gather(Xd.reshape(1, -1), X_loc.shape[1])[0].view(-1, X_loc.shape[1])
+    R = belief.root.rank
+    root = LowRankRoot(block=gather(belief.root.block(dt), C)) if R else \
+        LowRankRoot.zero(weights.numel())
+    return PosteriorBelief(prior=belief.prior, train_inputs=X.cpu().numpy(), weights=weights,
+                           root=root, newton_step=belief.newton_step,
+                           solver_iterations=belief.solver_iterations)

@@ -108,6 +108,7 @@ def posterior_mean(belief: PosteriorBelief, X_test, chunk: int = 512, dtype=None
         else:
             idx = torch.tensor(cols, device=V.device)
             out[:, cols] = op.apply(V.index_select(1, idx).contiguous())
+    K._allreduce(out)  # row-sharded belief: this rank's columns of K(X*, X) only
     res = to_host(out) + np.asarray(belief.prior.mean, dtype=np.float64)[None, :]
     return res
 
@@ -131,7 +132,10 @@ def posterior_marginal_var(belief: PosteriorBelief, X_test, chunk: int = 512, dt
     # K2: the fused cross-kernel posterior (ncgp_kop_posterior_var): each
     # kernel tile once per 128 root columns, square-reduce in the kernel's
     # fp64 reduction pass, A never stored
-    if dt == torch.float32 and C * R > 32:
+    # (a row-sharded belief holds a column slice of K(X*, X): the partial
+    # products must be summed over the ranks before squaring, so it takes the
+    # product path below)
+    if dt == torch.float32 and C * R > 32 and K.get_reducer() is None:
         done = True
         for op, cols in _cross_ops(belief, X_test, dt, w_max=128):
             if op.impl != "tcgen05" or op.w_max <= 32:
@@ -156,6 +160,7 @@ def posterior_marginal_var(belief: PosteriorBelief, X_test, chunk: int = 512, dt
             else:
                 for c in cols:
                     op.apply(W[:, c * R:(c + 1) * R], out=A[:, c * R:(c + 1) * R])
+        K._allreduce(A)
         K.marginal_var(A, C, R, s2d, out=var[t0:t1])
     return to_host(var)
 
