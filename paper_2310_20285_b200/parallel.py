@@ -477,19 +477,25 @@ class ShardedStateOperator:
     symmetric kernel exists: half the kernel evaluations).
     """
 
-    def __init__(self, prior, X, comm, dtype=None, gather: str = "auto"):
-        from .gp import PriorOperator
+    def __init__(self, prior, X, comm, dtype=None, gather: str = "auto", inner=None):
+        """``inner``: a pre-built replicated operator with :class:`gp.PriorOperator`'s
+        interface (``C``, ``n_rows``, ``dtype``, ``groups`` of (kernel operator,
+        output columns), ``supports_fused``); by default it is built from
+        ``prior`` and the full ``X``.  The CPU tests inject a stand-in."""
         if gather not in ("auto", "reduce", "rows"):
             raise ValueError(f"gather must be auto, reduce or rows, got {gather!r}")
         self.comm = comm
-        self.inner = PriorOperator(prior, X, dtype=dtype)
+        if inner is None:
+            from .gp import PriorOperator
+            inner = PriorOperator(prior, X, dtype=dtype)
+        self.inner = inner
         self.C, self.n_rows, self.dtype = self.inner.C, self.inner.n_rows, self.inner.dtype
         self.r0, self.r1, self.per = row_partition(self.n_rows, comm.world, comm.rank)
         if self.r1 <= self.r0:
             raise ValueError(f"rank {comm.rank} of {comm.world} holds no rows of {self.n_rows}")
         g0 = self.inner.groups[0]
         sym_ok = (len(self.inner.groups) == 1 and len(g0[1]) == self.C
-                  and g0[0].sym_acc_elems(self.C) > 0)
+                  and hasattr(g0[0], "sym_acc_elems") and g0[0].sym_acc_elems(self.C) > 0)
         if gather == "auto":
             gather = "reduce" if sym_ok else "rows"
         if gather == "reduce" and not sym_ok:
@@ -577,18 +583,21 @@ class ShardedStateOperator:
 
 
 def fit_sharded(prior, dataset, likelihood, outer_config, inner_config, policy_kind="residual",
-                comm=None, dtype=None, gather: str = "auto", on_step=None, on_inner=None):
+                comm=None, dtype=None, gather: str = "auto", on_step=None, on_inner=None,
+                operator=None):
     """:func:`outer.fit` with the solver state row-sharded over ``comm``'s
     ranks (default: the ``torch.distributed`` world).  Every rank passes the
     full dataset and likelihood (replicated inputs, as in SURVEY.md 8(e));
     it returns this rank's shard of the belief -- ``belief.train_inputs`` are
     its rows of X, ``belief.weights`` / ``belief.root`` its rows of v and Q --
-    and the trace (identical on every rank).  Use :func:`sharded_posterior`
+    and the trace (identical on every rank).  ``operator``: a pre-built
+    :class:`ShardedStateOperator` (reused across fits, or a test stand-in).  Use :func:`sharded_posterior`
     to predict from the sharded belief, or :func:`gather_belief`."""
     from .gp import Dataset
     from .outer import fit
     comm = comm if comm is not None else TorchDistComm()
-    op = ShardedStateOperator(prior, dataset.inputs, comm, dtype=dtype, gather=gather)
+    op = operator if operator is not None else \
+        ShardedStateOperator(prior, dataset.inputs, comm, dtype=dtype, gather=gather)
     r0, r1, C = op.r0, op.r1, op.C
     idx = np.arange(r0, r1)
     local = Dataset(inputs=dataset.inputs[r0:r1], targets=dataset.targets[r0:r1],
