@@ -502,6 +502,7 @@ def measure_fit(name, args, rank, world, local_rank, warmup_fits=1, timed_fits=1
     import torch.distributed as dist
     import paper_2310_20285_b200 as P
     from paper_2310_20285_b200 import configs
+    from paper_2310_20285_b200 import parallel as PP
     from paper_2310_20285_b200.parallel import ShardedPriorOperator
 
     torch.cuda.set_device(local_rank)
@@ -511,12 +512,27 @@ def measure_fit(name, args, rank, world, local_rank, warmup_fits=1, timed_fits=1
     prior = P.MultiOutputPrior(kernels=(P.KernelSpec(*c["kernel"]),) * C)
     ds = P.Dataset(c["X"], c["y"], "class-index", C)
     lik = P.SoftmaxLikelihood(ds.targets, C)
-    op = ShardedPriorOperator(prior, c["X"], dtype=dt, gather=args.gather) if world > 1 else \
-        P.PriorOperator(prior, c["X"], dtype=dt)
+    # N > 1: the solver state is row-sharded like the operator (
+    # --state replicated keeps every rank's full copy of v, r, S, T, Q)
+    sharded = world > 1 and args.state == "sharded"
+    if sharded:
+        comm = PP.TorchDistComm()
+        op = PP.ShardedStateOperator(prior, c["X"], comm, dtype=dt, gather={
+            "auto": "auto", "reduce": "reduce"}.get(args.gather, "rows"))
+
+        def run_fit_(oc_):
+            return PP.fit_sharded(prior, ds, lik, oc_, inner, c["policy"], comm=comm, dtype=dt,
+                                  operator=op)
+    else:
+        op = ShardedPriorOperator(prior, c["X"], dtype=dt, gather=args.gather) if world > 1 else \
+            P.PriorOperator(prior, c["X"], dtype=dt)
+
+        def run_fit_(oc_):
+            return P.fit(prior, ds, lik, oc_, inner, policy_kind=c["policy"], dtype=dt,
+                         operator=op)
     inner = P.InnerConfig(max_iters=1, residual=args.residual)
     for _ in range(max(0, warmup_fits)):
-        P.fit(prior, ds, lik, P.OuterConfig(max_newton_steps=1, inner_schedule=2), inner,
-              policy_kind=c["policy"], dtype=dt, operator=op)
+        run_fit_(P.OuterConfig(max_newton_steps=1, inner_schedule=2))
     oc = P.OuterConfig(max_newton_steps=c["steps"], delta=c["delta"], inner_schedule=c["inner"],
                        recycle=c["recycle"], compression_rank=c["rank"])
     sampler = ClockSampler(local_rank)
@@ -527,8 +543,7 @@ def measure_fit(name, args, rank, world, local_rank, warmup_fits=1, timed_fits=1
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        belief, trace = P.fit(prior, ds, lik, oc, inner, policy_kind=c["policy"], dtype=dt,
-                              operator=op)
+        belief, trace = run_fit_(oc)
         torch.cuda.synchronize()
         times.append(trace.wallclock_s)
     clocks = sampler.stop()
@@ -541,14 +556,25 @@ def measure_fit(name, args, rank, world, local_rank, warmup_fits=1, timed_fits=1
     variant = inner_kind.last_variant if inner_kind is not None else None
     del op
     rec = None
-    if rank == 0:
+    if sharded:  # every rank: its columns of K(X*, X) on its rows of v and Q, all-reduced
         Xt = c["X_test"]
         torch.cuda.synchronize()
+        dist.barrier()
         t0 = time.perf_counter()
-        mean = P.posterior_mean(belief, Xt)
-        t1 = time.perf_counter()
-        var = P.posterior_marginal_var(belief, Xt)
+        with PP.sharded_state(comm, 0, 0):
+            mean = P.posterior_mean(belief, Xt)
+            t1 = time.perf_counter()
+            var = P.posterior_marginal_var(belief, Xt)
         t2 = time.perf_counter()
+    if rank == 0:
+        Xt = c["X_test"]
+        if not sharded:
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            mean = P.posterior_mean(belief, Xt)
+            t1 = time.perf_counter()
+            var = P.posterior_marginal_var(belief, Xt)
+            t2 = time.perf_counter()
         probs = P.probit_predict(mean, var)
         rec = {"metric": f"IterNCGP fit time ({name})", "value": round(secs, 3), "unit": "s",
                "higher_is_better": False, "wallclock_s": round(secs, 3),
@@ -559,7 +585,9 @@ def measure_fit(name, args, rank, world, local_rank, warmup_fits=1, timed_fits=1
                           "d": int(c["X"].shape[1]), "kernel": list(c["kernel"]),
                           "schedule": [c["steps"], c["inner"]], "rank": c["rank"],
                           "policy": c["policy"], "recycle": c["recycle"],
-                          "residual": args.residual},
+                          "residual": args.residual,
+                          "solver_state": ("row-sharded" if sharded else
+                                           ("replicated" if world > 1 else "single"))},
                "k_product_variant": variant,
                "posterior": {"n_test": int(Xt.shape[0]), "root_rank": int(belief.root.rank),
                              "mean_s": round(t1 - t0, 3), "marginal_var_s": round(t2 - t1, 3),
@@ -620,6 +648,9 @@ def main():
                          "ranks + NCCL all-reduce of the accumulators; nccl = row blocks + in-place "
                          "all-gather; fused = row blocks stored by K1 into every rank's "
                          "symmetric-memory buffer; auto = reduce when available, else nccl")
+    ap.add_argument("--state", default="sharded", choices=["sharded", "replicated"],
+                    help="N > 1 fits: row-shard the solver state with the operator "
+                         "(SURVEY.md 8(e)) or replicate it on every rank")
     ap.add_argument("--cpu-rows", type=int, default=24)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--fits", default="cfg4,cfg5",

@@ -6,10 +6,12 @@ block of output rows with the fused kernel-matmul directly into its slice of
 the gather buffer, and the blocks are exchanged so every rank holds the full
 product for the next solver step: either by the kernel itself, which stores
 each finished row into every rank's symmetric-memory gather buffer over
-NVLink (``gather="fused"``), or by an in-place NCCL all-gather after it.  Solver state (v, r, s, z, d, Q, S, T) is replicated: the
-vector work is O(N C R) against the O(N^2) operator, and replication keeps
-every rank's control flow (tolerance / breakdown exits) identical without
-extra collectives.
+NVLink (``gather="fused"``), or by an in-place NCCL all-gather after it.
+With these operators (``ShardedPriorOperator``) the solver state (v, r, s, z,
+d, Q, S, T) is replicated; :func:`fit_sharded` (second half of this module)
+row-shards the state as well, as SURVEY.md 8(e) specifies: per-rank memory and
+vector work scale as 1 / world, and the exchanges become an all-gather of each
+product's operand plus all-reduces of the solver's global sums.
 
 Because the operator plans its column splits on the *full* row count and
 flushes its fp32 partial sums at fixed global column boundaries, a row is
