@@ -413,8 +413,11 @@ def run_ours(args, rank, world, local_rank):
         fits = {}
         for name in args.fits.split(","):
             if name:
+                # cfg4 (~6 s, two host syncs per inner iteration: sensitive to host
+                # noise) is timed three times and the median reported; cfg5 once
                 fits[name] = measure_fit(name, args, rank, world, local_rank, warmup_fits=1,
-                                         timed_fits=1, cpu_extrapolate=not args.no_cpu_baseline)
+                                         timed_fits=3 if name == "cfg4" else 1,
+                                         cpu_extrapolate=not args.no_cpu_baseline)
         if line is not None:
             line["fit"] = fits
             line["gpu_launches"] = int(line["gpu_launches"]) + sum(
@@ -548,10 +551,12 @@ def measure_fit(name, args, rank, world, local_rank, warmup_fits=1, timed_fits=1
         times.append(trace.wallclock_s)
     clocks = sampler.stop()
     launches = _native_launches() - launches0
-    t = torch.tensor([sum(times)], dtype=torch.float64, device="cuda")
+    t = torch.tensor(times, dtype=torch.float64, device="cuda")
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    secs = float(t[0]) / len(times)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)   # each fit: max over ranks
+    times = sorted(float(x) for x in t.tolist())
+    secs = times[len(times) // 2] if len(times) % 2 else \
+        0.5 * (times[len(times) // 2 - 1] + times[len(times) // 2])   # median over the timed fits
     inner_kind = getattr(getattr(op, "inner", op), "groups", [[None]])[0][0]
     variant = inner_kind.last_variant if inner_kind is not None else None
     del op
@@ -578,6 +583,7 @@ def measure_fit(name, args, rank, world, local_rank, warmup_fits=1, timed_fits=1
         probs = P.probit_predict(mean, var)
         rec = {"metric": f"IterNCGP fit time ({name})", "value": round(secs, 3), "unit": "s",
                "higher_is_better": False, "wallclock_s": round(secs, 3),
+               "timed_fits_s": [round(x, 3) for x in times],
                "kernel_matvecs": trace.total_kernel_matvecs,
                "inner_iters": [s.inner_iterations for s in trace.steps],
                "termination": trace.termination,
