@@ -43,7 +43,9 @@ def get_reducer():
     return getattr(_reduce_state, "fn", None)
 
 
-def _allreduce(t: torch.Tensor) -> torch.Tensor:
+def allreduce_partial(t: torch.Tensor) -> torch.Tensor:
+    """Sum a rank-local partial result over the ranks (in place); the identity
+    unless a reducer is installed."""
     fn = getattr(_reduce_state, "fn", None)
     if fn is not None:
         fn(t)
@@ -438,7 +440,7 @@ def dots(pairs: Sequence[Tuple[torch.Tensor, torch.Tensor]],
     ys = N.ptr_array([ptr(y) for _, y in pairs])
     N.call("ncgp_dots", code(x0), n, len(pairs), xs, ys, ptr(out), ptr(ws), ws.numel(),
            stream())
-    return _allreduce(out)
+    return allreduce_partial(out)
 
 
 def gemv_t(Q: torch.Tensor, z: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
@@ -452,7 +454,7 @@ def gemv_t(Q: torch.Tensor, z: torch.Tensor, out: Optional[torch.Tensor] = None)
     ws = _reduce_ws(n, k)
     N.call("ncgp_gemv_t", code(z), ptr(Qr), ldq, k, ptr(z), n, ptr(out), ptr(ws), ws.numel(),
            stream())
-    return _allreduce(out)
+    return allreduce_partial(out)
 
 
 def gemv_n(Q: torch.Tensor, y: torch.Tensor, s: Optional[torch.Tensor], alpha: float,
@@ -493,7 +495,7 @@ def gram(S: torch.Tensor, Y: torch.Tensor, out: Optional[torch.Tensor] = None) -
            out.stride(0), ptr(ws), ws.numel(), stream())
     if get_reducer() is not None:  # ``out`` may be a strided block of the Gram matrix
         tmp = out.contiguous()
-        _allreduce(tmp)
+        allreduce_partial(tmp)
         if tmp.data_ptr() != out.data_ptr():
             out.copy_(tmp)
     return out

@@ -108,7 +108,7 @@ def posterior_mean(belief: PosteriorBelief, X_test, chunk: int = 512, dtype=None
         else:
             idx = torch.tensor(cols, device=V.device)
             out[:, cols] = op.apply(V.index_select(1, idx).contiguous())
-    K._allreduce(out)  # row-sharded belief: this rank's columns of K(X*, X) only
+    K.allreduce_partial(out)  # row-sharded belief: this rank's columns of K(X*, X) only
     res = to_host(out) + np.asarray(belief.prior.mean, dtype=np.float64)[None, :]
     return res
 
@@ -160,7 +160,7 @@ def posterior_marginal_var(belief: PosteriorBelief, X_test, chunk: int = 512, dt
             else:
                 for c in cols:
                     op.apply(W[:, c * R:(c + 1) * R], out=A[:, c * R:(c + 1) * R])
-        K._allreduce(A)
+        K.allreduce_partial(A)
         K.marginal_var(A, C, R, s2d, out=var[t0:t1])
     return to_host(var)
 

@@ -284,3 +284,11 @@ def test_world_one_is_the_plain_fit():
     comm = PP.ThreadComm.create(1)[0]
     b2, _ = PP.fit_sharded(prior, ds, lik, oc, P.InnerConfig(max_iters=1), comm=comm, dtype=F64)
     np.testing.assert_array_equal(b1.weights, b2.weights)
+    # default communicator: the torch.distributed world (not initialised here: one rank)
+    b3, t3 = PP.fit_sharded(prior, ds, lik, oc, P.InnerConfig(max_iters=1), dtype=F64)
+    np.testing.assert_array_equal(b1.weights, b3.weights)
+    assert t3.shard == (0, ds.n_points)
+    mean, var = PP.sharded_posterior(b3, g["X_test"])
+    np.testing.assert_array_equal(mean, P.posterior_mean(b1, g["X_test"]))
+    np.testing.assert_array_equal(var, P.posterior_marginal_var(b1, g["X_test"]))
+    assert K.get_reducer() is None and K.get_shard() is None   # the context restored the hook
