@@ -645,6 +645,13 @@ constexpr uint32_t TP2 = 96;                // TMEM columns of one P region (hi 
 #define NCGP_SYM2_LATE 0  // epilogue: both chunks transformed before the P-buffer waits and stores
                           // (build-time A/B; measured slower: cfg3 293.1 vs 280.9 ms, n = 2e5 10.48 vs 9.75 ms)
 #endif
+#ifndef NCGP_SYM2_REG_LO
+#define NCGP_SYM2_REG_LO 40  // registers of the producer / MMA-issuing warps (build-time A/B)
+#endif
+#ifndef NCGP_SYM2_REG_DR
+#define NCGP_SYM2_REG_DR 56  // registers of the drain warps; LO * 4 + DR * 4 + 96 * 16 <= 80 * 24
+                             // (32 / 64: drain spills 220 -> 136 B, cfg3 282.3 vs 282.2 ms: +-0)
+#endif
 #ifndef NCGP_SYM2_ABL
 #define NCGP_SYM2_ABL 0  // timing ablations (wrong results): 1 no T MMAs, 2 no P stores for T,
                          // 4 no GEMM2 f16 MMAs, 8 no accumulator flushes, 16 no E4M3 conversion
@@ -2262,7 +2269,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym2_kernel(const TcParams p)
   auto par = [](uint32_t t) -> uint32_t { return (t / NR2) & 1u; };
 
   if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(NCGP_SYM2_REG_LO));
     if (warp == 0) {
       // ================= producers =================
       // lane 0: GEMM1's operands (XA per tile, XB per column tile); lane 1:
@@ -2565,7 +2572,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym2_kernel(const TcParams p)
       ti.next(p);
     }
   } else {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(NCGP_SYM2_REG_DR));
     // ================= drains: D_T per column tile, O_I at each item's end =================
     // Each accumulator is loaded into registers and released at once (D_T is
     // single-buffered at WP = 32), then rounded to int64 and bulk-reduced.
