@@ -165,12 +165,44 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 // Bounded wait: a pipeline bug traps (kernel error, ~17 s) instead of hanging the GPU.
+#ifndef NCGP_WAIT_CHEAP
+#define NCGP_WAIT_CHEAP 0  // poll loop reads the clock every 256th try only (build-time A/B:
+                           // cfg3 285.4 vs 281.6 ms -- the tighter loop polls more often and is slower)
+#endif
+#ifndef NCGP_WAIT_RELAX_NS
+#define NCGP_WAIT_RELAX_NS 0  // mbar_wait_relaxed sleeps this long between tries (0: same as mbar_wait;
+                              // 100 / 400 ns on K1-sym2's producer and drain waits: +-0)
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try(bar, parity)) return;
   const long long t0 = clock64();
+#if NCGP_WAIT_CHEAP
+  // the polling warps share issue slots with the epilogue: keep the loop to
+  // the try, a counter and the branch, and check the time-out rarely
+  uint32_t spins = 0;
+  while (!mbar_try(bar, parity)) {
+    if ((++spins & 255u) == 0u && clock64() - t0 > (1ll << 35)) __trap();
+  }
+#else
   while (!mbar_try(bar, parity)) {
     if (clock64() - t0 > (1ll << 35)) __trap();
   }
+#endif
+}
+// For waits off the critical path (a producer waiting for a free slot, a
+// drain warp waiting for its accumulator): back off between tries.
+__device__ __forceinline__ void mbar_wait_relaxed(uint64_t* bar, uint32_t parity) {
+#if NCGP_WAIT_RELAX_NS > 0
+  if (mbar_try(bar, parity)) return;
+  const long long t0 = clock64();
+  uint32_t spins = 0;
+  while (!mbar_try(bar, parity)) {
+    __nanosleep(NCGP_WAIT_RELAX_NS);
+    if ((++spins & 255u) == 0u && clock64() - t0 > (1ll << 35)) __trap();
+  }
+#else
+  mbar_wait(bar, parity);
+#endif
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
                                          uint64_t* bar) {
@@ -2287,7 +2319,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym2_kernel(const TcParams p)
           if (lane == 0) {
             if (ti.first_r()) {  // this column tile's XB, for its <= 4 tiles
               const uint8_t* rec = p.col_pack + (int64_t)ti.ct * p.tile_stride;
-              if (jq >= 2) mbar_wait(&xb_empty[s], ((jq >> 1) & 1u) ^ 1u);
+              if (jq >= 2) mbar_wait_relaxed(&xb_empty[s], ((jq >> 1) & 1u) ^ 1u);
               mbar_expect_tx(&xb_full[s], p.a_bytes);
               uint8_t* dx = sXB + (size_t)s * p.a_bytes;
               bulk_g2s(dx, rec, p.xbh_bytes, &xb_full[s]);
@@ -2295,7 +2327,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym2_kernel(const TcParams p)
             }
             if (g >= (uint32_t)p.sx) {  // XA slot freed by GEMM1(g - sx)
               const uint32_t t = g - (uint32_t)p.sx;
-              mbar_wait(&s_full[t % NR2], par(t));
+              mbar_wait_relaxed(&s_full[t % NR2], par(t));
             }
             mbar_expect_tx(&xa_full[r.idx], p.a_bytes);
             bulk_g2s(sXA + (size_t)r.idx * p.a_bytes, p.xa_pack + (int64_t)ti.r * p.a_bytes, p.a_bytes,
@@ -2308,13 +2340,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym2_kernel(const TcParams p)
               bulk_g2s(dst + vb_bytes, p.v8_pack + tile * p.v8_bytes, p.v8_bytes, bar);
             };
             if (ti.first_r()) {  // V_J for GEMM2
-              if (jq >= 2) mbar_wait(&vj_empty[s], ((jq >> 1) & 1u) ^ 1u);
+              if (jq >= 2) mbar_wait_relaxed(&vj_empty[s], ((jq >> 1) & 1u) ^ 1u);
               mbar_expect_tx(&vj_full[s], vi_bytes);
               load_v(sVJ + (size_t)s * vi_bytes, ti.ct, &vj_full[s]);
             }
             if (g >= (uint32_t)p.sv) {  // V_I slot freed by T(g - sv)
               const uint32_t t = g - (uint32_t)p.sv;
-              mbar_wait(&tdone[t % NR2], par(t));
+              mbar_wait_relaxed(&tdone[t % NR2], par(t));
             }
             mbar_expect_tx(&vi_full[r.idx], vi_bytes);
             load_v(sVI + (size_t)r.idx * vi_bytes, ti.r, &vi_full[r.idx]);
@@ -2597,7 +2629,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym2_kernel(const TcParams p)
     while (ti.valid) {
       if (ti.tp_last()) {
         if (wq == 0 && lane == 0) trace_ev<DBG>(p, g, 13);
-        mbar_wait(&dt_full[dq % NDT], (dq / NDT) & 1u);
+        mbar_wait_relaxed(&dt_full[dq % NDT], (dq / NDT) & 1u);
         tc_fence_after();
         float v[WP];
         const uint32_t ta = tDT(dq % NDT) + lane_off;
@@ -2619,7 +2651,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kop_sym2_kernel(const TcParams p)
       }
       if (ti.o_last()) {
         const int k = ti.k();
-        mbar_wait(&o_full[k], (ouse >> k) & 1u);
+        mbar_wait_relaxed(&o_full[k], (ouse >> k) & 1u);
         ouse ^= 1u << k;
         tc_fence_after();
         float v[WP];
