@@ -165,6 +165,9 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 // Bounded wait: a pipeline bug traps (kernel error, ~17 s) instead of hanging the GPU.
+#ifndef NCGP_WAIT_NS
+#define NCGP_WAIT_NS 0  // back-off between polls of every wait (build-time A/B: 20 / 60 / 150 ns +1 % slower at cfg3)
+#endif
 #ifndef NCGP_WAIT_CHEAP
 #define NCGP_WAIT_CHEAP 0  // poll loop reads the clock every 256th try only (build-time A/B:
                            // cfg3 285.4 vs 281.6 ms -- the tighter loop polls more often and is slower)
@@ -185,6 +188,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 #else
   while (!mbar_try(bar, parity)) {
+#if NCGP_WAIT_NS > 0
+    __nanosleep(NCGP_WAIT_NS);
+#endif
     if (clock64() - t0 > (1ll << 35)) __trap();
   }
 #endif
