@@ -98,6 +98,8 @@ class Epi:
         if self.noise is not None and self.gamma != 0.0:
             kind, st = self.noise
             e.noise = {"softmax": N.NOISE_SOFTMAX, "diag": N.NOISE_DIAG}[kind]
+            if r0 and w <= 0:
+                raise N.DimensionMismatch("a sharded noise state needs the apply's width")
             e.noise_state = st.data_ptr() - r0 * w * st.element_size()
         if self.out2 is not None:
             e.ld2 = self.out2.stride(0) if self.out2.dim() == 2 else 1
@@ -323,6 +325,8 @@ class KernelOperator:
                    out.data_ptr() - row_begin * ldo * out.element_size(), ldo, e, row_begin,
                    row_end, stream())
             return out
+        if epi is not None and epi.row0:
+            raise N.DimensionMismatch("a sharded epilogue needs the matching row range")
         if out is None:
             out = torch.empty((self.n_rows, w), dtype=self.dtype, device=acc.device)
         ldo = out.stride(0) if out.shape[0] > 1 else w
