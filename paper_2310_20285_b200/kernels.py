@@ -229,6 +229,8 @@ class KernelOperator:
                 raise N.DimensionMismatch("a fused epilogue does not combine with peer outputs")
             if epi.noise is not None and epi.gamma != 0.0 and w > self.w_max:
                 raise N.DimensionMismatch(f"a noise epilogue needs w <= {self.w_max}, got {w}")
+            if epi.row0 > row_begin:
+                raise N.DimensionMismatch("epilogue shard starts after the first row of the range")
             for t in (epi.base, epi.out2):
                 if t is not None and (t.dtype != self.dtype or
                                       epi.row0 + t.shape[0] < min(row_end, self.n_rows) or
