@@ -40,6 +40,8 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
+from .device import nvtx_range
+
 ROW_ALIGN = 256  # the tcgen05 operator's row-tile pair (2 x 128 rows)
 
 
@@ -537,6 +539,18 @@ class ShardedStateOperator:
         self.comm.all_gather_(self._full, mine)
         return self._full[:self.n_rows]
 
+    def _row_block(self, V, O, e):
+        """This rank's rows of K V by the plain kernel, straight into the shard."""
+        C, r0, r1 = self.C, self.r0, self.r1
+        for kop, cols in self.inner.groups:
+            if len(cols) == C:
+                kop.apply(V, out=O, row_begin=r0, row_end=r1, epi=e, out_row0=r0)
+            else:  # mixed specs: one pass per spec group on its outputs
+                idx = torch.tensor(cols, device=V.device)
+                sub = kop.apply(V.index_select(1, idx).contiguous(), row_begin=r0,
+                                row_end=r1, out_row0=r0)
+                O[:, cols] = sub[:self.n_local]
+
     def _product(self, v_loc, out, epi):
         from .kernels import Epi
         C, r0, r1 = self.C, self.r0, self.r1
@@ -544,7 +558,8 @@ class ShardedStateOperator:
         if v_loc.numel() != self.n_local * C:
             raise ValueError(f"operand shard has {v_loc.numel()} entries, expected "
                              f"{self.n_local} * {C}")
-        V = self.gather_vector(v_loc)
+        with nvtx_range("operand all-gather"):
+            V = self.gather_vector(v_loc)
         if out is None:
             out = torch.empty((self.n_local, C), dtype=self.dtype, device=V.device)
         O = out.view(self.n_local, C)
@@ -558,18 +573,15 @@ class ShardedStateOperator:
             if self._acc is None:
                 self._acc = torch.empty(int(kop.sym_acc_elems(C)), dtype=torch.int64,
                                         device=V.device)
-            kop.sym_partial(V, self.comm.rank, self.comm.world, self._acc)
-            self.comm.all_reduce_(self._acc)
-            kop.sym_finalize(self._acc, C, O, V=V, epi=e, row_begin=r0, row_end=r1)
+            with nvtx_range("K products"):
+                kop.sym_partial(V, self.comm.rank, self.comm.world, self._acc)
+            with nvtx_range("accumulator all-reduce"):
+                self.comm.all_reduce_(self._acc)
+            with nvtx_range("K products"):
+                kop.sym_finalize(self._acc, C, O, V=V, epi=e, row_begin=r0, row_end=r1)
         else:
-            for kop, cols in self.inner.groups:
-                if len(cols) == C:
-                    kop.apply(V, out=O, row_begin=r0, row_end=r1, epi=e, out_row0=r0)
-                else:  # mixed specs: one pass per spec group on its outputs
-                    idx = torch.tensor(cols, device=V.device)
-                    sub = kop.apply(V.index_select(1, idx).contiguous(), row_begin=r0,
-                                    row_end=r1, out_row0=r0)
-                    O[:, cols] = sub[:self.n_local]
+            with nvtx_range("K products"):
+                self._row_block(V, O, e)
         self.matvecs += 1
         return out.reshape(-1) if flat else out
 

@@ -25,6 +25,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2310_20285_b200 as P  # noqa: E402
 from paper_2310_20285_b200 import configs  # noqa: E402
 from paper_2310_20285_b200 import parallel as PP  # noqa: E402
+from paper_2310_20285_b200.device import profile_ranges  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
 W = int(sys.argv[2]) if len(sys.argv) > 2 else 8
@@ -135,8 +136,19 @@ for r in ranks:
     assert rp.i == len(rp.log), (rp.i, len(rp.log))
     assert [s.inner_iterations for s in trace.steps] == res["sharded_inner_iters"]
     eff = t1.wallclock_s / (W * trace.wallclock_s)
+    # where the rank's time goes: CUDA-event time per nvtx range (a range's time
+    # includes the stream's idle gaps while the host issues its launches)
+    rp.i = 0
+    with profile_ranges() as rt:
+        _, tb = one_fit(rp, oc)
+    groups = {}
+    for k, (t, n) in rt.totals().items():
+        g = "solver (host sync + control)" if k.startswith("itergp_solve") else k
+        groups[g] = round(groups.get(g, 0.0) + t, 4)
     res["ranks"][str(r)] = {"rows": [op.r0, op.r1], "fit_s": round(trace.wallclock_s, 3),
-                            "efficiency_vs_one_gpu": round(eff, 3), "gather": op.gather}
+                            "efficiency_vs_one_gpu": round(eff, 3), "gather": op.gather,
+                            "range_time_s": dict(sorted(groups.items())),
+                            "range_run_fit_s": round(tb.wallclock_s, 3)}
     print(f"rank {r} of {W} alone (rows {op.r0}:{op.r1}, gather={op.gather}): "
           f"{trace.wallclock_s:.3f} s -> efficiency {eff:.3f} (collective latency not included)",
           flush=True)
