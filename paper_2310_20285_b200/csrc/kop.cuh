@@ -36,7 +36,7 @@ struct ncgp_kop {
   // tuning / experiment knobs, read once at creation (NCGP_* environment variables)
   int knob_sym = -1;      // NCGP_SYM: -1 policy, 0 off, 1 forced on
   int knob_sym_cg = 0;    // NCGP_SYM_CG: 0 policy, 1, 2 or 3 forced flavour
-  int knob_item = 128;    // NCGP_SYM_ITEM: column tiles per work item
+  int knob_item = 0;      // NCGP_SYM_ITEM: column tiles per work item (0: by problem size, sym_auto_item)
   int knob_item2 = 16;    // NCGP_SYM2_ITEM: the same for the blocked kernel (its O accumulates
                           // in fp32 TMEM over a whole item)
   bool knob_pair_order = false;  // NCGP_SYM_ORDER=pair

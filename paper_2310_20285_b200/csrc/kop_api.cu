@@ -42,7 +42,7 @@ void read_knobs(ncgp_kop* op) {
   auto env = [](const char* k) -> const char* { return getenv(k); };
   if (const char* e = env("NCGP_SYM")) op->knob_sym = e[0] == '0' ? 0 : (e[0] == '1' ? 1 : -1);
   if (const char* e = env("NCGP_SYM_CG")) op->knob_sym_cg = (e[0] >= '1' && e[0] <= '3') ? e[0] - '0' : 0;
-  if (const char* e = env("NCGP_SYM_ITEM")) op->knob_item = atoi(e) > 0 ? atoi(e) : 128;
+  if (const char* e = env("NCGP_SYM_ITEM")) op->knob_item = atoi(e) > 0 ? atoi(e) : 0;
   if (const char* e = env("NCGP_SYM2_ITEM")) op->knob_item2 = atoi(e) > 0 ? atoi(e) : 16;
   if (const char* e = env("NCGP_SYM_ORDER")) op->knob_pair_order = e[0] == 'p';
   if (const char* e = env("NCGP_SYM_ATM")) op->knob_atm = e[0] != '0';

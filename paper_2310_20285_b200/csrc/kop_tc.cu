@@ -3486,16 +3486,33 @@ int tc_prepare(ncgp_kop* op, cudaStream_t st) {
                               (size_t)L.tile_stride, st));
   if (op->Xr == op->Xc && op->n_rows == op->n_cols) {
     op->sym_cg = sym_cg(op, op->d, op->w_max);
+    // Column tiles per work item of K1-sym1 / the pair kernel.  Long items
+    // flush O less often; short ones balance the triangular list over the CTAs
+    // (each CTA walks items round-robin, so the slowest one runs
+    // ceil(items / CTAs) of them).  128 from ~64 rounds per CTA up, halved
+    // down to 16 below that (tools/item_sweep.py: pair kernel, Matern D = 20
+    // w = 10: n = 1e5 3.43 -> 3.28 ms, n = 1.5e5 7.67 -> 7.25 ms with 16;
+    // K1-sym1 n = 45k 0.96 -> 0.81 ms; from n = 2e5 up 64 / 128 are ahead).
+    // The length depends on the operator alone, never on how many processes
+    // split the list: the N-GPU product stays bitwise the one-GPU product.
+    auto auto_item = [&](double tiles) {
+      int it = 128;
+      while (it > SYM_ITEM_MIN && tiles / ((double)op->sms * it) < 64.0) it >>= 1;
+      return it;
+    };
+    const double nbt = (double)L.col_tiles;
+    const int item1 = op->knob_item > 0 ? op->knob_item : auto_item(0.5 * nbt * nbt);
+    const int itemp = op->knob_item > 0 ? op->knob_item : auto_item(0.25 * nbt * nbt);  // 256-row pairs
     if (op->sym_cg == 1)
       sym1_walk(L.col_tiles, [&](int64_t r, int64_t c0, int64_t c1) {
         tab.push_back(make_int4((int)r, (int)c0, (int)c1, 0));
-      }, op->knob_item);
+      }, item1);
     else if (op->sym_cg == 3)  // items of 16 column tiles: O is flushed every 2048 columns
       sym2_walk(L.col_tiles, [&](int64_t b, int64_t c0, int64_t c1) {
         tab.push_back(make_int4((int)b, (int)c0, (int)c1, 0));
       }, op->knob_item2);
     else
-      tab = sym_items(L.row_tiles / 2, L.col_tiles, op->knob_item, op->knob_pair_order);
+      tab = sym_items(L.row_tiles / 2, L.col_tiles, itemp, op->knob_pair_order);
     NCGP_CUDA(cudaMemcpyAsync(op->sym_tab, tab.data(), tab.size() * sizeof(int4),
                               cudaMemcpyHostToDevice, st));
     op->sym_items = (int64_t)tab.size();  // the stream sync below keeps `tab` alive long enough
