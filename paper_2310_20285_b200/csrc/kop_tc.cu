@@ -3053,8 +3053,14 @@ float* g_sym_dump = nullptr;   // debug hook (ncgp_debug_set_sym_dump)
 bool sym_enabled(const ncgp_kop* op, int family, int wp, int64_t col_tiles, int cg) {
   if (op->knob_sym == 0) return false;
   if (op->knob_sym == 1) return true;
+  // thresholds from tools/sym_threshold.py (one B200, size-dependent item length):
+  // Matern-3/2 (two MUFU ops per pair, so the halving pays early) from ~15k
+  // points on every flavour (n = 16k: 0.75-0.82 of the plain kernel's time,
+  // 38k: 0.62-0.67); RBF from ~38k on the single-CTA kernels (0.93) and from
+  // ~65k at WP = 16 on the pair kernel (D = 50: 0.99-1.10 below that)
+  if (family == NCGP_MATERN32) return col_tiles >= 120;
   if (cg == 1 || cg == 3) return col_tiles >= 300;
-  return col_tiles >= 512 && (family == NCGP_MATERN32 || wp == 16);
+  return col_tiles >= 512 && wp == 16;
 }
 int g_debug_mode = 0;          // debug hook (ncgp_debug_set_mode)
 
