@@ -3495,20 +3495,22 @@ int tc_prepare(ncgp_kop* op, cudaStream_t st) {
     // Column tiles per work item of K1-sym1 / the pair kernel.  Long items
     // flush O less often; short ones balance the triangular list over the CTAs
     // (each CTA walks items round-robin, so the slowest one runs
-    // ceil(items / CTAs) of them).  128 from ~64 rounds per CTA up, halved
+    // ceil(items / CTAs) of them).  128 from ~64-128 rounds per CTA up, halved
     // down to 16 below that (tools/item_sweep.py: pair kernel, Matern D = 20
     // w = 10: n = 1e5 3.43 -> 3.28 ms, n = 1.5e5 7.67 -> 7.25 ms with 16;
     // K1-sym1 n = 45k 0.96 -> 0.81 ms; from n = 2e5 up 64 / 128 are ahead).
     // The length depends on the operator alone, never on how many processes
     // split the list: the N-GPU product stays bitwise the one-GPU product.
-    auto auto_item = [&](double tiles) {
+    auto auto_item = [&](double tiles, double rounds) {
       int it = 128;
-      while (it > SYM_ITEM_MIN && tiles / ((double)op->sms * it) < 64.0) it >>= 1;
+      while (it > SYM_ITEM_MIN && tiles / ((double)op->sms * it) < rounds) it >>= 1;
       return it;
     };
     const double nbt = (double)L.col_tiles;
-    const int item1 = op->knob_item > 0 ? op->knob_item : auto_item(0.5 * nbt * nbt);
-    const int itemp = op->knob_item > 0 ? op->knob_item : auto_item(0.25 * nbt * nbt);  // 256-row pairs
+    // K1-sym1 restarts an item cheaply: ~128 rounds (n = 1e5: 16 tiles, 3.19 against
+    // 3.36 ms with 128); the pair kernel reloads its row tile into TMEM per item: ~64
+    const int item1 = op->knob_item > 0 ? op->knob_item : auto_item(0.5 * nbt * nbt, 128.0);
+    const int itemp = op->knob_item > 0 ? op->knob_item : auto_item(0.25 * nbt * nbt, 64.0);  // 256-row pairs
     if (op->sym_cg == 1)
       sym1_walk(L.col_tiles, [&](int64_t r, int64_t c0, int64_t c1) {
         tab.push_back(make_int4((int)r, (int)c0, (int)c1, 0));

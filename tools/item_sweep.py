@@ -37,7 +37,7 @@ for n, d, w, fam in shapes:
             os.environ["NCGP_SYM_ITEM"] = str(item)
         else:
             os.environ.pop("NCGP_SYM_ITEM", None)
-        op = KernelOperator(fam, 3.0 if d >= 20 else 1.5, 1.0, X, w_max=32)
+        op = KernelOperator(fam, 3.0 if d >= 20 else 1.5, 1.0, X, w_max=w)
         row.append(f"{'auto' if not item else item}: {timed(op, V, 20 if n <= 200_000 else 5):8.3f}")
         code = op.last_variant_code
         del op
