@@ -3169,6 +3169,16 @@ int sym_cg(const ncgp_kop* op, int d, int w_max) {
   // keeps 3-deep rings there
   const int wpm = wp_of(w_max);
   if (smem1_bytes(a, wpm, 2, 4, 2) <= SMEM_MAX || smem1_bytes(a, wpm, 3, 2, 2) <= SMEM_MAX) return 1;
+  // Matern-3/2 at WP = 32 beyond D = 8 (tools/flavours.py, one B200, n = 1e5 / 4e5):
+  // the blocked kernel where its rings fit (D <= ~12: 4.05 / 63.8 ms against
+  // K1-sym1's 4.39 / 70.4 and the pair kernel's 5.15 / 80.0), then K1-sym1 on
+  // its shallowest rings with one P buffer (D = 20: 4.42 / 71.0 against 5.16 / 82.0;
+  // D = 32: 5.02 / 81.7 against 5.18 / 84.7) -- the epilogue's two MUFU ops
+  // per pair hide the shallower rings
+  if (op->family == NCGP_MATERN32 && wpm == 32) {
+    if (smem2_bytes(a, 32, 2, 2, 0) <= SMEM_MAX) return 3;
+    if (smem1_bytes(a, 32, 2, 2, 1) <= SMEM_MAX) return 1;  // one P buffer from D ~ 12 up
+  }
   // experiments (NCGP_SYM1_NPB=1): one-P-buffer single-CTA kernel
   if (op->knob_npb1 && smem1_bytes(a, wp_of(w_max), 2, 2, 1) <= SMEM_MAX) return 1;
   return 2;

@@ -23,7 +23,7 @@ for name, env in (("plain", {"NCGP_SYM": "0"}), ("pair", {"NCGP_SYM": "1", "NCGP
         os.environ.pop(k, None)
     os.environ.update(env)
     try:
-        op = KernelOperator(fam, ell, 1.0, X, w_max=32)
+        op = KernelOperator(fam, ell, 1.0, X, w_max=int(os.environ.get("FLAV_WMAX", "32")))
         out = op.apply(V)
         torch.cuda.synchronize()
         ts = []
