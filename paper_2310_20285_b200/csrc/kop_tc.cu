@@ -3058,7 +3058,10 @@ bool sym_enabled(const ncgp_kop* op, int family, int wp, int64_t col_tiles, int 
   // points on every flavour (n = 16k: 0.75-0.82 of the plain kernel's time,
   // 38k: 0.62-0.67); RBF from ~38k on the single-CTA kernels (0.93) and from
   // ~65k at WP = 16 on the pair kernel (D = 50: 0.99-1.10 below that)
-  if (family == NCGP_MATERN32) return col_tiles >= 120;
+  if (family == NCGP_MATERN32) return col_tiles >= 90;   // n = 12k: 0.90-0.92
+  // RBF on K1-sym1 at WP = 16 (the fits' C <= 16 operators): 0.87 of the plain
+  // kernel's time at n = 16k, 0.73-0.81 from 20k to 38k
+  if (cg == 1 && wp == 16) return col_tiles >= 120;
   if (cg == 1 || cg == 3) return col_tiles >= 300;
   return col_tiles >= 512 && wp == 16;
 }
