@@ -33,6 +33,7 @@ is unit-tested on CPU with the ``gloo`` backend (tests/test_parallel_gloo.py).
 
 from __future__ import annotations
 
+import threading
 from typing import Callable, Optional, Tuple
 
 import numpy as np
@@ -398,7 +399,6 @@ class ThreadComm:
 
     class _Shared:
         def __init__(self, world):
-            import threading
             self.world = world
             self.slots = [None] * world
             self.barrier = threading.Barrier(world)
