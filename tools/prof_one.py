@@ -1,5 +1,5 @@
 """Apply one K(X, X) product `reps` times (ncu target).
-usage: python tools/prof_one.py n d w fam [cg] [reps]"""
+usage: [PROF_WMAX=32] [PROF_ELL=1.5] python tools/prof_one.py n d w fam [cg] [reps]"""
 import os
 import sys
 
@@ -17,7 +17,8 @@ os.environ["NCGP_SYM"] = "1"
 rng = np.random.default_rng(0)
 X = torch.from_numpy(rng.standard_normal((n, d)).astype(np.float32)).cuda()
 V = torch.from_numpy(rng.standard_normal((n, w)).astype(np.float32)).cuda()
-op = KernelOperator(fam, 1.5, 1.0, X, w_max=32)
+op = KernelOperator(fam, float(os.environ.get("PROF_ELL", "1.5")), 1.0, X,
+                    w_max=int(os.environ.get("PROF_WMAX", "32")))
 for _ in range(reps):
     op.apply(V)
 torch.cuda.synchronize()
